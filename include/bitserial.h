@@ -1,0 +1,181 @@
+/*
+ * bitserial.h — C ABI of the B200 (sm_100a) bitserial hot path of arXiv 1810.11066,
+ * "Automating Generation of Low Precision Deep Learning Operators".
+ *
+ * The library (paper_1810_11066_b200/libbitserial.so) exports exactly the functions
+ * below.  Citations are PAPER.md line numbers (/root/reference/PAPER.md, assembled
+ * copy lines 416-831) and the section/equation they fall in.
+ *
+ * The operation (Sec. 2.2, Eq. 1 and Eq. 2):
+ *     x . y = sum_{n<N} sum_{m<M} popcount(x_n & y_m) * 2^(m+n)
+ * over bit-planes x_n of the activations and y_m of the weights, packed into 32-bit
+ * words.  Bipolar weights (north_star) take each
+ * weight bit-plane as a +/-1 digit: per plane pair popc(a & w) - popc(a & ~w).
+ * Results are exact int32 ("a higher machine supported precision").
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ * ---------------------------------------------------------------------------
+ * Codes.     Activation and weight codes are unsigned integers in [0, 2^bits),
+ *            one per uint8_t, bits in [1, 8].  Activations are unsigned; the weight
+ *            encoding is BS_UNIPOLAR (value = code) or BS_BIPOLAR
+ *            (value = sum_j 2^j (2 b_j - 1) = 2 code - (2^bits - 1): W1 -> {-1,+1},
+ *            W2 -> {-3,-1,+1,+3}).  Codes outside [0, 2^bits) are a precondition
+ *            violation: the packer uses only the low `bits` bits.
+ * Packed.    "Packed" tensors use layout BMK' (bit axis outermost):
+ *            uint32 [bits][rows][Kw_pad], Kw_pad = bs_packed_row_words(K); bit t of
+ *            word j of plane b is bit b of code [row][32 j + t] (LSB-first); bits at
+ *            reduction index >= K are 0.
+ * Pointers.  All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *            storage) unless the name ends in _host.  Tensor base pointers must be
+ *            16-byte aligned.  The caller owns every buffer; the library never
+ *            allocates or frees device memory and keeps no per-call state except a
+ *            thread-local error string.
+ * Streams.   `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *            stream).  Every call except *_host is asynchronous and stream-ordered:
+ *            it validates, launches and returns without synchronizing.
+ * Errors.    Every function validates all arguments BEFORE launching; on a non-OK
+ *            status nothing was launched and no output was written.  BS_ERR_CUDA
+ *            reports a launch failure (cudaPeekAtLastError / cudaGetLastError after
+ *            launch); faults of a running kernel surface at the caller's next
+ *            synchronization, as usual in CUDA.  bs_last_error() returns a
+ *            thread-local message for the last non-OK status.  No C++ exception
+ *            crosses this boundary.
+ * Accumulator bound.  K * (2^a_bits - 1) * (2^w_bits - 1) must be < 2^31
+ *            (BS_ERR_OVERFLOW otherwise) so every output is exact in int32.
+ */
+#ifndef BITSERIAL_H_
+#define BITSERIAL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_ABI_VERSION 1
+
+typedef enum {
+  BS_OK = 0,
+  BS_ERR_NULL = 1,          /* a required pointer is NULL */
+  BS_ERR_INVALID_ARG = 2,   /* bits not in [1,8], stride < 1, pad < 0, bad encoding/algo */
+  BS_ERR_UNSUPPORTED = 3,   /* valid but not implemented (e.g. algo not built for bits) */
+  BS_ERR_SHAPE = 4,         /* non-positive extent, or empty convolution output */
+  BS_ERR_ALIGN = 5,         /* a tensor pointer is not 16-byte aligned */
+  BS_ERR_OVERFLOW = 6,      /* K * (2^A-1) * (2^W-1) >= 2^31 */
+  BS_ERR_CUDA = 7,          /* CUDA runtime error at launch / copy */
+  BS_ERR_WORKSPACE = 8      /* workspace missing or smaller than *_workspace_bytes() */
+} bs_status;
+
+typedef enum { BS_UNIPOLAR = 0, BS_BIPOLAR = 1 } bs_encoding;
+
+/* Kernel family for the *_ex entry points.  BS_ALGO_AUTO picks per shape.
+ *   POPC     : AND + POPC per word pair (Eq. 1 inside Eq. 2) on the integer pipes;
+ *              bipolar applied as the exact identity 2*U - (2^W-1)*sum(a).
+ *   POPC_LIT : as POPC but bipolar evaluated literally, popc(a&w) - popc(a&~w) per
+ *              plane pair (north_star form; twice the POPC work; unipolar = POPC).
+ *   GEMV     : warp-per-rows matrix-vector kernel with butterfly multi-row reduction
+ *              (PAPER.md:694-705 micro-kernel ideas), for m <= 8 (dense only). */
+typedef enum {
+  BS_ALGO_AUTO = 0,
+  BS_ALGO_POPC = 1,
+  BS_ALGO_POPC_LIT = 2,
+  BS_ALGO_GEMV = 3
+} bs_algo;
+
+int bs_abi_version(void);
+const char* bs_status_string(int status);
+const char* bs_last_error(void);
+
+/* Words per packed row for reduction length k: ceil(k/32) rounded up to an even
+ * number (8-byte rows).  Returns 0 for k <= 0. */
+int64_t bs_packed_row_words(int64_t k);
+
+/* ---------------------------------------------------------------------------
+ * Bit-packing (Sec. 3.1; timed for activations, not
+ * for weights).
+ *   in   : device uint8 codes [rows][k], row-major.
+ *   out  : device uint32 [bits][rows][bs_packed_row_words(k)], written entirely
+ *          (pad words/bits are written as 0).
+ *   rows >= 1, k >= 1, bits in [1,8].  For conv activations rows = N*H*W, k = C
+ *   (NHWC); for conv weights rows = OC*KH*KW, k = C (OHWI); for dense rows = M or N.
+ */
+int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Bitserial dense / matrix multiply (Sec. 3.2 and 6.2.1).
+ *   out[m][n] = sum_{k<K} a[m][k] * value(w[n][k])          (int32 [m][n] row-major)
+ *   a_packed : device, bs_bitpack of the [m][k] activation codes at a_bits.
+ *   w_packed : device, bs_bitpack of the [n][k] weight codes at w_bits.
+ *   Both must be packed with the same k.
+ */
+int bs_bitserial_dense(const uint32_t* a_packed, int a_bits,
+                       const uint32_t* w_packed, int w_bits, int w_enc,
+                       int32_t* out, int64_t m, int64_t n, int64_t k, void* stream);
+
+int bs_bitserial_dense_ex(const uint32_t* a_packed, int a_bits,
+                          const uint32_t* w_packed, int w_bits, int w_enc,
+                          int32_t* out, int64_t m, int64_t n, int64_t k,
+                          int algo, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Bitserial 2-D convolution, NHWC ("NHWC ... efficient in place
+ * convolution", geometry of Table 1).  Cross-correlation (no
+ * kernel flip) with zero padding (pad positions are activation code 0, exact in
+ * both encodings):
+ *   out[b][oy][ox][o] = sum_{ky,kx,c} act[b][oy*sh+ky-ph][ox*sw+kx-pw][c] * value(wt[o][ky][kx][c])
+ *   oh = floor((h + 2 ph - kh) / sh) + 1,  ow = floor((w + 2 pw - kw) / sw) + 1.
+ *   act_packed : device, bs_bitpack of the NHWC codes viewed as [n*h*w][c].
+ *   w_packed   : device, bs_bitpack of the OHWI codes viewed as [oc*kh*kw][c].
+ *   out        : device int32 NHWC [n][oh][ow][oc].
+ * The convolution is implicit-GEMM (M = n*oh*ow, N = oc, K = kh*kw*c): no lowered
+ * (im2col) copy is materialized.
+ */
+int bs_bitserial_conv2d_nhwc(const uint32_t* act_packed, int a_bits,
+                             const uint32_t* w_packed, int w_bits, int w_enc,
+                             int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                             int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
+
+int bs_bitserial_conv2d_nhwc_ex(const uint32_t* act_packed, int a_bits,
+                                const uint32_t* w_packed, int w_bits, int w_enc,
+                                int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                int stride_h, int stride_w, int pad_h, int pad_w,
+                                int algo, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Entries that include activation packing — what the paper times (PAPER.md:715:
+ * "we include the cost of bitpacking activations ... but not ... weights").
+ * The activation operand is raw uint8 codes (device); the packed activations go to
+ * a caller-supplied device workspace of at least *_workspace_bytes() bytes.
+ */
+int64_t bs_dense_workspace_bytes(int64_t m, int64_t k, int a_bits);
+int bs_bitserial_dense_i8(const uint8_t* a, int a_bits,
+                          const uint32_t* w_packed, int w_bits, int w_enc,
+                          int32_t* out, int64_t m, int64_t n, int64_t k,
+                          void* workspace, int64_t workspace_bytes, void* stream);
+
+int64_t bs_conv2d_workspace_bytes(int n, int h, int w, int c, int a_bits);
+int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
+                                const uint32_t* w_packed, int w_bits, int w_enc,
+                                int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                int stride_h, int stride_w, int pad_h, int pad_w,
+                                void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * End-to-end entry with HOST activations and HOST output (used for the bench's
+ * e2e number).  Copies act_host (uint8 NHWC, pinned or pageable) into the device
+ * buffer act_dev, packs it into workspace, convolves into out_dev, copies out_dev
+ * into out_host, and synchronizes `stream` before returning (out_host is valid on
+ * return).  act_dev must hold n*h*w*c bytes and out_dev n*oh*ow*oc int32.
+ */
+int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits,
+                                  const uint32_t* w_packed, int w_bits, int w_enc,
+                                  int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+                                  int stride_h, int stride_w, int pad_h, int pad_w,
+                                  uint8_t* act_dev, int32_t* out_dev,
+                                  void* workspace, int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BITSERIAL_H_ */

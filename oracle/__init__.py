@@ -1,0 +1,145 @@
+"""CPU oracle for the bitserial hot path (arXiv 1810.11066) — TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_1810_11066_b200`` never imports it and shares no code with it.
+
+The arithmetic lives in ``oracle/oracle.c`` (plain C, OpenMP over the outermost
+output loop).  This module only builds that library with gcc and marshals numpy
+arrays into it.  Every function states the passage it follows; the pins that tie
+it to the paper are in ``tests/test_oracle_pins.py``.
+
+Parity status: every function below is pinned (no "parity unpinned" entries); see
+DESIGN.md §3 for the readings of the paper they rely on.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into oracle/liboracle.so with gcc (-O3 -march=native -fopenmp)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared",
+                               "-Wall", "-Wextra", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+        lib.oracle_weight_value.argtypes = [I, I, I]
+        lib.oracle_weight_value.restype = L
+        lib.oracle_dense.argtypes = [P, I, P, I, I, P, L, L, L]
+        lib.oracle_dense.restype = I
+        lib.oracle_conv2d_nhwc.argtypes = [P, I, P, I, I, P] + [I] * 11
+        lib.oracle_conv2d_nhwc.restype = I
+        lib.oracle_conv_out_extent.argtypes = [L, L, L, L]
+        lib.oracle_conv_out_extent.restype = L
+        lib.oracle_packed_row_words.argtypes = [L]
+        lib.oracle_packed_row_words.restype = L
+        lib.oracle_bitpack.argtypes = [P, P, L, L, I]
+        lib.oracle_bitpack.restype = I
+        lib.oracle_num_threads.restype = I
+        _lib = lib
+    return _lib
+
+
+def _u8(x) -> np.ndarray:
+    x = np.asarray(x)
+    if x.dtype != np.uint8:
+        if x.size and (x.min() < 0 or x.max() > 255):
+            raise ValueError("codes must lie in [0, 255]")
+        x = x.astype(np.uint8)
+    return np.ascontiguousarray(x)
+
+
+def _ptr(x: np.ndarray):
+    return x.ctypes.data_as(ctypes.c_void_p)
+
+
+def num_threads() -> int:
+    """OpenMP threads the oracle runs on (OMP_NUM_THREADS, else all host cores)."""
+    return int(_load().oracle_num_threads())
+
+
+def weight_value(code: int, bits: int, bipolar: bool) -> int:
+    """Value of one weight code: unipolar = code; bipolar = sum_j 2^j (2 b_j - 1)
+    (PAPER.md:503 bipolar +/-1 digits; readings R1-R3)."""
+    return int(_load().oracle_weight_value(int(code), int(bits), int(bool(bipolar))))
+
+
+def dense(a, a_bits: int, w, w_bits: int, bipolar: bool) -> np.ndarray:
+    """out[m][n] = sum_k a[m][k] * value(w[n][k]).
+
+    a: [M][K] unsigned activation codes; w: [N][K] weight codes; returns int32 [M][N]."""
+    a, w = _u8(a), _u8(w)
+    if a.ndim != 2 or w.ndim != 2 or a.shape[1] != w.shape[1]:
+        raise ValueError("dense: a [M][K], w [N][K] with equal K")
+    m, k = a.shape
+    n = w.shape[0]
+    out = np.empty((m, n), dtype=np.int32)
+    rc = _load().oracle_dense(_ptr(a), a_bits, _ptr(w), w_bits, int(bool(bipolar)), _ptr(out), m, n, k)
+    if rc != 0:
+        raise ValueError("oracle_dense rejected its arguments")
+    return out
+
+
+def conv_out_extent(size: int, k: int, stride: int, pad: int) -> int:
+    """floor((size + 2 pad - k) / stride) + 1, or 0 if the window does not fit."""
+    return int(_load().oracle_conv_out_extent(size, k, stride, pad))
+
+
+def conv2d_nhwc(act, a_bits: int, wt, w_bits: int, bipolar: bool,
+                stride=(1, 1), pad=(0, 0)) -> np.ndarray:
+    """NHWC cross-correlation with zero padding, OHWI weights (Table 1
+    PAPER.md:733-746).  act: [N][H][W][C] codes; wt: [OC][KH][KW][C] codes;
+    returns int32 [N][OH][OW][OC]."""
+    act, wt = _u8(act), _u8(wt)
+    if act.ndim != 4 or wt.ndim != 4 or act.shape[3] != wt.shape[3]:
+        raise ValueError("conv2d_nhwc: act [N][H][W][C], wt [OC][KH][KW][C]")
+    n, h, w, c = act.shape
+    oc, kh, kw, _ = wt.shape
+    sh, sw = stride
+    ph, pw = pad
+    oh, ow = conv_out_extent(h, kh, sh, ph), conv_out_extent(w, kw, sw, pw)
+    if oh <= 0 or ow <= 0:
+        raise ValueError("conv2d_nhwc: empty output")
+    out = np.empty((n, oh, ow, oc), dtype=np.int32)
+    rc = _load().oracle_conv2d_nhwc(_ptr(act), a_bits, _ptr(wt), w_bits, int(bool(bipolar)), _ptr(out),
+                                    n, h, w, c, oc, kh, kw, sh, sw, ph, pw)
+    if rc != 0:
+        raise ValueError("oracle_conv2d_nhwc rejected its arguments")
+    return out
+
+
+def packed_row_words(k: int) -> int:
+    """Words per packed row: ceil(k/32) rounded up to even (reading R7)."""
+    return int(_load().oracle_packed_row_words(k))
+
+
+def bitpack(x, bits: int) -> np.ndarray:
+    """Bit-plane packing, layout BMK': returns uint32
+    [bits][rows][Kw_pad]; bit t of word j of plane b = bit b of x[r][32 j + t]."""
+    x = _u8(x)
+    if x.ndim != 2:
+        raise ValueError("bitpack: x [rows][K]")
+    rows, k = x.shape
+    out = np.empty((bits, rows, packed_row_words(k)), dtype=np.uint32)
+    if _load().oracle_bitpack(_ptr(x), _ptr(out), rows, k, bits) != 0:
+        raise ValueError("oracle_bitpack rejected its arguments")
+    return out

@@ -1,0 +1,164 @@
+/*
+ * oracle.c — CPU oracle for the bitserial hot path of arXiv 1810.11066.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  The
+ * product path (paper_1810_11066_b200/) never links, imports or calls it, and
+ * this file shares no code, header, table or constant with the CUDA path.
+ *
+ * What it computes: the plain integer definitions that the bitserial method
+ * reaches exactly (Eq. 1, Eq. 2 are identities over
+ * integers, so the method's result IS the integer dot product / convolution):
+ *
+ *   oracle_weight_value  value of one weight code (unipolar / bipolar)
+ *   oracle_dense         out[m][n] = sum_k a[m][k] * value(w[n][k])
+ *   oracle_conv2d_nhwc   NHWC cross-correlation with zero padding, OHWI weights
+ *   oracle_bitpack       the packed bit-plane layout of the C ABI (defines it)
+ *
+ * No bit-planes, no popcount, no blocking or reordering: straight loops over the
+ * decoded integer values in the order of the definitions.  The only parallelism is
+ * an OpenMP split of the outermost output loop (each output is still one
+ * sequential sum), used so the CPU baseline is timed on all host cores.
+ *
+ * Pinned by tests/test_oracle_pins.py (brute-force Eq. 2 over bit-planes,
+ * torch float64 mm / conv2d, closed forms, invariants, tests/golden/ fixtures).
+ * Readings of the paper this file relies on are listed in DESIGN.md §3.
+ *
+ * Return codes: 0 = ok, -1 = invalid argument (codes out of range, bad shape,
+ * accumulator bound exceeded).  Outputs are int32 as on the GPU; every call checks
+ * that the largest possible |output| fits (bound check, not saturation).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Value of one weight code (readings R1-R3).
+ * Unipolar: the code itself (Eq. 2, weights are unsigned M-bit ints).
+ * Bipolar : each bit-plane is a +/-1 digit ("bipolar format (-1 and 1)";
+ *           north_star: per plane pair popc(a & w) - popc(a & ~w)), so bit b_j set
+ *           contributes +2^j and clear contributes -2^j:  value = sum_j 2^j (2 b_j - 1). */
+int64_t oracle_weight_value(int code, int bits, int bipolar) {
+  if (!bipolar) return code;
+  int64_t v = 0;
+  for (int j = 0; j < bits; ++j) {
+    int b = (code >> j) & 1;
+    v += (b ? 1 : -1) * ((int64_t)1 << j);
+  }
+  return v;
+}
+
+static int codes_in_range(const uint8_t* x, int64_t n, int bits) {
+  for (int64_t i = 0; i < n; ++i)
+    if (x[i] >= (1u << bits)) return 0;
+  return 1;
+}
+
+/* largest |value| a weight code can take */
+static int64_t max_abs_weight(int bits) { return ((int64_t)1 << bits) - 1; }
+
+/* Dense / matrix multiply: a [m][k] activation codes
+ * (unsigned, a_bits), w [n][k] weight codes (w_bits, unipolar or bipolar),
+ * out [m][n] int32 row-major. */
+int oracle_dense(const uint8_t* a, int a_bits, const uint8_t* w, int w_bits, int bipolar,
+                 int32_t* out, int64_t m, int64_t n, int64_t k) {
+  if (m <= 0 || n <= 0 || k <= 0 || a_bits < 1 || a_bits > 8 || w_bits < 1 || w_bits > 8) return -1;
+  if (!codes_in_range(a, m * k, a_bits) || !codes_in_range(w, n * k, w_bits)) return -1;
+  if ((double)k * (double)(((int64_t)1 << a_bits) - 1) * (double)max_abs_weight(w_bits) >= 2147483648.0) return -1;
+  int32_t* wv = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n * k));
+  if (!wv) return -1;
+  for (int64_t i = 0; i < n * k; ++i) wv[i] = (int32_t)oracle_weight_value(w[i], w_bits, bipolar);
+#pragma omp parallel for schedule(static)
+  for (int64_t mi = 0; mi < m; ++mi) {
+    for (int64_t ni = 0; ni < n; ++ni) {
+      int32_t acc = 0;
+      for (int64_t ki = 0; ki < k; ++ki) acc += (int32_t)a[mi * k + ki] * wv[ni * k + ki];
+      out[mi * n + ni] = acc;
+    }
+  }
+  free(wv);
+  return 0;
+}
+
+/* Output extent of a convolution along one axis: floor((in + 2p - r) / s) + 1. */
+int64_t oracle_conv_out_extent(int64_t in, int64_t r, int64_t s, int64_t p) {
+  int64_t span = in + 2 * p - r;
+  if (span < 0 || s < 1) return 0;
+  return span / s + 1;
+}
+
+/* 2-D convolution, NHWC activations, OHWI weights ("NHWC", Table 1
+ * PAPER.md:733-746 geometry): cross-correlation (no kernel flip) with zero padding
+ * (pad positions are activation code 0), out int32 NHWC [n][oh][ow][oc]. */
+int oracle_conv2d_nhwc(const uint8_t* act, int a_bits, const uint8_t* wt, int w_bits, int bipolar,
+                       int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                       int sh, int sw, int ph, int pw) {
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || oc <= 0 || kh <= 0 || kw <= 0) return -1;
+  if (sh < 1 || sw < 1 || ph < 0 || pw < 0) return -1;
+  if (a_bits < 1 || a_bits > 8 || w_bits < 1 || w_bits > 8) return -1;
+  int64_t oh = oracle_conv_out_extent(h, kh, sh, ph), ow = oracle_conv_out_extent(w, kw, sw, pw);
+  if (oh <= 0 || ow <= 0) return -1;
+  int64_t K = (int64_t)kh * kw * c;
+  if (!codes_in_range(act, (int64_t)n * h * w * c, a_bits) || !codes_in_range(wt, (int64_t)oc * K, w_bits)) return -1;
+  if ((double)K * (double)(((int64_t)1 << a_bits) - 1) * (double)max_abs_weight(w_bits) >= 2147483648.0) return -1;
+  int32_t* wv = (int32_t*)malloc(sizeof(int32_t) * (size_t)(oc * K));
+  if (!wv) return -1;
+  for (int64_t i = 0; i < oc * K; ++i) wv[i] = (int32_t)oracle_weight_value(wt[i], w_bits, bipolar);
+  int64_t rows = (int64_t)n * oh * ow;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    int64_t b = r / (oh * ow), oy = (r / ow) % oh, ox = r % ow;
+    for (int o = 0; o < oc; ++o) {
+      int32_t acc = 0;
+      for (int ky = 0; ky < kh; ++ky) {
+        int64_t iy = oy * sh + ky - ph;
+        if (iy < 0 || iy >= h) continue; /* zero padding contributes 0 */
+        for (int kx = 0; kx < kw; ++kx) {
+          int64_t ix = ox * sw + kx - pw;
+          if (ix < 0 || ix >= w) continue;
+          const uint8_t* ap = act + ((b * h + iy) * w + ix) * c;
+          const int32_t* wp = wv + (((int64_t)o * kh + ky) * kw + kx) * c;
+          for (int ci = 0; ci < c; ++ci) acc += (int32_t)ap[ci] * wp[ci];
+        }
+      }
+      out[r * oc + o] = acc;
+    }
+  }
+  free(wv);
+  return 0;
+}
+
+/* Words per packed row: ceil(k/32) rounded up to an even count (8-byte rows). */
+int64_t oracle_packed_row_words(int64_t k) {
+  int64_t kw = (k + 31) / 32;
+  return kw + (kw & 1);
+}
+
+/* Bit-packing: split codes into bit-planes and pack
+ * along the reduction axis into uint32 words.  Layout BMK' (bit axis outermost,
+ * PAPER.md:564-567): out[b][r][j], bit t of word j = bit b of in[r][32j + t]
+ * (LSB-first, reading R7); bits past k are 0. */
+int oracle_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits) {
+  if (rows <= 0 || k <= 0 || bits < 1 || bits > 8) return -1;
+  if (!codes_in_range(in, rows * k, bits)) return -1;
+  int64_t kwp = oracle_packed_row_words(k);
+  for (int b = 0; b < bits; ++b)
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t j = 0; j < kwp; ++j) {
+        uint32_t word = 0;
+        for (int t = 0; t < 32; ++t) {
+          int64_t ki = 32 * j + t;
+          if (ki < k && ((in[r * k + ki] >> b) & 1)) word |= (uint32_t)1 << t;
+        }
+        out[(b * rows + r) * kwp + j] = word;
+      }
+  return 0;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
