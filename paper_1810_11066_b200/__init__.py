@@ -1,0 +1,217 @@
+"""Python binding of the B200 bitserial C ABI (include/bitserial.h).
+
+Argument marshalling only: every function checks tensor placement/dtype/shape,
+allocates outputs with torch (device memory is PyTorch's job), and calls the
+same-named ``bs_*`` entry point of ``libbitserial.so`` on the current CUDA stream.
+All arithmetic of the hot path runs in the library's sm_100a kernels; there is no
+CPU fallback — if the library is missing or the device is not CUDA, calls raise.
+
+Packed tensors are returned as ``torch.int32`` tensors holding the uint32 words
+bit-for-bit (torch's uint32 dtype has too few kernels to be convenient); shape
+``[bits][rows][packed_row_words(k)]`` (layout BMK').
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "UNIPOLAR", "BIPOLAR", "ALGO_AUTO", "ALGO_POPC", "ALGO_POPC_LIT", "ALGO_GEMV",
+    "BitserialError", "library_path", "abi_version", "packed_row_words", "bitpack",
+    "bitserial_dense", "bitserial_dense_i8", "bitserial_conv2d_nhwc", "bitserial_conv2d_nhwc_i8",
+    "bitserial_conv2d_nhwc_host", "conv2d_workspace_bytes", "dense_workspace_bytes", "conv_out_extent",
+    "EXPORTED_SYMBOLS",
+]
+
+UNIPOLAR, BIPOLAR = 0, 1
+ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV = 0, 1, 2, 3
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libbitserial.so")
+_lib = None
+
+EXPORTED_SYMBOLS = (
+    "bs_abi_version", "bs_status_string", "bs_last_error", "bs_packed_row_words", "bs_bitpack",
+    "bs_bitserial_dense", "bs_bitserial_dense_ex", "bs_dense_workspace_bytes", "bs_bitserial_dense_i8",
+    "bs_bitserial_conv2d_nhwc", "bs_bitserial_conv2d_nhwc_ex", "bs_conv2d_workspace_bytes",
+    "bs_bitserial_conv2d_nhwc_i8", "bs_bitserial_conv2d_nhwc_host",
+)
+
+
+class BitserialError(RuntimeError):
+    pass
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise BitserialError(f"{_LIB_PATH} is missing: build it with `python -m paper_1810_11066_b200.build` "
+                             "(there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    sig = {
+        "bs_abi_version": ([], I),
+        "bs_status_string": ([I], ctypes.c_char_p),
+        "bs_last_error": ([], ctypes.c_char_p),
+        "bs_packed_row_words": ([L], L),
+        "bs_bitpack": ([P, P, L, L, I, P], I),
+        "bs_bitserial_dense": ([P, I, P, I, I, P, L, L, L, P], I),
+        "bs_bitserial_dense_ex": ([P, I, P, I, I, P, L, L, L, I, P], I),
+        "bs_dense_workspace_bytes": ([L, L, I], L),
+        "bs_bitserial_dense_i8": ([P, I, P, I, I, P, L, L, L, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc": ([P, I, P, I, I, P] + [I] * 11 + [P], I),
+        "bs_bitserial_conv2d_nhwc_ex": ([P, I, P, I, I, P] + [I] * 11 + [I, P], I),
+        "bs_conv2d_workspace_bytes": ([I, I, I, I, I], L),
+        "bs_bitserial_conv2d_nhwc_i8": ([P, I, P, I, I, P] + [I] * 11 + [P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_host": ([P, I, P, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes, f.restype = args, res
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != 0:
+        lib = _load()
+        raise BitserialError(f"{lib.bs_status_string(status).decode()}: {lib.bs_last_error().decode()}")
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str, dtype):
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise BitserialError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise BitserialError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise BitserialError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def abi_version() -> int:
+    return int(_load().bs_abi_version())
+
+
+def packed_row_words(k: int) -> int:
+    return int(_load().bs_packed_row_words(int(k)))
+
+
+def conv_out_extent(size: int, k: int, stride: int, pad: int) -> int:
+    span = size + 2 * pad - k
+    return span // stride + 1 if span >= 0 else 0
+
+
+def dense_workspace_bytes(m: int, k: int, a_bits: int) -> int:
+    return int(_load().bs_dense_workspace_bytes(m, k, a_bits))
+
+
+def conv2d_workspace_bytes(n: int, h: int, w: int, c: int, a_bits: int) -> int:
+    return int(_load().bs_conv2d_workspace_bytes(n, h, w, c, a_bits))
+
+
+def bitpack(x: torch.Tensor, bits: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """bs_bitpack: uint8 codes [rows][k] (or any shape, reduction axis last) ->
+    int32-viewed uint32 words [bits][rows][packed_row_words(k)]."""
+    k = x.shape[-1]
+    rows = x.numel() // k
+    if out is None:
+        out = torch.empty((bits, rows, packed_row_words(k)), dtype=torch.int32, device=x.device)
+    _check(_load().bs_bitpack(_dev(x, "x", torch.uint8), _dev(out, "out", torch.int32), rows, k, bits,
+                              _stream(stream)))
+    return out
+
+
+def bitserial_dense(a_packed, a_bits, w_packed, w_bits, w_enc, m, n, k, out=None, algo=ALGO_AUTO, stream=None):
+    """bs_bitserial_dense(_ex): out[m][n] = sum_k a[m][k] * value(w[n][k]) (int32)."""
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int32, device=a_packed.device)
+    _check(_load().bs_bitserial_dense_ex(_dev(a_packed, "a_packed", torch.int32), a_bits,
+                                         _dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc),
+                                         _dev(out, "out", torch.int32), m, n, k, int(algo), _stream(stream)))
+    return out
+
+
+def bitserial_dense_i8(a, a_bits, w_packed, w_bits, w_enc, n, out=None, workspace=None, stream=None):
+    """bs_bitserial_dense_i8: raw uint8 activation codes a [m][k] packed inside the call."""
+    m, k = a.shape
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    need = dense_workspace_bytes(m, k, a_bits)
+    if workspace is None:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=a.device)
+    _check(_load().bs_bitserial_dense_i8(_dev(a, "a", torch.uint8), a_bits, _dev(w_packed, "w_packed", torch.int32),
+                                         w_bits, int(w_enc), _dev(out, "out", torch.int32), m, n, k,
+                                         _dev(workspace, "workspace", torch.uint8), workspace.numel(),
+                                         _stream(stream)))
+    return out
+
+
+def _conv_geom(n, h, w, kh, kw, stride, pad):
+    sh, sw = (stride, stride) if isinstance(stride, int) else stride
+    ph, pw = (pad, pad) if isinstance(pad, int) else pad
+    return sh, sw, ph, pw, conv_out_extent(h, kh, sh, ph), conv_out_extent(w, kw, sw, pw)
+
+
+def bitserial_conv2d_nhwc(act_packed, a_bits, w_packed, w_bits, w_enc, n, h, w, c, oc, kh, kw,
+                          stride=1, pad=0, out=None, algo=ALGO_AUTO, stream=None):
+    """bs_bitserial_conv2d_nhwc(_ex): packed NHWC activations x packed OHWI weights ->
+    int32 NHWC [n][oh][ow][oc]."""
+    sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
+    if out is None:
+        out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act_packed.device)
+    _check(_load().bs_bitserial_conv2d_nhwc_ex(_dev(act_packed, "act_packed", torch.int32), a_bits,
+                                               _dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc),
+                                               _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
+                                               int(algo), _stream(stream)))
+    return out
+
+
+def bitserial_conv2d_nhwc_i8(act, a_bits, w_packed, w_bits, w_enc, oc, kh, kw, stride=1, pad=0,
+                             out=None, workspace=None, stream=None):
+    """bs_bitserial_conv2d_nhwc_i8: raw uint8 NHWC activations [n][h][w][c], packed
+    inside the call (the timed activation packing of PAPER.md:715)."""
+    n, h, w, c = act.shape
+    sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
+    if out is None:
+        out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act.device)
+    need = conv2d_workspace_bytes(n, h, w, c, a_bits)
+    if workspace is None:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=act.device)
+    _check(_load().bs_bitserial_conv2d_nhwc_i8(_dev(act, "act", torch.uint8), a_bits,
+                                               _dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc),
+                                               _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
+                                               _dev(workspace, "workspace", torch.uint8), workspace.numel(),
+                                               _stream(stream)))
+    return out
+
+
+def bitserial_conv2d_nhwc_host(act_host, a_bits, w_packed, w_bits, w_enc, oc, kh, kw, stride, pad,
+                               out_host, act_dev, out_dev, workspace, stream=None):
+    """bs_bitserial_conv2d_nhwc_host: host uint8 NHWC in, host int32 NHWC out; copies,
+    packs, convolves and synchronizes inside the call (the e2e path)."""
+    if act_host.device.type != "cpu" or out_host.device.type != "cpu":
+        raise BitserialError("act_host/out_host must be CPU tensors")
+    if not (act_host.is_contiguous() and out_host.is_contiguous()):
+        raise BitserialError("host buffers must be contiguous")
+    n, h, w, c = act_host.shape
+    sh, sw, ph, pw, _, _ = _conv_geom(n, h, w, kh, kw, stride, pad)
+    _check(_load().bs_bitserial_conv2d_nhwc_host(
+        ctypes.c_void_p(act_host.data_ptr()), a_bits, _dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc),
+        ctypes.c_void_p(out_host.data_ptr()), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
+        _dev(act_dev, "act_dev", torch.uint8), _dev(out_dev, "out_dev", torch.int32),
+        _dev(workspace, "workspace", torch.uint8), workspace.numel(), _stream(stream)))
+    return out_host

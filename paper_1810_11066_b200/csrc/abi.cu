@@ -1,0 +1,252 @@
+// abi.cu — the C ABI declared in include/bitserial.h: argument validation (all of it
+// before any launch), kernel selection, launch on the caller's stream.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/bitserial.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return BS_OK;
+  if (e == cudaErrorNotSupported) return fail(BS_ERR_UNSUPPORTED, "%s: no kernel instantiation for these arguments", where);
+  return fail(BS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int64_t row_words(int64_t k) {
+  if (k <= 0) return 0;
+  const int64_t kw = (k + 31) / 32;
+  return kw + (kw & 1);
+}
+
+int check_bits(int a_bits, int w_bits, int w_enc, const char* fn) {
+  if (a_bits < 1 || a_bits > 8) return fail(BS_ERR_INVALID_ARG, "%s: a_bits=%d not in [1,8]", fn, a_bits);
+  if (w_bits < 1 || w_bits > 8) return fail(BS_ERR_INVALID_ARG, "%s: w_bits=%d not in [1,8]", fn, w_bits);
+  if (w_enc != BS_UNIPOLAR && w_enc != BS_BIPOLAR) return fail(BS_ERR_INVALID_ARG, "%s: bad encoding %d", fn, w_enc);
+  return BS_OK;
+}
+
+int check_bound(int64_t k, int a_bits, int w_bits, const char* fn) {
+  const double bound = double(k) * double((1 << a_bits) - 1) * double((1 << w_bits) - 1);
+  if (bound >= 2147483648.0) return fail(BS_ERR_OVERFLOW, "%s: K*(2^A-1)*(2^W-1) = %.0f >= 2^31", fn, bound);
+  return BS_OK;
+}
+
+int check_algo(int algo, const char* fn) {
+  if (algo < BS_ALGO_AUTO || algo > BS_ALGO_GEMV) return fail(BS_ERR_INVALID_ARG, "%s: bad algo %d", fn, algo);
+  return BS_OK;
+}
+
+struct ConvArgs {
+  int n, h, w, c, oc, kh, kw, sh, sw, ph, pw;
+};
+
+int conv_out(int in, int k, int s, int p) {
+  const int span = in + 2 * p - k;
+  return span < 0 ? 0 : span / s + 1;
+}
+
+int check_conv(const ConvArgs& g, int a_bits, int w_bits, int w_enc, const char* fn) {
+  if (int s = check_bits(a_bits, w_bits, w_enc, fn)) return s;
+  if (g.n <= 0 || g.h <= 0 || g.w <= 0 || g.c <= 0 || g.oc <= 0 || g.kh <= 0 || g.kw <= 0)
+    return fail(BS_ERR_SHAPE, "%s: non-positive extent", fn);
+  if (g.sh < 1 || g.sw < 1) return fail(BS_ERR_INVALID_ARG, "%s: stride < 1", fn);
+  if (g.ph < 0 || g.pw < 0) return fail(BS_ERR_INVALID_ARG, "%s: pad < 0", fn);
+  if (conv_out(g.h, g.kh, g.sh, g.ph) <= 0 || conv_out(g.w, g.kw, g.sw, g.pw) <= 0)
+    return fail(BS_ERR_SHAPE, "%s: empty output (kernel larger than padded input)", fn);
+  if (int64_t(g.n) * g.h * g.w > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: too many pixels", fn);
+  return check_bound(int64_t(g.kh) * g.kw * g.c, a_bits, w_bits, fn);
+}
+
+bs::ConvProblem make_conv(const uint32_t* act, int a_bits, const uint32_t* wt, int w_bits, int w_enc, int32_t* out,
+                          const ConvArgs& g) {
+  bs::ConvProblem p{};
+  p.act = act; p.wt = wt; p.out = out;
+  p.n = g.n; p.h = g.h; p.w = g.w; p.kw_a = int(row_words(g.c));
+  p.oc = g.oc; p.kh = g.kh; p.kwid = g.kw;
+  p.sh = g.sh; p.sw = g.sw; p.ph = g.ph; p.pw = g.pw;
+  p.oh = conv_out(g.h, g.kh, g.sh, g.ph); p.ow = conv_out(g.w, g.kw, g.sw, g.pw);
+  p.a_bits = a_bits; p.w_bits = w_bits; p.bipolar = w_enc == BS_BIPOLAR;
+  p.act_plane = int64_t(g.n) * g.h * g.w * p.kw_a;
+  p.M = int64_t(g.n) * p.oh * p.ow;
+  p.kp = int64_t(g.kh) * g.kw * p.kw_a;
+  return p;
+}
+
+int launch_conv(const bs::ConvProblem& p, int algo, cudaStream_t s, const char* fn) {
+  if (algo == BS_ALGO_GEMV) return fail(BS_ERR_UNSUPPORTED, "%s: GEMV algo applies to dense only", fn);
+  const bs::Algo a = algo == BS_ALGO_POPC_LIT ? bs::Algo::PopcLit : bs::Algo::Popc;
+  return cuda_status(bs::launch_popc_conv(p, a, s), fn);
+}
+
+int dense_core(const uint32_t* a_packed, const uint8_t* a_codes, int a_bits, const uint32_t* w_packed, int w_bits,
+               int w_enc, int32_t* out, int64_t m, int64_t n, int64_t k, int algo, cudaStream_t s, const char* fn) {
+  const int64_t kwp = row_words(k);
+  const bool gemv_ok = bs::gemv_supported(m, k, a_bits, w_bits);
+  if (algo == BS_ALGO_GEMV && !gemv_ok) return fail(BS_ERR_UNSUPPORTED, "%s: GEMV needs m <= 8 and A in {1,2,4}, W in {1,2}", fn);
+  if (algo == BS_ALGO_GEMV || (algo == BS_ALGO_AUTO && gemv_ok))
+    return cuda_status(bs::launch_gemv(a_packed, a_codes, a_bits, w_packed, w_bits, w_enc == BS_BIPOLAR, out, m, n, k,
+                                       kwp, s), fn);
+  if (a_codes) return fail(BS_ERR_UNSUPPORTED, "%s: internal: codes path needs GEMV", fn);
+  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};  // dense = 1x1 conv over m "pixels"
+  bs::ConvProblem p = make_conv(a_packed, a_bits, w_packed, w_bits, w_enc, out, g);
+  return launch_conv(p, algo, s, fn);
+}
+
+int check_dense(const void* a, const uint32_t* w, const int32_t* out, int a_bits, int w_bits, int w_enc, int64_t m,
+                int64_t n, int64_t k, const char* fn) {
+  if (!a || !w || !out) return fail(BS_ERR_NULL, "%s: NULL tensor pointer", fn);
+  if (int st = check_bits(a_bits, w_bits, w_enc, fn)) return st;
+  if (m <= 0 || n <= 0 || k <= 0) return fail(BS_ERR_SHAPE, "%s: m, n, k must be >= 1", fn);
+  if (!aligned16(a) || !aligned16(w) || !aligned16(out)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return check_bound(k, a_bits, w_bits, fn);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bs_abi_version(void) { return BS_ABI_VERSION; }
+
+const char* bs_status_string(int status) {
+  switch (status) {
+    case BS_OK: return "BS_OK";
+    case BS_ERR_NULL: return "BS_ERR_NULL";
+    case BS_ERR_INVALID_ARG: return "BS_ERR_INVALID_ARG";
+    case BS_ERR_UNSUPPORTED: return "BS_ERR_UNSUPPORTED";
+    case BS_ERR_SHAPE: return "BS_ERR_SHAPE";
+    case BS_ERR_ALIGN: return "BS_ERR_ALIGN";
+    case BS_ERR_OVERFLOW: return "BS_ERR_OVERFLOW";
+    case BS_ERR_CUDA: return "BS_ERR_CUDA";
+    case BS_ERR_WORKSPACE: return "BS_ERR_WORKSPACE";
+    default: return "BS_ERR_UNKNOWN";
+  }
+}
+
+const char* bs_last_error(void) { return g_last_error; }
+
+int64_t bs_packed_row_words(int64_t k) { return row_words(k); }
+
+int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, void* stream) {
+  const char* fn = "bs_bitpack";
+  if (!in || !out) return fail(BS_ERR_NULL, "%s: NULL tensor pointer", fn);
+  if (bits < 1 || bits > 8) return fail(BS_ERR_INVALID_ARG, "%s: bits=%d not in [1,8]", fn, bits);
+  if (rows <= 0 || k <= 0) return fail(BS_ERR_SHAPE, "%s: rows and k must be >= 1", fn);
+  if (!aligned16(in) || !aligned16(out)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return cuda_status(bs::launch_bitpack(in, out, rows, k, row_words(k), bits, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_dense_ex(const uint32_t* a_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,
+                          int32_t* out, int64_t m, int64_t n, int64_t k, int algo, void* stream) {
+  const char* fn = "bs_bitserial_dense";
+  if (int st = check_dense(a_packed, w_packed, out, a_bits, w_bits, w_enc, m, n, k, fn)) return st;
+  if (int st = check_algo(algo, fn)) return st;
+  return dense_core(a_packed, nullptr, a_bits, w_packed, w_bits, w_enc, out, m, n, k, algo,
+                    static_cast<cudaStream_t>(stream), fn);
+}
+
+int bs_bitserial_dense(const uint32_t* a_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,
+                       int32_t* out, int64_t m, int64_t n, int64_t k, void* stream) {
+  return bs_bitserial_dense_ex(a_packed, a_bits, w_packed, w_bits, w_enc, out, m, n, k, BS_ALGO_AUTO, stream);
+}
+
+int64_t bs_dense_workspace_bytes(int64_t m, int64_t k, int a_bits) {
+  if (m <= 0 || k <= 0 || a_bits < 1 || a_bits > 8) return 0;
+  return int64_t(a_bits) * m * row_words(k) * 4;
+}
+
+int bs_bitserial_dense_i8(const uint8_t* a, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc, int32_t* out,
+                          int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes, void* stream) {
+  const char* fn = "bs_bitserial_dense_i8";
+  if (int st = check_dense(a, w_packed, out, a_bits, w_bits, w_enc, m, n, k, fn)) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (bs::gemv_supported(m, k, a_bits, w_bits))  // one fused launch: pack in-kernel + GEMV
+    return dense_core(nullptr, a, a_bits, w_packed, w_bits, w_enc, out, m, n, k, BS_ALGO_GEMV, s, fn);
+  const int64_t need = bs_dense_workspace_bytes(m, k, a_bits);
+  if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
+  if (!aligned16(workspace)) return fail(BS_ERR_ALIGN, "%s: workspace must be 16-byte aligned", fn);
+  uint32_t* ap = static_cast<uint32_t*>(workspace);
+  if (int st = cuda_status(bs::launch_bitpack(a, ap, m, k, row_words(k), a_bits, s), fn)) return st;
+  return dense_core(ap, nullptr, a_bits, w_packed, w_bits, w_enc, out, m, n, k, BS_ALGO_AUTO, s, fn);
+}
+
+int bs_bitserial_conv2d_nhwc_ex(const uint32_t* act_packed, int a_bits, const uint32_t* w_packed, int w_bits,
+                                int w_enc, int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                int stride_h, int stride_w, int pad_h, int pad_w, int algo, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, w_enc, fn)) return st;
+  if (!act_packed || !w_packed || !out) return fail(BS_ERR_NULL, "%s: NULL tensor pointer", fn);
+  if (int st = check_algo(algo, fn)) return st;
+  if (!aligned16(act_packed) || !aligned16(w_packed) || !aligned16(out))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  bs::ConvProblem p = make_conv(act_packed, a_bits, w_packed, w_bits, w_enc, out, g);
+  return launch_conv(p, algo, static_cast<cudaStream_t>(stream), fn);
+}
+
+int bs_bitserial_conv2d_nhwc(const uint32_t* act_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,
+                             int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw, int stride_h,
+                             int stride_w, int pad_h, int pad_w, void* stream) {
+  return bs_bitserial_conv2d_nhwc_ex(act_packed, a_bits, w_packed, w_bits, w_enc, out, n, h, w, c, oc, kh, kw,
+                                     stride_h, stride_w, pad_h, pad_w, BS_ALGO_AUTO, stream);
+}
+
+int64_t bs_conv2d_workspace_bytes(int n, int h, int w, int c, int a_bits) {
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || a_bits < 1 || a_bits > 8) return 0;
+  return int64_t(a_bits) * n * h * w * row_words(c) * 4;
+}
+
+int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,
+                                int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw, int stride_h,
+                                int stride_w, int pad_h, int pad_w, void* workspace, int64_t workspace_bytes,
+                                void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_i8";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, w_enc, fn)) return st;
+  if (!act || !w_packed || !out) return fail(BS_ERR_NULL, "%s: NULL tensor pointer", fn);
+  const int64_t need = bs_conv2d_workspace_bytes(n, h, w, c, a_bits);
+  if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
+  if (!aligned16(act) || !aligned16(w_packed) || !aligned16(out) || !aligned16(workspace))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* ap = static_cast<uint32_t*>(workspace);
+  if (int st = cuda_status(bs::launch_bitpack(act, ap, int64_t(n) * h * w, c, row_words(c), a_bits, s), fn)) return st;
+  bs::ConvProblem p = make_conv(ap, a_bits, w_packed, w_bits, w_enc, out, g);
+  return launch_conv(p, BS_ALGO_AUTO, s, fn);
+}
+
+int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits, const uint32_t* w_packed, int w_bits,
+                                  int w_enc, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+                                  int stride_h, int stride_w, int pad_h, int pad_w, uint8_t* act_dev,
+                                  int32_t* out_dev, void* workspace, int64_t workspace_bytes, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_host";
+  if (!act_host || !out_host || !act_dev || !out_dev) return fail(BS_ERR_NULL, "%s: NULL buffer pointer", fn);
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, w_enc, fn)) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t in_bytes = size_t(n) * h * w * c;
+  const size_t out_bytes = size_t(n) * conv_out(h, kh, stride_h, pad_h) * conv_out(w, kw, stride_w, pad_w) * oc * 4;
+  if (int st = cuda_status(cudaMemcpyAsync(act_dev, act_host, in_bytes, cudaMemcpyHostToDevice, s), fn)) return st;
+  if (int st = bs_bitserial_conv2d_nhwc_i8(act_dev, a_bits, w_packed, w_bits, w_enc, out_dev, n, h, w, c, oc, kh, kw,
+                                           stride_h, stride_w, pad_h, pad_w, workspace, workspace_bytes, stream))
+    return st;
+  if (int st = cuda_status(cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, s), fn)) return st;
+  return cuda_status(cudaStreamSynchronize(s), fn);
+}
+
+}  // extern "C"

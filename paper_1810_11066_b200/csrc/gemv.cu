@@ -1,0 +1,205 @@
+// gemv.cu — bitserial matrix-vector kernel (m <= 8 rows of activations), BASELINE
+// config 2 (K = N = 4096, A2W1 bipolar, batch 1).
+//
+// The B200 analogue of the paper's tensorized ARM micro-kernel (PAPER.md:694-705,
+// Sec. 5.2): "4 bitserial dot products ... accumulation and write back steps in a
+// tree reduction fashion allowing for vectorized loads and stores on all tensors".
+//  * The (tiny) activation operand is staged once per CTA in shared memory —
+//    either copied pre-packed, or packed in-kernel from uint8 codes (FUSED: the
+//    whole batch-1 dense op is one launch, the timed activation packing of
+//    PAPER.md:715 included).
+//  * Each warp owns R = 8 weight rows; every lane streams 16-byte (or 8-byte)
+//    chunks of all R rows, so R independent LDG.128 per lane are in flight.
+//  * The R x m per-lane partial sums are reduced with a transposed butterfly
+//    (log2(32) levels, halving the values exchanged at each level: 4+2+1+1+1
+//    shuffles for R = 8 instead of 8 x 5), after which lane 4r holds row r — the
+//    "tree reduction" of PAPER.md:698/705 — and the 8 results go out as one segment.
+//  * HBM-bound at large N*K (weights are read once: W*N*K/8 bytes), latency-bound
+//    at config 2's 2 MiB.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bs {
+
+namespace {
+
+constexpr int kGemvThreads = 128;  // 4 warps per CTA
+constexpr int kR = 8;              // weight rows per warp
+constexpr int kMaxM = 8;
+constexpr size_t kMaxSmem = 96 * 1024;
+
+template <int A, int W, int VEC, bool FUSED>
+__global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __restrict__ a_packed,
+                                                             const uint8_t* __restrict__ a_codes,
+                                                             const uint32_t* __restrict__ w_packed,
+                                                             int32_t* __restrict__ out, int m, int64_t n,
+                                                             int64_t k, int kwp, int bipolar) {
+  extern __shared__ __align__(16) uint32_t s_act[];  // [A][m][kwp], then rowsum[m]
+  int* s_rowsum = reinterpret_cast<int*>(s_act + A * m * kwp);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- stage the activation operand (packed) in shared memory
+  if (FUSED) {
+    const bool al16 = (reinterpret_cast<uintptr_t>(a_codes) % 16 == 0) && (k % 16 == 0);
+    for (int t = tid; t < m * kwp; t += kGemvThreads) {
+      const int r = t / kwp, j = t - r * kwp;
+      const int64_t e0 = 32 * int64_t(j);
+      const uint8_t* src = a_codes + r * k + e0;
+      uint32_t v[8];
+      if (al16 && e0 + 32 <= k) {
+        const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src)), hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+        v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w; v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t x = 0;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+            if (e0 + 4 * q + rr < k) x |= uint32_t(__ldg(src + 4 * q + rr)) << (8 * rr);
+          v[q] = x;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < A; ++b) s_act[(b * m + r) * kwp + j] = plane_word(v, b);
+    }
+  } else {
+    for (int t = tid; t < A * m * kwp; t += kGemvThreads) s_act[t] = __ldg(a_packed + t);
+  }
+  __syncthreads();
+  if (bipolar) {  // rowsum[r] = sum_k a[r][k] = sum_b 2^b popc(plane b)
+    for (int r = warp; r < m; r += kGemvThreads / 32) {
+      int s = 0;
+      for (int j = lane; j < kwp; j += 32)
+#pragma unroll
+        for (int b = 0; b < A; ++b) s += __popc(s_act[(b * m + r) * kwp + j]) << b;
+      s = __reduce_add_sync(0xffffffffu, s);
+      if (lane == 0) s_rowsum[r] = s;
+    }
+    __syncthreads();
+  }
+
+  const int64_t n0 = (int64_t(blockIdx.x) * (kGemvThreads / 32) + warp) * kR;
+  if (n0 >= n) return;
+  const int64_t w_plane = n * kwp;
+  const int nchunks = kwp / VEC;
+  for (int mi = 0; mi < m; ++mi) {
+    int part[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) part[r] = 0;
+    for (int c = lane; c < nchunks; c += 32) {
+      uint32_t wv[W][kR][VEC];
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const int64_t row = n0 + r < n ? n0 + r : n - 1;
+          const uint32_t* src = w_packed + q * w_plane + row * kwp + c * VEC;
+          if constexpr (VEC == 4) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
+            wv[q][r][0] = x.x; wv[q][r][1] = x.y; wv[q][r][2] = x.z; wv[q][r][3] = x.w;
+          } else {
+            const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
+            wv[q][r][0] = x.x; wv[q][r][1] = x.y;
+          }
+        }
+#pragma unroll
+      for (int b = 0; b < A; ++b) {
+        uint32_t av[VEC];
+        const uint32_t* ap = s_act + (b * m + mi) * kwp + c * VEC;
+        if constexpr (VEC == 4) {
+          const uint4 x = *reinterpret_cast<const uint4*>(ap);
+          av[0] = x.x; av[1] = x.y; av[2] = x.z; av[3] = x.w;
+        } else {
+          const uint2 x = *reinterpret_cast<const uint2*>(ap);
+          av[0] = x.x; av[1] = x.y;
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+#pragma unroll
+          for (int r = 0; r < kR; ++r) {
+            int d = 0;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) d += __popc(av[v] & wv[q][r][v]);
+            part[r] += d << (b + q);
+          }
+      }
+    }
+    // transposed butterfly: 8 values/lane -> lane (4*r') holds row r'
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool up = lane & 16;
+      const int send = up ? part[i] : part[i + 4];
+      const int keep = up ? part[i + 4] : part[i];
+      part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool up = lane & 8;
+      const int send = up ? part[i] : part[i + 2];
+      const int keep = up ? part[i + 2] : part[i];
+      part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const bool up = lane & 4;
+      const int send = up ? part[0] : part[1];
+      const int keep = up ? part[1] : part[0];
+      part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+    if ((lane & 3) == 0) {
+      const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      if (n0 + r < n) {
+        const int u = part[0];
+        out[int64_t(mi) * n + n0 + r] = bipolar ? 2 * u - ((1 << W) - 1) * s_rowsum[mi] : u;
+      }
+    }
+  }
+}
+
+template <int A, int W>
+cudaError_t launch_aw(const uint32_t* a_packed, const uint8_t* a_codes, const uint32_t* w_packed, int bipolar,
+                      int32_t* out, int64_t m, int64_t n, int64_t k, int64_t kwp, cudaStream_t stream) {
+  const size_t smem = size_t(A) * m * kwp * 4 + kMaxM * 4;
+  const int64_t warps = (n + kR - 1) / kR;
+  const unsigned grid = unsigned((warps + kGemvThreads / 32 - 1) / (kGemvThreads / 32));
+  const bool vec4 = (kwp % 4 == 0) && (reinterpret_cast<uintptr_t>(w_packed) % 16 == 0);
+#define BS_GEMV(VEC, FUSED)                                                                            \
+  {                                                                                                    \
+    auto kern = gemv_kernel<A, W, VEC, FUSED>;                                                         \
+    static int configured = 0;                                                                         \
+    if (int(smem) > configured) {                                                                      \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+      if (e != cudaSuccess) return e;                                                                  \
+      configured = int(smem);                                                                          \
+    }                                                                                                  \
+    kern<<<grid, kGemvThreads, smem, stream>>>(a_packed, a_codes, w_packed, out, int(m), n, k, int(kwp), bipolar); \
+  }
+  if (a_codes) {
+    if (vec4) BS_GEMV(4, true) else BS_GEMV(2, true)
+  } else {
+    if (vec4) BS_GEMV(4, false) else BS_GEMV(2, false)
+  }
+#undef BS_GEMV
+  return cudaPeekAtLastError();
+}
+
+}  // namespace
+
+bool gemv_supported(int64_t m, int64_t k, int a_bits, int w_bits) {
+  const bool bits_ok = (a_bits == 1 || a_bits == 2 || a_bits == 4) && (w_bits == 1 || w_bits == 2);
+  const int64_t kwp = ((k + 31) / 32 + 1) / 2 * 2;
+  return bits_ok && m >= 1 && m <= kMaxM && size_t(a_bits) * m * kwp * 4 + kMaxM * 4 <= kMaxSmem;
+}
+
+cudaError_t launch_gemv(const uint32_t* a_packed, const uint8_t* a_codes, int a_bits, const uint32_t* w_packed,
+                        int w_bits, int bipolar, int32_t* out, int64_t m, int64_t n, int64_t k, int64_t kwp,
+                        cudaStream_t stream) {
+#define BS_CASE(A, W) \
+  if (a_bits == A && w_bits == W) return launch_aw<A, W>(a_packed, a_codes, w_packed, bipolar, out, m, n, k, kwp, stream);
+  BS_CASE(1, 1) BS_CASE(2, 1) BS_CASE(2, 2) BS_CASE(1, 2) BS_CASE(4, 1) BS_CASE(4, 2)
+#undef BS_CASE
+  return cudaErrorNotSupported;
+}
+
+}  // namespace bs

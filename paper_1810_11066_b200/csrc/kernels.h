@@ -1,0 +1,47 @@
+// kernels.h — internal (C++) launch interface between abi.cu and the kernels.
+// Not part of the C ABI; see include/bitserial.h for the public boundary.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bs {
+
+// Implicit-GEMM problem.  A dense product is the 1x1 convolution of M "pixels"
+// (n = 1, h = M, w = 1, c = K), so one description serves both operators.
+//   act : packed activations, plane stride act_plane = rows_a * kw_a words,
+//         row (pixel) r at act + r * kw_a;            rows_a = n*h*w
+//   wt  : packed weights [w_bits][oc][kp], kp = taps * kw_a words per filter
+//   out : int32 [M][oc], M = n*oh*ow
+struct ConvProblem {
+  const uint32_t* act;
+  const uint32_t* wt;
+  int32_t* out;
+  int n, h, w, kw_a;        // input geometry, words per pixel per plane (Cw_pad)
+  int oc, kh, kwid;         // filters, kernel height/width
+  int sh, sw, ph, pw;       // stride, padding
+  int oh, ow;               // output extent
+  int a_bits, w_bits;
+  int bipolar;              // weight encoding
+  int64_t act_plane;        // rows_a * kw_a
+  int64_t M;                // n*oh*ow
+  int64_t kp;               // taps * kw_a
+};
+
+enum class Algo : int { Auto = 0, Popc = 1, PopcLit = 2, Gemv = 3 };
+
+cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int64_t kwp, int bits,
+                           cudaStream_t stream);
+
+// Tiled AND+POPC implicit-GEMM kernel (conv and dense); returns cudaErrorNotSupported
+// when no instantiation covers (a_bits, w_bits, algo).
+cudaError_t launch_popc_conv(const ConvProblem& p, Algo algo, cudaStream_t stream);
+
+// Matrix-vector kernel for m <= 8 dense products.
+//   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)
+//   a_codes  : uint8 [m][k] raw codes to pack in-kernel (fused; nullptr otherwise)
+cudaError_t launch_gemv(const uint32_t* a_packed, const uint8_t* a_codes, int a_bits,
+                        const uint32_t* w_packed, int w_bits, int bipolar,
+                        int32_t* out, int64_t m, int64_t n, int64_t k, int64_t kwp, cudaStream_t stream);
+bool gemv_supported(int64_t m, int64_t k, int a_bits, int w_bits);
+
+}  // namespace bs

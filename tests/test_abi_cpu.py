@@ -1,0 +1,110 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol that
+include/bitserial.h declares, and rejects bad arguments before touching CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1810_11066_b200 as bs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bitserial.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(bs.library_path()):
+        from paper_1810_11066_b200 import build
+        build.build()
+    return bs._load()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ("bs_bitpack", "bs_bitserial_dense", "bs_bitserial_conv2d_nhwc"):
+        assert required in names
+    assert set(names) == set(bs.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_exports_are_c_symbols():
+    out = os.popen(f"nm -D --defined-only {bs.library_path()}").read()
+    exported = set(re.findall(r"\bT (bs_[a-z0-9_]+)\b", out))
+    assert set(declared_functions()) <= exported
+
+
+def test_abi_version_and_row_words(lib):
+    import oracle
+    assert bs.abi_version() == 1
+    for k in (1, 31, 32, 33, 64, 65, 100, 576, 4096, 4097):
+        assert bs.packed_row_words(k) == oracle.packed_row_words(k)
+    assert bs.packed_row_words(0) == 0
+
+
+def test_status_strings(lib):
+    assert lib.bs_status_string(0) == b"BS_OK"
+    assert lib.bs_status_string(4) == b"BS_ERR_SHAPE"
+    assert lib.bs_status_string(99) == b"BS_ERR_UNKNOWN"
+
+
+NULL = ctypes.c_void_p(0)
+FAKE = ctypes.c_void_p(0x10000)       # never dereferenced: validation fails first
+MISALIGNED = ctypes.c_void_p(0x10004)
+
+
+def test_validation_before_launch(lib):
+    # null pointers
+    assert lib.bs_bitpack(NULL, FAKE, 4, 32, 2, NULL) == 1
+    assert lib.bs_bitserial_dense(FAKE, 2, NULL, 1, 1, FAKE, 1, 1, 1, NULL) == 1
+    # bits out of range / bad encoding / bad algo
+    assert lib.bs_bitpack(FAKE, FAKE, 4, 32, 9, NULL) == 2
+    assert lib.bs_bitserial_dense(FAKE, 0, FAKE, 1, 1, FAKE, 1, 1, 1, NULL) == 2
+    assert lib.bs_bitserial_dense(FAKE, 2, FAKE, 1, 7, FAKE, 1, 1, 1, NULL) == 2
+    assert lib.bs_bitserial_dense_ex(FAKE, 2, FAKE, 1, 1, FAKE, 1, 1, 1, 42, NULL) == 2
+    # shapes
+    assert lib.bs_bitpack(FAKE, FAKE, 0, 32, 2, NULL) == 4
+    assert lib.bs_bitserial_dense(FAKE, 2, FAKE, 1, 1, FAKE, 1, 0, 1, NULL) == 4
+    # empty conv output: 3x3 kernel on 2x2 input, no pad
+    assert lib.bs_bitserial_conv2d_nhwc(FAKE, 2, FAKE, 1, 1, FAKE, 1, 2, 2, 8, 4, 3, 3, 1, 1, 0, 0, NULL) == 4
+    # stride / pad
+    assert lib.bs_bitserial_conv2d_nhwc(FAKE, 2, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 4, 3, 3, 0, 1, 1, 1, NULL) == 2
+    assert lib.bs_bitserial_conv2d_nhwc(FAKE, 2, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 4, 3, 3, 1, 1, -1, 1, NULL) == 2
+    # alignment
+    assert lib.bs_bitpack(MISALIGNED, FAKE, 4, 32, 2, NULL) == 5
+    # accumulator bound: K (2^8-1)^2 >= 2^31
+    assert lib.bs_bitserial_dense(FAKE, 8, FAKE, 8, 0, FAKE, 1, 1, 40000, NULL) == 6
+    # workspace too small
+    assert lib.bs_bitserial_conv2d_nhwc_i8(FAKE, 2, FAKE, 1, 1, FAKE, 1, 8, 8, 64, 4, 3, 3, 1, 1, 1, 1,
+                                           FAKE, 16, NULL) == 8
+    assert b"workspace" in lib.bs_last_error()
+
+
+def test_gemv_algo_rejected_for_conv(lib):
+    assert lib.bs_bitserial_conv2d_nhwc_ex(FAKE, 2, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 4, 3, 3, 1, 1, 1, 1, 3, NULL) == 3
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    with pytest.raises(bs.BitserialError):
+        bs.bitpack(torch.zeros(4, 32, dtype=torch.uint8), 2)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1810_11066_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "liboracle" not in text and "oracle.c" not in text, f

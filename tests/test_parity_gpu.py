@@ -1,0 +1,236 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle,
+element by element, bit-exact (int32, zero tolerance: the method computes an exact
+integer result, DESIGN.md §3 R14).  Inputs come from paper_1810_11066_b200.inputs
+(seeded, uniform codes); expected values only ever come from oracle/."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1810_11066_b200 as bs
+from paper_1810_11066_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def enc(bipolar):
+    return bs.BIPOLAR if bipolar else bs.UNIPOLAR
+
+
+def gpu_pack(x_cpu, bits):
+    return bs.bitpack(x_cpu.to(DEV), bits)
+
+
+# ----------------------------------------------------------------------- bitpack
+@pytest.mark.parametrize("rows,k,bits", [(1, 1, 1), (3, 31, 2), (5, 32, 1), (7, 33, 3), (4, 100, 4),
+                                         (9, 64, 2), (2, 130, 8), (3136, 64, 2), (513, 4096, 2),
+                                         (1000, 48, 5), (37, 3, 2), (11, 576, 7)])
+def test_bitpack_parity(rows, k, bits):
+    g = inputs.gen(rows * 7919 + k * 31 + bits)
+    x = inputs.codes((rows, k), bits, g)
+    got = gpu_pack(x, bits).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got, oracle.bitpack(x.numpy(), bits))
+
+
+def test_bitpack_unaligned_source():
+    g = inputs.gen(5)
+    big = inputs.codes((4 * 64 + 16,), 2, g).to(DEV)
+    x = big[16:].view(4, 64)            # 16-byte aligned but offset view
+    got = bs.bitpack(x.contiguous(), 2).cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got, oracle.bitpack(x.cpu().numpy(), 2))
+
+
+# ------------------------------------------------------------------------- dense
+DENSE_SHAPES = [(1, 1, 1), (1, 7, 33), (3, 5, 100), (8, 64, 64), (129, 65, 250),
+                (300, 200, 576), (64, 256, 4096), (257, 130, 1000), (1, 4096, 4096), (5, 1000, 129)]
+PRECISIONS = [(1, 1), (2, 1), (2, 2), (4, 1), (4, 2), (1, 2), (3, 3), (4, 4), (5, 1), (8, 1), (2, 6)]
+
+
+@pytest.mark.parametrize("m,n,k", DENSE_SHAPES)
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2)])
+@pytest.mark.parametrize("bipolar", [False, True])
+def test_dense_parity_auto(m, n, k, a_bits, w_bits, bipolar):
+    a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=m * 1000 + n + k + a_bits)
+    ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+    got = bs.bitserial_dense(gpu_pack(a, a_bits), a_bits, gpu_pack(w, w_bits), w_bits, enc(bipolar), m, n, k)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("algo", [bs.ALGO_POPC, bs.ALGO_POPC_LIT])
+@pytest.mark.parametrize("a_bits,w_bits", PRECISIONS)
+@pytest.mark.parametrize("bipolar", [False, True])
+def test_dense_parity_tiled_all_precisions(algo, a_bits, w_bits, bipolar):
+    m, n, k = 150, 77, 300
+    a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=10 * a_bits + w_bits)
+    ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+    got = bs.bitserial_dense(gpu_pack(a, a_bits), a_bits, gpu_pack(w, w_bits), w_bits, enc(bipolar), m, n, k,
+                             algo=algo)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("m", [1, 2, 5, 8])
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (4, 1), (4, 2), (1, 2)])
+@pytest.mark.parametrize("k", [64, 100, 4096])
+def test_gemv_parity(m, a_bits, w_bits, k):
+    n = 300
+    for bipolar in (False, True):
+        a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=m + k + a_bits * 10 + w_bits)
+        ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+        got = bs.bitserial_dense(gpu_pack(a, a_bits), a_bits, gpu_pack(w, w_bits), w_bits, enc(bipolar), m, n, k,
+                                 algo=bs.ALGO_GEMV)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+        got = bs.bitserial_dense_i8(a.to(DEV), a_bits, gpu_pack(w, w_bits), w_bits, enc(bipolar), n)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+def test_dense_i8_tiled_path():
+    m, n, k = 100, 64, 200
+    a, w = inputs.dense_operands(m, n, k, 2, 1, seed=3)
+    ref = oracle.dense(a.numpy(), 2, w.numpy(), 1, True)
+    got = bs.bitserial_dense_i8(a.to(DEV), 2, gpu_pack(w, 1), 1, bs.BIPOLAR, n)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+# -------------------------------------------------------------------------- conv
+CONV_CASES = [
+    # n, h, w, c, oc, kh, kw, sh, sw, ph, pw
+    (1, 9, 7, 5, 3, 3, 3, 1, 1, 1, 1),
+    (2, 8, 11, 33, 20, 3, 3, 2, 2, 1, 1),
+    (3, 6, 5, 64, 70, 1, 1, 2, 2, 0, 0),
+    (1, 7, 7, 3, 5, 3, 2, 1, 2, 0, 1),
+    (2, 5, 9, 17, 6, 2, 3, 3, 1, 2, 0),
+    (1, 13, 13, 128, 129, 3, 3, 1, 1, 1, 1),
+    (2, 7, 7, 512, 64, 3, 3, 1, 1, 1, 1),
+    (1, 15, 15, 256, 130, 3, 3, 2, 2, 1, 1),
+    (4, 1, 1, 64, 8, 1, 1, 1, 1, 0, 0),
+    (1, 3, 3, 64, 4, 5, 5, 1, 1, 2, 2),   # kernel larger than image with pad
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (4, 2), (3, 1)])
+@pytest.mark.parametrize("bipolar", [False, True])
+def test_conv_parity(case, a_bits, w_bits, bipolar):
+    n, h, w, c, oc, kh, kw, sh, sw, ph, pw = case
+    g = inputs.gen(sum(case) * 100 + a_bits * 10 + w_bits)
+    act = inputs.codes((n, h, w, c), a_bits, g)
+    wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+    ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(sh, sw), pad=(ph, pw))
+    wp = gpu_pack(wt.view(oc * kh * kw, c), w_bits)
+    for algo in (bs.ALGO_POPC, bs.ALGO_POPC_LIT):
+        got = bs.bitserial_conv2d_nhwc(gpu_pack(act.view(-1, c), a_bits), a_bits, wp, w_bits, enc(bipolar),
+                                       n, h, w, c, oc, kh, kw, (sh, sw), (ph, pw), algo=algo)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    got = bs.bitserial_conv2d_nhwc_i8(act.to(DEV), a_bits, wp, w_bits, enc(bipolar), oc, kh, kw, (sh, sw), (ph, pw))
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+def _layer_run(L, batch, a_bits, w_bits, bipolar, seed):
+    act, wt = inputs.conv_operands(L, batch, a_bits, w_bits, seed)
+    wp = gpu_pack(wt.view(L.oc * L.k * L.k, L.ic), w_bits)
+    got = bs.bitserial_conv2d_nhwc_i8(act.to(DEV), a_bits, wp, w_bits, enc(bipolar), L.oc, L.k, L.k, L.s, L.pad)
+    return act, wt, got
+
+
+def test_config1_conv_l2_batch1_full():
+    """BASELINE configs[0]: 56x56x64 -> 64, 3x3 s1 p1, A2W1 bipolar, batch 1 — full compare."""
+    L = inputs.TABLE1[2]
+    act, wt, got = _layer_run(L, 1, 2, 1, True, inputs.seed_for(1, 2, 1, "bipolar", 2))
+    ref = oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(1, 1), pad=(1, 1))
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+def test_config2_gemv_full():
+    """BASELINE configs[1]: K = N = 4096, A2W1 bipolar, batch 1 — full compare, fused path."""
+    a, w = inputs.dense_operands(1, 4096, 4096, 2, 1, inputs.seed_for(2, 2, 1, "bipolar"))
+    ref = oracle.dense(a.numpy(), 2, w.numpy(), 1, True)
+    got = bs.bitserial_dense_i8(a.to(DEV), 2, gpu_pack(w, 1), 1, bs.BIPOLAR, 4096)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("layer", inputs.BASELINE_LAYERS + (3,))
+def test_config3_resnet_layers_batch1_full(layer):
+    """BASELINE configs[2]: every layer x {A1W1, A2W1, A2W2} x {uni, bip}, batch 1, full compare."""
+    L = inputs.TABLE1[layer]
+    for (a_bits, w_bits) in [(1, 1), (2, 1), (2, 2)]:
+        for bipolar in (False, True):
+            e = "bipolar" if bipolar else "unipolar"
+            act, wt, got = _layer_run(L, 1, a_bits, w_bits, bipolar, inputs.seed_for(3, a_bits, w_bits, e, layer))
+            ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar,
+                                     stride=(L.s, L.s), pad=(L.pad, L.pad))
+            np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"L{layer} A{a_bits}W{w_bits} {e}")
+
+
+@pytest.mark.parametrize("layer", inputs.BASELINE_LAYERS)
+def test_config4_batch256_sampled_images(layer):
+    """BASELINE configs[3]: batch 256, A2W1 bipolar, in the bench's launch configuration
+    (whole batch in one call); the oracle checks images 0, 131 and 255 in full."""
+    L = inputs.TABLE1[layer]
+    act, wt, got = _layer_run(L, 256, 2, 1, True, inputs.seed_for(4, 2, 1, "bipolar", layer))
+    got = got.cpu().numpy()
+    for img in (0, 131, 255):
+        ref = oracle.conv2d_nhwc(act[img:img + 1].numpy(), 2, wt.numpy(), 1, True,
+                                 stride=(L.s, L.s), pad=(L.pad, L.pad))
+        np.testing.assert_array_equal(got[img:img + 1], ref, err_msg=f"L{layer} image {img}")
+
+
+@pytest.mark.parametrize("size", [4096, 8192, 16384])
+@pytest.mark.parametrize("a_bits,w_bits,bipolar", [(1, 1, False), (2, 1, True), (4, 2, True)])
+def test_config5_gemm_sampled_rows(size, a_bits, w_bits, bipolar):
+    """BASELINE configs[4]: M = N = K GEMM; full GPU product, oracle on sampled rows."""
+    e = "bipolar" if bipolar else "unipolar"
+    a, w = inputs.dense_operands(size, size, size, a_bits, w_bits, inputs.seed_for(5, a_bits, w_bits, e))
+    wp = gpu_pack(w, w_bits)
+    got = bs.bitserial_dense_i8(a.to(DEV), a_bits, wp, w_bits, enc(bipolar), size)
+    rows = [0, 1, size // 2 + 3, size - 1]
+    ref = oracle.dense(a[rows].numpy(), a_bits, w.numpy(), w_bits, bipolar)
+    np.testing.assert_array_equal(got[rows].cpu().numpy(), ref)
+
+
+# ---------------------------------------------------------------- invariants / edges
+def test_bipolar_identity_and_literal_agree_on_gpu():
+    m, n, k = 200, 96, 1000
+    a, w = inputs.dense_operands(m, n, k, 2, 2, seed=77)
+    ap, wp = gpu_pack(a, 2), gpu_pack(w, 2)
+    uni = bs.bitserial_dense(ap, 2, wp, 2, bs.UNIPOLAR, m, n, k).long()
+    bip = bs.bitserial_dense(ap, 2, wp, 2, bs.BIPOLAR, m, n, k, algo=bs.ALGO_POPC).long()
+    lit = bs.bitserial_dense(ap, 2, wp, 2, bs.BIPOLAR, m, n, k, algo=bs.ALGO_POPC_LIT).long()
+    s = a.long().sum(1, keepdim=True).to(DEV)
+    assert torch.equal(bip, lit)
+    assert torch.equal(bip, 2 * uni - 3 * s)
+
+
+def test_extreme_values_max_bits():
+    """All-max codes at the accumulator bound region: A8W1 with K = 8000 (255*8000 < 2^31)."""
+    m, n, k = 3, 40, 8000
+    a = torch.full((m, k), 255, dtype=torch.uint8)
+    w = torch.ones((n, k), dtype=torch.uint8)
+    ref = oracle.dense(a.numpy(), 8, w.numpy(), 1, False)
+    got = bs.bitserial_dense(gpu_pack(a, 8), 8, gpu_pack(w, 1), 1, bs.UNIPOLAR, m, n, k, algo=bs.ALGO_POPC)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    assert int(ref[0, 0]) == 255 * 8000
+
+
+def test_errors_surface_as_exceptions():
+    x = torch.zeros(4, 32, dtype=torch.uint8, device=DEV)
+    with pytest.raises(bs.BitserialError, match="BS_ERR_INVALID_ARG"):
+        bs.bitpack(x, 9)
+    p = bs.bitpack(x, 2)
+    with pytest.raises(bs.BitserialError, match="BS_ERR_SHAPE"):
+        bs.bitserial_conv2d_nhwc(p, 2, p, 2, bs.UNIPOLAR, 1, 2, 2, 32, 4, 3, 3, 1, 0)
+
+
+def test_host_e2e_entry():
+    L = inputs.TABLE1[9]
+    act, wt = inputs.conv_operands(L, 2, 2, 1, seed=9)
+    wp = gpu_pack(wt.view(L.oc * 9, L.ic), 1)
+    oh = bs.conv_out_extent(L.h, 3, 1, 1)
+    out_host = torch.empty((2, oh, oh, L.oc), dtype=torch.int32).pin_memory()
+    act_host = act.pin_memory()
+    act_dev = torch.empty_like(act, device=DEV)
+    out_dev = torch.empty_like(out_host, device=DEV)
+    ws = torch.empty(bs.conv2d_workspace_bytes(2, L.h, L.w, L.ic, 2), dtype=torch.uint8, device=DEV)
+    bs.bitserial_conv2d_nhwc_host(act_host, 2, wp, 1, bs.BIPOLAR, L.oc, 3, 3, 1, 1, out_host, act_dev, out_dev, ws)
+    ref = oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(1, 1), pad=(1, 1))
+    np.testing.assert_array_equal(out_host.numpy(), ref)
