@@ -87,6 +87,11 @@ int bs_abi_version(void);
 const char* bs_status_string(int status);
 const char* bs_last_error(void);
 
+/* Number of kernels this library has launched in this process (host-side count,
+ * incremented per launch call; graph replays of captured launches are not counted).
+ * Used by bench.py to report how many of the library's kernels a step runs. */
+int64_t bs_kernel_launches(void);
+
 /* Words per packed row for reduction length k: ceil(k/32) rounded up to an even
  * number (8-byte rows).  Returns 0 for k <= 0. */
 int64_t bs_packed_row_words(int64_t k);

@@ -19,7 +19,7 @@ import torch
 
 __all__ = [
     "UNIPOLAR", "BIPOLAR", "ALGO_AUTO", "ALGO_POPC", "ALGO_POPC_LIT", "ALGO_GEMV",
-    "BitserialError", "library_path", "abi_version", "packed_row_words", "bitpack",
+    "BitserialError", "library_path", "abi_version", "kernel_launches", "packed_row_words", "bitpack",
     "bitserial_dense", "bitserial_dense_i8", "bitserial_conv2d_nhwc", "bitserial_conv2d_nhwc_i8",
     "bitserial_conv2d_nhwc_host", "conv2d_workspace_bytes", "dense_workspace_bytes", "conv_out_extent",
     "EXPORTED_SYMBOLS",
@@ -33,7 +33,7 @@ _LIB_PATH = os.path.join(_HERE, "libbitserial.so")
 _lib = None
 
 EXPORTED_SYMBOLS = (
-    "bs_abi_version", "bs_status_string", "bs_last_error", "bs_packed_row_words", "bs_bitpack",
+    "bs_abi_version", "bs_status_string", "bs_last_error", "bs_kernel_launches", "bs_packed_row_words", "bs_bitpack",
     "bs_bitserial_dense", "bs_bitserial_dense_ex", "bs_dense_workspace_bytes", "bs_bitserial_dense_i8",
     "bs_bitserial_conv2d_nhwc", "bs_bitserial_conv2d_nhwc_ex", "bs_conv2d_workspace_bytes",
     "bs_bitserial_conv2d_nhwc_i8", "bs_bitserial_conv2d_nhwc_host",
@@ -61,6 +61,7 @@ def _load():
         "bs_abi_version": ([], I),
         "bs_status_string": ([I], ctypes.c_char_p),
         "bs_last_error": ([], ctypes.c_char_p),
+        "bs_kernel_launches": ([], L),
         "bs_packed_row_words": ([L], L),
         "bs_bitpack": ([P, P, L, L, I, P], I),
         "bs_bitserial_dense": ([P, I, P, I, I, P, L, L, L, P], I),
@@ -104,6 +105,11 @@ def _dev(t: torch.Tensor, name: str, dtype):
 
 def abi_version() -> int:
     return int(_load().bs_abi_version())
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libbitserial.so so far in this process (bs_kernel_launches)."""
+    return int(_load().bs_kernel_launches())
 
 
 def packed_row_words(k: int) -> int:

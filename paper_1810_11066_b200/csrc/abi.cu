@@ -1,11 +1,18 @@
 // abi.cu — the C ABI declared in include/bitserial.h: argument validation (all of it
 // before any launch), kernel selection, launch on the caller's stream.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 
 #include "../../include/bitserial.h"
 #include "kernels.h"
+
+namespace bs {
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+}  // namespace bs
 
 namespace {
 
@@ -141,6 +148,8 @@ const char* bs_status_string(int status) {
 const char* bs_last_error(void) { return g_last_error; }
 
 int64_t bs_packed_row_words(int64_t k) { return row_words(k); }
+
+int64_t bs_kernel_launches(void) { return bs::launch_count(); }
 
 int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, void* stream) {
   const char* fn = "bs_bitpack";

@@ -75,6 +75,7 @@ cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64
     case 4: bitpack_kernel<4><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
     default: bitpack_kernel<0><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
   }
+  note_launch();
   return cudaPeekAtLastError();
 }
 

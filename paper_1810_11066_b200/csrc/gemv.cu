@@ -181,6 +181,7 @@ cudaError_t launch_aw(const uint32_t* a_packed, const uint8_t* a_codes, const ui
     if (vec4) BS_GEMV(4, false) else BS_GEMV(2, false)
   }
 #undef BS_GEMV
+  note_launch();
   return cudaPeekAtLastError();
 }
 

@@ -27,6 +27,10 @@ struct ConvProblem {
   int64_t kp;               // taps * kw_a
 };
 
+// Count of kernels this library has launched (host-side, incremented per launch).
+void note_launch();
+int64_t launch_count();
+
 enum class Algo : int { Auto = 0, Popc = 1, PopcLit = 2, Gemv = 3 };
 
 cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int64_t kwp, int bits,

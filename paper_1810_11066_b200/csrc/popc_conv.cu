@@ -249,6 +249,7 @@ cudaError_t launch_cfg(const ConvProblem& p, int BK, cudaStream_t stream) {
   }
   dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.oc + BN - 1) / BN));
   kern<<<grid, kThreads, smem, stream>>>(p, BK);
+  note_launch();
   return cudaPeekAtLastError();
 }
 
