@@ -363,11 +363,15 @@ def run_ours(args):
     value = total_binops / (ms / 1e3) / 1e12
 
     # roofline of the dominant kernel (the conv kernel): algorithmic binary ops / its
-    # own device time, against R_popc = 64 binary ops per POPC x 16 POPC/clk/SM x SMs x f_max
+    # own device time, against the integer-pipe bound R_int: per 32-bit
+    # word pair one LOP3 (AND) on the ALU (64/clk/SM) plus counting, either one POPC on
+    # the XU (16/clk/SM) or a carry-save full adder (2 LOP3); balancing the two pipes
+    # gives 32 word pairs/clk/SM = 2 x R_popc (R_popc: one POPC per word pair).
     pack_ms, conv_ms = kernel_durations(runs, max(3, min(args.steps, 10)), world, dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = (clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or MAX_MHZ_FALLBACK)
     r_popc = 64.0 * POPC_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
+    r_int = 2.0 * r_popc
     conv_total_ms = sum(conv_ms)
     rank_binops = sum(r.binops() for r in runs)
     achieved = rank_binops / (conv_total_ms / 1e3) / 1e12
@@ -403,11 +407,13 @@ def run_ours(args):
                 "step": "per layer: bitpack(act) + bitserial conv2d (weights prepacked, untimed)",
                 "l2": "256 MiB buffer zeroed between timed steps (outside the events)", "cuda_graph": graphed,
             },
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": r_popc, "unit": "binary TOPS",
-                         "frac": achieved / r_popc, "traffic": traffic,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": r_int, "unit": "binary TOPS",
+                         "frac": achieved / r_int, "traffic": traffic, "r_popc": r_popc,
+                         "frac_r_popc": achieved / r_popc,
                          "kernel": "popc_conv_kernel (sum over the 10 layer launches of one step, rank 0)",
-                         "peak_basis": f"64 binary ops/POPC x {POPC_PER_CLK_PER_SM:.0f} POPC/clk/SM (measured) x "
-                                       f"{sms} SMs x {f_max:.0f} MHz"},
+                         "peak_basis": f"integer pipes (measured rates, profiles/r01_int_pipe_rates.json): per "
+                                       f"32-bit word pair 1 LOP3 + {{1 POPC | 2 LOP3}} balanced -> 32 word pairs/"
+                                       f"clk/SM x 64 binary ops x {sms} SMs x {f_max:.0f} MHz (= 2 x R_popc)"},
             "breakdown": {"conv_ms": conv_ms, "pack_ms": pack_ms, "pack_gbs": pack_gbs,
                           "pack_frac_hbm": pack_gbs / peaks["hbm_gbs"], "hbm_peak_gbs": peaks["hbm_gbs"],
                           "peaks_source": peaks_src},

@@ -29,7 +29,9 @@ UNIPOLAR, BIPOLAR = 0, 1
 ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV = 0, 1, 2, 3
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libbitserial.so")
+# BITSERIAL_LIB selects an alternative build of the same library (A/B timing of
+# compile-time variants in tools/); default is the in-tree product library.
+_LIB_PATH = os.environ.get("BITSERIAL_LIB") or os.path.join(_HERE, "libbitserial.so")
 _lib = None
 
 EXPORTED_SYMBOLS = (

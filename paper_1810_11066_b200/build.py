@@ -40,10 +40,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, force, verbose):
-    obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
+def _compile(src, force, verbose, objdir=BUILD, defines=()):
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
     if force or _stale(obj, [src] + _headers()):
-        cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        cmd = [NVCC] + ARCH + FLAGS + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else []) + \
+            ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -52,17 +53,20 @@ def _compile(src, force, verbose):
     return obj
 
 
-def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, jobs: int = 0, verbose: bool = False, defines=(), out: str = LIB,
+          objdir: str = BUILD) -> str:
+    """Compile and link.  `defines`/`out`/`objdir` build experimental variants (e.g.
+    -DBS_FORCE_G=2) into a separate library for A/B timing; the product is `LIB`."""
+    os.makedirs(objdir, exist_ok=True)
     srcs = _sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, verbose), srcs))
-    if force or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda s: _compile(s, force, verbose, objdir, defines), srcs))
+    if force or _stale(out, objs):
+        tmp = out + f".tmp{os.getpid()}"
         subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcuda"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
@@ -70,5 +74,8 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=0)
     ap.add_argument("-v", action="store_true", help="print ptxas register/smem usage")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for a variant build")
+    ap.add_argument("--out", default=LIB)
+    ap.add_argument("--objdir", default=BUILD)
     a = ap.parse_args()
-    print(build(a.force, a.j, a.v))
+    print(build(a.force, a.j, a.v, a.defines, a.out, a.objdir))

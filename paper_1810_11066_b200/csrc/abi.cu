@@ -76,6 +76,7 @@ int check_conv(const ConvArgs& g, int a_bits, int w_bits, int w_enc, const char*
   if (conv_out(g.h, g.kh, g.sh, g.ph) <= 0 || conv_out(g.w, g.kw, g.sw, g.pw) <= 0)
     return fail(BS_ERR_SHAPE, "%s: empty output (kernel larger than padded input)", fn);
   if (int64_t(g.n) * g.h * g.w > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: too many pixels", fn);
+  if (int64_t(g.kh) * g.kw * row_words(g.c) > (int64_t(1) << 30)) return fail(BS_ERR_SHAPE, "%s: reduction too long", fn);
   return check_bound(int64_t(g.kh) * g.kw * g.c, a_bits, w_bits, fn);
 }
 
@@ -91,6 +92,7 @@ bs::ConvProblem make_conv(const uint32_t* act, int a_bits, const uint32_t* wt, i
   p.act_plane = int64_t(g.n) * g.h * g.w * p.kw_a;
   p.M = int64_t(g.n) * p.oh * p.ow;
   p.kp = int64_t(g.kh) * g.kw * p.kw_a;
+  p.one = 1;
   return p;
 }
 

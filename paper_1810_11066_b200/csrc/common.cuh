@@ -51,4 +51,15 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   return v;
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// Plain (compiler-scheduled) shared-memory vector loads through generic pointers
+// into the dynamic smem array.
+__device__ __forceinline__ uint4 lds128p(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ uint2 lds64p(const uint32_t* p) { return *reinterpret_cast<const uint2*>(p); }
+
 }  // namespace bs

@@ -25,6 +25,7 @@ struct ConvProblem {
   int64_t act_plane;        // rows_a * kw_a
   int64_t M;                // n*oh*ow
   int64_t kp;               // taps * kw_a
+  int one;                  // always 1: opaque to the compiler (keeps plane weights in registers)
 };
 
 // Count of kernels this library has launched (host-side, incremented per launch).
