@@ -1,18 +1,23 @@
 #!/usr/bin/env python
 """bench.py — device-timed throughput of the bitserial hot path on B200.
 
-Default workload (BASELINE.json configs[3], the multi-GPU ResNet-18 config the
-north_star reports at 1/2/4/8 GPUs): the ten ResNet-18 body conv layers (PAPER.md
-Table 1 without layer 3) at global batch 256, A2W1 bipolar, NHWC, sharded by batch
-across ranks with no collective on the data path.  One step = for every layer, pack
-the uint8 activations (timed) + bitserial conv (int32 out); weights are
+Default workload (BASELINE.json configs[3], the ResNet-18 config the north_star
+reports at 1/2/4/8 GPUs): the ten ResNet-18 body conv layers (Table 1
+without layer 3) at global batch 256, A2W1 bipolar, NHWC, sharded by batch across
+ranks with no collective on the data path.  One step = for every layer, pack the
+uint8 activations (timed) + bitserial conv (int32 out); weights are
 packed once, untimed.  Metric: binary TOPS = sum_layers 2*M*N*K*A*W / step time.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload resnet256|conv1|gemv|resnet1|gemm] ...
+                    [--workload resnet256|conv1|gemv|resnet1|gemm] [--size S]
+                    [--a-bits A] [--w-bits W] [--unipolar]
 
-Prints ONE JSON line on rank 0 (the contract in DESIGN.md §6).  `--impl reference`
-times the CPU oracle (the reference arm of this tier) on the host cores instead.
+Other workloads (the remaining BASELINE configs, for measurement; the driver uses
+the default): conv1 = configs[0], gemv = configs[1], resnet1 = configs[2] (one
+precision per run), gemm = configs[4] (row-sharded, NCCL all-gather of the int32 C).
+
+Prints ONE JSON line on rank 0 (contract in DESIGN.md §6).  `--impl reference` times
+the CPU oracle (this tier's reference arm) on the host cores instead.
 """
 from __future__ import annotations
 
@@ -29,65 +34,33 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1810_11066_b200 import dist as bsdist  # noqa: E402
 from paper_1810_11066_b200 import inputs  # noqa: E402
 
+METRIC = "bitserial conv/GEMM binary TOPS (device-timed) and % of int-pipe/HBM roofline"
 MAX_MHZ_FALLBACK = 1965.0
 POPC_PER_CLK_PER_SM = 16.0   # measured, profiles/r01_int_pipe_rates.json
 L2_FLUSH_BYTES = 256 << 20
 
 
-# ---------------------------------------------------------------------------- setup
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
-def init_dist(world, local, backend):
-    if world > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if backend == "nccl":
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-
-
-def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-
-
-def allreduce_max(x: float, world: int, device) -> float:
-    if world == 1:
-        return x
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": MAX_MHZ_FALLBACK}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": MAX_MHZ_FALLBACK}, \
+            "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons during the timed region."""
+    """NVML sampling of SM clock + clock-event (throttle) reasons during the timed region."""
 
     REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+        0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x10: "sync_boost",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
     }
 
-    def __init__(self, index, period=0.01):
+    def __init__(self, index, period=0.005):
         self.samples, self.reasons, self.ok = [], set(), False
         self.period, self._stop = period, threading.Event()
         try:
@@ -97,7 +70,7 @@ class ClockSampler:
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
             self.ok = True
-        except Exception:  # noqa: BLE001 — clocks are reported as unavailable
+        except Exception:  # noqa: BLE001 — reported as unavailable
             self.max_mhz = None
 
     def _run(self):
@@ -106,7 +79,7 @@ class ClockSampler:
                 self.samples.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
+                    if r & bit:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
@@ -130,7 +103,16 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------------ workloads
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def binops_conv(L, n, a_bits, w_bits):
+    oh = (L.h + 2 * L.pad - L.k) // L.s + 1
+    return 2 * n * oh * oh * L.oc * L.k * L.k * L.ic * a_bits * w_bits
+
+
+# ----------------------------------------------------------------------- conv layers
 class ConvLayerRun:
     """One conv layer on this rank's batch shard: resident inputs/outputs in HBM."""
 
@@ -139,6 +121,7 @@ class ConvLayerRun:
         self.bs, self.L = bs, L
         self.a_bits, self.w_bits, self.enc = a_bits, w_bits, (bs.BIPOLAR if bipolar else bs.UNIPOLAR)
         self.n = act_cpu.shape[0]
+        self.act_cpu = act_cpu
         self.act = act_cpu.to(dev)
         self.wp = bs.bitpack(wt_cpu.reshape(L.oc * L.k * L.k, L.ic).to(dev), w_bits)  # untimed
         self.oh = bs.conv_out_extent(L.h, L.k, L.s, L.pad)
@@ -146,12 +129,10 @@ class ConvLayerRun:
         self.ws = torch.empty(bs.conv2d_workspace_bytes(self.n, L.h, L.w, L.ic, a_bits), dtype=torch.uint8, device=dev)
         self.packed = self.ws.view(torch.int32).view(a_bits, self.n * L.h * L.w, bs.packed_row_words(L.ic))
 
-    def binops(self, n=None):
-        n = self.n if n is None else n
-        L = self.L
-        return 2 * n * self.oh * self.oh * L.oc * L.k * L.k * L.ic * self.a_bits * self.w_bits
+    def binops(self):
+        return binops_conv(self.L, self.n, self.a_bits, self.w_bits)
 
-    def step(self):  # pack + conv (timed unit)
+    def step(self):  # pack + conv (the timed unit)
         L = self.L
         self.bs.bitserial_conv2d_nhwc_i8(self.act, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k,
                                          L.s, L.pad, out=self.out, workspace=self.ws)
@@ -164,24 +145,273 @@ class ConvLayerRun:
         self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h, L.w,
                                       L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
 
+    def host_buffers(self):
+        return (self.act_cpu.contiguous().pin_memory(), torch.empty(self.out.shape, dtype=torch.int32).pin_memory(),
+                torch.empty_like(self.act), torch.empty_like(self.out))
 
-def build_resnet(args, rank, world, dev, batch):
-    lo, hi = inputs.shard_range(batch, rank, world)
-    enc = "bipolar" if args.bipolar else "unipolar"
-    runs = []
-    for li in inputs.BASELINE_LAYERS:
-        L = inputs.TABLE1[li]
-        act, wt = inputs.conv_operands(L, batch, args.a_bits, args.w_bits,
-                                       inputs.seed_for(4 if batch > 1 else 3, args.a_bits, args.w_bits, enc, li))
-        runs.append(ConvLayerRun(L, act[lo:hi].contiguous(), wt, args.a_bits, args.w_bits, args.bipolar, dev))
-    return runs, (lo, hi)
+    def host_step(self, bufs):
+        L = self.L
+        ah, oh_, ad, od = bufs
+        self.bs.bitserial_conv2d_nhwc_host(ah, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k, L.s,
+                                           L.pad, oh_, ad, od, self.ws)
 
 
-# --------------------------------------------------------------------------- timing
-def time_steps(step_fn, steps, warmup, world, dev, flush=None, use_graph=True):
+class ConvWorkload:
+    """configs[0] (conv1), configs[2] (resnet1), configs[3] (resnet256)."""
+
+    def __init__(self, args, rank, world, dev, layers, batch, config_id, name):
+        self.args, self.dev, self.batch = args, dev, batch
+        # batch-1 configs do not shard: N independent replicas ("replicas only", DESIGN.md §7)
+        self.replicas = world if batch < world else 1
+        lo, hi = (0, batch) if self.replicas > 1 else bsdist.shard_range(batch, rank, world)
+        self.images = (lo, hi)
+        enc = "bipolar" if args.bipolar else "unipolar"
+        self.runs, self.layers = [], layers
+        for li in layers:
+            L = inputs.TABLE1[li]
+            act, wt = inputs.conv_operands(L, batch, args.a_bits, args.w_bits,
+                                           inputs.seed_for(config_id, args.a_bits, args.w_bits, enc, li))
+            self.runs.append(ConvLayerRun(L, act[lo:hi].contiguous(), wt, args.a_bits, args.w_bits, args.bipolar,
+                                          dev))
+        self.total_binops = self.replicas * sum(binops_conv(inputs.TABLE1[li], batch, args.a_bits, args.w_bits)
+                                                for li in layers)
+        self.config_id = config_id
+        self.name = name
+        self.graph_ok = True
+        self.config = {
+            "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
+            "layout": "NHWC/OHWI",
+            "parallelism": (f"{world} independent replicas (batch 1 does not shard)" if self.replicas > 1 else
+                            f"batch-sharded dp{world} (no collective)"),
+            "rank0_images": [lo, hi],
+            "step": "per layer: bitpack(act) + bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights prepacked, "
+                    "untimed)",
+        }
+
+    def step(self):
+        for r in self.runs:
+            r.step()
+
+    def roofline(self, reps):
+        """Per-launch device time of the pack and conv kernels (events around each
+        launch on the launching stream); the conv kernel is the dominant one."""
+        stream = torch.cuda.current_stream()
+        for r in self.runs:
+            r.pack_only()
+            r.conv_only()
+        torch.cuda.synchronize()
+        pack_ms, conv_ms = [0.0] * len(self.runs), [0.0] * len(self.runs)
+        for _ in range(reps):
+            for i, r in enumerate(self.runs):
+                a0, a1, b1 = ev(), ev(), ev()
+                a0.record(stream)
+                r.pack_only()
+                a1.record(stream)
+                r.conv_only()
+                b1.record(stream)
+                torch.cuda.synchronize()
+                pack_ms[i] += a0.elapsed_time(a1) / reps
+                conv_ms[i] += a1.elapsed_time(b1) / reps
+        ops = sum(r.binops() for r in self.runs)
+        pack_bytes = sum(r.act.numel() * (1 + r.a_bits / 8) for r in self.runs)
+        return {"kind": "alu", "kernel": f"popc_conv_kernel (sum over the {len(self.runs)} layer launches of one "
+                                         f"step, rank 0)",
+                "ops": ops, "ms": sum(conv_ms),
+                "breakdown": {"layers": list(self.layers), "conv_ms": conv_ms, "pack_ms": pack_ms,
+                              "pack_gbs": pack_bytes / (sum(pack_ms) / 1e3) / 1e9}}
+
+    def e2e(self, steps):
+        bufs = [r.host_buffers() for r in self.runs]
+
+        def step():
+            for r, b in zip(self.runs, bufs):
+                r.host_step(b)
+        step()
+        bsdist.barrier()
+        torch.cuda.synchronize()
+        stream = torch.cuda.current_stream()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bsdist.barrier()
+        ms = e0.elapsed_time(e1) / steps
+        return ms, sum(b[0].numel() for b in bufs), sum(b[1].numel() * 4 for b in bufs)
+
+    def oracle_sample(self, images):
+        """The oracle on `images` images of every layer (same seeds as the GPU arm)."""
+        import oracle
+        a = self.args
+        enc = "bipolar" if a.bipolar else "unipolar"
+        ops, t = 0, 0.0
+        for li in self.layers:
+            L = inputs.TABLE1[li]
+            g = inputs.gen(inputs.seed_for(self.config_id, a.a_bits, a.w_bits, enc, li))
+            act = inputs.codes((images, L.h, L.w, L.ic), a.a_bits, g).numpy()
+            wt = inputs.codes((L.oc, L.k, L.k, L.ic), a.w_bits, g).numpy()
+            t0 = time.perf_counter()
+            oracle.conv2d_nhwc(act, a.a_bits, wt, a.w_bits, a.bipolar, stride=(L.s, L.s), pad=(L.pad, L.pad))
+            t += time.perf_counter() - t0
+            ops += binops_conv(L, images, a.a_bits, a.w_bits)
+        return ops, t, f"{images} image(s) of layers {list(self.layers)}"
+
+    def oracle_units(self, budget_s):
+        ops1, t1, _ = self.oracle_sample(1)
+        return max(1, min(16, self.batch, int(budget_s / max(t1, 1e-3))))
+
+
+# ----------------------------------------------------------------------------- dense
+class DenseWorkload:
+    """configs[1] (gemv: M=1, N=K=4096) and configs[4] (gemm: M=N=K=size,
+    row-sharded, NCCL all-gather of the int32 result)."""
+
+    def __init__(self, args, rank, world, dev, m, n, k, config_id, name, gather):
+        import paper_1810_11066_b200 as bs
+        self.bs, self.args, self.dev = bs, args, dev
+        self.m, self.n, self.k, self.gather, self.world = m, n, k, gather, world
+        self.a_bits, self.w_bits = args.a_bits, args.w_bits
+        self.enc = bs.BIPOLAR if args.bipolar else bs.UNIPOLAR
+        enc = "bipolar" if args.bipolar else "unipolar"
+        a, w = inputs.dense_operands(m, n, k, args.a_bits, args.w_bits,
+                                     inputs.seed_for(config_id, args.a_bits, args.w_bits, enc))
+        if gather and m % world:
+            raise SystemExit(f"gemm rows {m} not divisible by {world} ranks")
+        lo, hi = bsdist.shard_range(m, rank, world) if gather else (0, m)
+        self.rows = (lo, hi)
+        self.a_cpu = a[lo:hi].contiguous()
+        self.a = self.a_cpu.to(dev)
+        self.wp = bs.bitpack(w.to(dev), args.w_bits)  # untimed
+        del w
+        self.out = torch.empty((hi - lo, n), dtype=torch.int32, device=dev)
+        self.full = torch.empty((m, n), dtype=torch.int32, device=dev) if gather else None
+        self.ws = torch.empty(max(16, bs.dense_workspace_bytes(hi - lo, k, args.a_bits)), dtype=torch.uint8, device=dev)
+        kwp = bs.packed_row_words(k)
+        self.packed = self.ws[:args.a_bits * (hi - lo) * kwp * 4].view(torch.int32).view(args.a_bits, hi - lo, kwp)
+        self.replicas = 1 if gather else world
+        self.total_binops = 2 * m * n * k * args.a_bits * args.w_bits * self.replicas
+        self.config_id, self.name = config_id, name
+        self.graph_ok = not (gather and world > 1)
+        self.config = {
+            "workload": f"{name}_m{m}_n{n}_k{k}_a{args.a_bits}w{args.w_bits}_{enc}", "m": m, "n": n, "k": k,
+            "parallelism": (f"row-sharded tp{world} + all_gather_into_tensor(int32 C) over NCCL" if gather else
+                            "single GPU (replicas only)"),
+            "step": "bs_bitserial_dense_i8 (activation pack + dense" + (", fused single launch" if (hi - lo) <= 8
+                                                                        else "") + ")"
+                    + (" + NCCL all-gather of C" if gather else ""),
+        }
+
+    def step(self):
+        self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
+                                   workspace=self.ws)
+        if self.gather:
+            bsdist.gather_rows(self.full, self.out)
+
+    def roofline(self, reps):
+        stream = torch.cuda.current_stream()
+        rows = self.rows[1] - self.rows[0]
+        gemv = rows <= 8
+
+        def kernel():
+            if gemv:
+                self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
+                                           workspace=self.ws)
+            else:
+                self.bs.bitserial_dense(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, rows, self.n,
+                                        self.k, out=self.out)
+        if not gemv:
+            self.bs.bitpack(self.a, self.a_bits, out=self.packed)
+        kernel()
+        torch.cuda.synchronize()
+        flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=self.dev)
+        ms = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            kernel()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1) / reps
+        comm_ms = None
+        if self.gather and self.world > 1:
+            e0, e1 = ev(), ev()
+            bsdist.barrier()
+            e0.record(stream)
+            for _ in range(reps):
+                bsdist.gather_rows(self.full, self.out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            comm_ms = e0.elapsed_time(e1) / reps
+        ops = 2 * rows * self.n * self.k * self.a_bits * self.w_bits
+        if gemv:
+            nbytes = self.wp.numel() * 4 + self.a.numel() + self.out.numel() * 4
+            return {"kind": "hbm", "kernel": "gemv_kernel (fused pack + GEMV, one launch, cold L2)", "bytes": nbytes,
+                    "ops": ops, "ms": ms, "breakdown": {"gemv_ms": ms}}
+        return {"kind": "alu", "kernel": "popc_conv_kernel (dense = 1x1 implicit GEMM, rank 0 shard)", "ops": ops,
+                "ms": ms, "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
+
+    def e2e(self, steps):
+        a_host = self.a_cpu.pin_memory()
+        c_host = torch.empty((self.m if self.gather else self.out.shape[0], self.n), dtype=torch.int32).pin_memory()
+        stream = torch.cuda.current_stream()
+
+        def step():
+            self.a.copy_(a_host, non_blocking=True)
+            self.step()
+            c_host.copy_(self.full if self.gather else self.out, non_blocking=True)
+        step()
+        torch.cuda.synchronize()
+        bsdist.barrier()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bsdist.barrier()
+        return e0.elapsed_time(e1) / steps, a_host.numel(), c_host.numel() * 4
+
+    def oracle_sample(self, rows):
+        import oracle
+        a = self.args
+        enc = "bipolar" if a.bipolar else "unipolar"
+        am, w = inputs.dense_operands(self.m, self.n, self.k, a.a_bits, a.w_bits,
+                                      inputs.seed_for(self.config_id, a.a_bits, a.w_bits, enc))
+        am = am[:rows].numpy()
+        w = w.numpy()
+        t0 = time.perf_counter()
+        oracle.dense(am, a.a_bits, w, a.w_bits, a.bipolar)
+        t = time.perf_counter() - t0
+        return 2 * rows * self.n * self.k * a.a_bits * a.w_bits, t, f"{rows} row(s) of the {self.m}x{self.n}x{self.k} " \
+                                                                    "product"
+
+    def oracle_units(self, budget_s):
+        ops1, t1, _ = self.oracle_sample(1)
+        return max(1, min(self.m, 256, int(budget_s / max(t1, 1e-4))))
+
+
+def make_workload(args, rank, world, dev):
+    if args.workload == "resnet256":
+        return ConvWorkload(args, rank, world, dev, inputs.BASELINE_LAYERS, 256, 4, "resnet18_layers2-12_b256")
+    if args.workload == "resnet1":
+        return ConvWorkload(args, rank, world, dev, inputs.BASELINE_LAYERS, 1, 3, "resnet18_layers2-12_b1")
+    if args.workload == "conv1":
+        return ConvWorkload(args, rank, world, dev, (2,), 1, 1, "conv_l2_56x56x64_b1")
+    if args.workload == "gemv":
+        return DenseWorkload(args, rank, world, dev, 1, 4096, 4096, 2, "gemv", gather=False)
+    if args.workload == "gemm":
+        s = args.size
+        return DenseWorkload(args, rank, world, dev, s, s, s, 5, "gemm", gather=True)
+    raise SystemExit(f"unknown workload {args.workload}")
+
+
+# ---------------------------------------------------------------------------- timing
+def time_steps(step_fn, steps, warmup, dev, flush, use_graph):
     """W untimed warm-ups, then K steps each bracketed by CUDA events on the launching
-    stream (L2 flushed between steps, outside the events); barrier + synchronize on
-    both sides; returns max-over-ranks mean ms/step."""
+    stream, the L2 flushed between steps outside the events; barrier + synchronize on
+    both sides; returns the max-over-ranks mean ms/step."""
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         step_fn()
@@ -199,229 +429,98 @@ def time_steps(step_fn, steps, warmup, world, dev, flush=None, use_graph=True):
         graph.replay()
         torch.cuda.synchronize()
     run = graph.replay if graph is not None else step_fn
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    barrier(world)
+    evs = [(ev(), ev()) for _ in range(steps)]
+    bsdist.barrier()
     torch.cuda.synchronize()
-    for e0, e1 in ev:
-        if flush is not None:
-            flush.zero_()
+    for e0, e1 in evs:
+        flush.zero_()
         e0.record(stream)
         run()
         e1.record(stream)
     torch.cuda.synchronize()
-    barrier(world)
-    ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / steps
-    return allreduce_max(ms, world, dev), graph is not None
+    bsdist.barrier()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+    return bsdist.max_over_ranks(ms, dev), graph is not None
 
 
-def kernel_durations(runs, reps, world, dev):
-    """Per-launch device time of the pack and conv kernels, eager, events on the
-    launching stream around each launch (the roofline's denominator)."""
-    stream = torch.cuda.current_stream()
-    pack_ms, conv_ms = [0.0] * len(runs), [0.0] * len(runs)
-    for i, r in enumerate(runs):
-        r.pack_only()
-        r.conv_only()
-    torch.cuda.synchronize()
-    for _ in range(reps):
-        for i, r in enumerate(runs):
-            a0, a1, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            a0.record(stream)
-            r.pack_only()
-            a1.record(stream)
-            r.conv_only()
-            b1.record(stream)
-            torch.cuda.synchronize()
-            pack_ms[i] += a0.elapsed_time(a1) / reps
-            conv_ms[i] += a1.elapsed_time(b1) / reps
-    return pack_ms, conv_ms
-
-
-def e2e_resnet(runs, steps, world, dev):
-    """Same metric through the host-buffer C-ABI entry (bs_bitserial_conv2d_nhwc_host):
-    H2D of pinned uint8 activations, pack, conv, D2H of the int32 outputs, per layer."""
-    import paper_1810_11066_b200 as bs
-    host = []
-    for r in runs:
-        host.append((r.act.cpu().pin_memory(), torch.empty(r.out.shape, dtype=torch.int32).pin_memory(),
-                     torch.empty_like(r.act), torch.empty_like(r.out)))
-    stream = torch.cuda.current_stream()
-
-    def step():
-        for r, (ah, oh_, ad, od) in zip(runs, host):
-            L = r.L
-            bs.bitserial_conv2d_nhwc_host(ah, r.a_bits, r.wp, r.w_bits, r.enc, L.oc, L.k, L.k, L.s, L.pad,
-                                          oh_, ad, od, r.ws)
-    step()
-    barrier(world)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier(world)
-    ms = allreduce_max(e0.elapsed_time(e1) / steps, world, dev)
-    h2d = sum(h[0].numel() for h in host)
-    d2h = sum(h[1].numel() * 4 for h in host)
-    return ms, h2d, d2h
-
-
-# ------------------------------------------------------------------------ reference
-def oracle_resnet_sample(args, images):
-    """CPU oracle on `images` images of the ten layers (same seeds as the GPU arm)."""
-    import oracle
-    enc = "bipolar" if args.bipolar else "unipolar"
-    total_ops, t = 0, 0.0
-    for li in inputs.BASELINE_LAYERS:
-        L = inputs.TABLE1[li]
-        g = inputs.gen(inputs.seed_for(4, args.a_bits, args.w_bits, enc, li))
-        act = inputs.codes((images, L.h, L.w, L.ic), args.a_bits, g).numpy()
-        wt = inputs.codes((L.oc, L.k, L.k, L.ic), args.w_bits, g).numpy()
-        t0 = time.perf_counter()
-        oracle.conv2d_nhwc(act, args.a_bits, wt, args.w_bits, args.bipolar, stride=(L.s, L.s), pad=(L.pad, L.pad))
-        t += time.perf_counter() - t0
-        oh = (L.h + 2 * L.pad - L.k) // L.s + 1
-        total_ops += 2 * images * oh * oh * L.oc * L.k * L.k * L.ic * args.a_bits * args.w_bits
-    return total_ops, t
-
-
-def cpu_baseline(args, budget_s=15.0):
-    import oracle
-    ops1, t1 = oracle_resnet_sample(args, 1)
-    imgs = max(1, min(16, int(budget_s / max(t1, 1e-3))))
-    if imgs > 1:
-        ops, t = oracle_resnet_sample(args, imgs)
-    else:
-        ops, t = ops1, t1
-    return {"value": ops / t / 1e12, "unit": "binary TOPS", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{imgs} image(s) of the 10 ResNet-18 layers (batch-256 seeds, images 0..{imgs - 1}), "
-                      f"A{args.a_bits}W{args.w_bits} {'bipolar' if args.bipolar else 'unipolar'}, OpenMP C oracle",
-            "seconds": t}
-
-
-def run_reference(args):
-    world, rank, _ = dist_env()
-    if rank != 0:
-        return 0
-    import oracle
-    oracle.build()
-    for _ in range(max(0, min(args.warmup, 1))):
-        oracle_resnet_sample(args, 1)
-    ts, ops = [], 0
-    for _ in range(args.steps):
-        ops, t = oracle_resnet_sample(args, 1)
-        ts.append(t)
-    ms = 1e3 * sum(ts) / len(ts)
-    value = ops / (ms / 1e3) / 1e12
-    line = {
-        "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u8->i32", "data": "synthetic (seeded uniform codes)", "impl": "reference",
-        "config": {"workload": "resnet18_layers2-12_b256_a2w1_bipolar", "sample_per_step": "1 image of the 10 layers",
-                   "a_bits": args.a_bits, "w_bits": args.w_bits},
-        "cpu_baseline": {"value": value, "unit": "binary TOPS", "cores": oracle.num_threads(), "kind": "oracle",
-                         "sample": "1 image of the 10 ResNet-18 layers per step (the batch-256 workload's images "
-                                   "are independent; the oracle runs a bounded sample)"},
-        "e2e": {"value": value, "unit": "binary TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-METRIC = "bitserial conv/GEMM binary TOPS (device-timed) and % of int-pipe/HBM roofline"
-
-
-# ---------------------------------------------------------------------------- main
 def run_ours(args):
-    world, rank, local = dist_env()
-    if world != args.gpus and world > 1:
-        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
-    init_dist(world, local, "nccl")
+    world, rank, local = bsdist.env()
+    bsdist.init("nccl", local)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     import paper_1810_11066_b200 as bs
     bs._load()
     peaks, peaks_src = measured_peaks()
-    batch = 256
-    runs, (lo, hi) = build_resnet(args, rank, world, dev, batch)
-    step = lambda: [r.step() for r in runs]  # noqa: E731
+    wl = make_workload(args, rank, world, dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
-    # launches per step, counted by the library itself on one eager step
-    n0 = bs.kernel_launches()
-    step()
+    n0 = bs.kernel_launches()  # launches per step, counted by the library on one eager step
+    wl.step()
     torch.cuda.synchronize()
     launches_per_step = bs.kernel_launches() - n0
 
     with ClockSampler(local) as clk:
-        ms, graphed = time_steps(step, args.steps, args.warmup, world, dev, flush=flush, use_graph=not args.no_graph)
+        ms, graphed = time_steps(wl.step, args.steps, args.warmup, dev, flush,
+                                 use_graph=wl.graph_ok and not args.no_graph)
     clocks = clk.summary()
+    value = wl.total_binops / (ms / 1e3) / 1e12
 
-    total_binops = sum(r.binops(batch) for r in runs)  # whole job: global batch
-    value = total_binops / (ms / 1e3) / 1e12
-
-    # roofline of the dominant kernel (the conv kernel): algorithmic binary ops / its
-    # own device time, against the integer-pipe bound R_int (DESIGN.md §5): per 32-bit
-    # word pair one LOP3 (AND) on the ALU (64/clk/SM) plus counting, either one POPC on
-    # the XU (16/clk/SM) or a carry-save full adder (2 LOP3); balancing the two pipes
-    # gives 32 word pairs/clk/SM = 2 x R_popc (R_popc: one POPC per word pair).
-    pack_ms, conv_ms = kernel_durations(runs, max(3, min(args.steps, 10)), world, dev)
+    roof = wl.roofline(max(3, min(args.steps, 10)))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    f_max = (clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or MAX_MHZ_FALLBACK)
+    f_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or MAX_MHZ_FALLBACK
     r_popc = 64.0 * POPC_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     r_int = 2.0 * r_popc
-    conv_total_ms = sum(conv_ms)
-    rank_binops = sum(r.binops() for r in runs)
-    achieved = rank_binops / (conv_total_ms / 1e3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_conv_traffic.json")
+    if roof["kind"] == "alu":
+        achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": r_int, "unit": "binary TOPS",
+                    "frac": achieved / r_int, "traffic": None, "r_popc": r_popc, "frac_r_popc": achieved / r_popc,
+                    "kernel": roof["kernel"],
+                    "peak_basis": f"integer pipes (measured rates, profiles/r01_int_pipe_rates.json): per 32-bit word "
+                                  f"pair 1 LOP3 + {{1 POPC | 2 LOP3}} balanced -> 32 word pairs/clk/SM x 64 binary "
+                                  f"ops x {sms} SMs x {f_max:.0f} MHz (= 2 x R_popc)"}
+    else:
+        achieved = roof["bytes"] / (roof["ms"] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": roof["kernel"],
+                    "peak_basis": f"HBM copy bandwidth, {peaks_src}",
+                    "binary_tops": roof["ops"] / (roof["ms"] / 1e3) / 1e12}
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("dram_bytes_per_step")
-    pack_bytes = sum(r.act.numel() * (1 + r.a_bits / 8) for r in runs)
-    pack_gbs = pack_bytes / (sum(pack_ms) / 1e3) / 1e9
+            roofline["traffic"] = json.load(f).get("dram_bytes_per_launch_unit")
 
     e2e = None
     if not args.no_e2e:
-        ems, h2d, d2h = e2e_resnet(runs, max(1, min(args.steps, 5)), world, dev)
-        e2e = {"value": total_binops / (ems / 1e3) / 1e12, "unit": "binary TOPS",
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "ms_per_step": ems}
+        ems, h2d, d2h = wl.e2e(max(1, min(args.steps, 5)))
+        ems = bsdist.max_over_ranks(ems, dev)
+        e2e = {"value": wl.total_binops / (ems / 1e3) / 1e12, "unit": "binary TOPS",
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * (1 if isinstance(wl, DenseWorkload)
+                                                                               and wl.gather else world),
+               "ms_per_step": ems}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args)
+        import oracle
+        units = wl.oracle_units(10.0)
+        ops, t, sample = wl.oracle_sample(units)
+        cpu = {"value": ops / t / 1e12, "unit": "binary TOPS", "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": sample + " (bounded sample of the same workload, same seeds), OpenMP C oracle",
+               "seconds": t}
 
     if rank == 0:
+        cfg = dict(wl.config)
+        cfg.update({"l2": f"{L2_FLUSH_BYTES >> 20} MiB buffer zeroed between timed steps (outside the events)",
+                    "cuda_graph": graphed})
         line = {
             "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u8->i32 (AND/POPC on packed u32 bit-planes)",
-            "data": "synthetic (seeded uniform codes, PAPER.md Table 1 shapes; no dataset)",
-            "config": {
-                "workload": f"resnet18_layers2-12_b{batch}_a{args.a_bits}w{args.w_bits}_"
-                            f"{'bipolar' if args.bipolar else 'unipolar'}",
-                "global_batch": batch, "layers": list(inputs.BASELINE_LAYERS), "layout": "NHWC/OHWI",
-                "parallelism": f"batch-sharded dp{world} (no collective)", "rank0_images": [lo, hi],
-                "step": "per layer: bitpack(act) + bitserial conv2d (weights prepacked, untimed)",
-                "l2": "256 MiB buffer zeroed between timed steps (outside the events)", "cuda_graph": graphed,
-            },
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": r_int, "unit": "binary TOPS",
-                         "frac": achieved / r_int, "traffic": traffic, "r_popc": r_popc,
-                         "frac_r_popc": achieved / r_popc,
-                         "kernel": "popc_conv_kernel (sum over the 10 layer launches of one step, rank 0)",
-                         "peak_basis": f"integer pipes (measured rates, profiles/r01_int_pipe_rates.json): per "
-                                       f"32-bit word pair 1 LOP3 + {{1 POPC | 2 LOP3}} balanced -> 32 word pairs/"
-                                       f"clk/SM x 64 binary ops x {sms} SMs x {f_max:.0f} MHz (= 2 x R_popc)"},
-            "breakdown": {"conv_ms": conv_ms, "pack_ms": pack_ms, "pack_gbs": pack_gbs,
-                          "pack_frac_hbm": pack_gbs / peaks["hbm_gbs"], "hbm_peak_gbs": peaks["hbm_gbs"],
-                          "peaks_source": peaks_src},
-            "clocks": clocks,
-            "gpu_launches": launches_per_step * args.steps,
-            "launches_per_step": launches_per_step,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "vs_baseline": None, "dtype": "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32",
+            "scaling": "weak" if getattr(wl, "replicas", 1) > 1 else "strong",
+            "data": "synthetic (seeded uniform codes, PAPER.md Table 1 / BASELINE shapes; no dataset)",
+            "config": cfg, "roofline": roofline,
+            "breakdown": dict(roof.get("breakdown", {}), hbm_peak_gbs=peaks["hbm_gbs"], peaks_source=peaks_src),
+            "clocks": clocks, "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
+            "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -430,12 +529,71 @@ def run_ours(args):
     return 0
 
 
+def run_reference(args):
+    """The reference arm of this tier: the CPU oracle, as it stands, on the host
+    cores, each step a bounded sample of the same workload (rank 0 only)."""
+    world, rank, _ = bsdist.env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    wl = make_workload_cpu(args)
+    units = max(1, wl.oracle_units(max(1.0, 60.0 / max(1, args.steps + args.warmup))))
+    for _ in range(args.warmup):
+        wl.oracle_sample(units)
+    ts, ops, sample = [], 0, ""
+    for _ in range(args.steps):
+        ops, t, sample = wl.oracle_sample(units)
+        ts.append(t)
+    ms = 1e3 * sum(ts) / len(ts)
+    value = ops / (ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u8 codes -> i32 (plain integer loops)", "data": "synthetic (seeded uniform codes)",
+        "impl": "reference", "config": dict(wl.config, sample_per_step=sample),
+        "cpu_baseline": {"value": value, "unit": "binary TOPS", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample + " per step (bounded sample of the workload; OpenMP C oracle)"},
+        "e2e": {"value": value, "unit": "binary TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def make_workload_cpu(args):
+    """Workload descriptions for the oracle arm (no device allocations)."""
+    class Conv(ConvWorkload):
+        def __init__(self, layers, batch, cid, name):  # noqa: D401 — light init, oracle only
+            self.args, self.layers, self.batch, self.config_id, self.name = args, layers, batch, cid, name
+            enc = "bipolar" if args.bipolar else "unipolar"
+            self.config = {"workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch,
+                           "layers": list(layers)}
+
+    class Dense(DenseWorkload):
+        def __init__(self, m, n, k, cid, name):  # noqa: D401
+            self.args, self.m, self.n, self.k, self.config_id, self.name = args, m, n, k, cid, name
+            enc = "bipolar" if args.bipolar else "unipolar"
+            self.config = {"workload": f"{name}_m{m}_n{n}_k{k}_a{args.a_bits}w{args.w_bits}_{enc}"}
+
+    if args.workload == "resnet256":
+        return Conv(inputs.BASELINE_LAYERS, 256, 4, "resnet18_layers2-12_b256")
+    if args.workload == "resnet1":
+        return Conv(inputs.BASELINE_LAYERS, 1, 3, "resnet18_layers2-12_b1")
+    if args.workload == "conv1":
+        return Conv((2,), 1, 1, "conv_l2_56x56x64_b1")
+    if args.workload == "gemv":
+        return Dense(1, 4096, 4096, 2, "gemv")
+    return Dense(args.size, args.size, args.size, 5, "gemm")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="resnet256", choices=["resnet256", "resnet1", "conv1", "gemv", "gemm"])
+    ap.add_argument("--size", type=int, default=8192, help="gemm: M = N = K")
     ap.add_argument("--a-bits", type=int, default=2)
     ap.add_argument("--w-bits", type=int, default=1)
     ap.add_argument("--unipolar", dest="bipolar", action="store_false")
@@ -443,11 +601,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
+    if args.impl == "ours" and args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
-        return run_reference(args)
-    return run_ours(args)
+    return run_reference(args) if args.impl == "reference" else run_ours(args)
 
 
 if __name__ == "__main__":

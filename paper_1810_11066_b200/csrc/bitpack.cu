@@ -18,15 +18,26 @@
 
 namespace bs {
 
-template <int BITS>
+template <int B, int BITS>
+__device__ __forceinline__ void store_planes(uint32_t* dst, int64_t plane_stride, const uint32_t (&v)[8]) {
+  if constexpr (B < BITS) {
+    dst[B * plane_stride] = plane_word_c<B>(v);
+    store_planes<B + 1, BITS>(dst, plane_stride, v);
+  }
+}
+
+// POW2: kwp is a power of two (every ResNet channel count and the dense K of the
+// configs) -> the (row, word) split is a shift instead of a 64-bit division.
+template <int BITS, bool POW2>
 __global__ void __launch_bounds__(256) bitpack_kernel(const uint8_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                      int64_t rows, int64_t k, int64_t kwp, int bits_rt,
-                                                      bool aligned16) {
+                                                      int64_t rows, int64_t k, int64_t kwp, int kwp_shift,
+                                                      int bits_rt, bool aligned16) {
   const int bits = BITS > 0 ? BITS : bits_rt;
   const int64_t tasks = rows * kwp;
   const int64_t plane_stride = rows * kwp;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tasks; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = t / kwp, j = t - r * kwp;
+    const int64_t r = POW2 ? (t >> kwp_shift) : t / kwp;
+    const int64_t j = t - r * kwp;
     const int64_t e0 = 32 * j;  // first element of this word
     uint32_t v[8];
     const uint8_t* src = in + r * k + e0;
@@ -52,10 +63,10 @@ __global__ void __launch_bounds__(256) bitpack_kernel(const uint8_t* __restrict_
       }
     }
     uint32_t* dst = out + r * kwp + j;
-#pragma unroll
-    for (int b = 0; b < (BITS > 0 ? BITS : 8); ++b) {
-      if (BITS == 0 && b >= bits) break;
-      dst[b * plane_stride] = plane_word(v, b);
+    if constexpr (BITS > 0) {
+      store_planes<0, BITS>(dst, plane_stride, v);
+    } else {
+      for (int b = 0; b < bits; ++b) dst[b * plane_stride] = plane_word(v, b);
     }
   }
 }
@@ -68,13 +79,22 @@ cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64
   const int64_t max_blocks = int64_t(kNumSMs) * 8 * 4;  // grid-stride beyond 4 waves of 8 CTAs/SM
   if (blocks > max_blocks) blocks = max_blocks;
   const bool aligned16 = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (k % 16 == 0);
+  const bool pow2 = (kwp & (kwp - 1)) == 0;
+  int shift = 0;
+  while ((int64_t(1) << shift) < kwp) ++shift;
+#define BS_PACK(BITS)                                                                                         \
+  if (pow2)                                                                                                   \
+    bitpack_kernel<BITS, true><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16); \
+  else                                                                                                        \
+    bitpack_kernel<BITS, false><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16);
   switch (bits) {
-    case 1: bitpack_kernel<1><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
-    case 2: bitpack_kernel<2><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
-    case 3: bitpack_kernel<3><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
-    case 4: bitpack_kernel<4><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
-    default: bitpack_kernel<0><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, bits, aligned16); break;
+    case 1: BS_PACK(1) break;
+    case 2: BS_PACK(2) break;
+    case 3: BS_PACK(3) break;
+    case 4: BS_PACK(4) break;
+    default: BS_PACK(0) break;
   }
+#undef BS_PACK
   note_launch();
   return cudaPeekAtLastError();
 }

@@ -30,6 +30,22 @@ __device__ __forceinline__ uint32_t plane_word(const uint32_t (&v)[8], int b) {
   return w;
 }
 
+// Same result with compile-time plane B: mask the plane's bits in place (LOP3 with an
+// immediate), gather them with one IMAD (bits land at 21+B..24+B), move the nibble
+// to 4q with one funnel shift and merge with LOP3 — 4 integer ops per 4 codes.
+template <int B>
+__device__ __forceinline__ uint32_t plane_word_c(const uint32_t (&v)[8]) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t prod = (v[q] & (0x01010101u << B)) * 0x00204081u;
+    const int sh = 21 + B - 4 * q;  // compile-time after unrolling
+    const uint32_t nib = sh >= 0 ? (prod >> sh) : (prod << (-sh));
+    w |= nib & (0xFu << (4 * q));
+  }
+  return w;
+}
+
 // ---------------------------------------------------------------------------
 // cp.async (LDGSTS) helpers: 8- and 16-byte copies with zero fill (src_size = 0).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

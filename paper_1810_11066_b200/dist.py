@@ -1,0 +1,75 @@
+"""Multi-GPU plumbing of the hot path: one process per GPU,
+torch.distributed for process groups and collectives.
+
+* Batch-sharded conv (BASELINE configs[3]): independent images, contiguous blocks per
+  rank, weights replicated, no collective on the data path.
+* Row-sharded GEMM (BASELINE configs[4]): A rows split across ranks, W replicated,
+  one exchange step — an all-gather of the int32 result rows (NCCL over NVLink on
+  the GPU box; `gloo` for the CPU tests).
+
+Nothing here computes the method; it only partitions work and moves results.
+"""
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def env():
+    """(world, rank, local_rank) from the torchrun environment (1, 0, 0 without it)."""
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def init(backend: str, local_rank: int = 0):
+    """Initialise the default process group when WORLD_SIZE > 1 (MASTER_ADDR defaults
+    to 127.0.0.1)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world <= 1 or dist.is_initialized():
+        return
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if backend == "nccl":
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        dist.init_process_group(backend)
+
+
+def shard_range(total: int, rank: int, world: int):
+    """Contiguous block [lo, hi) of `total` units owned by `rank`; blocks differ in size
+    by at most one and cover [0, total) exactly once."""
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def barrier():
+    if dist.is_initialized():
+        dist.barrier()
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank scalar (timing: the job is as slow as its slowest rank)."""
+    if not dist.is_initialized():
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_rows(out_full: torch.Tensor, shard: torch.Tensor):
+    """All-gather equal-size row shards into out_full ([world * rows][...]); the one
+    exchange step of the row-sharded GEMM.  NCCL: all_gather_into_tensor (one
+    collective over NVLink/NVSwitch); gloo: all_gather into views of out_full."""
+    if not dist.is_initialized():
+        out_full.copy_(shard)
+        return out_full
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out_full, shard)
+    else:
+        world = dist.get_world_size()
+        parts = list(out_full.chunk(world, dim=0))
+        dist.all_gather(parts, shard)
+    return out_full

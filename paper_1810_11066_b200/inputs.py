@@ -89,10 +89,3 @@ def dense_operands(m: int, n: int, k: int, a_bits: int, w_bits: int, seed: int):
     """(a [m][k], w [n][k]) uint8 codes."""
     g = gen(seed)
     return codes((m, k), a_bits, g), codes((n, k), w_bits, g)
-
-
-def shard_range(total: int, rank: int, world: int):
-    """Contiguous block [lo, hi) of `total` units owned by `rank`."""
-    base, rem = divmod(total, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
