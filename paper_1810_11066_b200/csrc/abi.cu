@@ -93,6 +93,7 @@ bs::ConvProblem make_conv(const uint32_t* act, int a_bits, const uint32_t* wt, i
   p.M = int64_t(g.n) * p.oh * p.ow;
   p.kp = int64_t(g.kh) * g.kw * p.kw_a;
   p.one = 1;
+  p.ksplit = 1;
   return p;
 }
 

@@ -37,6 +37,30 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
   extern __shared__ __align__(16) uint32_t s_act[];  // [A][m][kwp], then rowsum[m]
   int* s_rowsum = reinterpret_cast<int*>(s_act + A * m * kwp);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n0 = (int64_t(blockIdx.x) * (kGemvThreads / 32) + warp) * kR;
+  const int64_t w_plane = n * kwp;
+  const int nchunks = kwp / VEC;
+  auto load_w = [&](int c, uint32_t (&wv)[W][kR][VEC]) {
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int64_t row = n0 + r < n ? n0 + r : n - 1;
+        const uint32_t* src = w_packed + q * w_plane + row * kwp + c * VEC;
+        if constexpr (VEC == 4) {
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
+          wv[q][r][0] = x.x; wv[q][r][1] = x.y; wv[q][r][2] = x.z; wv[q][r][3] = x.w;
+        } else {
+          const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
+          wv[q][r][0] = x.x; wv[q][r][1] = x.y;
+        }
+      }
+  };
+  // Weight loads of the first chunk are issued before the activation is staged, so
+  // the HBM latency of the (dominant) weight stream overlaps the staging.
+  uint32_t wv0[W][kR][VEC];
+  const bool prefetched = n0 < n && lane < nchunks;
+  if (prefetched) load_w(lane, wv0);
 
   // ---- stage the activation operand (packed) in shared memory
   if (FUSED) {
@@ -78,30 +102,23 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
     __syncthreads();
   }
 
-  const int64_t n0 = (int64_t(blockIdx.x) * (kGemvThreads / 32) + warp) * kR;
   if (n0 >= n) return;
-  const int64_t w_plane = n * kwp;
-  const int nchunks = kwp / VEC;
   for (int mi = 0; mi < m; ++mi) {
     int part[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) part[r] = 0;
     for (int c = lane; c < nchunks; c += 32) {
       uint32_t wv[W][kR][VEC];
+      if (mi == 0 && c == lane) {
 #pragma unroll
-      for (int q = 0; q < W; ++q)
+        for (int q = 0; q < W; ++q)
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const int64_t row = n0 + r < n ? n0 + r : n - 1;
-          const uint32_t* src = w_packed + q * w_plane + row * kwp + c * VEC;
-          if constexpr (VEC == 4) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(src));
-            wv[q][r][0] = x.x; wv[q][r][1] = x.y; wv[q][r][2] = x.z; wv[q][r][3] = x.w;
-          } else {
-            const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
-            wv[q][r][0] = x.x; wv[q][r][1] = x.y;
-          }
-        }
+          for (int r = 0; r < kR; ++r)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) wv[q][r][v] = wv0[q][r][v];
+      } else {
+        load_w(c, wv);
+      }
 #pragma unroll
       for (int b = 0; b < A; ++b) {
         uint32_t av[VEC];

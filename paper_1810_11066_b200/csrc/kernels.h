@@ -26,6 +26,7 @@ struct ConvProblem {
   int64_t M;                // n*oh*ow
   int64_t kp;               // taps * kw_a
   int one;                  // always 1: opaque to the compiler (keeps plane weights in registers)
+  int ksplit;               // K slices across blockIdx.z (set by the launcher)
 };
 
 // Count of kernels this library has launched (host-side, incremented per launch).

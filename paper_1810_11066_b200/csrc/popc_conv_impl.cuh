@@ -36,10 +36,16 @@ namespace popc_detail {
 constexpr int kThreads = 256;
 constexpr int kThrN = 16;     // thread grid is kThrM x kThrN = 16 x 16
 constexpr int kThrM = 16;
-constexpr int kBKMax = 12;    // k-words per stage (runtime BK in {2,4,6,8,12})
-constexpr int kStride = 14;   // smem words per staged row: 8-byte rows, 14r mod 32 gives 16
-                              // distinct even banks for 16 rows -> LDS.64 conflict-free
+#ifndef BS_KSTRIDE
+#define BS_KSTRIDE 14
+#endif
+constexpr int kStride = BS_KSTRIDE;  // smem words per staged row (>= BK max, 8-byte rows): 14r mod 32
+                                     // gives 16 distinct even banks for 16 rows -> LDS.64 conflict-free
+constexpr int kBKMax = kStride >= 16 ? 16 : 12;  // k-words per stage (runtime BK <= kBKMax)
 constexpr int kStages = 3;
+#ifndef BS_MINB2
+#define BS_MINB2 2
+#endif
 
 template <int BM, int BN>
 struct SmemLayout {
@@ -51,6 +57,19 @@ struct SmemLayout {
     return size_t(kStages) * stage_words(a_bits, w_bits) * 4;
   }
 };
+
+// Registers a thread holds in the carry-save loop: the W words of its TN columns for
+// one group, the A words of one row, the AND/full-adder slots of one output and the
+// TM x TN accumulators.
+constexpr int csa_regs(int A, int W, int G, int TM, int TN) {
+  return TN * W * 2 * G + A * 2 * G + TM * TN + A * W * 2 * G;
+}
+
+// Plans whose register estimate stays <= 112 fit in 128 registers: pin 2 CTAs (16 warps)
+// per SM so ptxas does not trade that occupancy away; larger plans run one CTA per SM.
+constexpr int min_ctas(int A, int W, int G, int TM, int TN) {
+  return (G == 0 || csa_regs(A, W, G, TM, TN) <= 112) ? BS_MINB2 : 1;
+}
 
 // One group of 2*GG k-words starting at word kw of the stage: for every output of the
 // thread, acc += carry-save dot of its A row and W column over those words.
@@ -88,7 +107,7 @@ __device__ __forceinline__ void csa_group(int32_t (&acc)[TM][TN], const uint32_t
 // "apply [unroll] to small dimensions such as the bit axis");  0: runtime widths.
 // G: carry-save group size in k-word pairs (0 = direct AND+POPC loop).
 template <int A_T, int W_T, int BM, int BN, bool LIT, int G>
-__global__ void __launch_bounds__(kThreads) popc_conv_kernel(const ConvProblem p, const int BK) {
+__global__ void __launch_bounds__(kThreads, min_ctas(A_T > 0 ? A_T : 1, W_T > 0 ? W_T : 1, G, BM / kThrM, BN / kThrN)) popc_conv_kernel(const ConvProblem p, const int BK) {
   constexpr int TM = BM / kThrM, TN = BN / kThrN;
   constexpr int TPR_A = kThreads / BM;   // threads per A row in the loader / row-sum
   constexpr int TPR_W = kThreads / BN;
@@ -171,10 +190,13 @@ __global__ void __launch_bounds__(kThreads) popc_conv_kernel(const ConvProblem p
 #pragma unroll
   for (int l = 0; l < int(sizeof(wgt) / sizeof(int)); ++l) wgt[l] = p.one << l;
 
-  const int ktiles = (kp + BK - 1) / BK;
+  // split-K (small M*N, e.g. batch-1 layers): blockIdx.z owns k-tiles [kt0, kt0 + ktiles)
+  const int ktiles_all = (kp + BK - 1) / BK;
+  const int kt0 = int(int64_t(ktiles_all) * blockIdx.z / p.ksplit);
+  const int ktiles = int(int64_t(ktiles_all) * (blockIdx.z + 1) / p.ksplit) - kt0;
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
-    if (s < ktiles) load_stage(s, s * BK);
+    if (s < ktiles) load_stage(s, (kt0 + s) * BK);
     cp_async_commit();
   }
 
@@ -183,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) popc_conv_kernel(const ConvProblem p
     __syncthreads();
     {
       const int nk = kt + kStages - 1;
-      if (nk < ktiles) load_stage(nk % kStages, nk * BK);
+      if (nk < ktiles) load_stage(nk % kStages, (kt0 + nk) * BK);
       cp_async_commit();
     }
     const int stage = kt % kStages;
@@ -280,7 +302,13 @@ __global__ void __launch_bounds__(kThreads) popc_conv_kernel(const ConvProblem p
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int n = n0 + tn + j * kThrN;
-      if (n < p.oc) orow[n] = need_rowsum ? 2 * acc[i][j] - corr : acc[i][j];
+      if (n < p.oc) {
+        const int32_t v = need_rowsum ? 2 * acc[i][j] - corr : acc[i][j];
+        if (p.ksplit > 1)
+          atomicAdd(orow + n, v);  // partial over this K slice; int32 addition is exact in any order
+        else
+          orow[n] = v;
+      }
     }
   }
 }
@@ -295,8 +323,25 @@ cudaError_t launch_cfg(const ConvProblem& p, int BK, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured_bytes = int(smem);
   }
-  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.oc + BN - 1) / BN));
-  kern<<<grid, kThreads, smem, stream>>>(p, BK);
+  // Split K across CTAs when the M x N tiles cannot fill the 148 SMs twice (batch-1
+  // layers): keep >= 2 k-tiles per slice; partials are summed with int32 atomics into
+  // a zeroed output (exact: integer addition is associative).
+  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.oc + BN - 1) / BN);
+  const int ktiles = int((p.kp + BK - 1) / BK);
+  int ksplit = 1;
+  if (tiles < 2 * kNumSMs) {
+    ksplit = int((2 * kNumSMs + tiles - 1) / tiles);
+    if (ksplit > ktiles / 2) ksplit = ktiles / 2;
+    if (ksplit < 1) ksplit = 1;
+  }
+  ConvProblem q = p;
+  q.ksplit = ksplit;
+  if (ksplit > 1) {
+    cudaError_t e = cudaMemsetAsync(p.out, 0, size_t(p.M) * p.oc * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.oc + BN - 1) / BN), unsigned(ksplit));
+  kern<<<grid, kThreads, smem, stream>>>(q, BK);
   note_launch();
   return cudaPeekAtLastError();
 }
@@ -307,7 +352,8 @@ cudaError_t launch_cfg(const ConvProblem& p, int BK, cudaStream_t stream) {
 inline int choose_bk(int kp, int g, double cost_g, double cost_1, double overhead) {
   int best = 8;
   double best_cost = -1.0;
-  for (int bk : {12, 8, 6, 4, 2}) {
+  for (int bk : {16, 12, 8, 6, 4, 2}) {
+    if (bk > kBKMax) continue;
     const int stages = (kp + bk - 1) / bk;
     const int groups = g > 0 ? bk / (2 * g) : 0;
     const int pairs = g > 0 ? (bk - groups * 2 * g) / 2 : bk / 2;
@@ -317,19 +363,13 @@ inline int choose_bk(int kp, int g, double cost_g, double cost_1, double overhea
   return best;
 }
 
-// Registers a thread holds in the carry-save loop: the W words of its TN columns for
-// one group, the A words of one row, the AND/full-adder slots of one output and the
-// TM x TN accumulators.
-constexpr int csa_regs(int A, int W, int G, int TM, int TN) {
-  return TN * W * 2 * G + A * 2 * G + TM * TN + A * W * 2 * G;
-}
-
 // Group cost in SMSP cycles (cost model of csa.cuh).  Measured on B200 (tools/
-// layer_sweep.py, profiles/r01_csa_group_sweep.jsonl) G = 3 runs ~25% above its model
-// (175 registers -> one CTA per SM, deeper LOP3 chains), so it is charged that much.
-template <int A, int W, int G>
+// layer_sweep.py, profiles/r01_csa_group_sweep.jsonl): plans whose register estimate
+// exceeds ~112 end up above 128 registers (one CTA of 8 warps per SM) and run ~25%
+// above their model, so they are charged that much.
+template <int A, int W, int G, int TM, int TN>
 constexpr double group_cost() {
-  return csa_cycles_per_word_pair<A, W, G>() * (A * W * 2 * G) * (G >= 3 ? 1.25 : 1.0);
+  return csa_cycles_per_word_pair<A, W, G>() * (A * W * 2 * G) * (csa_regs(A, W, G, TM, TN) > 112 ? 1.25 : 1.0);
 }
 
 template <int A_T, int W_T, int BM, int BN, int G>
@@ -343,10 +383,11 @@ cudaError_t launch_csa_g(const ConvProblem& p, cudaStream_t stream, int bk) {
 template <int A_T, int W_T, int BM, int BN>
 cudaError_t launch_csa(const ConvProblem& p, cudaStream_t stream) {
   constexpr int TM = BM / kThrM, TN = BN / kThrN;
+  constexpr bool g4_ok = csa_regs(A_T, W_T, 4, TM, TN) <= 150;
   constexpr bool g3_ok = csa_regs(A_T, W_T, 3, TM, TN) <= 150;
   constexpr bool g2_ok = csa_regs(A_T, W_T, 2, TM, TN) <= 150;
   const int kp = int(p.kp);
-  const double ovh = 4.0 * A_T * W_T, c1 = group_cost<A_T, W_T, 1>();
+  const double ovh = 4.0 * A_T * W_T, c1 = group_cost<A_T, W_T, 1, TM, TN>();
   auto plan_cost = [&](int g, double cg, int* bk_out) {
     const int bk = choose_bk(kp, g, cg, c1, ovh);
     const int stages = (kp + bk - 1) / bk, groups = bk / (2 * g), pairs = (bk - groups * 2 * g) / 2;
@@ -354,21 +395,26 @@ cudaError_t launch_csa(const ConvProblem& p, cudaStream_t stream) {
     return stages * (groups * cg + pairs * c1 + ovh);
   };
 #ifdef BS_FORCE_G
+  constexpr int GF = BS_FORCE_G > 0 ? BS_FORCE_G : 1;
   int bkf = 0;
-  plan_cost(BS_FORCE_G > 0 ? BS_FORCE_G : 1, BS_FORCE_G > 0 ? group_cost<A_T, W_T, (BS_FORCE_G > 0 ? BS_FORCE_G : 1)>() : c1, &bkf);
-  return launch_csa_g<A_T, W_T, BM, BN, BS_FORCE_G>(p, stream, bkf);
+  plan_cost(GF, group_cost<A_T, W_T, GF, TM, TN>(), &bkf);
+  return launch_cfg<A_T, W_T, BM, BN, false, BS_FORCE_G>(p, bkf, stream);
 #else
-  int bk1 = 0, bk2 = 0, bk3 = 0;
+  int bk1 = 0, bk2 = 0, bk3 = 0, bk4 = 0;
   const double cost1 = plan_cost(1, c1, &bk1);
-  const double cost2 = g2_ok ? plan_cost(2, group_cost<A_T, W_T, 2>(), &bk2) : 1e30;
-  const double cost3 = g3_ok ? plan_cost(3, group_cost<A_T, W_T, 3>(), &bk3) : 1e30;
+  const double cost2 = g2_ok ? plan_cost(2, group_cost<A_T, W_T, 2, TM, TN>(), &bk2) : 1e30;
+  const double cost3 = g3_ok ? plan_cost(3, group_cost<A_T, W_T, 3, TM, TN>(), &bk3) : 1e30;
+  const double cost4 = g4_ok ? plan_cost(4, group_cost<A_T, W_T, 4, TM, TN>(), &bk4) : 1e30;
+  if constexpr (g4_ok) {
+    if (cost4 < cost3 && cost4 < cost2 && cost4 < cost1) return launch_cfg<A_T, W_T, BM, BN, false, 4>(p, bk4, stream);
+  }
   if constexpr (g3_ok) {
-    if (cost3 < cost2 && cost3 < cost1) return launch_csa_g<A_T, W_T, BM, BN, 3>(p, stream, bk3);
+    if (cost3 < cost2 && cost3 < cost1) return launch_cfg<A_T, W_T, BM, BN, false, 3>(p, bk3, stream);
   }
   if constexpr (g2_ok) {
-    if (cost2 <= cost1) return launch_csa_g<A_T, W_T, BM, BN, 2>(p, stream, bk2);
+    if (cost2 <= cost1) return launch_cfg<A_T, W_T, BM, BN, false, 2>(p, bk2, stream);
   }
-  return launch_csa_g<A_T, W_T, BM, BN, 1>(p, stream, bk1);
+  return launch_cfg<A_T, W_T, BM, BN, false, 1>(p, bk1, stream);
 #endif
 }
 
