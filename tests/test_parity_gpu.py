@@ -234,3 +234,31 @@ def test_host_e2e_entry():
     bs.bitserial_conv2d_nhwc_host(act_host, 2, wp, 1, bs.BIPOLAR, L.oc, 3, 3, 1, 1, out_host, act_dev, out_dev, ws)
     ref = oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(1, 1), pad=(1, 1))
     np.testing.assert_array_equal(out_host.numpy(), ref)
+
+
+@pytest.mark.parametrize("a_bits", [1, 2, 3, 4])
+@pytest.mark.parametrize("w_bits", [1, 2, 3, 4])
+def test_limit_study_grid_parity(a_bits, w_bits):
+    """layer 9 at every A, W in 1..4, both encodings,
+    batch 2 — the kernels the limit study times — full compare."""
+    L = inputs.TABLE1[9]
+    for bipolar in (False, True):
+        act, wt, got = _layer_run(L, 2, a_bits, w_bits, bipolar, seed=7 * a_bits + w_bits + 100 * bipolar)
+        ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(1, 1), pad=(1, 1))
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"A{a_bits}W{w_bits} bipolar={bipolar}")
+
+
+@pytest.mark.parametrize("case", [(1, 4, 4, 600, 40, 3, 3, 1, 1, 1, 1), (1, 7, 7, 512, 512, 3, 3, 1, 1, 1, 1),
+                                  (2, 14, 14, 256, 512, 1, 1, 2, 2, 0, 0), (1, 2, 3, 2048, 16, 1, 3, 1, 1, 0, 1)])
+def test_split_k_small_mn(case):
+    """Small M x N with long K takes the split-K path (int32 atomics into a zeroed
+    output); exact regardless of the order partials land."""
+    n, h, w, c, oc, kh, kw, sh, sw, ph, pw = case
+    g = inputs.gen(sum(case))
+    act = inputs.codes((n, h, w, c), 2, g)
+    wt = inputs.codes((oc, kh, kw, c), 1, g)
+    ref = oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(sh, sw), pad=(ph, pw))
+    wp = gpu_pack(wt.view(oc * kh * kw, c), 1)
+    for _ in range(3):
+        got = bs.bitserial_conv2d_nhwc_i8(act.to(DEV), 2, wp, 1, bs.BIPOLAR, oc, kh, kw, (sh, sw), (ph, pw))
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
