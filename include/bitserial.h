@@ -75,7 +75,8 @@ typedef enum { BS_UNIPOLAR = 0, BS_BIPOLAR = 1 } bs_encoding;
  *   POPC_LIT : as POPC but bipolar evaluated literally, popc(a&w) - popc(a&~w) per
  *              plane pair (north_star form; twice the POPC work; unipolar = POPC).
  *   GEMV     : warp-per-rows matrix-vector kernel with butterfly multi-row reduction
- *              (PAPER.md:694-705 micro-kernel ideas), for m <= 8 (dense only). */
+ *              (PAPER.md:694-705 micro-kernel ideas), for m <= 8 (dense only).
+ *   (tensor-core path: see bs_bitserial_conv2d_nhwc_tc below) */
 typedef enum {
   BS_ALGO_AUTO = 0,
   BS_ALGO_POPC = 1,
@@ -165,6 +166,29 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
                                 int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
                                 int stride_h, int stride_w, int pad_h, int pad_w,
                                 void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Tensor-core bitserial (tcgen05.mma kind::i8 on sm_100a).  Same operation and
+ * operands as bs_bitserial_conv2d_nhwc / bs_bitserial_dense.  Each activation plane i
+ * and weight plane j is expanded inside the kernel (weights: by a first kernel into
+ * `workspace`) to bytes 2^i*a_i and 2^j*b_j (unipolar) or 2^j*(2b_j-1) (bipolar), and
+ * every plane pair is one exact int8 x int8 -> int32 binary dot product on the tensor
+ * cores: popcount(a_i AND w_j) = sum_k a_i[k] w_j[k] (Eq. 1), weighted
+ * 2^(i+j) (Eq. 2); cost still grows with A*W.
+ * Supported: a_bits in [1,4], w_bits in [1,2] (BS_ERR_UNSUPPORTED otherwise).
+ * workspace: device, >= *_tc_workspace_bytes(), 16-byte aligned, overwritten.
+ */
+int64_t bs_conv2d_tc_workspace_bytes(int oc, int kh, int kw, int c, int w_bits);
+int bs_bitserial_conv2d_nhwc_tc(const uint32_t* act_packed, int a_bits,
+                                const uint32_t* w_packed, int w_bits, int w_enc,
+                                int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                int stride_h, int stride_w, int pad_h, int pad_w,
+                                void* workspace, int64_t workspace_bytes, void* stream);
+int64_t bs_dense_tc_workspace_bytes(int64_t n, int64_t k, int w_bits);
+int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits,
+                          const uint32_t* w_packed, int w_bits, int w_enc,
+                          int32_t* out, int64_t m, int64_t n, int64_t k,
+                          void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * End-to-end entry with HOST activations and HOST output (used for the bench's

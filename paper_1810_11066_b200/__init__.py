@@ -22,6 +22,7 @@ __all__ = [
     "BitserialError", "library_path", "abi_version", "kernel_launches", "packed_row_words", "bitpack",
     "bitserial_dense", "bitserial_dense_i8", "bitserial_conv2d_nhwc", "bitserial_conv2d_nhwc_i8",
     "bitserial_conv2d_nhwc_host", "conv2d_workspace_bytes", "dense_workspace_bytes", "conv_out_extent",
+    "bitserial_conv2d_nhwc_tc", "bitserial_dense_tc", "conv2d_tc_workspace_bytes", "dense_tc_workspace_bytes",
     "EXPORTED_SYMBOLS",
 ]
 
@@ -38,7 +39,8 @@ EXPORTED_SYMBOLS = (
     "bs_abi_version", "bs_status_string", "bs_last_error", "bs_kernel_launches", "bs_packed_row_words", "bs_bitpack",
     "bs_bitserial_dense", "bs_bitserial_dense_ex", "bs_dense_workspace_bytes", "bs_bitserial_dense_i8",
     "bs_bitserial_conv2d_nhwc", "bs_bitserial_conv2d_nhwc_ex", "bs_conv2d_workspace_bytes",
-    "bs_bitserial_conv2d_nhwc_i8", "bs_bitserial_conv2d_nhwc_host",
+    "bs_bitserial_conv2d_nhwc_i8", "bs_bitserial_conv2d_nhwc_host", "bs_conv2d_tc_workspace_bytes",
+    "bs_bitserial_conv2d_nhwc_tc", "bs_dense_tc_workspace_bytes", "bs_bitserial_dense_tc",
 )
 
 
@@ -75,6 +77,10 @@ def _load():
         "bs_conv2d_workspace_bytes": ([I, I, I, I, I], L),
         "bs_bitserial_conv2d_nhwc_i8": ([P, I, P, I, I, P] + [I] * 11 + [P, L, P], I),
         "bs_bitserial_conv2d_nhwc_host": ([P, I, P, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
+        "bs_conv2d_tc_workspace_bytes": ([I, I, I, I, I], L),
+        "bs_bitserial_conv2d_nhwc_tc": ([P, I, P, I, I, P] + [I] * 11 + [P, L, P], I),
+        "bs_dense_tc_workspace_bytes": ([L, L, I], L),
+        "bs_bitserial_dense_tc": ([P, I, P, I, I, P, L, L, L, P, L, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -204,6 +210,46 @@ def bitserial_conv2d_nhwc_i8(act, a_bits, w_packed, w_bits, w_enc, oc, kh, kw, s
                                                _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
                                                _dev(workspace, "workspace", torch.uint8), workspace.numel(),
                                                _stream(stream)))
+    return out
+
+
+def conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits) -> int:
+    return int(_load().bs_conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits))
+
+
+def dense_tc_workspace_bytes(n, k, w_bits) -> int:
+    return int(_load().bs_dense_tc_workspace_bytes(n, k, w_bits))
+
+
+def bitserial_conv2d_nhwc_tc(act_packed, a_bits, w_packed, w_bits, w_enc, n, h, w, c, oc, kh, kw,
+                             stride=1, pad=0, out=None, workspace=None, stream=None):
+    """bs_bitserial_conv2d_nhwc_tc: the tensor-core bitserial conv (tcgen05, kind::i8)."""
+    sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
+    if out is None:
+        out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act_packed.device)
+    if workspace is None:
+        workspace = torch.empty(max(16, conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits)), dtype=torch.uint8,
+                                device=act_packed.device)
+    _check(_load().bs_bitserial_conv2d_nhwc_tc(_dev(act_packed, "act_packed", torch.int32), a_bits,
+                                               _dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc),
+                                               _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
+                                               _dev(workspace, "workspace", torch.uint8), workspace.numel(),
+                                               _stream(stream)))
+    return out
+
+
+def bitserial_dense_tc(a_packed, a_bits, w_packed, w_bits, w_enc, m, n, k, out=None, workspace=None, stream=None):
+    """bs_bitserial_dense_tc: the tensor-core bitserial dense product (tcgen05, kind::i8)."""
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int32, device=a_packed.device)
+    if workspace is None:
+        workspace = torch.empty(max(16, dense_tc_workspace_bytes(n, k, w_bits)), dtype=torch.uint8,
+                                device=a_packed.device)
+    _check(_load().bs_bitserial_dense_tc(_dev(a_packed, "a_packed", torch.int32), a_bits,
+                                         _dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc),
+                                         _dev(out, "out", torch.int32), m, n, k,
+                                         _dev(workspace, "workspace", torch.uint8), workspace.numel(),
+                                         _stream(stream)))
     return out
 
 

@@ -242,6 +242,48 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits, const uint32_t* 
   return launch_conv(p, BS_ALGO_AUTO, s, fn);
 }
 
+int64_t bs_conv2d_tc_workspace_bytes(int oc, int kh, int kw, int c, int w_bits) {
+  if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0 || w_bits < 1 || w_bits > 8) return 0;
+  return bs::tc_weight_bytes(oc, int64_t(kh) * kw * row_words(c), w_bits);
+}
+
+int64_t bs_dense_tc_workspace_bytes(int64_t n, int64_t k, int w_bits) {
+  if (n <= 0 || k <= 0 || w_bits < 1 || w_bits > 8) return 0;
+  return bs::tc_weight_bytes(n, row_words(k), w_bits);
+}
+
+int bs_bitserial_conv2d_nhwc_tc(const uint32_t* act_packed, int a_bits, const uint32_t* w_packed, int w_bits,
+                                int w_enc, int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                int stride_h, int stride_w, int pad_h, int pad_w, void* workspace,
+                                int64_t workspace_bytes, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tc";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, w_enc, fn)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!act_packed || !w_packed || !out || !workspace) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  const int64_t need = bs_conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits);
+  if (workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
+  if (!aligned16(act_packed) || !aligned16(w_packed) || !aligned16(out) || !aligned16(workspace))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  bs::ConvProblem p = make_conv(act_packed, a_bits, w_packed, w_bits, w_enc, out, g);
+  return cuda_status(bs::launch_tc_conv(p, static_cast<int8_t*>(workspace), static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,
+                          int32_t* out, int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes,
+                          void* stream) {
+  const char* fn = "bs_bitserial_dense_tc";
+  if (int st = check_dense(a_packed, w_packed, out, a_bits, w_bits, w_enc, m, n, k, fn)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  const int64_t need = bs_dense_tc_workspace_bytes(n, k, w_bits);
+  if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
+  if (!aligned16(workspace)) return fail(BS_ERR_ALIGN, "%s: workspace must be 16-byte aligned", fn);
+  ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
+  bs::ConvProblem p = make_conv(a_packed, a_bits, w_packed, w_bits, w_enc, out, g);
+  return cuda_status(bs::launch_tc_conv(p, static_cast<int8_t*>(workspace), static_cast<cudaStream_t>(stream)), fn);
+}
+
 int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits, const uint32_t* w_packed, int w_bits,
                                   int w_enc, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
                                   int stride_h, int stride_w, int pad_h, int pad_w, uint8_t* act_dev,

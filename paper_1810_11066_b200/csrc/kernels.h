@@ -42,6 +42,13 @@ cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64
 // when no instantiation covers (a_bits, w_bits, algo).
 cudaError_t launch_popc_conv(const ConvProblem& p, Algo algo, cudaStream_t stream);
 
+// Tensor-core (tcgen05, kind::i8) bitserial kernel: one MMA per activation/weight
+// plane pair on expanded bit-planes (tc_conv.cu).  `wexp_ws` receives the expanded
+// weight planes (tc_weight_bytes bytes); cudaErrorNotSupported outside A<=4, W<=2.
+int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits);
+bool tc_supported(int a_bits, int w_bits);
+cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, cudaStream_t stream);
+
 // Matrix-vector kernel for m <= 8 dense products.
 //   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)
 //   a_codes  : uint8 [m][k] raw codes to pack in-kernel (fused; nullptr otherwise)

@@ -262,3 +262,46 @@ def test_split_k_small_mn(case):
     for _ in range(3):
         got = bs.bitserial_conv2d_nhwc_i8(act.to(DEV), 2, wp, 1, bs.BIPOLAR, oc, kh, kw, (sh, sw), (ph, pw))
         np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------ tensor-core path
+TC_PRECISIONS = [(1, 1), (2, 1), (2, 2), (1, 2), (3, 1), (3, 2), (4, 1), (4, 2)]
+
+
+@pytest.mark.parametrize("a_bits,w_bits", TC_PRECISIONS)
+@pytest.mark.parametrize("bipolar", [False, True])
+@pytest.mark.parametrize("m,n,k", [(1, 16, 32), (130, 64, 200), (257, 130, 1000), (128, 256, 4096), (300, 300, 33)])
+def test_dense_tc_parity(a_bits, w_bits, bipolar, m, n, k):
+    a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=31 * a_bits + w_bits + m + k)
+    ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+    got = bs.bitserial_dense_tc(gpu_pack(a, a_bits), a_bits, gpu_pack(w, w_bits), w_bits, enc(bipolar), m, n, k)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (4, 2)])
+@pytest.mark.parametrize("bipolar", [False, True])
+def test_conv_tc_parity(case, a_bits, w_bits, bipolar):
+    n, h, w, c, oc, kh, kw, sh, sw, ph, pw = case
+    g = inputs.gen(sum(case) * 100 + a_bits * 10 + w_bits + 5)
+    act = inputs.codes((n, h, w, c), a_bits, g)
+    wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+    ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(sh, sw), pad=(ph, pw))
+    wp = gpu_pack(wt.view(oc * kh * kw, c), w_bits)
+    got = bs.bitserial_conv2d_nhwc_tc(gpu_pack(act.view(-1, c), a_bits), a_bits, wp, w_bits, enc(bipolar),
+                                      n, h, w, c, oc, kh, kw, (sh, sw), (ph, pw))
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("layer", inputs.BASELINE_LAYERS)
+def test_conv_tc_resnet_layers(layer):
+    """TC path on every BASELINE layer, batch 2, A2W1 bipolar and A2W2 unipolar, full compare."""
+    L = inputs.TABLE1[layer]
+    for a_bits, w_bits, bipolar in ((2, 1, True), (2, 2, False)):
+        act, wt = inputs.conv_operands(L, 2, a_bits, w_bits, seed=layer + 11 * a_bits + w_bits)
+        wp = gpu_pack(wt.view(L.oc * L.k * L.k, L.ic), w_bits)
+        got = bs.bitserial_conv2d_nhwc_tc(gpu_pack(act.view(-1, L.ic), a_bits), a_bits, wp, w_bits, enc(bipolar),
+                                          2, L.h, L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad)
+        ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(L.s, L.s),
+                                 pad=(L.pad, L.pad))
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"L{layer} A{a_bits}W{w_bits}")

@@ -20,6 +20,7 @@ ap.add_argument("--unipolar", action="store_true")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--layers", default=",".join(map(str, inputs.BASELINE_LAYERS)))
 ap.add_argument("--algo", type=int, default=0)
+ap.add_argument("--tc", action="store_true", help="tensor-core path (bs_bitserial_conv2d_nhwc_tc)")
 args = ap.parse_args()
 dev = torch.device("cuda")
 enc = bs.UNIPOLAR if args.unipolar else bs.BIPOLAR
@@ -32,8 +33,15 @@ for li in map(int, args.layers.split(",")):
     wt = inputs.codes((L.oc * L.k * L.k, L.ic), args.w, g).to(dev)
     ap_ = bs.bitpack(act, args.a)
     wp = bs.bitpack(wt, args.w)
-    run = lambda: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc, L.k, L.k,  # noqa
-                                           L.s, L.pad, algo=args.algo)
+    out = torch.empty((args.batch, bs.conv_out_extent(L.h, L.k, L.s, L.pad), bs.conv_out_extent(L.w, L.k, L.s, L.pad),
+                       L.oc), dtype=torch.int32, device=dev)
+    ws = torch.empty(max(16, bs.conv2d_tc_workspace_bytes(L.oc, L.k, L.k, L.ic, args.w)), dtype=torch.uint8, device=dev)
+    if args.tc:
+        run = lambda: bs.bitserial_conv2d_nhwc_tc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc,  # noqa
+                                                  L.k, L.k, L.s, L.pad, out=out, workspace=ws)
+    else:
+        run = lambda: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc, L.k,  # noqa
+                                               L.k, L.s, L.pad, out=out, algo=args.algo)
     run()
     torch.cuda.synchronize()
     ts = []
@@ -50,5 +58,5 @@ for li in map(int, args.layers.split(",")):
     res[li] = {"ms": ms, "tops": ops / ms / 1e9}
     tot_ops += ops
     tot_ms += ms
-print(json.dumps({"lib": bs.library_path(), "a": args.a, "w": args.w, "layers": res, "total_ms": tot_ms,
+print(json.dumps({"lib": bs.library_path(), "tc": args.tc, "a": args.a, "w": args.w, "layers": res, "total_ms": tot_ms,
                   "total_tops": tot_ops / tot_ms / 1e9}))
