@@ -31,7 +31,7 @@
 namespace bs {
 namespace tc {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;  // 8 warps: two threads per A row; warps w and w+4 share TMEM lanes
 constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BKB = 128;         // K bytes per stage = one 128B swizzle row
 constexpr int kWordsPerStage = BKB / 32;  // 4 packed words per plane per row
@@ -89,12 +89,25 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
 }
 
-// Spread the 4 bits of nibble q of `w` into bytes (bit r -> byte r, value `val`):
-// (nibble * 0x00204081) puts bit r at 8r (with other partial products elsewhere), the
-// mask keeps bit 0 of every byte, the final multiply scales it to 2^i.
-__device__ __forceinline__ uint32_t spread_nibble(uint32_t w, int q, uint32_t scale) {
-  const uint32_t n = (w >> (4 * q)) & 0xFu;
-  return ((n * 0x00204081u) & 0x01010101u) * scale;
+// Spread the 4 bits of a nibble (already isolated in the low bits of n) into bytes:
+// n * (0x00204081 << i) puts bit r at 8r + i (other partial products elsewhere) and the
+// mask keeps exactly those: byte r = 2^i * bit r.
+template <int I>
+__device__ __forceinline__ uint32_t spread4(uint32_t n) {
+  return (n * (0x00204081u << I)) & (0x01010101u << I);
+}
+
+// 32 activation bits of one plane word -> 8 words of bytes (element 4q + r in byte r
+// of word q), value 2^I * bit.  The 8 nibbles are isolated with two masks and a
+// byte permute each (PRMT) instead of a shift + mask per nibble.
+template <int I>
+__device__ __forceinline__ void expand_word(uint32_t w, uint32_t (&o)[8]) {
+  const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    o[2 * b] = spread4<I>(__byte_perm(lo, 0u, 0x4440u + b));
+    o[2 * b + 1] = spread4<I>(__byte_perm(hi, 0u, 0x4440u + b));
+  }
 }
 
 // ------------------------------------------------------------------ weight expansion
@@ -132,18 +145,19 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
 
 // ----------------------------------------------------------------------- main kernel
 template <int A_BITS, int W_BITS, int BN, int STAGES>
-struct TcSmem {
+struct TcSmem {  // 1024 B of alignment slack + mbarriers / TMEM slot
   static constexpr int kABytes = A_BITS * BM * BKB;   // per stage
   static constexpr int kBBytes = W_BITS * BN * BKB;   // per stage
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int A_BITS, int W_BITS, int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem p, const int8_t* __restrict__ wexp,
+template <int A_BITS, int W_BITS, int BN, int STAGES, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) tc_conv_kernel(const ConvProblem p, const int8_t* __restrict__ wexp,
                                                               const int64_t kpad) {
   using S = TcSmem<A_BITS, W_BITS, BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  static_assert(MINB >= 1, "");
   // 1024-byte aligned tile region (SWIZZLE_128B atoms), barriers after the tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStageBytes);
@@ -169,8 +183,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // ---- this thread's A row (output pixel) and its receptive-field origin
-  const int64_t m = m0 + tid;
+  // ---- this thread's A row (output pixel), its receptive-field origin, and which
+  // half of the 128-byte K chunk it expands (packed words 2*half, 2*half+1)
+  const int arow = tid & (BM - 1), half = tid >> 7;
+  const int64_t m = m0 + arow;
   const bool row_ok = m < p.M;
   int iy0 = 0, ix0 = 0;
   int64_t img_base = 0;
@@ -183,10 +199,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem 
     ix0 = ox * p.sw - p.pw;
     img_base = b * int64_t(p.h) * p.w;
   }
-  const uint32_t sw = uint32_t(tid & 7);  // 128B swizzle phase of this row
+  const uint32_t sw = uint32_t(arow & 7);  // 128B swizzle phase of this row
+
+  // 8-byte piece (2 packed words per plane) this thread gathers for K chunk kc; the
+  // piece lies inside one tap because Cw is even (implicit im2col, zero padding)
+  auto gather = [&](int kc, uint2 (&v)[A_BITS]) {
+    const int kk = kc * kWordsPerStage + 2 * half;
+    const int tap = kk / p.kw_a;
+    const int cw = kk - tap * p.kw_a;
+    const int ky = tap / p.kwid, kx = tap - ky * p.kwid;
+    const int iy = iy0 + ky, ix = ix0 + kx;
+    const bool ok = row_ok && kk < kp && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
+    const uint32_t* src = p.act + (img_base + int64_t(iy) * p.w + ix) * p.kw_a + cw;
+#pragma unroll
+    for (int i = 0; i < A_BITS; ++i) {
+      v[i] = make_uint2(0u, 0u);
+      if (ok) v[i] = __ldg(reinterpret_cast<const uint2*>(src + i * p.act_plane));
+    }
+  };
 
   constexpr uint32_t kIdesc = idesc_i8<BN>();
   uint32_t phase_bits = 0;  // bit s = parity to wait for on stage s
+  uint2 wa[A_BITS];
+  gather(0, wa);
 
   for (int kc = 0; kc < nchunks; ++kc) {
     const int s = kc % STAGES;
@@ -211,41 +246,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem 
       }
       cp_async_commit();
     }
-    // A: gather 4 packed words per plane (two 8-byte pieces, each inside one tap)
-    uint32_t wa[A_BITS][kWordsPerStage];
-#pragma unroll
-    for (int piece = 0; piece < 2; ++piece) {
-      const int kk = kc * kWordsPerStage + 2 * piece;
-      const int tap = kk / p.kw_a;
-      const int cw = kk - tap * p.kw_a;
-      const int ky = tap / p.kwid, kx = tap - ky * p.kwid;
-      const int iy = iy0 + ky, ix = ix0 + kx;
-      const bool ok = row_ok && kk < kp && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
-      const uint32_t* src = p.act + (img_base + int64_t(iy) * p.w + ix) * p.kw_a + cw;
-#pragma unroll
-      for (int i = 0; i < A_BITS; ++i) {
-        uint2 v = make_uint2(0u, 0u);
-        if (ok) v = __ldg(reinterpret_cast<const uint2*>(src + i * p.act_plane));
-        wa[i][2 * piece] = v.x;
-        wa[i][2 * piece + 1] = v.y;
-      }
-    }
+    // A: prefetch the next chunk's words, then expand this chunk's into swizzled smem
+    uint2 wn[A_BITS];
+    if (kc + 1 < nchunks) gather(kc + 1, wn);
 #pragma unroll
     for (int i = 0; i < A_BITS; ++i) {
-      uint8_t* rowp = sA + i * (BM * BKB) + (tid >> 3) * 1024 + (tid & 7) * 128;
-      const uint32_t scale = 1u << i;
+      uint8_t* rowp = sA + i * (BM * BKB) + (arow >> 3) * 1024 + (arow & 7) * 128;
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {  // 16-byte chunk ch = elements 16ch..16ch+15
-        const uint32_t w = wa[i][ch >> 1];
-        const int qb = (ch & 1) * 4;
-        uint4 v;
-        v.x = spread_nibble(w, qb + 0, scale);
-        v.y = spread_nibble(w, qb + 1, scale);
-        v.z = spread_nibble(w, qb + 2, scale);
-        v.w = spread_nibble(w, qb + 3, scale);
-        *reinterpret_cast<uint4*>(rowp + ((uint32_t(ch) ^ sw) << 4)) = v;
+      for (int wsel = 0; wsel < 2; ++wsel) {
+        const uint32_t w = wsel ? wa[i].y : wa[i].x;
+        uint32_t o[8];
+        switch (i) {  // compile-time after unrolling
+          case 0: expand_word<0>(w, o); break;
+          case 1: expand_word<1>(w, o); break;
+          case 2: expand_word<2>(w, o); break;
+          default: expand_word<3>(w, o); break;
+        }
+        const uint32_t ch0 = uint32_t(4 * half + 2 * wsel);  // 16-byte chunks of this word
+        *reinterpret_cast<uint4*>(rowp + ((ch0 ^ sw) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(rowp + (((ch0 + 1) ^ sw) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
       }
     }
+#pragma unroll
+    for (int i = 0; i < A_BITS; ++i) wa[i] = wn[i];
     cp_async_wait<0>();
     fence_proxy_async();
     __syncthreads();
@@ -272,12 +295,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem 
   }
   tc_fence_after();
 
-  // ---- epilogue: warp w reads TMEM lanes 32w.. (rows), 32 columns per load
-  const int64_t row = m0 + warp * 32 + (tid & 31);
+  // ---- epilogue, 64 columns at a time: warp w loads TMEM lanes 32*(w%4).. (rows) x 32
+  // columns (half w/4 of the block) into a padded smem tile (ring buffers are free now),
+  // then all threads write the 128 x 64 int32 block with coalesced 16-byte stores (each
+  // output row segment is contiguous in NHWC / row-major memory).
+  constexpr int kCB = 64, kLd = kCB + 4;  // +4 words: conflict-free 16-byte smem rows
+  uint32_t* stile = reinterpret_cast<uint32_t*>(smem);
+  const int quarter = warp & 3, colhalf = warp >> 2;
+  const int trow = quarter * 32 + (tid & 31);
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
+  for (int cb = 0; cb < BN; cb += kCB) {
     uint32_t r[32];
-    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0);
+    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(cb + colhalf * 32);
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -287,20 +316,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem 
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < p.M) {
-      int32_t* orow = p.out + row * p.oc + n0 + c0;
-      const int nvalid = p.oc - (n0 + c0);
-      if (nvalid >= 32 && (p.oc & 3) == 0) {
+    uint32_t* srow = stile + trow * kLd + colhalf * 32;
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          reinterpret_cast<int4*>(orow)[v] = make_int4(int(r[4 * v]), int(r[4 * v + 1]), int(r[4 * v + 2]),
-                                                      int(r[4 * v + 3]));
-      } else {
+    for (int v = 0; v < 8; ++v)
+      *reinterpret_cast<uint4*>(srow + 4 * v) = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+    __syncthreads();
+    const int ncols = min(kCB, p.oc - (n0 + cb));  // valid columns of this block
+    if ((p.oc & 3) == 0 && ncols == kCB) {
 #pragma unroll
-        for (int v = 0; v < 32; ++v)
-          if (v < nvalid) orow[v] = int(r[v]);
+      for (int c = tid; c < BM * (kCB / 4); c += kThreads) {
+        const int rr = c / (kCB / 4), c4 = c - rr * (kCB / 4);
+        const int64_t grow = m0 + rr;
+        if (grow < p.M)
+          *reinterpret_cast<uint4*>(p.out + grow * p.oc + n0 + cb + 4 * c4) =
+              *reinterpret_cast<const uint4*>(stile + rr * kLd + 4 * c4);
+      }
+    } else if (ncols > 0) {
+      for (int c = tid; c < BM * kCB; c += kThreads) {
+        const int rr = c / kCB, cc = c - rr * kCB;
+        const int64_t grow = m0 + rr;
+        if (grow < p.M && cc < ncols) p.out[grow * p.oc + n0 + cb + cc] = int32_t(stile[rr * kLd + cc]);
       }
     }
+    __syncthreads();
   }
   tc_fence_before();
   __syncthreads();
@@ -309,13 +347,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_conv_kernel(const ConvProblem 
   }
 }
 
+// Stages: as many as fit while two CTAs (16 warps) still share an SM — a second CTA
+// overlaps one tile's prologue / epilogue with another's main loop — else as many as fit
+// one CTA (at least 2).
 template <int A_BITS, int W_BITS, int BN>
 cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
   constexpr int kStageBytes = TcSmem<A_BITS, W_BITS, BN, 1>::kStageBytes;
-  constexpr int STAGES = (200 * 1024) / kStageBytes >= 4 ? 4 : ((200 * 1024) / kStageBytes >= 3 ? 3 : 2);
+  constexpr int kPerCta2 = (227 * 1024) / 2 - 2304;
+  constexpr int kStages2 = kPerCta2 / kStageBytes;
+  constexpr bool kTwo = kStages2 >= 2;
+  constexpr int kStages1 = ((227 * 1024) - 2304) / kStageBytes;
+  constexpr int STAGES = kTwo ? (kStages2 > 4 ? 4 : kStages2) : (kStages1 > 4 ? 4 : kStages1);
+  static_assert(STAGES >= 2, "tensor-core tile does not fit two stages of shared memory");
   using S = TcSmem<A_BITS, W_BITS, BN, STAGES>;
   static_assert(S::kBytes <= 227 * 1024, "tensor-core tile does not fit shared memory");
-  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, STAGES>;
+  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, STAGES, kTwo ? 2 : 1>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
