@@ -190,6 +190,38 @@ int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits,
                           int32_t* out, int64_t m, int64_t n, int64_t k,
                           void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Prepared weights for the tensor-core path.  Weight packing is done ahead of time
+ * and is not timed; the expansion of the packed weight planes into the
+ * tensor-core byte layout is part of that offline step:
+ *   w_tc : device int8 [w_bits][oc][Kpad*32] (dense: [w_bits][n][Kpad*32]) with
+ *          Kpad = K words (kh*kw*bs_packed_row_words(c), dense bs_packed_row_words(k))
+ *          rounded up to a multiple of 4; byte = 2^j*b_j (unipolar) or 2^j*(2b_j-1)
+ *          (bipolar), so the encoding is baked into w_tc.
+ *   w_tc_bytes >= bs_conv2d_tc_workspace_bytes() / bs_dense_tc_workspace_bytes().
+ */
+int bs_conv2d_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                                 int8_t* w_tc, int64_t w_tc_bytes, void* stream);
+int bs_dense_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t k,
+                                int8_t* w_tc, int64_t w_tc_bytes, void* stream);
+
+/* Tensor-core conv / dense on prepared weights (one launch: the persistent tcgen05
+ * kernel; out as in bs_bitserial_conv2d_nhwc / bs_bitserial_dense). */
+int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, const int8_t* w_tc, int w_bits,
+                                         int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                         int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
+int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, const int8_t* w_tc, int w_bits,
+                                   int32_t* out, int64_t m, int64_t n, int64_t k, void* stream);
+
+/* The timed step of the paper on the tensor-core path: activation
+ * bit-packing (raw uint8 codes -> workspace of *_workspace_bytes() bytes) followed by
+ * the tensor-core conv / dense on prepared weights.  Two launches. */
+int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out,
+                                   int n, int h, int w, int c, int oc, int kh, int kw,
+                                   int stride_h, int stride_w, int pad_h, int pad_w,
+                                   void* workspace, int64_t workspace_bytes, void* stream);
+int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out,
+                             int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * End-to-end entry with HOST activations and HOST output (used for the bench's
  * e2e number).  Copies act_host (uint8 NHWC, pinned or pageable) into the device
@@ -203,6 +235,13 @@ int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits,
                                   int stride_h, int stride_w, int pad_h, int pad_w,
                                   uint8_t* act_dev, int32_t* out_dev,
                                   void* workspace, int64_t workspace_bytes, void* stream);
+
+/* As above on the tensor-core path with prepared weights (bs_bitserial_conv2d_nhwc_tc_i8). */
+int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, const int8_t* w_tc, int w_bits,
+                                     int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+                                     int stride_h, int stride_w, int pad_h, int pad_w,
+                                     uint8_t* act_dev, int32_t* out_dev,
+                                     void* workspace, int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

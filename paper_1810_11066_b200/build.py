@@ -64,7 +64,7 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False, defines=(),
         objs = list(ex.map(lambda s: _compile(s, force, verbose, objdir, defines), srcs))
     if force or _stale(out, objs):
         tmp = out + f".tmp{os.getpid()}"
-        subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcuda"])
+        subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs)
         os.replace(tmp, out)
     return out
 

@@ -284,6 +284,118 @@ int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits, const uint32_t* 
   return cuda_status(bs::launch_tc_conv(p, static_cast<int8_t*>(workspace), static_cast<cudaStream_t>(stream)), fn);
 }
 
+int bs_conv2d_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                                 int8_t* w_tc, int64_t w_tc_bytes, void* stream) {
+  const char* fn = "bs_conv2d_tc_prepare_weights";
+  if (!w_packed || !w_tc) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (int st = check_bits(1, w_bits, w_enc, fn)) return st;
+  if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,2]", fn);
+  if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0) return fail(BS_ERR_SHAPE, "%s: non-positive extent", fn);
+  const int64_t need = bs_conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits);
+  if (w_tc_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_tc needs %lld bytes", fn, (long long)need);
+  if (!aligned16(w_packed) || !aligned16(w_tc)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return cuda_status(bs::launch_tc_expand_weights(w_packed, w_bits, w_enc == BS_BIPOLAR, oc,
+                                                  int64_t(kh) * kw * row_words(c), w_tc,
+                                                  static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_dense_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t k, int8_t* w_tc,
+                                int64_t w_tc_bytes, void* stream) {
+  const char* fn = "bs_dense_tc_prepare_weights";
+  if (!w_packed || !w_tc) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (int st = check_bits(1, w_bits, w_enc, fn)) return st;
+  if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,2]", fn);
+  if (n <= 0 || k <= 0 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: bad n or k", fn);
+  const int64_t need = bs_dense_tc_workspace_bytes(n, k, w_bits);
+  if (w_tc_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_tc needs %lld bytes", fn, (long long)need);
+  if (!aligned16(w_packed) || !aligned16(w_tc)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return cuda_status(bs::launch_tc_expand_weights(w_packed, w_bits, w_enc == BS_BIPOLAR, n, row_words(k), w_tc,
+                                                  static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, const int8_t* w_tc, int w_bits,
+                                         int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                         int stride_h, int stride_w, int pad_h, int pad_w, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tc_prepared";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!act_packed || !w_tc || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (!aligned16(act_packed) || !aligned16(w_tc) || !aligned16(out))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  bs::ConvProblem p = make_conv(act_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out,
+                                   int n, int h, int w, int c, int oc, int kh, int kw, int stride_h, int stride_w,
+                                   int pad_h, int pad_w, void* workspace, int64_t workspace_bytes, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tc_i8";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!act || !w_tc || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  const int64_t need = bs_conv2d_workspace_bytes(n, h, w, c, a_bits);
+  if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
+  if (!aligned16(act) || !aligned16(w_tc) || !aligned16(out) || !aligned16(workspace))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* ap = static_cast<uint32_t*>(workspace);
+  if (int st = cuda_status(bs::launch_bitpack(act, ap, int64_t(n) * h * w, c, row_words(c), a_bits, s), fn)) return st;
+  bs::ConvProblem p = make_conv(ap, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, s), fn);
+}
+
+int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out,
+                                   int64_t m, int64_t n, int64_t k, void* stream) {
+  const char* fn = "bs_bitserial_dense_tc_prepared";
+  if (int st = check_dense(a_packed, reinterpret_cast<const uint32_t*>(w_tc), out, a_bits, w_bits, BS_UNIPOLAR, m, n,
+                           k, fn))
+    return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
+  bs::ConvProblem p = make_conv(a_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out, int64_t m,
+                             int64_t n, int64_t k, void* workspace, int64_t workspace_bytes, void* stream) {
+  const char* fn = "bs_bitserial_dense_tc_i8";
+  if (int st = check_dense(a, reinterpret_cast<const uint32_t*>(w_tc), out, a_bits, w_bits, BS_UNIPOLAR, m, n, k, fn))
+    return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  const int64_t need = bs_dense_workspace_bytes(m, k, a_bits);
+  if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
+  if (!aligned16(workspace)) return fail(BS_ERR_ALIGN, "%s: workspace must be 16-byte aligned", fn);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* ap = static_cast<uint32_t*>(workspace);
+  if (int st = cuda_status(bs::launch_bitpack(a, ap, m, k, row_words(k), a_bits, s), fn)) return st;
+  ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
+  bs::ConvProblem p = make_conv(ap, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, s), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, const int8_t* w_tc, int w_bits,
+                                     int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+                                     int stride_h, int stride_w, int pad_h, int pad_w, uint8_t* act_dev,
+                                     int32_t* out_dev, void* workspace, int64_t workspace_bytes, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tc_host";
+  if (!act_host || !out_host || !act_dev || !out_dev) return fail(BS_ERR_NULL, "%s: NULL buffer pointer", fn);
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t in_bytes = size_t(n) * h * w * c;
+  const size_t out_bytes = size_t(n) * conv_out(h, kh, stride_h, pad_h) * conv_out(w, kw, stride_w, pad_w) * oc * 4;
+  if (int st = cuda_status(cudaMemcpyAsync(act_dev, act_host, in_bytes, cudaMemcpyHostToDevice, s), fn)) return st;
+  if (int st = bs_bitserial_conv2d_nhwc_tc_i8(act_dev, a_bits, w_tc, w_bits, out_dev, n, h, w, c, oc, kh, kw,
+                                              stride_h, stride_w, pad_h, pad_w, workspace, workspace_bytes, stream))
+    return st;
+  if (int st = cuda_status(cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, s), fn)) return st;
+  return cuda_status(cudaStreamSynchronize(s), fn);
+}
+
 int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits, const uint32_t* w_packed, int w_bits,
                                   int w_enc, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
                                   int stride_h, int stride_w, int pad_h, int pad_w, uint8_t* act_dev,

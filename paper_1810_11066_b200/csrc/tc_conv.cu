@@ -3,27 +3,45 @@
 // Eq. 2: out = sum_{i<A} sum_{j<W} 2^(i+j) * popcount(a_i AND w_j).
 // For 0/1 vectors popcount(a_i AND w_j) = sum_k a_i[k] * w_j[k] (Eq. 1),
 // a dense contraction, so every plane pair (i, j) is one binary dot product that the
-// tensor core can evaluate exactly in int8 x int8 -> int32:
+// tensor core evaluates exactly in int8 x int8 -> int32:
 //   * activation plane i is expanded from its packed uint32 words into bytes 2^i * a_i
 //     (u8) inside shared memory — operands stay bit-packed in HBM (A/8 bytes per
 //     element, the point of bit-packing);
-//   * weight plane j is expanded once per call into bytes 2^j * b_j (unipolar) or
-//     2^j * (2 b_j - 1) (bipolar: each weight bit-plane a +/-1 digit, reading R2);
-//   * the A*W plane-pair products are accumulated into one TMEM int32 accumulator with
+//   * weight plane j is expanded once, ahead of time like the weight packing itself
+//     (PAPER.md:715), into bytes 2^j * b_j (unipolar) or 2^j * (2 b_j - 1) (bipolar:
+//     each weight bit-plane a +/-1 digit, reading R2);
+//   * the A*W plane-pair products accumulate into one TMEM int32 accumulator with
 //     tcgen05.mma.kind::i8 (bipolar needs no correction term in this form).
-// The cost still grows with A*W (one MMA per plane pair), so this is the
+// The cost still grows with A*W (one MMA per plane pair): this is the
 // bitserial method with its binary dot products on the tensor cores instead of the
 // integer pipes.
 //
-// Structure (one CTA = 128 output rows x BN output channels, 128 threads):
-//   per K-chunk of 128 reduction elements (4 packed words per plane per row):
-//     - all threads: B tile (expanded weights) -> swizzled smem with 16-byte cp.async,
-//       A rows gathered (implicit im2col, zero padding) from the packed activations and
-//       expanded to bytes straight into the 128B-swizzled K-major smem layout;
-//     - fence.proxy.async + barrier; one thread issues A*W*4 tcgen05.mma (K = 32 each)
-//       and commits them to the stage's mbarrier, releasing the buffers;
-//   epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes 32w..32w+31 = rows), int32 store.
+// Kernel structure (persistent, warp-specialized, one CTA per SM, (4T + 6) warps):
+//   warps 0..4T-1  expansion producers: T teams (T = 4) of 4 warps, one thread per output
+//               row; team t expands the chunks g = t, t+T, ... of the CTA's (tile, K chunk)
+//               sequence (T chunks in flight hide the per-chunk latency chain).  Implicit
+//               im2col gather of the packed words with zero padding
+//               through a thread-private cp.async ring; expansion to bytes in registers;
+//               tcgen05.st straight into the stage's A operand in TENSOR memory (lane =
+//               output row, 4 bytes per column); one arrive per warp on full_a.
+//   warps 4T..4T+3 epilogue: TMEM (double-buffered accumulators, 2*BN columns) ->
+//               tcgen05.ld 32x32b.x32 -> swizzled smem -> TMA store of 32x32 int32
+//               boxes (clipped at ragged M / OC), overlapping the next tile's main loop.
+//   warp 4T+4   TMA producer: expanded weight tile [W planes][BN rows][128 B] per stage
+//               (cp.async.bulk.tensor, SWIZZLE_128B) onto full_b — or, when all of OC fits
+//               one tile and all of K fits shared memory, the whole B once (resident).
+//   warp 4T+5   MMA issuer: the whole warp walks the loop (warp-uniform operands), one
+//               elected lane issues A*W*4 tcgen05.mma.kind::i8 (A from TMEM, B from smem,
+//               K = 32 bytes each) per stage; tcgen05.commit frees the stage; the last
+//               chunk of a tile commits to acc_full.
+// Measured design points (profiles/r01d_*): the MMA warp's instruction count per MMA
+// matters because it shares an SM sub-partition with ALU-bound producers; the producers
+// are latency-bound (4 teams beat 2); the TMA-store epilogue beats direct stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -31,15 +49,43 @@
 namespace bs {
 namespace tc {
 
-constexpr int kThreads = 256;  // 8 warps: two threads per A row; warps w and w+4 share TMEM lanes
-constexpr int BM = 128;          // UMMA M (cta_group::1)
-constexpr int BKB = 128;         // K bytes per stage = one 128B swizzle row
+constexpr int BM = 128;                   // UMMA M (cta_group::1): output rows per tile
+constexpr int BKB = 128;                  // K bytes per stage = one 128B swizzle row
 constexpr int kWordsPerStage = BKB / 32;  // 4 packed words per plane per row
+#ifndef BS_TC_TEAMS
+#define BS_TC_TEAMS 4
+#endif
+constexpr int kTeams = BS_TC_TEAMS;                    // producer teams (K chunks in flight)
+constexpr int kProducerWarps = 4 * kTeams;             // a team = 4 warps = one thread per row
+constexpr int kProducerThreads = kProducerWarps * 32;
+constexpr int kEpiWarp0 = kProducerWarps;              // 4 epilogue warps (warp % 4 = lane quarter)
 
+constexpr int kTmaWarp = kProducerWarps + 4;
+constexpr int kMmaWarp = kProducerWarps + 5;
+constexpr int kThreads = (kProducerWarps + 6) * 32;
+constexpr int kEpiBufBytes = 32 * 128;  // one 32 x 32 int32 box
+constexpr int kEpiBufs = 2;             // per epilogue warp
+constexpr int kEpiBytes = 4 * kEpiBufs * kEpiBufBytes;
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kMinSmem = 116 * 1024;  // > half the SM: guarantees one CTA per SM (TMEM)
+
+// BS_TC_PROFILE builds (tools only) count cycles spent in each role's waits and print
+// them per CTA 0 at exit; the product build compiles these to nothing.
+#ifdef BS_TC_PROFILE
+#define PROF_DECL long long _pt = 0, _pacc[4] = {0, 0, 0, 0};
+#define PROF_BEGIN _pt = clock64();
+#define PROF_END(i) _pacc[i] += clock64() - _pt;
+#else
+#define PROF_DECL
+#define PROF_BEGIN
+#define PROF_END(i)
+#endif
+
+// ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
 }
-__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t phase) {
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -47,11 +93,38 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t phase) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(addr),
-      "r"(phase));
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // 128B-swizzled K-major UMMA shared-memory descriptor (SM100 layout, version 1):
 // start address >> 4, LBO (unused for swizzled K-major) = 1, SBO = 1024 B (8 rows x
@@ -85,34 +158,125 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// A operand from tensor memory (lane = row, 4 int8 per 32-bit column), B from smem.
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// The 4 K-steps (32 bytes each) of one plane pair in one 128-byte K chunk, issued by one
+// elected lane of the (converged) MMA warp: A columns +8 per step, B descriptor start
+// +32 bytes (+2 encoded) per step.  Keeping the whole warp on the issue path makes every
+// operand warp-uniform (uniform registers, no per-MMA R2UR / waterfall) — the MMA warp
+// shares its SM sub-partition with ALU-bound producer warps, so its instruction count
+// per MMA sets the tensor-core feed rate.
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
+      "elect.sync x|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n"
+      "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "}" ::"r"(d),
+      "r"(a), "l"(b), "r"(accumulate), "n"(IDESC));
+}
+
+// tcgen05.commit from the elected lane (the lane that issued the MMAs).
+__device__ __forceinline__ void mma_commit_elect(uint32_t mbar) {
+  asm volatile(
+      "{.reg .pred e; .reg .b32 x; elect.sync x|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];}" ::"r"(mbar)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
 }
 
-// Spread the 4 bits of a nibble (already isolated in the low bits of n) into bytes:
-// n * (0x00204081 << i) puts bit r at 8r + i (other partial products elsewhere) and the
-// mask keeps exactly those: byte r = 2^i * bit r.
-template <int I>
-__device__ __forceinline__ uint32_t spread4(uint32_t n) {
-  return (n * (0x00204081u << I)) & (0x01010101u << I);
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// 32 activation bits of one plane word -> 8 words of bytes (element 4q + r in byte r
-// of word q), value 2^I * bit.  The 8 nibbles are isolated with two masks and a
-// byte permute each (PRMT) instead of a shift + mask per nibble.
+// K order inside a packed word.  The tensor core only needs activations and weights
+// in the SAME order along K, and each 32-byte MMA K-step covers exactly one packed
+// word (32 elements), so within every word the elements are laid out transposed:
+// byte position 4q + r (expanded word q, byte r) holds element 8r + q.  Expanded word
+// q is then bit q of every byte of the packed word, so one shift and one AND make it.
+// 32 activation bits of one plane word -> 8 words of bytes 2^I * bit; the shifts are
+// multiplications (IMAD / IMAD.HI on the FMA pipe) so the ALU pipe only does the ANDs.
 template <int I>
 __device__ __forceinline__ void expand_word(uint32_t w, uint32_t (&o)[8]) {
-  const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+  constexpr uint32_t M = 0x01010101u << I;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    o[2 * b] = spread4<I>(__byte_perm(lo, 0u, 0x4440u + b));
-    o[2 * b + 1] = spread4<I>(__byte_perm(hi, 0u, 0x4440u + b));
+  for (int q = 0; q < 8; ++q) {
+    uint32_t t;
+    if (q == I)
+      t = w;
+    else if (q < I)
+      t = w * (1u << (I - q));  // bit 8r+q -> 8r+I
+    else
+      t = __umulhi(w, 1u << (32 - (q - I)));  // w >> (q - I)
+    o[q] = t & M;
   }
 }
 
+// 32 consecutive 32-bit TMEM columns of this thread's lane <- o[0..31].
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&o)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]), "r"(o[9]),
+      "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15]), "r"(o[16]), "r"(o[17]), "r"(o[18]),
+      "r"(o[19]), "r"(o[20]), "r"(o[21]), "r"(o[22]), "r"(o[23]), "r"(o[24]), "r"(o[25]), "r"(o[26]), "r"(o[27]),
+      "r"(o[28]), "r"(o[29]), "r"(o[30]), "r"(o[31])
+      : "memory");
+}
+
+// One plane's four packed words of this thread (one 128-element K chunk) -> bytes
+// 2^I * bit -> the 32 TMEM columns of the thread's lane for that plane.
+template <int I>
+__device__ __forceinline__ void expand_to_tmem(uint32_t taddr, uint4 v) {
+  uint32_t o[32];
+  uint32_t t[8];
+  expand_word<I>(v.x, t);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = t[q];
+  expand_word<I>(v.y, t);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[8 + q] = t[q];
+  expand_word<I>(v.z, t);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[16 + q] = t[q];
+  expand_word<I>(v.w, t);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[24 + q] = t[q];
+  tmem_st32(taddr, o);
+}
+
 // ------------------------------------------------------------------ weight expansion
-// w_packed [W][N][kp] words -> wexp [W][n_pad][kpad*32] bytes (kpad = kp rounded up to
-// 4 words; bytes past kp*32 are 0).  Plane j byte = 2^j b (unipolar) or 2^j (2b - 1)
+// w_packed [W][N][kp] words -> wexp [W][N][kpad*32] bytes (kpad = kp rounded up to
+// 4 words; bytes past kp*32 are 0), each 32-byte group in the transposed K order of
+// expand_word.  Plane j byte = 2^j b (unipolar) or 2^j (2b - 1)
 // (bipolar); zero padding of the activations makes the value of pad bytes irrelevant.
 __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __restrict__ w_packed,
                                                              int8_t* __restrict__ wexp, int w_bits, int n,
@@ -125,13 +289,11 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
     const int32_t mag = 1 << j;
     uint32_t out[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t n4 = (w >> (4 * q)) & 0xFu;
-      const uint32_t bits = (n4 * 0x00204081u) & 0x01010101u;  // 0/1 per byte
+    for (int q = 0; q < 8; ++q) {  // byte r of expanded word q = element 8r + q (see expand_word)
       uint32_t v = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int b = (bits >> (8 * r)) & 1;
+        const int b = (w >> (8 * r + q)) & 1;
         const int32_t val = bipolar ? (b ? mag : -mag) : (b ? mag : 0);
         v |= (uint32_t(val) & 0xFFu) << (8 * r);
       }
@@ -144,274 +306,549 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
 }
 
 // ----------------------------------------------------------------------- main kernel
-template <int A_BITS, int W_BITS, int BN, int STAGES>
-struct TcSmem {  // 1024 B of alignment slack + mbarriers / TMEM slot
-  static constexpr int kABytes = A_BITS * BM * BKB;   // per stage
-  static constexpr int kBBytes = W_BITS * BN * BKB;   // per stage
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+template <int A_BITS, int W_BITS, int BN>
+struct Cfg {
+  static constexpr int kRawDepth = A_BITS <= 2 ? 3 : 2;
+  static constexpr int kACols = A_BITS * (BKB / 4);  // TMEM columns of one stage's A planes
+  static constexpr int kBBytes = W_BITS * BN * BKB;  // shared memory per stage (B only)
+  static constexpr int kRawBytes = kRawDepth * A_BITS * kProducerThreads * 16;
+  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + kEpiBytes + kRawBytes;
+  static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
+  static constexpr int kFitTmem = (512 - 2 * BN) / kACols;  // accumulators: 2 x BN columns
+  static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
+  // Every stage must always be filled by the same producer team: mbarrier waits are by
+  // phase parity, and a team that could reach a stage two phases ahead of another team
+  // would pass the wait early.  So the stage count is a multiple of the teams in use.
+  static constexpr int kTeamsUsed = kFit < kTeams ? kFit : kTeams;
+  static constexpr int kStagesRaw = kFit > 6 ? 6 : kFit;
+  static constexpr int kStages = kTeamsUsed > 0 ? (kStagesRaw / kTeamsUsed) * kTeamsUsed : 0;
+  static constexpr int kUsed = kFixed + kStages * kBBytes;
+  static constexpr int kBytes = kUsed < kMinSmem ? kMinSmem : kUsed;
+  static constexpr int kTmemCols = 512;  // 2*BN accumulator columns + the A ring; one CTA per SM
+  static constexpr int kAcol0 = 2 * BN;  // first A-ring column
 };
 
-template <int A_BITS, int W_BITS, int BN, int STAGES, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) tc_conv_kernel(const ConvProblem p, const int8_t* __restrict__ wexp,
-                                                              const int64_t kpad) {
-  using S = TcSmem<A_BITS, W_BITS, BN, STAGES>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  static_assert(MINB >= 1, "");
-  // 1024-byte aligned tile region (SWIZZLE_128B atoms), barriers after the tiles
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStageBytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES + 1);
+enum EpiMode : int { kEpiDirect = 0, kEpiTma = 1, kEpiScalar = 2 };
 
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t m0 = int64_t(blockIdx.x) * BM;
-  const int n0 = blockIdx.y * BN;
-  const int kp = int(p.kp);
-  const int nchunks = int(kpad / kWordsPerStage);
+struct TcArgs {
+  ConvProblem p;
+  int ntiles, ntn;  // tiles, N-tiles per M block
+  int nchunks;      // K chunks (of 4 words) per tile
+  int epi;          // EpiMode: direct 16-byte stores (OC % 4 == 0), TMA stores, or scalar
+  int b_resident;   // ntn == 1 and the whole expanded B fits: loaded once, kept in smem
+  int b_bytes;      // bytes of the B region (resident: nchunks stages, else kStages)
+  int debug;        // BS_TC_PROFILE builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
+                    // 2 skip accumulator tcgen05.ld (timing experiments; results are wrong)
+};
+#ifdef BS_TC_PROFILE
+#define DBG(bit) (args.debug & (1 << (bit)))
+#else
+#define DBG(bit) 0
+#endif
+
+template <int A_BITS, int W_BITS, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_conv_kernel(const TcArgs args, const __grid_constant__ CUtensorMap tmap_w,
+                   const __grid_constant__ CUtensorMap tmap_out) {
+  using C = Cfg<A_BITS, W_BITS, BN>;
+  constexpr int S = C::kStages;
+  static_assert(S >= 2, "tensor-core tile does not fit two stages of shared memory");
+  static_assert(C::kBytes <= kSmemLimit, "shared memory");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* s_stage = smem;                            // B: S ring stages, or nchunks resident
+  uint8_t* s_epi = smem + args.b_bytes;               // 4 warps x 2 x 4 KB (1024-aligned)
+  uint8_t* s_rawb = s_epi + kEpiBytes;                // producer raw ring
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_rawb + C::kRawBytes);
+  uint64_t* full_a = bars;
+  uint64_t* full_b = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* acc_full = bars + 3 * S;
+  uint64_t* acc_empty = bars + 3 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+  const ConvProblem& p = args.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  PROF_DECL
+#ifdef BS_TC_PROFILE
+  const long long _t_start = clock64();
+#endif
+  const int ntiles = args.ntiles, ntn = args.ntn, nchunks = args.nchunks;
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(mbar + s), 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(full_a + s), 4);  // the 4 warps of one team
+      mbar_init(smem_u32(full_b + s), 1);
+      mbar_init(smem_u32(empty + s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(acc_full + a), 1);
+      mbar_init(smem_u32(acc_empty + a), 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {  // TMEM: BN int32 columns x 128 lanes
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN < 32 ? 32 : BN));
+                 "r"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (warp == kTmaWarp && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_out)) : "memory");
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // all 512 columns belong to this CTA (one CTA per SM): the allocation starts at lane 0,
+  // column 0, so TMEM addresses are compile-time constants
+  if (*tmem_slot != 0u) asm volatile("trap;");
+  constexpr uint32_t tmem = 0;
 
-  // ---- this thread's A row (output pixel), its receptive-field origin, and which
-  // half of the 128-byte K chunk it expands (packed words 2*half, 2*half+1)
-  const int arow = tid & (BM - 1), half = tid >> 7;
-  const int64_t m = m0 + arow;
-  const bool row_ok = m < p.M;
-  int iy0 = 0, ix0 = 0;
-  int64_t img_base = 0;
-  {
-    const int64_t mm = row_ok ? m : 0;
+  if (warp < 4 * C::kTeamsUsed) {
+    // ================= expansion producers.  kTeams teams of 4 warps; team t expands the
+    // chunks g = t, t+kTeams, ... of this CTA's (tile, K chunk) sequence, so kTeams chunks
+    // are in flight.  Within a team, thread `arow` (warp % 4 == its TMEM lane quarter)
+    // owns output row arow and all 4 packed words of each plane of the chunk.
+    constexpr int kTeams = C::kTeamsUsed;
+    const int team = warp >> 2, arow = tid & (BM - 1);
+    const int kp = int(p.kp);
     const int64_t hw = int64_t(p.oh) * p.ow;
-    const int64_t b = mm / hw, rem = mm - b * hw;
-    const int oy = int(rem / p.ow), ox = int(rem - int64_t(oy) * p.ow);
-    iy0 = oy * p.sh - p.ph;
-    ix0 = ox * p.sw - p.pw;
-    img_base = b * int64_t(p.h) * p.w;
-  }
-  const uint32_t sw = uint32_t(arow & 7);  // 128B swizzle phase of this row
-
-  // 8-byte piece (2 packed words per plane) this thread gathers for K chunk kc; the
-  // piece lies inside one tap because Cw is even (implicit im2col, zero padding)
-  auto gather = [&](int kc, uint2 (&v)[A_BITS]) {
-    const int kk = kc * kWordsPerStage + 2 * half;
-    const int tap = kk / p.kw_a;
-    const int cw = kk - tap * p.kw_a;
-    const int ky = tap / p.kwid, kx = tap - ky * p.kwid;
-    const int iy = iy0 + ky, ix = ix0 + kx;
-    const bool ok = row_ok && kk < kp && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
-    const uint32_t* src = p.act + (img_base + int64_t(iy) * p.w + ix) * p.kw_a + cw;
+    const bool split = (p.kw_a & 3) != 0;  // a 4-word group spans two taps (Cw = 2 mod 4)
+    struct Geo {
+      bool ok;
+      int iy0, ix0;
+      int64_t base;
+    };
+    auto geo = [&](int tile) {
+      Geo g;
+      const int64_t m = int64_t(tile / ntn) * BM + arow;
+      g.ok = m < p.M;
+      const int64_t mm = g.ok ? m : 0;
+      const int64_t b = mm / hw, rem = mm - b * hw;
+      const int oy = int(rem / p.ow), ox = int(rem - int64_t(oy) * p.ow);
+      g.iy0 = oy * p.sh - p.ph;
+      g.ix0 = ox * p.sw - p.pw;
+      g.base = b * int64_t(p.h) * p.w;
+      return g;
+    };
+    // fetch iterator (runs kRawDepth-1 of this team's chunks ahead of the expansion);
+    // the filter word index kk = 4*kc is tracked as (tap ky, kx; word cw) incrementally.
+    int f_tile = blockIdx.x, f_kc = team, f_kk = 0, f_cw = 0, f_kx = 0, f_ky = 0;
+    auto norm = [&]() {
+      while (f_cw >= p.kw_a) {
+        f_cw -= p.kw_a;
+        if (++f_kx == p.kwid) {
+          f_kx = 0;
+          ++f_ky;
+        }
+      }
+    };
+    auto seek = [&]() {  // normalise (f_tile, f_kc) and restart the tap walk at kk = 4*kc
+      while (f_kc >= nchunks) {
+        f_kc -= nchunks;
+        f_tile += gridDim.x;
+      }
+      f_kk = f_kc * kWordsPerStage;
+      f_cw = f_kk;
+      f_kx = f_ky = 0;
+      norm();
+    };
+    seek();
+    Geo fg = geo(f_tile < ntiles ? f_tile : 0);
+    const uint32_t raw_base = smem_u32(s_rawb) + uint32_t(tid) * 16u;
+    constexpr uint32_t kRawPlane = kProducerThreads * 16;
+    auto fetch = [&](int slot) {
+      if (f_tile < ntiles) {
+        const uint32_t dst = raw_base + uint32_t(slot * A_BITS) * kRawPlane;
+        const int iy = fg.iy0 + f_ky, ix = fg.ix0 + f_kx;
+        const bool ok = fg.ok && f_kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
+        const uint32_t* src = ok ? p.act + (fg.base + int64_t(iy) * p.w + ix) * p.kw_a + f_cw : p.act;
+        if (!split) {
 #pragma unroll
-    for (int i = 0; i < A_BITS; ++i) {
-      v[i] = make_uint2(0u, 0u);
-      if (ok) v[i] = __ldg(reinterpret_cast<const uint2*>(src + i * p.act_plane));
-    }
-  };
-
-  constexpr uint32_t kIdesc = idesc_i8<BN>();
-  uint32_t phase_bits = 0;  // bit s = parity to wait for on stage s
-  uint2 wa[A_BITS];
-  gather(0, wa);
-
-  for (int kc = 0; kc < nchunks; ++kc) {
-    const int s = kc % STAGES;
-    uint8_t* sA = smem + s * S::kStageBytes;
-    uint8_t* sB = sA + S::kABytes;
-    if (kc >= STAGES) {  // wait until the MMAs that read this stage have completed
-      mbar_wait(smem_u32(mbar + s), (phase_bits >> s) & 1u);
-      phase_bits ^= 1u << s;
-    }
-    // B: expanded weight rows n0..n0+BN, bytes [kc*128, kc*128+128) per plane
-    {
-      constexpr int kChunks = W_BITS * BN * (BKB / 16);
-#pragma unroll 4
-      for (int c = tid; c < kChunks; c += kThreads) {
-        const int j = c / (BN * 8), rem = c - j * (BN * 8);
-        const int r = rem >> 3, ch = rem & 7;
-        const int n = n0 + r;
-        const bool ok = n < p.oc;
-        const int8_t* src = ok ? wexp + (int64_t(j) * p.oc + n) * (kpad * 32) + int64_t(kc) * BKB + ch * 16 : wexp;
-        const uint32_t dst = smem_u32(sB + j * (BN * BKB) + r * BKB + ((ch ^ (r & 7)) << 4));
-        cp_async16(dst, src, ok);
+          for (int i = 0; i < A_BITS; ++i) cp_async16(dst + i * kRawPlane, src + i * p.act_plane, ok);
+        } else {  // Cw = 2 mod 4: two 8-byte pieces (words 0-1, words 2-3 of the group)
+#pragma unroll
+          for (int i = 0; i < A_BITS; ++i) cp_async8(dst + i * kRawPlane, src + i * p.act_plane, ok);
+          const uint32_t* src2;
+          bool ok2;
+          if (f_cw + 2 < p.kw_a) {  // same tap
+            ok2 = ok && f_kk + 2 < kp;
+            src2 = src + 2;
+          } else {  // words 2-3 are word 0-1 of the next tap
+            int kx2 = f_kx + 1, ky2 = f_ky;
+            if (kx2 == p.kwid) {
+              kx2 = 0;
+              ++ky2;
+            }
+            const int iy2 = fg.iy0 + ky2, ix2 = fg.ix0 + kx2;
+            ok2 = fg.ok && f_kk + 2 < kp && unsigned(iy2) < unsigned(p.h) && unsigned(ix2) < unsigned(p.w);
+            src2 = ok2 ? p.act + (fg.base + int64_t(iy2) * p.w + ix2) * p.kw_a : p.act;
+          }
+#pragma unroll
+          for (int i = 0; i < A_BITS; ++i) cp_async8(dst + i * kRawPlane + 8, src2 + i * p.act_plane, ok2);
+        }
+        f_kc += kTeams;
+        if (f_kc >= nchunks) {
+          const int old_tile = f_tile;
+          seek();
+          if (f_tile != old_tile && f_tile < ntiles) fg = geo(f_tile);
+        } else {
+          f_kk += kTeams * kWordsPerStage;
+          f_cw += kTeams * kWordsPerStage;
+          norm();
+        }
       }
       cp_async_commit();
-    }
-    // A: prefetch the next chunk's words, then expand this chunk's into swizzled smem
-    uint2 wn[A_BITS];
-    if (kc + 1 < nchunks) gather(kc + 1, wn);
+    };
 #pragma unroll
-    for (int i = 0; i < A_BITS; ++i) {
-      uint8_t* rowp = sA + i * (BM * BKB) + (arow >> 3) * 1024 + (arow & 7) * 128;
+    for (int d = 0; d < C::kRawDepth - 1; ++d) fetch(d);
+    int slot = 0;
+    int g = team;  // this team's position in the CTA's chunk sequence
+    const int my_tiles = ntiles > int(blockIdx.x) ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+    const int total = my_tiles * nchunks;
+    const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
+    for (; g < total; g += kTeams) {
+      fetch(slot == 0 ? C::kRawDepth - 1 : slot - 1);
+      PROF_BEGIN
+      cp_async_wait<C::kRawDepth - 1>();
+      PROF_END(0)
+      uint4 v[A_BITS];
 #pragma unroll
-      for (int wsel = 0; wsel < 2; ++wsel) {
-        const uint32_t w = wsel ? wa[i].y : wa[i].x;
-        uint32_t o[8];
-        switch (i) {  // compile-time after unrolling
-          case 0: expand_word<0>(w, o); break;
-          case 1: expand_word<1>(w, o); break;
-          case 2: expand_word<2>(w, o); break;
-          default: expand_word<3>(w, o); break;
-        }
-        const uint32_t ch0 = uint32_t(4 * half + 2 * wsel);  // 16-byte chunks of this word
-        *reinterpret_cast<uint4*>(rowp + ((ch0 ^ sw) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
-        *reinterpret_cast<uint4*>(rowp + (((ch0 + 1) ^ sw) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < A_BITS; ++i) wa[i] = wn[i];
-    cp_async_wait<0>();
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
+      for (int i = 0; i < A_BITS; ++i) v[i] = lds128(raw_base + uint32_t(slot * A_BITS + i) * kRawPlane);
+      if (++slot == C::kRawDepth) slot = 0;
+      const int stage = g % S;
+      PROF_BEGIN
+      mbar_wait(smem_u32(empty + stage), ((g / S) & 1) ^ 1u);
+      PROF_END(1)
       tc_fence_after();
-      const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+      const uint32_t ta = lane_base + uint32_t(C::kAcol0 + stage * C::kACols);
+      if (DBG(1)) {
+        uint32_t x = 0;
 #pragma unroll
-      for (int i = 0; i < A_BITS; ++i)
+        for (int i = 0; i < A_BITS; ++i) x ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
+        if (x == 0x9e3779b9u) asm volatile("trap;");
+      } else {
+      expand_to_tmem<0>(ta, v[0]);
+      if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
+      if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2]);
+      if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(full_a + stage));
+    }
+    cp_async_wait<0>();
+  } else if (warp < kProducerWarps) {
+    // producer warps of teams this configuration does not use: idle
+  } else if (warp == kTmaWarp) {
+    // ================= weight tiles by TMA
+    if (lane == 0 && args.b_resident) {  // whole B once (one N block): every K chunk, W planes
+      const uint32_t fb = smem_u32(full_b);
+      mbar_expect_tx(fb, uint32_t(C::kBBytes) * uint32_t(nchunks));
+      for (int kc = 0; kc < nchunks; ++kc) {
+        const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
 #pragma unroll
-        for (int j = 0; j < W_BITS; ++j)
+        for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * BKB, &tmap_w, kc * BKB, j * p.oc, fb);
+      }
+    } else if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int n0 = (tile % ntn) * BN;
+        for (int kc = 0; kc < nchunks; ++kc) {
+          PROF_BEGIN
+          mbar_wait(smem_u32(empty + stage), phase ^ 1u);
+          PROF_END(0)
+          const uint32_t fb = smem_u32(full_b + stage);
+          mbar_expect_tx(fb, uint32_t(C::kBBytes));
+          const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
 #pragma unroll
-          for (int k = 0; k < BKB / 32; ++k) {
-            const uint64_t ad = smem_desc_sw128(a_base + i * (BM * BKB) + k * 32);
-            const uint64_t bd = smem_desc_sw128(b_base + j * (BN * BKB) + k * 32);
-            mma_i8(tmem, ad, bd, kIdesc, (kc | i | j | k) != 0);
+          for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * BKB, &tmap_w, kc * BKB, j * p.oc + n0, fb);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
           }
-      mma_commit(smem_u32(mbar + s));
+        }
+      }
     }
+  } else if (warp == kMmaWarp) {
+    // ================= MMA issuer: the whole warp walks the loop (uniform values); one
+    // elected lane issues.  TMEM base is column 0 (all 512 columns are this CTA's).
+    constexpr uint32_t kIdesc = idesc_i8<BN>();
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    const bool resident = args.b_resident;
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(s_stage));
+    if (resident) mbar_wait(smem_u32(full_b), 0);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      PROF_BEGIN
+      mbar_wait(smem_u32(acc_empty + acc), acc_phase ^ 1u);
+      PROF_END(0)
+      tc_fence_after();
+      const uint32_t tacc = uint32_t(acc * BN);
+      for (int kc = 0; kc < nchunks; ++kc) {
+        PROF_BEGIN
+        mbar_wait(smem_u32(full_a + stage), phase);
+        PROF_END(1)
+        PROF_BEGIN
+        if (!resident) mbar_wait(smem_u32(full_b + stage), phase);
+        PROF_END(2)
+        tc_fence_after();
+        const uint32_t a_base = uint32_t(C::kAcol0 + stage * C::kACols);
+        const uint64_t b_desc = bdesc0 + uint64_t(((resident ? kc : stage) * C::kBBytes) >> 4);
+#pragma unroll
+        for (int i = 0; i < A_BITS; ++i)
+#pragma unroll
+          for (int j = 0; j < W_BITS; ++j)
+            mma4_ts<kIdesc>(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4),
+                            (kc | i | j) != 0);
+        mma_commit_elect(smem_u32(empty + stage));
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+      mma_commit_elect(smem_u32(acc_full + acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  } else {
+    // ================= epilogue: warp q = warp % 4 owns TMEM lanes / tile rows 32q..32q+31
+    const int q = warp & 3;
+    uint8_t* ebuf = s_epi + q * (kEpiBufs * kEpiBufBytes);
+    int acc = 0, buf = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t m0 = int64_t(tile / ntn) * BM;
+      const int n0 = (tile % ntn) * BN;
+      const int ncb = min(BN, p.oc - n0 + 31) / 32;  // 32-column blocks holding valid columns
+      PROF_BEGIN
+      mbar_wait(smem_u32(acc_full + acc), acc_phase);
+      PROF_END(0)
+      tc_fence_after();
+      for (int cb = 0; cb < ncb; ++cb) {
+        uint32_t r[32];
+        if (DBG(2)) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) r[c] = c;
+        } else {
+          tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + cb * 32), r);
+        }
+        if (cb == ncb - 1) {  // accumulator drained: release it to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(acc_empty + acc));
+        }
+        const int64_t row = m0 + q * 32 + lane;
+        if (DBG(0)) {
+          if (r[0] == 0x9e3779b9u) asm volatile("trap;");
+        } else if (args.epi == kEpiDirect) {  // this lane's row segment: 128 contiguous bytes, 8 x 16-byte stores
+          if (row < p.M && n0 + cb * 32 + 32 <= p.oc) {
+            uint4* dst = reinterpret_cast<uint4*>(p.out + row * p.oc + n0 + cb * 32);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) dst[c] = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+          } else if (row < p.M) {
+            int32_t* dst = p.out + row * p.oc;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const int col = n0 + cb * 32 + c;
+              if (col < p.oc) dst[col] = int32_t(r[c]);
+            }
+          }
+        } else if (args.epi == kEpiTma) {
+          if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // the store that last used `buf` has read it
+          __syncwarp();
+          uint8_t* sb = ebuf + buf * kEpiBufBytes + lane * 128;
+          const uint32_t swz = uint32_t(lane & 7);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(sb + ((uint32_t(c) ^ swz) << 4)) =
+                make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_out, n0 + cb * 32, int(m0) + q * 32, smem_u32(ebuf + buf * kEpiBufBytes));
+            bulk_commit();
+          }
+          buf ^= 1;
+        } else {  // OC % 4 != 0: plain bounded stores
+          if (row < p.M) {
+            int32_t* dst = p.out + row * p.oc;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const int col = n0 + cb * 32 + c;
+              if (col < p.oc) dst[col] = int32_t(r[c]);
+            }
+          }
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+    if (lane == 0) bulk_wait_all();
   }
-  // wait for the last commit (covers all earlier MMAs)
-  {
-    const int s = (nchunks - 1) % STAGES;
-    mbar_wait(smem_u32(mbar + s), (phase_bits >> s) & 1u);
-  }
-  tc_fence_after();
 
-  // ---- epilogue, 64 columns at a time: warp w loads TMEM lanes 32*(w%4).. (rows) x 32
-  // columns (half w/4 of the block) into a padded smem tile (ring buffers are free now),
-  // then all threads write the 128 x 64 int32 block with coalesced 16-byte stores (each
-  // output row segment is contiguous in NHWC / row-major memory).
-  constexpr int kCB = 64, kLd = kCB + 4;  // +4 words: conflict-free 16-byte smem rows
-  uint32_t* stile = reinterpret_cast<uint32_t*>(smem);
-  const int quarter = warp & 3, colhalf = warp >> 2;
-  const int trow = quarter * 32 + (tid & 31);
-#pragma unroll 1
-  for (int cb = 0; cb < BN; cb += kCB) {
-    uint32_t r[32];
-    const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(cb + colhalf * 32);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    uint32_t* srow = stile + trow * kLd + colhalf * 32;
-#pragma unroll
-    for (int v = 0; v < 8; ++v)
-      *reinterpret_cast<uint4*>(srow + 4 * v) = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-    __syncthreads();
-    const int ncols = min(kCB, p.oc - (n0 + cb));  // valid columns of this block
-    if ((p.oc & 3) == 0 && ncols == kCB) {
-#pragma unroll
-      for (int c = tid; c < BM * (kCB / 4); c += kThreads) {
-        const int rr = c / (kCB / 4), c4 = c - rr * (kCB / 4);
-        const int64_t grow = m0 + rr;
-        if (grow < p.M)
-          *reinterpret_cast<uint4*>(p.out + grow * p.oc + n0 + cb + 4 * c4) =
-              *reinterpret_cast<const uint4*>(stile + rr * kLd + 4 * c4);
-      }
-    } else if (ncols > 0) {
-      for (int c = tid; c < BM * kCB; c += kThreads) {
-        const int rr = c / kCB, cc = c - rr * kCB;
-        const int64_t grow = m0 + rr;
-        if (grow < p.M && cc < ncols) p.out[grow * p.oc + n0 + cb + cc] = int32_t(stile[rr * kLd + cc]);
-      }
-    }
-    __syncthreads();
-  }
+#ifdef BS_TC_PROFILE
+  if (blockIdx.x == 0 && lane == 0)
+    printf("TCPROF warp %d total %lld w0 %lld w1 %lld w2 %lld\n", warp, clock64() - _t_start, _pacc[0], _pacc[1],
+           _pacc[2]);
+#endif
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN < 32 ? 32 : BN));
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
   }
 }
 
-// Stages: as many as fit while two CTAs (16 warps) still share an SM — a second CTA
-// overlaps one tile's prologue / epilogue with another's main loop — else as many as fit
-// one CTA (at least 2).
+// ------------------------------------------------------------------------ host side
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library does not
+// link libcuda, so it still loads on hosts without a driver).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int A_BITS, int W_BITS, int BN>
 cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
-  constexpr int kStageBytes = TcSmem<A_BITS, W_BITS, BN, 1>::kStageBytes;
-  constexpr int kPerCta2 = (227 * 1024) / 2 - 2304;
-  constexpr int kStages2 = kPerCta2 / kStageBytes;
-  constexpr bool kTwo = kStages2 >= 2;
-  constexpr int kStages1 = ((227 * 1024) - 2304) / kStageBytes;
-  constexpr int STAGES = kTwo ? (kStages2 > 4 ? 4 : kStages2) : (kStages1 > 4 ? 4 : kStages1);
-  static_assert(STAGES >= 2, "tensor-core tile does not fit two stages of shared memory");
-  using S = TcSmem<A_BITS, W_BITS, BN, STAGES>;
-  static_assert(S::kBytes <= 227 * 1024, "tensor-core tile does not fit shared memory");
-  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, STAGES, kTwo ? 2 : 1>;
+  using C = Cfg<A_BITS, W_BITS, BN>;
+  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.oc + BN - 1) / BN));
-  kern<<<grid, kThreads, S::kBytes, stream>>>(p, wexp, kpad);
+  TcArgs a;
+  a.p = p;
+  a.ntn = (p.oc + BN - 1) / BN;
+  const int64_t mtiles = (p.M + BM - 1) / BM;
+  if (mtiles * a.ntn > (int64_t(1) << 31) - 1) return cudaErrorInvalidValue;
+  a.ntiles = int(mtiles * a.ntn);
+  a.nchunks = int(kpad / kWordsPerStage);
+  // TMA-store epilogue by default (direct 16-byte stores of one row segment per lane
+  // measured 1.4-1.8x slower on the output-bound layers); BS_TC_EPI=direct selects them.
+  const char* epi_env = getenv("BS_TC_EPI");
+  const bool want_direct = epi_env && epi_env[0] == 'd';
+  a.epi = (p.oc % 4) != 0 ? kEpiScalar : (want_direct ? kEpiDirect : kEpiTma);
+  const char* res_env = getenv("BS_TC_RESIDENT");
+  const bool allow_res = !(res_env && res_env[0] == '0');
+  const int64_t fixed = C::kFixed;
+  const int64_t res_bytes = int64_t(a.nchunks) * C::kBBytes;
+  a.b_resident = allow_res && a.ntn == 1 && fixed + res_bytes <= kSmemLimit;
+  a.b_bytes = int(a.b_resident ? res_bytes : int64_t(C::kStages) * C::kBBytes);
+  const char* dbg_env = getenv("BS_TC_DEBUG");
+  a.debug = dbg_env ? atoi(dbg_env) : 0;
+  int smem_bytes = int(fixed) + a.b_bytes;
+  if (smem_bytes < kMinSmem) smem_bytes = kMinSmem;
+  CUtensorMap tw, to;
+  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, uint64_t(kpad) * 32, uint64_t(W_BITS) * p.oc,
+                 uint64_t(kpad) * 32, BKB, BN))
+    return cudaErrorInvalidValue;
+  if (a.epi == kEpiTma) {
+    if (!encode_2d(&to, CU_TENSOR_MAP_DATA_TYPE_INT32, p.out, uint64_t(p.oc), uint64_t(p.M), uint64_t(p.oc) * 4, 32,
+                   32))
+      return cudaErrorInvalidValue;
+  } else {
+    to = tw;  // unused
+  }
+  const int grid = a.ntiles < num_sms() ? a.ntiles : num_sms();
+  kern<<<grid, kThreads, smem_bytes, stream>>>(a, tw, to);
   note_launch();
   return cudaPeekAtLastError();
 }
 
+// Tile width: BN = 64 when the filters fit it, else 128 (the widest tile whose double-
+// buffered accumulators leave TMEM room for the A ring).  BS_TC_BN overrides (tests).
+template <int A_BITS, int W_BITS>
+int pick_bn(const ConvProblem& p, int64_t) {
+  if (const char* e = getenv("BS_TC_BN")) {
+    const int v = atoi(e);
+    if (v == 64 || v == 128) return v;
+  }
+  return p.oc <= 64 ? 64 : 128;
+}
+
 template <int A_BITS, int W_BITS>
 cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
-  if (p.oc <= 64) return launch_bn<A_BITS, W_BITS, 64>(p, wexp, kpad, stream);
-  if constexpr (A_BITS * W_BITS <= 4) {
-    if (p.oc > 128) return launch_bn<A_BITS, W_BITS, 256>(p, wexp, kpad, stream);
+  switch (pick_bn<A_BITS, W_BITS>(p, kpad)) {
+    case 128:
+      if constexpr (Cfg<A_BITS, W_BITS, 128>::kFit >= 2) return launch_bn<A_BITS, W_BITS, 128>(p, wexp, kpad, stream);
+      [[fallthrough]];
+    default:
+      return launch_bn<A_BITS, W_BITS, 64>(p, wexp, kpad, stream);
   }
-  return launch_bn<A_BITS, W_BITS, 128>(p, wexp, kpad, stream);
 }
 
 }  // namespace tc
 
-int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits) {
-  const int64_t kpad = (kp + tc::kWordsPerStage - 1) / tc::kWordsPerStage * tc::kWordsPerStage;
-  return int64_t(w_bits) * n * kpad * 32;
+int64_t tc_kpad(int64_t kp) { return (kp + tc::kWordsPerStage - 1) / tc::kWordsPerStage * tc::kWordsPerStage; }
+
+int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits) { return int64_t(w_bits) * n * tc_kpad(kp) * 32; }
+
+bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 2; }
+
+cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int bipolar, int64_t n, int64_t kp,
+                                     int8_t* wexp, cudaStream_t stream) {
+  const int64_t kpad = tc_kpad(kp);
+  const int64_t words = int64_t(w_bits) * n * kpad;
+  int64_t blocks = (words + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  tc::expand_weights_kernel<<<unsigned(blocks), 256, 0, stream>>>(w_packed, wexp, w_bits, int(n), kp, kpad, bipolar);
+  note_launch();
+  return cudaPeekAtLastError();
 }
 
-bool tc_supported(int a_bits, int w_bits) {
-  return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 2;
+cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream) {
+  if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
+  const int64_t kpad = tc_kpad(p.kp);
+#define BS_TC(A, W) \
+  if (p.a_bits == A && p.w_bits == W) return tc::launch_aw<A, W>(p, wexp, kpad, stream);
+  BS_TC(1, 1) BS_TC(2, 1) BS_TC(2, 2) BS_TC(1, 2) BS_TC(3, 1) BS_TC(3, 2) BS_TC(4, 1) BS_TC(4, 2)
+#undef BS_TC
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, cudaStream_t stream) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
-  const int64_t kpad = (p.kp + tc::kWordsPerStage - 1) / tc::kWordsPerStage * tc::kWordsPerStage;
-  {
-    const int64_t words = int64_t(p.w_bits) * p.oc * kpad;
-    int64_t blocks = (words + 255) / 256;
-    if (blocks > 4096) blocks = 4096;
-    tc::expand_weights_kernel<<<unsigned(blocks), 256, 0, stream>>>(p.wt, wexp_ws, p.w_bits, p.oc, p.kp, kpad,
-                                                                    p.bipolar);
-    note_launch();
-    cudaError_t e = cudaPeekAtLastError();
-    if (e != cudaSuccess) return e;
-  }
-#define BS_TC(A, W) \
-  if (p.a_bits == A && p.w_bits == W) return tc::launch_aw<A, W>(p, wexp_ws, kpad, stream);
-  BS_TC(1, 1) BS_TC(2, 1) BS_TC(2, 2) BS_TC(1, 2) BS_TC(3, 1) BS_TC(3, 2) BS_TC(4, 1) BS_TC(4, 2)
-#undef BS_TC
-  return cudaErrorNotSupported;
+  cudaError_t e = launch_tc_expand_weights(p.wt, p.w_bits, p.bipolar, p.oc, p.kp, wexp_ws, stream);
+  if (e != cudaSuccess) return e;
+  return launch_tc_conv_prepared(p, wexp_ws, stream);
 }
 
 }  // namespace bs

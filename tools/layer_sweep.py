@@ -1,6 +1,8 @@
 """Time the conv kernel of each BASELINE layer (batch 256 by default) for the library
-selected by BITSERIAL_LIB (default: in-tree).  Events around each launch, median of
-reps.  Usage: python tools/layer_sweep.py [--batch 256] [--a 2 --w 1] [--unipolar]"""
+selected by BITSERIAL_LIB (default: in-tree).  Each layer's launch is captured R times
+back to back in a CUDA graph and timed with events around the replay (no host launch
+overhead in the number); per-launch time = graph time / R, median over trials.
+Usage: python tools/layer_sweep.py [--batch 256] [--a 2 --w 1] [--unipolar] [--tc] [--fused]"""
 import argparse
 import json
 import os
@@ -17,15 +19,18 @@ ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--a", type=int, default=2)
 ap.add_argument("--w", type=int, default=1)
 ap.add_argument("--unipolar", action="store_true")
-ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--reps", type=int, default=20, help="launches per graph")
+ap.add_argument("--trials", type=int, default=5)
 ap.add_argument("--layers", default=",".join(map(str, inputs.BASELINE_LAYERS)))
 ap.add_argument("--algo", type=int, default=0)
-ap.add_argument("--tc", action="store_true", help="tensor-core path (bs_bitserial_conv2d_nhwc_tc)")
+ap.add_argument("--tc", action="store_true", help="tensor-core path on prepared weights")
+ap.add_argument("--fused", action="store_true", help="include activation packing (the *_i8 entry)")
 args = ap.parse_args()
 dev = torch.device("cuda")
 enc = bs.UNIPOLAR if args.unipolar else bs.BIPOLAR
 res = {}
 tot_ops, tot_ms = 0, 0.0
+stream = torch.cuda.Stream()
 for li in map(int, args.layers.split(",")):
     L = inputs.TABLE1[li]
     g = inputs.gen(li)
@@ -33,30 +38,50 @@ for li in map(int, args.layers.split(",")):
     wt = inputs.codes((L.oc * L.k * L.k, L.ic), args.w, g).to(dev)
     ap_ = bs.bitpack(act, args.a)
     wp = bs.bitpack(wt, args.w)
-    out = torch.empty((args.batch, bs.conv_out_extent(L.h, L.k, L.s, L.pad), bs.conv_out_extent(L.w, L.k, L.s, L.pad),
-                       L.oc), dtype=torch.int32, device=dev)
-    ws = torch.empty(max(16, bs.conv2d_tc_workspace_bytes(L.oc, L.k, L.k, L.ic, args.w)), dtype=torch.uint8, device=dev)
-    if args.tc:
-        run = lambda: bs.bitserial_conv2d_nhwc_tc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc,  # noqa
-                                                  L.k, L.k, L.s, L.pad, out=out, workspace=ws)
+    oh = bs.conv_out_extent(L.h, L.k, L.s, L.pad)
+    out = torch.empty((args.batch, oh, oh, L.oc), dtype=torch.int32, device=dev)
+    ws = torch.empty(max(16, bs.conv2d_workspace_bytes(args.batch, L.h, L.w, L.ic, args.a)), dtype=torch.uint8,
+                     device=dev)
+    w_tc = bs.conv2d_tc_prepare_weights(wp, args.w, enc, L.oc, L.k, L.k, L.ic) if args.tc else None
+    if args.tc and args.fused:
+        run = lambda s: bs.bitserial_conv2d_nhwc_tc_i8(act, args.a, w_tc, args.w, L.oc, L.k, L.k, L.s, L.pad,  # noqa
+                                                       out=out, workspace=ws, stream=s)
+    elif args.tc:
+        run = lambda s: bs.bitserial_conv2d_nhwc_tc_prepared(ap_, args.a, w_tc, args.w, args.batch, L.h, L.w,  # noqa
+                                                             L.ic, L.oc, L.k, L.k, L.s, L.pad, out=out, stream=s)
+    elif args.fused:
+        run = lambda s: bs.bitserial_conv2d_nhwc_i8(act, args.a, wp, args.w, enc, L.oc, L.k, L.k, L.s, L.pad,  # noqa
+                                                    out=out, workspace=ws, stream=s)
     else:
-        run = lambda: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc, L.k,  # noqa
-                                               L.k, L.s, L.pad, out=out, algo=args.algo)
-    run()
+        run = lambda s: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc,  # noqa
+                                                 L.k, L.k, L.s, L.pad, out=out, algo=args.algo, stream=s)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        run(stream)
+        run(stream)
+        stream.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for _ in range(args.reps):
+                run(stream)
+    graph.replay()
     torch.cuda.synchronize()
     ts = []
-    for _ in range(args.reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        run()
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
+    with torch.cuda.stream(stream):  # replay() launches on the current stream: time that one
+        for _ in range(args.trials):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / args.reps)
     ms = sorted(ts)[len(ts) // 2]
-    oh = bs.conv_out_extent(L.h, L.k, L.s, L.pad)
     ops = 2 * args.batch * oh * oh * L.oc * L.k * L.k * L.ic * args.a * args.w
-    res[li] = {"ms": ms, "tops": ops / ms / 1e9}
+    out_gb = out.numel() * 4 / 1e9
+    res[li] = {"us": round(ms * 1e3, 2), "tops": round(ops / ms / 1e9, 1), "out_gbs": round(out_gb / ms * 1e3, 1)}
     tot_ops += ops
     tot_ms += ms
-print(json.dumps({"lib": bs.library_path(), "tc": args.tc, "a": args.a, "w": args.w, "layers": res, "total_ms": tot_ms,
-                  "total_tops": tot_ops / tot_ms / 1e9}))
+    del graph
+print(json.dumps({"lib": bs.library_path(), "tc": args.tc, "fused": args.fused, "a": args.a, "w": args.w,
+                  "batch": args.batch, "bn": os.environ.get("BS_TC_BN"), "layers": res,
+                  "total_us": round(tot_ms * 1e3, 1), "total_tops": round(tot_ops / tot_ms / 1e9, 1)}))
