@@ -116,9 +116,9 @@ def binops_conv(L, n, a_bits, w_bits):
 class ConvLayerRun:
     """One conv layer on this rank's batch shard: resident inputs/outputs in HBM."""
 
-    def __init__(self, L, act_cpu, wt_cpu, a_bits, w_bits, bipolar, dev):
+    def __init__(self, L, act_cpu, wt_cpu, a_bits, w_bits, bipolar, dev, path="tc"):
         import paper_1810_11066_b200 as bs
-        self.bs, self.L = bs, L
+        self.bs, self.L, self.path = bs, L, path
         self.a_bits, self.w_bits, self.enc = a_bits, w_bits, (bs.BIPOLAR if bipolar else bs.UNIPOLAR)
         self.n = act_cpu.shape[0]
         self.act_cpu = act_cpu
@@ -128,22 +128,33 @@ class ConvLayerRun:
         self.out = torch.empty((self.n, self.oh, self.oh, L.oc), dtype=torch.int32, device=dev)
         self.ws = torch.empty(bs.conv2d_workspace_bytes(self.n, L.h, L.w, L.ic, a_bits), dtype=torch.uint8, device=dev)
         self.packed = self.ws.view(torch.int32).view(a_bits, self.n * L.h * L.w, bs.packed_row_words(L.ic))
+        # tensor-core path: weight planes expanded once, offline like the packing itself
+        self.w_tc = (bs.conv2d_tc_prepare_weights(self.wp, w_bits, self.enc, L.oc, L.k, L.k, L.ic)
+                     if path == "tc" else None)
 
     def binops(self):
         return binops_conv(self.L, self.n, self.a_bits, self.w_bits)
 
     def step(self):  # pack + conv (the timed unit)
         L = self.L
-        self.bs.bitserial_conv2d_nhwc_i8(self.act, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k,
-                                         L.s, L.pad, out=self.out, workspace=self.ws)
+        if self.path == "tc":
+            self.bs.bitserial_conv2d_nhwc_tc_i8(self.act, self.a_bits, self.w_tc, self.w_bits, L.oc, L.k, L.k,
+                                                L.s, L.pad, out=self.out, workspace=self.ws)
+        else:
+            self.bs.bitserial_conv2d_nhwc_i8(self.act, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k,
+                                             L.s, L.pad, out=self.out, workspace=self.ws)
 
     def pack_only(self):
         self.bs.bitpack(self.act, self.a_bits, out=self.packed)
 
     def conv_only(self):
         L = self.L
-        self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h, L.w,
-                                      L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
+        if self.path == "tc":
+            self.bs.bitserial_conv2d_nhwc_tc_prepared(self.packed, self.a_bits, self.w_tc, self.w_bits, self.n, L.h,
+                                                      L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
+        else:
+            self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h,
+                                          L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
 
     def host_buffers(self):
         return (self.act_cpu.contiguous().pin_memory(), torch.empty(self.out.shape, dtype=torch.int32).pin_memory(),
@@ -152,8 +163,12 @@ class ConvLayerRun:
     def host_step(self, bufs):
         L = self.L
         ah, oh_, ad, od = bufs
-        self.bs.bitserial_conv2d_nhwc_host(ah, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k, L.s,
-                                           L.pad, oh_, ad, od, self.ws)
+        if self.path == "tc":
+            self.bs.bitserial_conv2d_nhwc_tc_host(ah, self.a_bits, self.w_tc, self.w_bits, L.oc, L.k, L.k, L.s,
+                                                  L.pad, oh_, ad, od, self.ws)
+        else:
+            self.bs.bitserial_conv2d_nhwc_host(ah, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k, L.s,
+                                               L.pad, oh_, ad, od, self.ws)
 
 
 class ConvWorkload:
@@ -172,7 +187,7 @@ class ConvWorkload:
             act, wt = inputs.conv_operands(L, batch, args.a_bits, args.w_bits,
                                            inputs.seed_for(config_id, args.a_bits, args.w_bits, enc, li))
             self.runs.append(ConvLayerRun(L, act[lo:hi].contiguous(), wt, args.a_bits, args.w_bits, args.bipolar,
-                                          dev))
+                                          dev, args.path))
         self.total_binops = self.replicas * sum(binops_conv(inputs.TABLE1[li], batch, args.a_bits, args.w_bits)
                                                 for li in layers)
         self.config_id = config_id
@@ -184,8 +199,11 @@ class ConvWorkload:
             "parallelism": (f"{world} independent replicas (batch 1 does not shard)" if self.replicas > 1 else
                             f"batch-sharded dp{world} (no collective)"),
             "rank0_images": [lo, hi],
-            "step": "per layer: bitpack(act) + bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights prepacked, "
-                    "untimed)",
+            "step": ("per layer: bitpack(act) + tensor-core bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_i8 "
+                     "(weights packed + plane-expanded once, untimed)" if args.path == "tc" else
+                     "per layer: bitpack(act) + AND/POPC bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights "
+                     "prepacked, untimed)"),
+            "path": args.path,
         }
 
     def step(self):
@@ -193,32 +211,27 @@ class ConvWorkload:
             r.step()
 
     def roofline(self, reps):
-        """Per-launch device time of the pack and conv kernels (events around each
-        launch on the launching stream); the conv kernel is the dominant one."""
-        stream = torch.cuda.current_stream()
+        """Per-launch device time of the pack and conv kernels of every layer: each
+        kernel captured `reps` times back to back in a CUDA graph, timed with events on
+        the stream that replays it (no host launch gaps), per launch = graph time / reps."""
         for r in self.runs:
             r.pack_only()
             r.conv_only()
         torch.cuda.synchronize()
-        pack_ms, conv_ms = [0.0] * len(self.runs), [0.0] * len(self.runs)
-        for _ in range(reps):
-            for i, r in enumerate(self.runs):
-                a0, a1, b1 = ev(), ev(), ev()
-                a0.record(stream)
-                r.pack_only()
-                a1.record(stream)
-                r.conv_only()
-                b1.record(stream)
-                torch.cuda.synchronize()
-                pack_ms[i] += a0.elapsed_time(a1) / reps
-                conv_ms[i] += a1.elapsed_time(b1) / reps
+        pack_ms = [graph_launch_ms(r.pack_only, reps) for r in self.runs]
+        conv_ms = [graph_launch_ms(r.conv_only, reps) for r in self.runs]
         ops = sum(r.binops() for r in self.runs)
         pack_bytes = sum(r.act.numel() * (1 + r.a_bits / 8) for r in self.runs)
-        return {"kind": "alu", "kernel": f"popc_conv_kernel (sum over the {len(self.runs)} layer launches of one "
-                                         f"step, rank 0)",
-                "ops": ops, "ms": sum(conv_ms),
-                "breakdown": {"layers": list(self.layers), "conv_ms": conv_ms, "pack_ms": pack_ms,
-                              "pack_gbs": pack_bytes / (sum(pack_ms) / 1e3) / 1e9}}
+        tc = self.args.path == "tc"
+        kname = "tc_conv_kernel (tcgen05 kind::i8" if tc else "popc_conv_kernel ("
+        return {"kind": "tensor" if tc else "alu",
+                "kernel": f"{kname} sum over the {len(self.runs)} layer launches of one step, rank 0)",
+                "ops": ops, "ms": sum(conv_ms), "launches": len(self.runs),
+                "breakdown": {"layers": list(self.layers), "conv_us": [1e3 * t for t in conv_ms],
+                              "pack_us": [1e3 * t for t in pack_ms],
+                              "conv_binary_tops": [r.binops() / (t / 1e3) / 1e12 for r, t in zip(self.runs, conv_ms)],
+                              "pack_gbs": pack_bytes / (sum(pack_ms) / 1e3) / 1e9,
+                              "out_gbs": sum(r.out.numel() * 4 for r in self.runs) / (sum(conv_ms) / 1e3) / 1e9}}
 
     def e2e(self, steps):
         bufs = [r.host_buffers() for r in self.runs]
@@ -259,7 +272,7 @@ class ConvWorkload:
 
     def oracle_units(self, budget_s):
         ops1, t1, _ = self.oracle_sample(1)
-        return max(1, min(16, self.batch, int(budget_s / max(t1, 1e-3))))
+        return max(1, min(self.batch, int(budget_s / max(t1, 1e-3))))
 
 
 # ----------------------------------------------------------------------------- dense
@@ -284,6 +297,8 @@ class DenseWorkload:
         self.a = self.a_cpu.to(dev)
         self.wp = bs.bitpack(w.to(dev), args.w_bits)  # untimed
         del w
+        self.tc = args.path == "tc" and (hi - lo) > 8  # GEMV (m <= 8) stays on the HBM-bound matvec kernel
+        self.w_tc = bs.dense_tc_prepare_weights(self.wp, args.w_bits, self.enc, n, k) if self.tc else None
         self.out = torch.empty((hi - lo, n), dtype=torch.int32, device=dev)
         self.full = torch.empty((m, n), dtype=torch.int32, device=dev) if gather else None
         self.ws = torch.empty(max(16, bs.dense_workspace_bytes(hi - lo, k, args.a_bits)), dtype=torch.uint8, device=dev)
@@ -297,14 +312,20 @@ class DenseWorkload:
             "workload": f"{name}_m{m}_n{n}_k{k}_a{args.a_bits}w{args.w_bits}_{enc}", "m": m, "n": n, "k": k,
             "parallelism": (f"row-sharded tp{world} + all_gather_into_tensor(int32 C) over NCCL" if gather else
                             "single GPU (replicas only)"),
-            "step": "bs_bitserial_dense_i8 (activation pack + dense" + (", fused single launch" if (hi - lo) <= 8
-                                                                        else "") + ")"
+            "step": ("bs_bitserial_dense_tc_i8 (activation pack + tensor-core dense)" if self.tc else
+                     "bs_bitserial_dense_i8 (activation pack + dense" + (", fused single launch" if (hi - lo) <= 8
+                                                                         else "") + ")")
                     + (" + NCCL all-gather of C" if gather else ""),
+            "path": "tc" if self.tc else ("gemv" if (hi - lo) <= 8 else "popc"),
         }
 
     def step(self):
-        self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
-                                   workspace=self.ws)
+        if self.tc:
+            self.bs.bitserial_dense_tc_i8(self.a, self.a_bits, self.w_tc, self.w_bits, self.n, out=self.out,
+                                          workspace=self.ws)
+        else:
+            self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
+                                       workspace=self.ws)
         if self.gather:
             bsdist.gather_rows(self.full, self.out)
 
@@ -317,6 +338,9 @@ class DenseWorkload:
             if gemv:
                 self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
                                            workspace=self.ws)
+            elif self.tc:
+                self.bs.bitserial_dense_tc_prepared(self.packed, self.a_bits, self.w_tc, self.w_bits, rows, self.n,
+                                                    self.k, out=self.out)
             else:
                 self.bs.bitserial_dense(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, rows, self.n,
                                         self.k, out=self.out)
@@ -349,8 +373,10 @@ class DenseWorkload:
             nbytes = self.wp.numel() * 4 + self.a.numel() + self.out.numel() * 4
             return {"kind": "hbm", "kernel": "gemv_kernel (fused pack + GEMV, one launch, cold L2)", "bytes": nbytes,
                     "ops": ops, "ms": ms, "breakdown": {"gemv_ms": ms}}
-        return {"kind": "alu", "kernel": "popc_conv_kernel (dense = 1x1 implicit GEMM, rank 0 shard)", "ops": ops,
-                "ms": ms, "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
+        return {"kind": "tensor" if self.tc else "alu",
+                "kernel": ("tc_conv_kernel (tcgen05 kind::i8; dense = 1x1 implicit GEMM, rank 0 shard)" if self.tc else
+                           "popc_conv_kernel (dense = 1x1 implicit GEMM, rank 0 shard)"), "ops": ops,
+                "ms": ms, "launches": 1, "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
 
     def e2e(self, steps):
         a_host = self.a_cpu.pin_memory()
@@ -408,6 +434,31 @@ def make_workload(args, rank, world, dev):
 
 
 # ---------------------------------------------------------------------------- timing
+def graph_launch_ms(fn, reps, trials=5):
+    """Median per-launch ms of `fn` captured `reps` times in one CUDA graph."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        s.synchronize()
+        ts = []
+        for _ in range(trials):
+            e0, e1 = ev(), ev()
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+            s.synchronize()
+            ts.append(e0.elapsed_time(e1) / reps)
+    torch.cuda.current_stream().wait_stream(s)
+    return sorted(ts)[len(ts) // 2]
+
+
 def time_steps(step_fn, steps, warmup, dev, flush, use_graph):
     """W untimed warm-ups, then K steps each bracketed by CUDA events on the launching
     stream, the L2 flushed between steps outside the events; barrier + synchronize on
@@ -465,12 +516,27 @@ def run_ours(args):
     clocks = clk.summary()
     value = wl.total_binops / (ms / 1e3) / 1e12
 
-    roof = wl.roofline(max(3, min(args.steps, 10)))
+    roof = wl.roofline(10)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or MAX_MHZ_FALLBACK
     r_popc = 64.0 * POPC_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     r_int = 2.0 * r_popc
-    if roof["kind"] == "alu":
+    if roof["kind"] == "tensor":
+        # binary dot products as int8 x int8 -> int32 MMAs on 0/1 (or +-2^j) bytes: one
+        # binary MAC = one int8 MAC, so the roofline is the int8 tensor peak = 2 x the
+        # measured bf16 peak (tools/mma_bench.cu: kind::i8 sustains exactly 2x the
+        # kind::f16 MACs per clock per SM); burst figure (kernels timed alone).
+        peak = 2.0 * peaks["bf16_tflops"]
+        achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "binary TOPS",
+                    "frac": achieved / peak, "traffic": None, "kernel": roof["kernel"],
+                    "peak_basis": f"int8 dense tensor peak = 2 x bf16_tflops ({peaks['bf16_tflops']:.1f}, "
+                                  f"{peaks_src}); 1 binary MAC = 1 int8 MAC",
+                    "peak_sustained": 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                    "frac_sustained": achieved / (2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])),
+                    "frac_of_nominal_4500": achieved / 4500.0,
+                    "r_popc": r_popc, "x_r_popc": achieved / r_popc}
+    elif roof["kind"] == "alu":
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": achieved, "peak": r_int, "unit": "binary TOPS",
                     "frac": achieved / r_int, "traffic": None, "r_popc": r_popc, "frac_r_popc": achieved / r_popc,
@@ -514,7 +580,9 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "vs_baseline": None, "dtype": "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32",
+            "vs_baseline": None,
+            "dtype": ("u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32"
+                      if args.path == "tc" else "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32"),
             "scaling": "weak" if getattr(wl, "replicas", 1) > 1 else "strong",
             "data": "synthetic (seeded uniform codes, PAPER.md Table 1 / BASELINE shapes; no dataset)",
             "config": cfg, "roofline": roofline,
@@ -598,6 +666,8 @@ def main():
     ap.add_argument("--w-bits", type=int, default=1)
     ap.add_argument("--unipolar", dest="bipolar", action="store_false")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--path", choices=["tc", "popc"], default="tc",
+                    help="conv/GEMM kernel: tensor-core bitserial (default) or the AND/POPC integer-pipe kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
