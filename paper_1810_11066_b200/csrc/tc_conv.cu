@@ -82,6 +82,18 @@ constexpr int kMinSmem = 116 * 1024;  // > half the SM: guarantees one CTA per S
 #endif
 
 // ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ldg_nc_v2(const uint32_t* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
 }
@@ -308,11 +320,9 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
 // ----------------------------------------------------------------------- main kernel
 template <int A_BITS, int W_BITS, int BN>
 struct Cfg {
-  static constexpr int kRawDepth = A_BITS <= 2 ? 3 : 2;
   static constexpr int kACols = A_BITS * (BKB / 4);  // TMEM columns of one stage's A planes
   static constexpr int kBBytes = W_BITS * BN * BKB;  // shared memory per stage (B only)
-  static constexpr int kRawBytes = kRawDepth * A_BITS * kProducerThreads * 16;
-  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + kEpiBytes + kRawBytes;
+  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
@@ -330,6 +340,23 @@ struct Cfg {
 
 enum EpiMode : int { kEpiDirect = 0, kEpiTma = 1, kEpiScalar = 2 };
 
+// n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method):
+// q = (umulhi(n, mul) + n) >> shr, shr = ceil(log2 d), mul = floor(2^32 (2^shr - d) / d) + 1.
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shr; }
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  if (d > 1) {
+    uint32_t p = 0;
+    while ((uint64_t(1) << p) < d) ++p;
+    f.shr = p;
+    f.mul = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << p) - d)) / d + 1);
+  }
+  return f;
+}
+
 struct TcArgs {
   ConvProblem p;
   int ntiles, ntn;  // tiles, N-tiles per M block
@@ -337,6 +364,8 @@ struct TcArgs {
   int epi;          // EpiMode: direct 16-byte stores (OC % 4 == 0), TMA stores, or scalar
   int b_resident;   // ntn == 1 and the whole expanded B fits: loaded once, kept in smem
   int b_bytes;      // bytes of the B region (resident: nchunks stages, else kStages)
+  FastDiv div_hw, div_ow, div_kwid, div_ntn, div_kwa;  // n / (oh*ow), / ow, / kw, / ntn, / Cw
+  int kwa_shift;    // log2(Cw) when Cw is a power of two, else -1
   int debug;        // BS_TC_PROFILE builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                     // 2 skip accumulator tcgen05.ld (timing experiments; results are wrong)
 };
@@ -358,8 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* s_stage = smem;                            // B: S ring stages, or nchunks resident
   uint8_t* s_epi = smem + args.b_bytes;               // 4 warps x 2 x 4 KB (1024-aligned)
-  uint8_t* s_rawb = s_epi + kEpiBytes;                // producer raw ring
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_rawb + C::kRawBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_epi + kEpiBytes);
   uint64_t* full_a = bars;
   uint64_t* full_b = bars + S;
   uint64_t* empty = bars + 2 * S;
@@ -408,114 +436,97 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= expansion producers.  kTeams teams of 4 warps; team t expands the
     // chunks g = t, t+kTeams, ... of this CTA's (tile, K chunk) sequence, so kTeams chunks
     // are in flight.  Within a team, thread `arow` (warp % 4 == its TMEM lane quarter)
-    // owns output row arow and all 4 packed words of each plane of the chunk.
+    // owns output row arow and all 4 packed words of each plane of the chunk.  The
+    // packed words are loaded straight into registers one team step ahead (the kTeams
+    // chunks in flight cover the load latency); all index arithmetic is shifts and
+    // precomputed fast divisions (a team changes tile almost every step when K is short).
     constexpr int kTeams = C::kTeamsUsed;
     const int team = warp >> 2, arow = tid & (BM - 1);
-    const int kp = int(p.kp);
-    const int64_t hw = int64_t(p.oh) * p.ow;
-    const bool split = (p.kw_a & 3) != 0;  // a 4-word group spans two taps (Cw = 2 mod 4)
-    struct Geo {
-      bool ok;
-      int iy0, ix0;
-      int64_t base;
+    const int kp = int(p.kp), kwa = p.kw_a;
+    const bool split = (kwa & 3) != 0;  // a 4-word group spans two taps (Cw = 2 mod 4)
+    const uint32_t* __restrict__ act = p.act;
+    const int64_t plane = p.act_plane;
+    // geometry of this thread's row in tile `t`
+    bool rok = false;
+    int iy0 = 0, ix0 = 0;
+    const uint32_t* rbase = act;  // image base (pixel 0 of the row's image), word units
+    auto set_tile = [&](int t) {
+      const uint32_t mblk = args.div_ntn.div(uint32_t(t));
+      const int64_t m = int64_t(mblk) * BM + arow;
+      rok = m < p.M;
+      const uint32_t mm = rok ? uint32_t(m) : 0u;
+      const uint32_t b = args.div_hw.div(mm), rem = mm - b * args.div_hw.d;
+      const uint32_t oy = args.div_ow.div(rem), ox = rem - oy * args.div_ow.d;
+      iy0 = int(oy) * p.sh - p.ph;
+      ix0 = int(ox) * p.sw - p.pw;
+      rbase = act + int64_t(b) * p.h * p.w * kwa;
     };
-    auto geo = [&](int tile) {
-      Geo g;
-      const int64_t m = int64_t(tile / ntn) * BM + arow;
-      g.ok = m < p.M;
-      const int64_t mm = g.ok ? m : 0;
-      const int64_t b = mm / hw, rem = mm - b * hw;
-      const int oy = int(rem / p.ow), ox = int(rem - int64_t(oy) * p.ow);
-      g.iy0 = oy * p.sh - p.ph;
-      g.ix0 = ox * p.sw - p.pw;
-      g.base = b * int64_t(p.h) * p.w;
-      return g;
+    // source of the 2- or 4-word piece starting at filter word kk (kk even)
+    auto piece = [&](int kk, bool& ok) -> const uint32_t* {
+      int tap, cw;
+      if (args.kwa_shift >= 0) {
+        tap = kk >> args.kwa_shift;
+        cw = kk & (kwa - 1);
+      } else {
+        tap = int(args.div_kwa.div(uint32_t(kk)));
+        cw = kk - tap * kwa;
+      }
+      const int ky = int(args.div_kwid.div(uint32_t(tap))), kx = tap - ky * p.kwid;
+      const int iy = iy0 + ky, ix = ix0 + kx;
+      ok = rok && kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
+      return rbase + (int64_t(iy) * p.w + ix) * kwa + cw;
     };
-    // fetch iterator (runs kRawDepth-1 of this team's chunks ahead of the expansion);
-    // the filter word index kk = 4*kc is tracked as (tap ky, kx; word cw) incrementally.
-    int f_tile = blockIdx.x, f_kc = team, f_kk = 0, f_cw = 0, f_kx = 0, f_ky = 0;
-    auto norm = [&]() {
-      while (f_cw >= p.kw_a) {
-        f_cw -= p.kw_a;
-        if (++f_kx == p.kwid) {
-          f_kx = 0;
-          ++f_ky;
+    auto load = [&](int kc, uint4 (&v)[A_BITS]) {
+      const int kk = kc * kWordsPerStage;
+      bool ok0;
+      const uint32_t* s0 = piece(kk, ok0);
+      if (!split) {
+#pragma unroll
+        for (int i = 0; i < A_BITS; ++i)
+          v[i] = ok0 ? ldg_nc_v4(s0 + i * plane) : make_uint4(0u, 0u, 0u, 0u);
+      } else {
+        bool ok1;
+        const uint32_t* s1 = piece(kk + 2, ok1);
+#pragma unroll
+        for (int i = 0; i < A_BITS; ++i) {
+          const uint2 lo = ok0 ? ldg_nc_v2(s0 + i * plane) : make_uint2(0u, 0u);
+          const uint2 hi = ok1 ? ldg_nc_v2(s1 + i * plane) : make_uint2(0u, 0u);
+          v[i] = make_uint4(lo.x, lo.y, hi.x, hi.y);
         }
       }
     };
-    auto seek = [&]() {  // normalise (f_tile, f_kc) and restart the tap walk at kk = 4*kc
-      while (f_kc >= nchunks) {
-        f_kc -= nchunks;
-        f_tile += gridDim.x;
-      }
-      f_kk = f_kc * kWordsPerStage;
-      f_cw = f_kk;
-      f_kx = f_ky = 0;
-      norm();
-    };
-    seek();
-    Geo fg = geo(f_tile < ntiles ? f_tile : 0);
-    const uint32_t raw_base = smem_u32(s_rawb) + uint32_t(tid) * 16u;
-    constexpr uint32_t kRawPlane = kProducerThreads * 16;
-    auto fetch = [&](int slot) {
-      if (f_tile < ntiles) {
-        const uint32_t dst = raw_base + uint32_t(slot * A_BITS) * kRawPlane;
-        const int iy = fg.iy0 + f_ky, ix = fg.ix0 + f_kx;
-        const bool ok = fg.ok && f_kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
-        const uint32_t* src = ok ? p.act + (fg.base + int64_t(iy) * p.w + ix) * p.kw_a + f_cw : p.act;
-        if (!split) {
-#pragma unroll
-          for (int i = 0; i < A_BITS; ++i) cp_async16(dst + i * kRawPlane, src + i * p.act_plane, ok);
-        } else {  // Cw = 2 mod 4: two 8-byte pieces (words 0-1, words 2-3 of the group)
-#pragma unroll
-          for (int i = 0; i < A_BITS; ++i) cp_async8(dst + i * kRawPlane, src + i * p.act_plane, ok);
-          const uint32_t* src2;
-          bool ok2;
-          if (f_cw + 2 < p.kw_a) {  // same tap
-            ok2 = ok && f_kk + 2 < kp;
-            src2 = src + 2;
-          } else {  // words 2-3 are word 0-1 of the next tap
-            int kx2 = f_kx + 1, ky2 = f_ky;
-            if (kx2 == p.kwid) {
-              kx2 = 0;
-              ++ky2;
-            }
-            const int iy2 = fg.iy0 + ky2, ix2 = fg.ix0 + kx2;
-            ok2 = fg.ok && f_kk + 2 < kp && unsigned(iy2) < unsigned(p.h) && unsigned(ix2) < unsigned(p.w);
-            src2 = ok2 ? p.act + (fg.base + int64_t(iy2) * p.w + ix2) * p.kw_a : p.act;
-          }
-#pragma unroll
-          for (int i = 0; i < A_BITS; ++i) cp_async8(dst + i * kRawPlane + 8, src2 + i * p.act_plane, ok2);
-        }
-        f_kc += kTeams;
-        if (f_kc >= nchunks) {
-          const int old_tile = f_tile;
-          seek();
-          if (f_tile != old_tile && f_tile < ntiles) fg = geo(f_tile);
-        } else {
-          f_kk += kTeams * kWordsPerStage;
-          f_cw += kTeams * kWordsPerStage;
-          norm();
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int d = 0; d < C::kRawDepth - 1; ++d) fetch(d);
-    int slot = 0;
-    int g = team;  // this team's position in the CTA's chunk sequence
     const int my_tiles = ntiles > int(blockIdx.x) ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
     const int total = my_tiles * nchunks;
+    // iterator of the next chunk to load: (local tile lt, kc)
+    int lt = 0, kc = team;
+    while (kc >= nchunks && lt < my_tiles) {
+      kc -= nchunks;
+      ++lt;
+    }
+    int cur_tile = -1;
+    uint4 nxt[A_BITS];
+    auto advance_load = [&]() {
+      if (lt < my_tiles) {
+        const int t = int(blockIdx.x) + lt * int(gridDim.x);
+        if (t != cur_tile) {
+          set_tile(t);
+          cur_tile = t;
+        }
+        load(kc, nxt);
+        kc += kTeams;
+        while (kc >= nchunks) {
+          kc -= nchunks;
+          ++lt;
+        }
+      }
+    };
+    advance_load();
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
-    for (; g < total; g += kTeams) {
-      fetch(slot == 0 ? C::kRawDepth - 1 : slot - 1);
-      PROF_BEGIN
-      cp_async_wait<C::kRawDepth - 1>();
-      PROF_END(0)
+    for (int g = team; g < total; g += kTeams) {
       uint4 v[A_BITS];
 #pragma unroll
-      for (int i = 0; i < A_BITS; ++i) v[i] = lds128(raw_base + uint32_t(slot * A_BITS + i) * kRawPlane);
-      if (++slot == C::kRawDepth) slot = 0;
+      for (int i = 0; i < A_BITS; ++i) v[i] = nxt[i];
+      advance_load();  // next step's words in flight during this step's expansion
       const int stage = g % S;
       PROF_BEGIN
       mbar_wait(smem_u32(empty + stage), ((g / S) & 1) ^ 1u);
@@ -528,17 +539,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < A_BITS; ++i) x ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
         if (x == 0x9e3779b9u) asm volatile("trap;");
       } else {
-      expand_to_tmem<0>(ta, v[0]);
-      if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
-      if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2]);
-      if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
+        expand_to_tmem<0>(ta, v[0]);
+        if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
+        if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2]);
+        if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(full_a + stage));
     }
-    cp_async_wait<0>();
   } else if (warp < kProducerWarps) {
     // producer warps of teams this configuration does not use: idle
   } else if (warp == kTmaWarp) {
@@ -772,6 +782,14 @@ cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cu
   const int64_t res_bytes = int64_t(a.nchunks) * C::kBBytes;
   a.b_resident = allow_res && a.ntn == 1 && fixed + res_bytes <= kSmemLimit;
   a.b_bytes = int(a.b_resident ? res_bytes : int64_t(C::kStages) * C::kBBytes);
+  a.div_hw = make_fastdiv(uint32_t(p.oh) * uint32_t(p.ow));
+  a.div_ow = make_fastdiv(uint32_t(p.ow));
+  a.div_kwid = make_fastdiv(uint32_t(p.kwid));
+  a.div_ntn = make_fastdiv(uint32_t(a.ntn));
+  a.div_kwa = make_fastdiv(uint32_t(p.kw_a));
+  a.kwa_shift = -1;
+  for (int sh = 0; sh < 31; ++sh)
+    if ((1 << sh) == p.kw_a) a.kwa_shift = sh;
   const char* dbg_env = getenv("BS_TC_DEBUG");
   a.debug = dbg_env ? atoi(dbg_env) : 0;
   int smem_bytes = int(fixed) + a.b_bytes;
