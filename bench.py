@@ -107,6 +107,11 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+def tc_fmt(args):
+    import paper_1810_11066_b200 as bs
+    return bs.TC_I8 if args.tc_format == "i8" else bs.TC_F4
+
+
 def binops_conv(L, n, a_bits, w_bits):
     oh = (L.h + 2 * L.pad - L.k) // L.s + 1
     return 2 * n * oh * oh * L.oc * L.k * L.k * L.ic * a_bits * w_bits
@@ -116,7 +121,7 @@ def binops_conv(L, n, a_bits, w_bits):
 class ConvLayerRun:
     """One conv layer on this rank's batch shard: resident inputs/outputs in HBM."""
 
-    def __init__(self, L, act_cpu, wt_cpu, a_bits, w_bits, bipolar, dev, path="tc"):
+    def __init__(self, L, act_cpu, wt_cpu, a_bits, w_bits, bipolar, dev, path="tc", fmt=0):
         import paper_1810_11066_b200 as bs
         self.bs, self.L, self.path = bs, L, path
         self.a_bits, self.w_bits, self.enc = a_bits, w_bits, (bs.BIPOLAR if bipolar else bs.UNIPOLAR)
@@ -129,7 +134,8 @@ class ConvLayerRun:
         self.ws = torch.empty(bs.conv2d_workspace_bytes(self.n, L.h, L.w, L.ic, a_bits), dtype=torch.uint8, device=dev)
         self.packed = self.ws.view(torch.int32).view(a_bits, self.n * L.h * L.w, bs.packed_row_words(L.ic))
         # tensor-core path: weight planes expanded once, offline like the packing itself
-        self.w_tc = (bs.conv2d_tc_prepare_weights(self.wp, w_bits, self.enc, L.oc, L.k, L.k, L.ic)
+        self.fmt = fmt
+        self.w_tc = (bs.conv2d_tc_prepare_weights(self.wp, w_bits, self.enc, L.oc, L.k, L.k, L.ic, tc_format=fmt)
                      if path == "tc" else None)
 
     def binops(self):
@@ -139,7 +145,7 @@ class ConvLayerRun:
         L = self.L
         if self.path == "tc":
             self.bs.bitserial_conv2d_nhwc_tc_i8(self.act, self.a_bits, self.w_tc, self.w_bits, L.oc, L.k, L.k,
-                                                L.s, L.pad, out=self.out, workspace=self.ws)
+                                                L.s, L.pad, out=self.out, workspace=self.ws, tc_format=self.fmt)
         else:
             self.bs.bitserial_conv2d_nhwc_i8(self.act, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k,
                                              L.s, L.pad, out=self.out, workspace=self.ws)
@@ -151,7 +157,8 @@ class ConvLayerRun:
         L = self.L
         if self.path == "tc":
             self.bs.bitserial_conv2d_nhwc_tc_prepared(self.packed, self.a_bits, self.w_tc, self.w_bits, self.n, L.h,
-                                                      L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
+                                                      L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out,
+                                                      tc_format=self.fmt)
         else:
             self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h,
                                           L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
@@ -165,7 +172,7 @@ class ConvLayerRun:
         ah, oh_, ad, od = bufs
         if self.path == "tc":
             self.bs.bitserial_conv2d_nhwc_tc_host(ah, self.a_bits, self.w_tc, self.w_bits, L.oc, L.k, L.k, L.s,
-                                                  L.pad, oh_, ad, od, self.ws)
+                                                  L.pad, oh_, ad, od, self.ws, tc_format=self.fmt)
         else:
             self.bs.bitserial_conv2d_nhwc_host(ah, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k, L.s,
                                                L.pad, oh_, ad, od, self.ws)
@@ -187,7 +194,7 @@ class ConvWorkload:
             act, wt = inputs.conv_operands(L, batch, args.a_bits, args.w_bits,
                                            inputs.seed_for(config_id, args.a_bits, args.w_bits, enc, li))
             self.runs.append(ConvLayerRun(L, act[lo:hi].contiguous(), wt, args.a_bits, args.w_bits, args.bipolar,
-                                          dev, args.path))
+                                          dev, args.path, tc_fmt(args)))
         self.total_binops = self.replicas * sum(binops_conv(inputs.TABLE1[li], batch, args.a_bits, args.w_bits)
                                                 for li in layers)
         self.config_id = config_id
@@ -204,6 +211,7 @@ class ConvWorkload:
                      "per layer: bitpack(act) + AND/POPC bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights "
                      "prepacked, untimed)"),
             "path": args.path,
+            "tc_format": args.tc_format if args.path == "tc" else None,
         }
 
     def step(self):
@@ -223,7 +231,8 @@ class ConvWorkload:
         ops = sum(r.binops() for r in self.runs)
         pack_bytes = sum(r.act.numel() * (1 + r.a_bits / 8) for r in self.runs)
         tc = self.args.path == "tc"
-        kname = "tc_conv_kernel (tcgen05 kind::i8" if tc else "popc_conv_kernel ("
+        kname = (f"tc_conv_kernel (tcgen05 kind::{'mxf4' if self.args.tc_format == 'f4' else 'i8'};" if tc else
+                 "popc_conv_kernel (")
         return {"kind": "tensor" if tc else "alu",
                 "kernel": f"{kname} sum over the {len(self.runs)} layer launches of one step, rank 0)",
                 "ops": ops, "ms": sum(conv_ms), "launches": len(self.runs),
@@ -298,7 +307,9 @@ class DenseWorkload:
         self.wp = bs.bitpack(w.to(dev), args.w_bits)  # untimed
         del w
         self.tc = args.path == "tc" and (hi - lo) > 8  # GEMV (m <= 8) stays on the HBM-bound matvec kernel
-        self.w_tc = bs.dense_tc_prepare_weights(self.wp, args.w_bits, self.enc, n, k) if self.tc else None
+        self.fmt = tc_fmt(args)
+        self.w_tc = (bs.dense_tc_prepare_weights(self.wp, args.w_bits, self.enc, n, k, tc_format=self.fmt)
+                     if self.tc else None)
         self.out = torch.empty((hi - lo, n), dtype=torch.int32, device=dev)
         self.full = torch.empty((m, n), dtype=torch.int32, device=dev) if gather else None
         self.ws = torch.empty(max(16, bs.dense_workspace_bytes(hi - lo, k, args.a_bits)), dtype=torch.uint8, device=dev)
@@ -322,7 +333,7 @@ class DenseWorkload:
     def step(self):
         if self.tc:
             self.bs.bitserial_dense_tc_i8(self.a, self.a_bits, self.w_tc, self.w_bits, self.n, out=self.out,
-                                          workspace=self.ws)
+                                          workspace=self.ws, tc_format=self.fmt)
         else:
             self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
                                        workspace=self.ws)
@@ -340,7 +351,7 @@ class DenseWorkload:
                                            workspace=self.ws)
             elif self.tc:
                 self.bs.bitserial_dense_tc_prepared(self.packed, self.a_bits, self.w_tc, self.w_bits, rows, self.n,
-                                                    self.k, out=self.out)
+                                                    self.k, out=self.out, tc_format=self.fmt)
             else:
                 self.bs.bitserial_dense(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, rows, self.n,
                                         self.k, out=self.out)
@@ -374,7 +385,8 @@ class DenseWorkload:
             return {"kind": "hbm", "kernel": "gemv_kernel (fused pack + GEMV, one launch, cold L2)", "bytes": nbytes,
                     "ops": ops, "ms": ms, "breakdown": {"gemv_ms": ms}}
         return {"kind": "tensor" if self.tc else "alu",
-                "kernel": ("tc_conv_kernel (tcgen05 kind::i8; dense = 1x1 implicit GEMM, rank 0 shard)" if self.tc else
+                "kernel": (f"tc_conv_kernel (tcgen05 kind::{'mxf4' if self.args.tc_format == 'f4' else 'i8'}; dense = "
+                           "1x1 implicit GEMM, rank 0 shard)" if self.tc else
                            "popc_conv_kernel (dense = 1x1 implicit GEMM, rank 0 shard)"), "ops": ops,
                 "ms": ms, "launches": 1, "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
 
@@ -522,19 +534,24 @@ def run_ours(args):
     r_popc = 64.0 * POPC_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     r_int = 2.0 * r_popc
     if roof["kind"] == "tensor":
-        # binary dot products as int8 x int8 -> int32 MMAs on 0/1 (or +-2^j) bytes: one
-        # binary MAC = one int8 MAC, so the roofline is the int8 tensor peak = 2 x the
-        # measured bf16 peak (tools/mma_bench.cu: kind::i8 sustains exactly 2x the
-        # kind::f16 MACs per clock per SM); burst figure (kernels timed alone).
-        peak = 2.0 * peaks["bf16_tflops"]
+        # binary dot products on the tensor cores: one binary MAC = one MAC of the MMA kind
+        # in use.  FP4 (kind::mxf4, the default format): peak = 4 x the measured bf16 peak
+        # (B200_PROFILING.md nominal 9 vs 2.25 PFLOP/s); I8 (kind::i8): 2 x (measured with
+        # tools/mma_bench.cu: kind::i8 sustains exactly 2x the kind::f16 MACs per clock).
+        # Burst figure (each kernel timed alone).
+        f4 = args.tc_format != "i8"
+        ratio = 4.0 if f4 else 2.0
+        peak = ratio * peaks["bf16_tflops"]
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
+        sustained = ratio * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "binary TOPS",
                     "frac": achieved / peak, "traffic": None, "kernel": roof["kernel"],
-                    "peak_basis": f"int8 dense tensor peak = 2 x bf16_tflops ({peaks['bf16_tflops']:.1f}, "
-                                  f"{peaks_src}); 1 binary MAC = 1 int8 MAC",
-                    "peak_sustained": 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
-                    "frac_sustained": achieved / (2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])),
-                    "frac_of_nominal_4500": achieved / 4500.0,
+                    "mma_kind": "kind::mxf4 (E2M1 bits, UE8M0 plane scales, FP32 accum)" if f4 else
+                                "kind::i8 (0/1 bytes, int32 accum)",
+                    "peak_basis": f"{'FP4' if f4 else 'INT8'} dense tensor peak = {ratio:.0f} x bf16_tflops "
+                                  f"({peaks['bf16_tflops']:.1f}, {peaks_src}); 1 binary MAC = 1 MMA MAC",
+                    "peak_sustained": sustained, "frac_sustained": achieved / sustained,
+                    "frac_of_int8_peak": achieved / (2.0 * peaks["bf16_tflops"]),
                     "r_popc": r_popc, "x_r_popc": achieved / r_popc}
     elif roof["kind"] == "alu":
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
@@ -581,7 +598,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "vs_baseline": None,
-            "dtype": ("u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32"
+            "dtype": (("u8 codes -> packed u32 bit-planes -> e2m1 0/0.5 planes x ue8m0 2^i scales on tcgen05 "
+                       "kind::mxf4 (fp32 accum, exact) -> i32" if args.tc_format == "f4" else
+                       "u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32")
                       if args.path == "tc" else "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32"),
             "scaling": "weak" if getattr(wl, "replicas", 1) > 1 else "strong",
             "data": "synthetic (seeded uniform codes, PAPER.md Table 1 / BASELINE shapes; no dataset)",
@@ -666,6 +685,8 @@ def main():
     ap.add_argument("--w-bits", type=int, default=1)
     ap.add_argument("--unipolar", dest="bipolar", action="store_false")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
+                    help="tensor-core operand format: block-scaled FP4 (default) or INT8")
     ap.add_argument("--path", choices=["tc", "popc"], default="tc",
                     help="conv/GEMM kernel: tensor-core bitserial (default) or the AND/POPC integer-pipe kernel")
     ap.add_argument("--no-e2e", action="store_true")

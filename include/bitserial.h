@@ -168,7 +168,7 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
                                 void* workspace, int64_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
- * Tensor-core bitserial (tcgen05.mma kind::i8 on sm_100a).  Same operation and
+ * Tensor-core bitserial (tcgen05.mma on sm_100a, format BS_TC_DEFAULT).  Same operation and
  * operands as bs_bitserial_conv2d_nhwc / bs_bitserial_dense.  Each activation plane i
  * and weight plane j is expanded inside the kernel (weights: by a first kernel into
  * `workspace`) to bytes 2^i*a_i and 2^j*b_j (unipolar) or 2^j*(2b_j-1) (bipolar), and
@@ -176,7 +176,8 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
  * cores: popcount(a_i AND w_j) = sum_k a_i[k] w_j[k] (Eq. 1), weighted
  * 2^(i+j) (Eq. 2); cost still grows with A*W.
  * Supported: a_bits in [1,4], w_bits in [1,2] (BS_ERR_UNSUPPORTED otherwise).
- * workspace: device, >= *_tc_workspace_bytes(), 16-byte aligned, overwritten.
+ * workspace: device, >= *_tc_workspace_bytes() (the larger, I8, size), 16-byte aligned,
+ * overwritten.
  */
 int64_t bs_conv2d_tc_workspace_bytes(int oc, int kh, int kw, int c, int w_bits);
 int bs_bitserial_conv2d_nhwc_tc(const uint32_t* act_packed, int a_bits,
@@ -190,37 +191,54 @@ int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits,
                           int32_t* out, int64_t m, int64_t n, int64_t k,
                           void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Operand format of the tensor-core path (same results, bit-exact; different speed):
+ *   BS_TC_I8  : every plane pair as tcgen05.mma.kind::i8 on bytes 2^i*a_i (u8) and
+ *               2^j*b_j or 2^j*(2b_j-1) (s8), int32 accumulation.
+ *   BS_TC_F4  : tcgen05.mma.kind::mxf4 (block-scaled FP4): bits as packed E2M1 nibbles
+ *               0.5*b (weights +-0.5 when bipolar), the plane weights 2^(i+1), 2^(j+1) as
+ *               UE8M0 block scales, FP32 accumulation.  Every product and partial sum is
+ *               an integer (times 2^-2) far below 2^24, so the FP32 result is exact and is
+ *               converted to int32 (tools/mxf4_probe.cu checks exactness up to |sum| >
+ *               the 737,280 accumulator bound of the configs).  Twice the MAC rate of i8.
+ *   BS_TC_DEFAULT (0): the library's choice (BS_TC_F4).
+ * Prepared weights are format-specific: prepare and run with the same format. */
+typedef enum { BS_TC_DEFAULT = 0, BS_TC_I8 = 1, BS_TC_F4 = 2 } bs_tc_format;
+
 /* Prepared weights for the tensor-core path.  Weight packing is done ahead of time
  * and is not timed; the expansion of the packed weight planes into the
- * tensor-core byte layout is part of that offline step:
- *   w_tc : device int8 [w_bits][oc][Kpad*32] (dense: [w_bits][n][Kpad*32]) with
- *          Kpad = K words (kh*kw*bs_packed_row_words(c), dense bs_packed_row_words(k))
- *          rounded up to a multiple of 4; byte = 2^j*b_j (unipolar) or 2^j*(2b_j-1)
- *          (bipolar), so the encoding is baked into w_tc.
- *   w_tc_bytes >= bs_conv2d_tc_workspace_bytes() / bs_dense_tc_workspace_bytes().
+ * tensor-core operand layout is part of that offline step:
+ *   w_tc : device [w_bits][oc][Kpad*B] bytes (dense: [w_bits][n][Kpad*B]), B = 32 (I8)
+ *          or 16 (F4) bytes per packed word, Kpad = K words (kh*kw*bs_packed_row_words(c),
+ *          dense bs_packed_row_words(k)) rounded up to a multiple of 4; the encoding
+ *          (unipolar / bipolar) is baked into w_tc.
+ *   w_tc_bytes >= bs_conv2d_tc_weight_bytes() / bs_dense_tc_weight_bytes() (0 on bad
+ *   arguments).
  */
+int64_t bs_conv2d_tc_weight_bytes(int oc, int kh, int kw, int c, int w_bits, int tc_format);
+int64_t bs_dense_tc_weight_bytes(int64_t n, int64_t k, int w_bits, int tc_format);
 int bs_conv2d_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
-                                 int8_t* w_tc, int64_t w_tc_bytes, void* stream);
+                                 int tc_format, int8_t* w_tc, int64_t w_tc_bytes, void* stream);
 int bs_dense_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t k,
-                                int8_t* w_tc, int64_t w_tc_bytes, void* stream);
+                                int tc_format, int8_t* w_tc, int64_t w_tc_bytes, void* stream);
 
 /* Tensor-core conv / dense on prepared weights (one launch: the persistent tcgen05
  * kernel; out as in bs_bitserial_conv2d_nhwc / bs_bitserial_dense). */
 int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, const int8_t* w_tc, int w_bits,
-                                         int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
-                                         int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
+                                         int tc_format, int32_t* out, int n, int h, int w, int c, int oc, int kh,
+                                         int kw, int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
 int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, const int8_t* w_tc, int w_bits,
-                                   int32_t* out, int64_t m, int64_t n, int64_t k, void* stream);
+                                   int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k, void* stream);
 
 /* The timed step of the paper on the tensor-core path: activation
  * bit-packing (raw uint8 codes -> workspace of *_workspace_bytes() bytes) followed by
  * the tensor-core conv / dense on prepared weights.  Two launches. */
-int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out,
-                                   int n, int h, int w, int c, int oc, int kh, int kw,
+int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t* w_tc, int w_bits, int tc_format,
+                                   int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
                                    int stride_h, int stride_w, int pad_h, int pad_w,
                                    void* workspace, int64_t workspace_bytes, void* stream);
-int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, int w_bits, int32_t* out,
-                             int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes, void* stream);
+int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, int w_bits, int tc_format,
+                             int32_t* out, int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes,
+                             void* stream);
 
 /* ---------------------------------------------------------------------------
  * End-to-end entry with HOST activations and HOST output (used for the bench's
@@ -238,7 +256,7 @@ int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits,
 
 /* As above on the tensor-core path with prepared weights (bs_bitserial_conv2d_nhwc_tc_i8). */
 int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, const int8_t* w_tc, int w_bits,
-                                     int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+                                     int tc_format, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
                                      int stride_h, int stride_w, int pad_h, int pad_w,
                                      uint8_t* act_dev, int32_t* out_dev,
                                      void* workspace, int64_t workspace_bytes, void* stream);

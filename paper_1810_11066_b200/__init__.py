@@ -25,10 +25,12 @@ __all__ = [
     "bitserial_conv2d_nhwc_tc", "bitserial_dense_tc", "conv2d_tc_workspace_bytes", "dense_tc_workspace_bytes",
     "conv2d_tc_prepare_weights", "dense_tc_prepare_weights", "bitserial_conv2d_nhwc_tc_prepared",
     "bitserial_dense_tc_prepared", "bitserial_conv2d_nhwc_tc_i8", "bitserial_dense_tc_i8",
-    "bitserial_conv2d_nhwc_tc_host", "EXPORTED_SYMBOLS",
+    "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
+    "TC_F4", "EXPORTED_SYMBOLS",
 ]
 
 UNIPOLAR, BIPOLAR = 0, 1
+TC_DEFAULT, TC_I8, TC_F4 = 0, 1, 2  # bs_tc_format
 ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV = 0, 1, 2, 3
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -45,7 +47,7 @@ EXPORTED_SYMBOLS = (
     "bs_bitserial_conv2d_nhwc_tc", "bs_dense_tc_workspace_bytes", "bs_bitserial_dense_tc",
     "bs_conv2d_tc_prepare_weights", "bs_dense_tc_prepare_weights", "bs_bitserial_conv2d_nhwc_tc_prepared",
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
-    "bs_bitserial_conv2d_nhwc_tc_host",
+    "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
 )
 
 
@@ -86,13 +88,15 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tc": ([P, I, P, I, I, P] + [I] * 11 + [P, L, P], I),
         "bs_dense_tc_workspace_bytes": ([L, L, I], L),
         "bs_bitserial_dense_tc": ([P, I, P, I, I, P, L, L, L, P, L, P], I),
-        "bs_conv2d_tc_prepare_weights": ([P, I, I, I, I, I, I, P, L, P], I),
-        "bs_dense_tc_prepare_weights": ([P, I, I, L, L, P, L, P], I),
-        "bs_bitserial_conv2d_nhwc_tc_prepared": ([P, I, P, I, P] + [I] * 11 + [P], I),
-        "bs_bitserial_dense_tc_prepared": ([P, I, P, I, P, L, L, L, P], I),
-        "bs_bitserial_conv2d_nhwc_tc_i8": ([P, I, P, I, P] + [I] * 11 + [P, L, P], I),
-        "bs_bitserial_dense_tc_i8": ([P, I, P, I, P, L, L, L, P, L, P], I),
-        "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, P, I, P] + [I] * 11 + [P, P, P, L, P], I),
+        "bs_conv2d_tc_weight_bytes": ([I, I, I, I, I, I], L),
+        "bs_dense_tc_weight_bytes": ([L, L, I, I], L),
+        "bs_conv2d_tc_prepare_weights": ([P, I, I, I, I, I, I, I, P, L, P], I),
+        "bs_dense_tc_prepare_weights": ([P, I, I, L, L, I, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_prepared": ([P, I, P, I, I, P] + [I] * 11 + [P], I),
+        "bs_bitserial_dense_tc_prepared": ([P, I, P, I, I, P, L, L, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_i8": ([P, I, P, I, I, P] + [I] * 11 + [P, L, P], I),
+        "bs_bitserial_dense_tc_i8": ([P, I, P, I, I, P, L, L, L, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, P, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -265,50 +269,62 @@ def bitserial_dense_tc(a_packed, a_bits, w_packed, w_bits, w_enc, m, n, k, out=N
     return out
 
 
-def conv2d_tc_prepare_weights(w_packed, w_bits, w_enc, oc, kh, kw, c, out=None, stream=None):
-    """bs_conv2d_tc_prepare_weights: packed OHWI weights -> prepared (expanded) int8
-    tensor-core weights [w_bits][oc][Kpad*32] (offline, like weight packing)."""
+def conv2d_tc_weight_bytes(oc, kh, kw, c, w_bits, tc_format=TC_DEFAULT) -> int:
+    return int(_load().bs_conv2d_tc_weight_bytes(oc, kh, kw, c, w_bits, int(tc_format)))
+
+
+def dense_tc_weight_bytes(n, k, w_bits, tc_format=TC_DEFAULT) -> int:
+    return int(_load().bs_dense_tc_weight_bytes(n, k, w_bits, int(tc_format)))
+
+
+def conv2d_tc_prepare_weights(w_packed, w_bits, w_enc, oc, kh, kw, c, tc_format=TC_DEFAULT, out=None, stream=None):
+    """bs_conv2d_tc_prepare_weights: packed OHWI weights -> prepared (expanded) tensor-core
+    weights for `tc_format` (offline, like weight packing)."""
     if out is None:
-        out = torch.empty(max(16, conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits)), dtype=torch.int8,
+        out = torch.empty(max(16, conv2d_tc_weight_bytes(oc, kh, kw, c, w_bits, tc_format)), dtype=torch.int8,
                           device=w_packed.device)
     _check(_load().bs_conv2d_tc_prepare_weights(_dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc), oc, kh, kw,
-                                                c, _dev(out, "w_tc", torch.int8), out.numel(), _stream(stream)))
+                                                c, int(tc_format), _dev(out, "w_tc", torch.int8), out.numel(),
+                                                _stream(stream)))
     return out
 
 
-def dense_tc_prepare_weights(w_packed, w_bits, w_enc, n, k, out=None, stream=None):
-    """bs_dense_tc_prepare_weights: packed [n][k] weights -> prepared int8 tensor-core weights."""
+def dense_tc_prepare_weights(w_packed, w_bits, w_enc, n, k, tc_format=TC_DEFAULT, out=None, stream=None):
+    """bs_dense_tc_prepare_weights: packed [n][k] weights -> prepared tensor-core weights."""
     if out is None:
-        out = torch.empty(max(16, dense_tc_workspace_bytes(n, k, w_bits)), dtype=torch.int8, device=w_packed.device)
+        out = torch.empty(max(16, dense_tc_weight_bytes(n, k, w_bits, tc_format)), dtype=torch.int8,
+                          device=w_packed.device)
     _check(_load().bs_dense_tc_prepare_weights(_dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc), n, k,
-                                               _dev(out, "w_tc", torch.int8), out.numel(), _stream(stream)))
+                                               int(tc_format), _dev(out, "w_tc", torch.int8), out.numel(),
+                                               _stream(stream)))
     return out
 
 
 def bitserial_conv2d_nhwc_tc_prepared(act_packed, a_bits, w_tc, w_bits, n, h, w, c, oc, kh, kw, stride=1, pad=0,
-                                      out=None, stream=None):
+                                      out=None, tc_format=TC_DEFAULT, stream=None):
     """bs_bitserial_conv2d_nhwc_tc_prepared: packed activations x prepared weights -> int32 NHWC."""
     sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
     if out is None:
         out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act_packed.device)
     _check(_load().bs_bitserial_conv2d_nhwc_tc_prepared(
-        _dev(act_packed, "act_packed", torch.int32), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits,
+        _dev(act_packed, "act_packed", torch.int32), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
         _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _stream(stream)))
     return out
 
 
-def bitserial_dense_tc_prepared(a_packed, a_bits, w_tc, w_bits, m, n, k, out=None, stream=None):
+def bitserial_dense_tc_prepared(a_packed, a_bits, w_tc, w_bits, m, n, k, out=None, tc_format=TC_DEFAULT,
+                                stream=None):
     """bs_bitserial_dense_tc_prepared: packed activations x prepared weights -> int32 [m][n]."""
     if out is None:
         out = torch.empty((m, n), dtype=torch.int32, device=a_packed.device)
     _check(_load().bs_bitserial_dense_tc_prepared(_dev(a_packed, "a_packed", torch.int32), a_bits,
-                                                  _dev(w_tc, "w_tc", torch.int8), w_bits,
+                                                  _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
                                                   _dev(out, "out", torch.int32), m, n, k, _stream(stream)))
     return out
 
 
 def bitserial_conv2d_nhwc_tc_i8(act, a_bits, w_tc, w_bits, oc, kh, kw, stride=1, pad=0, out=None, workspace=None,
-                                stream=None):
+                                tc_format=TC_DEFAULT, stream=None):
     """bs_bitserial_conv2d_nhwc_tc_i8: raw uint8 NHWC activations packed inside the call,
     then the tensor-core conv on prepared weights (the timed step)."""
     n, h, w, c = act.shape
@@ -319,13 +335,14 @@ def bitserial_conv2d_nhwc_tc_i8(act, a_bits, w_tc, w_bits, oc, kh, kw, stride=1,
         workspace = torch.empty(max(conv2d_workspace_bytes(n, h, w, c, a_bits), 16), dtype=torch.uint8,
                                 device=act.device)
     _check(_load().bs_bitserial_conv2d_nhwc_tc_i8(
-        _dev(act, "act", torch.uint8), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, _dev(out, "out", torch.int32),
+        _dev(act, "act", torch.uint8), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
+        _dev(out, "out", torch.int32),
         n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _dev(workspace, "workspace", torch.uint8), workspace.numel(),
         _stream(stream)))
     return out
 
 
-def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, stream=None):
+def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, tc_format=TC_DEFAULT, stream=None):
     """bs_bitserial_dense_tc_i8: raw uint8 activations [m][k] packed inside the call, then
     the tensor-core dense product on prepared weights."""
     m, k = a.shape
@@ -334,14 +351,14 @@ def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, 
     if workspace is None:
         workspace = torch.empty(max(dense_workspace_bytes(m, k, a_bits), 16), dtype=torch.uint8, device=a.device)
     _check(_load().bs_bitserial_dense_tc_i8(_dev(a, "a", torch.uint8), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits,
-                                            _dev(out, "out", torch.int32), m, n, k,
+                                            int(tc_format), _dev(out, "out", torch.int32), m, n, k,
                                             _dev(workspace, "workspace", torch.uint8), workspace.numel(),
                                             _stream(stream)))
     return out
 
 
 def bitserial_conv2d_nhwc_tc_host(act_host, a_bits, w_tc, w_bits, oc, kh, kw, stride, pad, out_host, act_dev, out_dev,
-                                  workspace, stream=None):
+                                  workspace, tc_format=TC_DEFAULT, stream=None):
     """bs_bitserial_conv2d_nhwc_tc_host: the e2e path (host in, host out) on the tensor-core kernel."""
     if act_host.device.type != "cpu" or out_host.device.type != "cpu":
         raise BitserialError("act_host/out_host must be CPU tensors")
@@ -350,7 +367,7 @@ def bitserial_conv2d_nhwc_tc_host(act_host, a_bits, w_tc, w_bits, oc, kh, kw, st
     n, h, w, c = act_host.shape
     sh, sw, ph, pw, _, _ = _conv_geom(n, h, w, kh, kw, stride, pad)
     _check(_load().bs_bitserial_conv2d_nhwc_tc_host(
-        ctypes.c_void_p(act_host.data_ptr()), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits,
+        ctypes.c_void_p(act_host.data_ptr()), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
         ctypes.c_void_p(out_host.data_ptr()), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
         _dev(act_dev, "act_dev", torch.uint8), _dev(out_dev, "out_dev", torch.int32),
         _dev(workspace, "workspace", torch.uint8), workspace.numel(), _stream(stream)))

@@ -45,14 +45,19 @@ cudaError_t launch_popc_conv(const ConvProblem& p, Algo algo, cudaStream_t strea
 // Tensor-core (tcgen05, kind::i8) bitserial kernel: one MMA per activation/weight
 // plane pair on expanded bit-planes (tc_conv.cu).  `wexp_ws` receives the expanded
 // weight planes (tc_weight_bytes bytes); cudaErrorNotSupported outside A<=4, W<=2.
+// Operand formats of the tensor-core path: kind::i8 bytes, or kind::mxf4 packed E2M1
+// nibbles with per-plane UE8M0 scales (tc_conv.cu).  kTcDefault is what format 0 means.
+constexpr int kTcI8 = 1, kTcF4 = 2;
+constexpr int kTcDefault = kTcF4;
+int tc_resolve_format(int fmt);
 int64_t tc_kpad(int64_t kp);
-int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits);
+int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt);
 bool tc_supported(int a_bits, int w_bits);
-// expanded ("prepared") weights: [w_bits][n][tc_kpad(kp)*32] bytes, offline like packing
+// expanded ("prepared") weights: [w_bits][n][tc_kpad(kp)*(32 | 16)] bytes, offline like packing
 cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int bipolar, int64_t n, int64_t kp,
-                                     int8_t* wexp, cudaStream_t stream);
-cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream);
-cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, cudaStream_t stream);
+                                     int8_t* wexp, int fmt, cudaStream_t stream);
+cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream);
+cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream);
 
 // Matrix-vector kernel for m <= 8 dense products.
 //   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)

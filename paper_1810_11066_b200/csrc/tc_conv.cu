@@ -285,6 +285,84 @@ __device__ __forceinline__ void expand_to_tmem(uint32_t taddr, uint4 v) {
   tmem_st32(taddr, o);
 }
 
+// ---- FP4 (kind::mxf4) operand format.  Elements are packed E2M1 nibbles, 8 per 32-bit
+// word; a bit b becomes the nibble 0b0001 (= 0.5) * b, and the plane weights 2^(i+1),
+// 2^(j+1) are the UE8M0 block scale factors (constant per plane), so 0.5*2^(i+1) * a_i *
+// 0.5*2^(j+1) * w_j = 2^(i+j) a_i w_j.  Bipolar weight bits are the nibbles +0.5 / -0.5
+// (0b0001 / 0b1001).  K order inside a packed word (shared with the weights): nibble r
+// of expanded word q (q < 4) holds element 4r + q, so expanded word q = (w >> q) & 0x1..1.
+// Products and partial sums are small integers times powers of two, exact in the FP32
+// accumulator (tools/mxf4_probe.cu: bit-exact up to |sum| = 803,600 > the 737,280 bound).
+__device__ __forceinline__ void expand_word_f4(uint32_t w, uint32_t (&o)[4]) {
+  o[0] = w & 0x11111111u;
+  o[1] = __umulhi(w, 1u << 31) & 0x11111111u;  // w >> 1 on the FMA pipe
+  o[2] = __umulhi(w, 1u << 30) & 0x11111111u;
+  o[3] = __umulhi(w, 1u << 29) & 0x11111111u;
+}
+
+// 16 consecutive 32-bit TMEM columns of this thread's lane <- o[0..15].
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7]), "r"(o[8]), "r"(o[9]),
+      "r"(o[10]), "r"(o[11]), "r"(o[12]), "r"(o[13]), "r"(o[14]), "r"(o[15])
+      : "memory");
+}
+
+// One plane's four packed words (128 K elements) -> 16 TMEM columns of packed E2M1.
+__device__ __forceinline__ void expand_to_tmem_f4(uint32_t taddr, uint4 v) {
+  uint32_t o[16], t[4];
+  expand_word_f4(v.x, t);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = t[q];
+  expand_word_f4(v.y, t);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[4 + q] = t[q];
+  expand_word_f4(v.z, t);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[8 + q] = t[q];
+  expand_word_f4(v.w, t);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[12 + q] = t[q];
+  tmem_st16(taddr, o);
+}
+
+// The 2 K-steps (64 elements = 8 TMEM columns / 32 bytes of B each) of one plane pair in
+// one 128-element chunk, kind::mxf4 with per-plane scale-factor regions in TMEM.
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma2_f4(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
+      "elect.sync x|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
+      "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "}" ::"r"(d),
+      "r"(a), "l"(b), "r"(accumulate), "n"(IDESC), "r"(sfa), "r"(sfb));
+}
+
+// Block-scaled instruction descriptor, kind::mxf4: A, B = E2M1, scales UE8M0, K = 64,
+// K-major, M = 128, N = BN (D is always F32).
+template <int BN>
+constexpr uint32_t idesc_mxf4() {
+  return (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
+}
+
+// 64B-swizzled K-major UMMA descriptor (FP4 B tiles: 64-byte rows of 128 elements):
+// SBO = 8 rows x 64 B = 512 B, layout type 4 = SWIZZLE_64B; base 512-byte aligned.
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
+
 // ------------------------------------------------------------------ weight expansion
 // w_packed [W][N][kp] words -> wexp [W][N][kpad*32] bytes (kpad = kp rounded up to
 // 4 words; bytes past kp*32 are 0), each 32-byte group in the transposed K order of
@@ -317,14 +395,48 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
   }
 }
 
+// FP4 layout: w_packed [W][N][kp] words -> wexp [W][N][kpad*16] bytes, 16 bytes (4
+// expanded words of 8 nibbles) per packed word in the order of expand_word_f4; nibble
+// = 0b0001 * b (unipolar) or b ? 0b0001 : 0b1001 (bipolar, +-0.5); scale 2^(j+1) at run time.
+__global__ void __launch_bounds__(256) expand_weights_f4_kernel(const uint32_t* __restrict__ w_packed,
+                                                                uint8_t* __restrict__ wexp, int w_bits, int n,
+                                                                int64_t kp, int64_t kpad, int bipolar) {
+  const int64_t words = int64_t(w_bits) * n * kpad;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < words; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t kk = t % kpad, rest = t / kpad;
+    const int64_t row = rest % n, j = rest / n;
+    const uint32_t w = kk < kp ? w_packed[(j * n + row) * kp + kk] : 0u;
+    uint32_t out[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // nibble r of expanded word q = element 4r + q
+      uint32_t v = 0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint32_t b = (w >> (4 * r + q)) & 1u;
+        const uint32_t nib = bipolar ? (b ? 0x1u : 0x9u) : b;
+        v |= nib << (4 * r);
+      }
+      out[q] = v;
+    }
+    *reinterpret_cast<uint4*>(wexp + (j * int64_t(n) + row) * kpad * 16 + kk * 16) =
+        make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
 // ----------------------------------------------------------------------- main kernel
-template <int A_BITS, int W_BITS, int BN>
+// F4 = false: kind::i8 (bytes, 128-byte B rows, SWIZZLE_128B); F4 = true: kind::mxf4
+// (packed E2M1, 64-byte B rows, SWIZZLE_64B, scale-factor regions in TMEM).  A chunk is
+// 128 K elements (4 packed words per plane per row) in both formats.
+template <int A_BITS, int W_BITS, int BN, bool F4>
 struct Cfg {
-  static constexpr int kACols = A_BITS * (BKB / 4);  // TMEM columns of one stage's A planes
-  static constexpr int kBBytes = W_BITS * BN * BKB;  // shared memory per stage (B only)
+  static constexpr int kBRow = F4 ? 64 : BKB;             // B bytes per row per plane per stage
+  static constexpr int kAColsPlane = F4 ? 16 : BKB / 4;    // TMEM columns per plane per stage
+  static constexpr int kACols = A_BITS * kAColsPlane;     // TMEM columns of one stage's A planes
+  static constexpr int kBBytes = W_BITS * BN * kBRow;     // shared memory per stage (B only)
+  static constexpr int kSFCols = F4 ? 32 : 0;             // SFA: 4 planes x 4 cols; SFB: 2 x 8
   static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
-  static constexpr int kFitTmem = (512 - 2 * BN) / kACols;  // accumulators: 2 x BN columns
+  static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
   // Every stage must always be filled by the same producer team: mbarrier waits are by
   // phase parity, and a team that could reach a stage two phases ahead of another team
@@ -335,7 +447,8 @@ struct Cfg {
   static constexpr int kUsed = kFixed + kStages * kBBytes;
   static constexpr int kBytes = kUsed < kMinSmem ? kMinSmem : kUsed;
   static constexpr int kTmemCols = 512;  // 2*BN accumulator columns + the A ring; one CTA per SM
-  static constexpr int kAcol0 = 2 * BN;  // first A-ring column
+  static constexpr int kSF0 = 2 * BN;               // first scale-factor column (F4)
+  static constexpr int kAcol0 = 2 * BN + kSFCols;   // first A-ring column
 };
 
 enum EpiMode : int { kEpiDirect = 0, kEpiTma = 1, kEpiScalar = 2 };
@@ -375,11 +488,11 @@ struct TcArgs {
 #define DBG(bit) 0
 #endif
 
-template <int A_BITS, int W_BITS, int BN>
+template <int A_BITS, int W_BITS, int BN, bool F4>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_conv_kernel(const TcArgs args, const __grid_constant__ CUtensorMap tmap_w,
                    const __grid_constant__ CUtensorMap tmap_out) {
-  using C = Cfg<A_BITS, W_BITS, BN>;
+  using C = Cfg<A_BITS, W_BITS, BN, F4>;
   constexpr int S = C::kStages;
   static_assert(S >= 2, "tensor-core tile does not fit two stages of shared memory");
   static_assert(C::kBytes <= kSmemLimit, "shared memory");
@@ -431,6 +544,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   // column 0, so TMEM addresses are compile-time constants
   if (*tmem_slot != 0u) asm volatile("trap;");
   constexpr uint32_t tmem = 0;
+  if constexpr (F4) {
+    // uniform UE8M0 scale factors: SFA plane i (4 columns) = 2^(i+1), SFB plane j (8
+    // columns) = 2^(j+1); every byte of a region holds the plane's scale, so the MMA reads
+    // the right value whatever its scale-factor layout (tools/mxf4_probe.cu: an M=128 /
+    // N<=128 region spans 4 columns, N=256 8)
+    if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+      uint32_t v[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = 0x01010101u * uint32_t(c < 16 ? 128 + (c >> 2) : 128 + ((c - 16) >> 3));
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+          "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+              tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::kSF0)),
+          "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+          "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+          "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),
+          "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+          : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   if (warp < 4 * C::kTeamsUsed) {
     // ================= expansion producers.  kTeams teams of 4 warps; team t expands the
@@ -539,10 +676,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < A_BITS; ++i) x ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
         if (x == 0x9e3779b9u) asm volatile("trap;");
       } else {
-        expand_to_tmem<0>(ta, v[0]);
-        if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
-        if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2]);
-        if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
+        if constexpr (F4) {
+#pragma unroll
+          for (int i = 0; i < A_BITS; ++i) expand_to_tmem_f4(ta + uint32_t(i * C::kAColsPlane), v[i]);
+        } else {
+          expand_to_tmem<0>(ta, v[0]);
+          if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
+          if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2]);
+          if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
+        }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
@@ -559,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kc = 0; kc < nchunks; ++kc) {
         const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
 #pragma unroll
-        for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * BKB, &tmap_w, kc * BKB, j * p.oc, fb);
+        for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc, fb);
       }
     } else if (lane == 0) {
       int stage = 0;
@@ -574,7 +716,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(fb, uint32_t(C::kBBytes));
           const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
 #pragma unroll
-          for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * BKB, &tmap_w, kc * BKB, j * p.oc + n0, fb);
+          for (int j = 0; j < W_BITS; ++j)
+            tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc + n0, fb);
           if (++stage == S) {
             stage = 0;
             phase ^= 1u;
@@ -585,11 +728,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer: the whole warp walks the loop (uniform values); one
     // elected lane issues.  TMEM base is column 0 (all 512 columns are this CTA's).
-    constexpr uint32_t kIdesc = idesc_i8<BN>();
+    constexpr uint32_t kIdesc = F4 ? idesc_mxf4<BN>() : idesc_i8<BN>();
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
     const bool resident = args.b_resident;
-    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(s_stage));
+    const uint64_t bdesc0 = F4 ? smem_desc_sw64(smem_u32(s_stage)) : smem_desc_sw128(smem_u32(s_stage));
     if (resident) mbar_wait(smem_u32(full_b), 0);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       PROF_BEGIN
@@ -610,9 +753,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < A_BITS; ++i)
 #pragma unroll
-          for (int j = 0; j < W_BITS; ++j)
-            mma4_ts<kIdesc>(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4),
-                            (kc | i | j) != 0);
+          for (int j = 0; j < W_BITS; ++j) {
+            if constexpr (F4)
+              mma2_f4<kIdesc>(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
+                              uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), (kc | i | j) != 0);
+            else
+              mma4_ts<kIdesc>(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4),
+                              (kc | i | j) != 0);
+          }
         mma_commit_elect(smem_u32(empty + stage));
         if (++stage == S) {
           stage = 0;
@@ -646,6 +794,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 32; ++c) r[c] = c;
         } else {
           tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + cb * 32), r);
+          if constexpr (F4) {  // FP32 accumulator holding an exact integer |v| < 2^22 -> int32:
+            // v + 1.5*2^23 puts v in the low mantissa bits (one FADD + one IADD instead of
+            // the quarter-rate F2I)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              r[c] = uint32_t(__float_as_int(__uint_as_float(r[c]) + 12582912.0f) - 0x4B400000);
+          }
         }
         if (cb == ncb - 1) {  // accumulator drained: release it to the MMA warp
           tc_fence_before();
@@ -742,7 +897,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
-               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[2] = {inner, outer};
@@ -750,14 +905,14 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int A_BITS, int W_BITS, int BN>
+template <int A_BITS, int W_BITS, int BN, bool F4>
 cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
-  using C = Cfg<A_BITS, W_BITS, BN>;
-  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN>;
+  using C = Cfg<A_BITS, W_BITS, BN, F4>;
+  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -795,12 +950,13 @@ cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cu
   int smem_bytes = int(fixed) + a.b_bytes;
   if (smem_bytes < kMinSmem) smem_bytes = kMinSmem;
   CUtensorMap tw, to;
-  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, uint64_t(kpad) * 32, uint64_t(W_BITS) * p.oc,
-                 uint64_t(kpad) * 32, BKB, BN))
+  const uint64_t wrow = uint64_t(kpad) * (F4 ? 16 : 32);  // prepared-weight row bytes
+  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, wrow, uint64_t(W_BITS) * p.oc, wrow, C::kBRow, BN,
+                 F4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   if (a.epi == kEpiTma) {
     if (!encode_2d(&to, CU_TENSOR_MAP_DATA_TYPE_INT32, p.out, uint64_t(p.oc), uint64_t(p.M), uint64_t(p.oc) * 4, 32,
-                   32))
+                   32, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   } else {
     to = tw;  // unused
@@ -822,51 +978,71 @@ int pick_bn(const ConvProblem& p, int64_t) {
   return p.oc <= 64 ? 64 : 128;
 }
 
-template <int A_BITS, int W_BITS>
+template <int A_BITS, int W_BITS, bool F4>
 cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
   switch (pick_bn<A_BITS, W_BITS>(p, kpad)) {
     case 128:
-      if constexpr (Cfg<A_BITS, W_BITS, 128>::kFit >= 2) return launch_bn<A_BITS, W_BITS, 128>(p, wexp, kpad, stream);
+      if constexpr (Cfg<A_BITS, W_BITS, 128, F4>::kFit >= 2)
+        return launch_bn<A_BITS, W_BITS, 128, F4>(p, wexp, kpad, stream);
       [[fallthrough]];
     default:
-      return launch_bn<A_BITS, W_BITS, 64>(p, wexp, kpad, stream);
+      return launch_bn<A_BITS, W_BITS, 64, F4>(p, wexp, kpad, stream);
   }
 }
 
 }  // namespace tc
 
+int tc_resolve_format(int fmt) {
+  if (fmt == kTcI8 || fmt == kTcF4) return fmt;
+  if (const char* e = getenv("BS_TC_FORMAT")) {  // experiments: i8 / f4
+    if (e[0] == 'i') return kTcI8;
+    if (e[0] == 'f') return kTcF4;
+  }
+  return kTcDefault;
+}
+
 int64_t tc_kpad(int64_t kp) { return (kp + tc::kWordsPerStage - 1) / tc::kWordsPerStage * tc::kWordsPerStage; }
 
-int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits) { return int64_t(w_bits) * n * tc_kpad(kp) * 32; }
+int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt) {
+  return int64_t(w_bits) * n * tc_kpad(kp) * (tc_resolve_format(fmt) == kTcF4 ? 16 : 32);
+}
 
 bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 2; }
 
 cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int bipolar, int64_t n, int64_t kp,
-                                     int8_t* wexp, cudaStream_t stream) {
+                                     int8_t* wexp, int fmt, cudaStream_t stream) {
   const int64_t kpad = tc_kpad(kp);
   const int64_t words = int64_t(w_bits) * n * kpad;
   int64_t blocks = (words + 255) / 256;
   if (blocks > 4096) blocks = 4096;
-  tc::expand_weights_kernel<<<unsigned(blocks), 256, 0, stream>>>(w_packed, wexp, w_bits, int(n), kp, kpad, bipolar);
+  if (tc_resolve_format(fmt) == kTcF4)
+    tc::expand_weights_f4_kernel<<<unsigned(blocks), 256, 0, stream>>>(w_packed, reinterpret_cast<uint8_t*>(wexp),
+                                                                       w_bits, int(n), kp, kpad, bipolar);
+  else
+    tc::expand_weights_kernel<<<unsigned(blocks), 256, 0, stream>>>(w_packed, wexp, w_bits, int(n), kp, kpad,
+                                                                    bipolar);
   note_launch();
   return cudaPeekAtLastError();
 }
 
-cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream) {
+cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
   const int64_t kpad = tc_kpad(p.kp);
-#define BS_TC(A, W) \
-  if (p.a_bits == A && p.w_bits == W) return tc::launch_aw<A, W>(p, wexp, kpad, stream);
+  const bool f4 = tc_resolve_format(fmt) == kTcF4;
+#define BS_TC(A, W)                                                                 \
+  if (p.a_bits == A && p.w_bits == W)                                               \
+    return f4 ? tc::launch_aw<A, W, true>(p, wexp, kpad, stream)                    \
+              : tc::launch_aw<A, W, false>(p, wexp, kpad, stream);
   BS_TC(1, 1) BS_TC(2, 1) BS_TC(2, 2) BS_TC(1, 2) BS_TC(3, 1) BS_TC(3, 2) BS_TC(4, 1) BS_TC(4, 2)
 #undef BS_TC
   return cudaErrorNotSupported;
 }
 
-cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, cudaStream_t stream) {
+cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
-  cudaError_t e = launch_tc_expand_weights(p.wt, p.w_bits, p.bipolar, p.oc, p.kp, wexp_ws, stream);
+  cudaError_t e = launch_tc_expand_weights(p.wt, p.w_bits, p.bipolar, p.oc, p.kp, wexp_ws, fmt, stream);
   if (e != cudaSuccess) return e;
-  return launch_tc_conv_prepared(p, wexp_ws, stream);
+  return launch_tc_conv_prepared(p, wexp_ws, fmt, stream);
 }
 
 }  // namespace bs

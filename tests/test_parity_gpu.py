@@ -308,21 +308,26 @@ def test_conv_tc_resnet_layers(layer):
 
 
 # ------------------------------------------- tensor-core path, prepared weights
-def _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, stride, pad, fused):
+TC_FORMATS = [bs.TC_I8, bs.TC_F4]
+
+
+def _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, stride, pad, fused, fmt=bs.TC_DEFAULT):
     n, h, w, c = act.shape
     oc, kh, kw, _ = wt.shape
     wp = gpu_pack(wt.reshape(oc * kh * kw, c), w_bits)
-    w_tc = bs.conv2d_tc_prepare_weights(wp, w_bits, enc(bipolar), oc, kh, kw, c)
+    w_tc = bs.conv2d_tc_prepare_weights(wp, w_bits, enc(bipolar), oc, kh, kw, c, tc_format=fmt)
     if fused:
-        return bs.bitserial_conv2d_nhwc_tc_i8(act.to(DEV), a_bits, w_tc, w_bits, oc, kh, kw, stride, pad)
+        return bs.bitserial_conv2d_nhwc_tc_i8(act.to(DEV), a_bits, w_tc, w_bits, oc, kh, kw, stride, pad,
+                                              tc_format=fmt)
     return bs.bitserial_conv2d_nhwc_tc_prepared(gpu_pack(act.reshape(-1, c), a_bits), a_bits, w_tc, w_bits,
-                                                n, h, w, c, oc, kh, kw, stride, pad)
+                                                n, h, w, c, oc, kh, kw, stride, pad, tc_format=fmt)
 
 
-@pytest.mark.parametrize("bn", ["64", "128", "256"])
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+@pytest.mark.parametrize("bn", ["64", "128"])
 @pytest.mark.parametrize("a_bits,w_bits", TC_PRECISIONS)
 @pytest.mark.parametrize("bipolar", [False, True])
-def test_conv_tc_every_tile_width(monkeypatch, bn, a_bits, w_bits, bipolar):
+def test_conv_tc_every_tile_width(monkeypatch, fmt, bn, a_bits, w_bits, bipolar):
     """Each compiled tile width (BS_TC_BN forces it; configurations that do not fit shared
     memory fall back to a narrower one) on a ragged case: M = 2*13*11 = 286 (3 row tiles,
     tail 30), OC = 300 (ragged column tiles, OC % 4 = 0 so the TMA-store epilogue runs),
@@ -332,15 +337,16 @@ def test_conv_tc_every_tile_width(monkeypatch, bn, a_bits, w_bits, bipolar):
     act = inputs.codes((2, 13, 11, 96), a_bits, g)
     wt = inputs.codes((300, 3, 3, 96), w_bits, g)
     ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(1, 1), pad=(1, 1))
-    got = _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, 1, 1, fused=True)
+    got = _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, 1, 1, fused=True, fmt=fmt)
     np.testing.assert_array_equal(got.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("fmt", TC_FORMATS)
 @pytest.mark.parametrize("resident", ["0", "1"])
 @pytest.mark.parametrize("epi", ["direct", "tma"])
 @pytest.mark.parametrize("a_bits,w_bits,bipolar", [(2, 1, True), (1, 2, False), (4, 2, True)])
 @pytest.mark.parametrize("oc", [64, 100, 128])
-def test_conv_tc_b_modes(monkeypatch, resident, epi, a_bits, w_bits, bipolar, oc):
+def test_conv_tc_b_modes(monkeypatch, fmt, resident, epi, a_bits, w_bits, bipolar, oc):
     """Weights resident in shared memory (one N block, whole K loaded once) versus the
     per-stage TMA ring, and the direct-store versus TMA-store epilogue, on a ragged
     3x3 s2 case (M = 3*10*10 = 300: 3 row tiles; K = 9 taps x 2 words = 5 chunks)."""
@@ -350,13 +356,14 @@ def test_conv_tc_b_modes(monkeypatch, resident, epi, a_bits, w_bits, bipolar, oc
     act = inputs.codes((3, 19, 20, 64), a_bits, g)
     wt = inputs.codes((oc, 3, 3, 64), w_bits, g)
     ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(2, 2), pad=(1, 1))
-    got = _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, 2, 1, fused=True)
+    got = _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, 2, 1, fused=True, fmt=fmt)
     np.testing.assert_array_equal(got.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("fmt", TC_FORMATS)
 @pytest.mark.parametrize("case", CONV_CASES)
 @pytest.mark.parametrize("fused", [False, True])
-def test_conv_tc_prepared_cases(case, fused):
+def test_conv_tc_prepared_cases(fmt, case, fused):
     """Prepared-weight entries (with and without in-call packing) on the ragged /
     odd-geometry cases, including OC % 4 != 0 (plain-store epilogue) and K tails."""
     n, h, w, c, oc, kh, kw, sh, sw, ph, pw = case
@@ -365,43 +372,64 @@ def test_conv_tc_prepared_cases(case, fused):
         act = inputs.codes((n, h, w, c), a_bits, g)
         wt = inputs.codes((oc, kh, kw, c), w_bits, g)
         ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(sh, sw), pad=(ph, pw))
-        got = _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, (sh, sw), (ph, pw), fused)
+        got = _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, (sh, sw), (ph, pw), fused, fmt)
         np.testing.assert_array_equal(got.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("fmt", TC_FORMATS)
 @pytest.mark.parametrize("m,n,k", [(1, 16, 32), (130, 64, 200), (257, 132, 1000), (384, 512, 4096), (300, 300, 33)])
 @pytest.mark.parametrize("a_bits,w_bits,bipolar", [(1, 1, False), (2, 1, True), (4, 2, True), (3, 2, False)])
-def test_dense_tc_prepared(m, n, k, a_bits, w_bits, bipolar):
+def test_dense_tc_prepared(fmt, m, n, k, a_bits, w_bits, bipolar):
     a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=17 * a_bits + w_bits + m + n + k)
     ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
-    w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, enc(bipolar), n, k)
-    got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n)
+    w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, enc(bipolar), n, k, tc_format=fmt)
+    got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=fmt)
     np.testing.assert_array_equal(got.cpu().numpy(), ref)
-    got2 = bs.bitserial_dense_tc_prepared(gpu_pack(a, a_bits), a_bits, w_tc, w_bits, m, n, k)
+    got2 = bs.bitserial_dense_tc_prepared(gpu_pack(a, a_bits), a_bits, w_tc, w_bits, m, n, k, tc_format=fmt)
     assert torch.equal(got, got2)
 
 
+@pytest.mark.parametrize("fmt", TC_FORMATS)
 @pytest.mark.parametrize("layer", inputs.BASELINE_LAYERS)
-def test_config4_batch256_tc_sampled_images(layer):
+def test_config4_batch256_tc_sampled_images(fmt, layer):
     """BASELINE configs[3] in the bench's launch configuration on the tensor-core path
     (prepared weights, whole batch of 256 in one bs_bitserial_conv2d_nhwc_tc_i8 call,
     persistent kernel over every tile); the oracle checks images 0, 77, 200 and 255."""
     L = inputs.TABLE1[layer]
     act, wt = inputs.conv_operands(L, 256, 2, 1, inputs.seed_for(4, 2, 1, "bipolar", layer))
-    got = _tc_conv_prepared(act, 2, wt, 1, True, L.s, L.pad, fused=True).cpu().numpy()
+    got = _tc_conv_prepared(act, 2, wt, 1, True, L.s, L.pad, fused=True, fmt=fmt).cpu().numpy()
     for img in (0, 77, 200, 255):
         ref = oracle.conv2d_nhwc(act[img:img + 1].numpy(), 2, wt.numpy(), 1, True,
                                  stride=(L.s, L.s), pad=(L.pad, L.pad))
         np.testing.assert_array_equal(got[img:img + 1], ref, err_msg=f"L{layer} image {img}")
 
 
-def test_tc_repeated_calls_stable():
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+def test_tc_repeated_calls_stable(fmt):
     """Persistent kernel re-launched back to back on one stream (as in the bench's CUDA
     graph): identical results every time (no stale TMEM / barrier state)."""
     L = inputs.TABLE1[6]
     act, wt = inputs.conv_operands(L, 8, 2, 1, seed=99)
-    first = _tc_conv_prepared(act, 2, wt, 1, True, L.s, L.pad, fused=True)
+    first = _tc_conv_prepared(act, 2, wt, 1, True, L.s, L.pad, fused=True, fmt=fmt)
     ref = oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(L.s, L.s), pad=(L.pad, L.pad))
     np.testing.assert_array_equal(first.cpu().numpy(), ref)
     for _ in range(5):
-        assert torch.equal(_tc_conv_prepared(act, 2, wt, 1, True, L.s, L.pad, fused=True), first)
+        assert torch.equal(_tc_conv_prepared(act, 2, wt, 1, True, L.s, L.pad, fused=True, fmt=fmt), first)
+
+
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+@pytest.mark.parametrize("a_bits,w_bits", [(4, 2), (2, 2)])
+def test_tc_accumulator_bound_extremes(fmt, a_bits, w_bits):
+    """All-max codes on a long reduction: the largest |out| the configs reach
+    (K * (2^A-1) * (2^W-1), BASELINE configs[4] A4W2 at K = 16384 -> 737,280) computed
+    exactly by both formats (the FP4 path accumulates in FP32, exact below 2^24)."""
+    m, n, k = 130, 72, 16384
+    for bipolar in (False, True):
+        a = torch.full((m, k), (1 << a_bits) - 1, dtype=torch.uint8)
+        w = torch.full((n, k), (1 << w_bits) - 1, dtype=torch.uint8)
+        w[1::2, ::3] = 0  # mixed signs / zeros in half the rows
+        ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+        w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, enc(bipolar), n, k, tc_format=fmt)
+        got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=fmt)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    assert int(np.abs(ref).max()) == k * ((1 << a_bits) - 1) * ((1 << w_bits) - 1)
