@@ -150,8 +150,8 @@ class ConvLayerRun:
             self.bs.bitserial_conv2d_nhwc_i8(self.act, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k,
                                              L.s, L.pad, out=self.out, workspace=self.ws)
 
-    def pack_only(self):
-        self.bs.bitpack(self.act, self.a_bits, out=self.packed)
+    def pack_only(self, max_ctas=0):
+        self.bs.bitpack(self.act, self.a_bits, out=self.packed, max_ctas=max_ctas)
 
     def conv_only(self):
         L = self.L
@@ -200,14 +200,22 @@ class ConvWorkload:
         self.config_id = config_id
         self.name = name
         self.graph_ok = True
+        # pack/conv overlap across layers (two streams) for the tensor-core path
+        self.overlap = args.path == "tc" and not args.no_overlap
+        if self.overlap:
+            self.side_stream = torch.cuda.Stream(device=dev)
+            self.pack_events = [torch.cuda.Event() for _ in self.runs]
+            self.pack_ctas = args.pack_ctas_per_sm * torch.cuda.get_device_properties(dev).multi_processor_count
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
             "layout": "NHWC/OHWI",
             "parallelism": (f"{world} independent replicas (batch 1 does not shard)" if self.replicas > 1 else
                             f"batch-sharded dp{world} (no collective)"),
             "rank0_images": [lo, hi],
-            "step": ("per layer: bitpack(act) + tensor-core bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_i8 "
-                     "(weights packed + plane-expanded once, untimed)" if args.path == "tc" else
+            "step": (("per layer: bitpack(act) [side stream, overlapping earlier layers' convs] + tensor-core "
+                      "bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_prepared" if not args.no_overlap else
+                      "per layer: bitpack(act) + tensor-core bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_i8")
+                     + " (weights packed + plane-expanded once, untimed)" if args.path == "tc" else
                      "per layer: bitpack(act) + AND/POPC bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights "
                      "prepacked, untimed)"),
             "path": args.path,
@@ -215,8 +223,30 @@ class ConvWorkload:
         }
 
     def step(self):
+        if self.overlap:
+            return self.step_overlapped()
         for r in self.runs:
             r.step()
+
+    def step_overlapped(self):
+        """Same work, two streams: the activation packing of every layer (bs_bitpack)
+        runs on a side stream, each layer's tensor-core conv (bs_..._tc_prepared) waits
+        only for its own layer's pack — packing of later layers overlaps the convs of
+        earlier ones (the layers' inputs are independent).  Captured into the step's CUDA
+        graph as parallel branches."""
+        main = torch.cuda.current_stream()
+        side = self.side_stream
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            for i, (r, e) in enumerate(zip(self.runs, self.pack_events)):
+                # the first layer's pack has nothing to overlap: full grid; later packs run beside
+                # the previous layer's persistent conv CTAs: a capped grid leaves them room
+                r.pack_only(0 if i == 0 else self.pack_ctas)
+                e.record(side)
+        for r, e in zip(self.runs, self.pack_events):
+            main.wait_event(e)
+            r.conv_only()
+        main.wait_stream(side)
 
     def roofline(self, reps):
         """Per-launch device time of the pack and conv kernels of every layer: each
@@ -685,6 +715,9 @@ def main():
     ap.add_argument("--w-bits", type=int, default=1)
     ap.add_argument("--unipolar", dest="bipolar", action="store_false")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="pack and conv of every layer in one stream")
+    ap.add_argument("--pack-ctas-per-sm", type=int, default=0,
+                    help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
     ap.add_argument("--path", choices=["tc", "popc"], default="tc",

@@ -108,6 +108,12 @@ int64_t bs_packed_row_words(int64_t k);
  */
 int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, void* stream);
 
+/* As bs_bitpack, with at most max_ctas thread blocks (0 = library choice).  A small
+ * grid (e.g. one block per SM) leaves the SMs room for a kernel running concurrently on
+ * another stream — the packing of one layer overlapping the tensor-core conv of another;
+ * each thread keeps several 32-byte groups in flight, so the pack stays near HBM speed. */
+int bs_bitpack_ex(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, int max_ctas, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Bitserial dense / matrix multiply (Sec. 3.2 and 6.2.1).
  *   out[m][n] = sum_{k<K} a[m][k] * value(w[n][k])          (int32 [m][n] row-major)

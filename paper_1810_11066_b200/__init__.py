@@ -41,6 +41,7 @@ _lib = None
 
 EXPORTED_SYMBOLS = (
     "bs_abi_version", "bs_status_string", "bs_last_error", "bs_kernel_launches", "bs_packed_row_words", "bs_bitpack",
+    "bs_bitpack_ex",
     "bs_bitserial_dense", "bs_bitserial_dense_ex", "bs_dense_workspace_bytes", "bs_bitserial_dense_i8",
     "bs_bitserial_conv2d_nhwc", "bs_bitserial_conv2d_nhwc_ex", "bs_conv2d_workspace_bytes",
     "bs_bitserial_conv2d_nhwc_i8", "bs_bitserial_conv2d_nhwc_host", "bs_conv2d_tc_workspace_bytes",
@@ -75,6 +76,7 @@ def _load():
         "bs_kernel_launches": ([], L),
         "bs_packed_row_words": ([L], L),
         "bs_bitpack": ([P, P, L, L, I, P], I),
+        "bs_bitpack_ex": ([P, P, L, L, I, I, P], I),
         "bs_bitserial_dense": ([P, I, P, I, I, P, L, L, L, P], I),
         "bs_bitserial_dense_ex": ([P, I, P, I, I, P, L, L, L, I, P], I),
         "bs_dense_workspace_bytes": ([L, L, I], L),
@@ -153,15 +155,15 @@ def conv2d_workspace_bytes(n: int, h: int, w: int, c: int, a_bits: int) -> int:
     return int(_load().bs_conv2d_workspace_bytes(n, h, w, c, a_bits))
 
 
-def bitpack(x: torch.Tensor, bits: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """bs_bitpack: uint8 codes [rows][k] (or any shape, reduction axis last) ->
-    int32-viewed uint32 words [bits][rows][packed_row_words(k)]."""
+def bitpack(x: torch.Tensor, bits: int, out: torch.Tensor | None = None, stream=None, max_ctas: int = 0) -> torch.Tensor:
+    """bs_bitpack(_ex): uint8 codes [rows][k] (or any shape, reduction axis last) ->
+    int32-viewed uint32 words [bits][rows][packed_row_words(k)]; max_ctas > 0 caps the grid."""
     k = x.shape[-1]
     rows = x.numel() // k
     if out is None:
         out = torch.empty((bits, rows, packed_row_words(k)), dtype=torch.int32, device=x.device)
-    _check(_load().bs_bitpack(_dev(x, "x", torch.uint8), _dev(out, "out", torch.int32), rows, k, bits,
-                              _stream(stream)))
+    _check(_load().bs_bitpack_ex(_dev(x, "x", torch.uint8), _dev(out, "out", torch.int32), rows, k, bits,
+                                 int(max_ctas), _stream(stream)))
     return out
 
 

@@ -172,12 +172,18 @@ int64_t bs_packed_row_words(int64_t k) { return row_words(k); }
 int64_t bs_kernel_launches(void) { return bs::launch_count(); }
 
 int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, void* stream) {
+  return bs_bitpack_ex(in, out, rows, k, bits, 0, stream);
+}
+
+int bs_bitpack_ex(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, int max_ctas, void* stream) {
   const char* fn = "bs_bitpack";
   if (!in || !out) return fail(BS_ERR_NULL, "%s: NULL tensor pointer", fn);
   if (bits < 1 || bits > 8) return fail(BS_ERR_INVALID_ARG, "%s: bits=%d not in [1,8]", fn, bits);
   if (rows <= 0 || k <= 0) return fail(BS_ERR_SHAPE, "%s: rows and k must be >= 1", fn);
   if (!aligned16(in) || !aligned16(out)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
-  return cuda_status(bs::launch_bitpack(in, out, rows, k, row_words(k), bits, static_cast<cudaStream_t>(stream)), fn);
+  if (max_ctas < 0) return fail(BS_ERR_INVALID_ARG, "%s: max_ctas < 0", fn);
+  return cuda_status(bs::launch_bitpack(in, out, rows, k, row_words(k), bits, static_cast<cudaStream_t>(stream),
+                                        max_ctas), fn);
 }
 
 int bs_bitserial_dense_ex(const uint32_t* a_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,

@@ -26,67 +26,105 @@ __device__ __forceinline__ void store_planes(uint32_t* dst, int64_t plane_stride
   }
 }
 
+// One (row, word) task: 32 codes -> one word per plane.
+template <int BITS>
+__device__ __forceinline__ void pack_word(const uint8_t* __restrict__ in, uint32_t* __restrict__ out, int64_t r,
+                                          int64_t j, int64_t k, int64_t kwp, int64_t plane_stride, int bits,
+                                          bool aligned16) {
+  const int64_t e0 = 32 * j;  // first element of this word
+  uint32_t v[8];
+  const uint8_t* src = in + r * k + e0;
+  if (aligned16 && e0 + 32 <= k) {
+    uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
+    uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+    v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+    v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+  } else if (aligned16 && e0 + 16 == k) {  // k % 32 == 16: last word half full
+    uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
+    v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+    v[4] = v[5] = v[6] = v[7] = 0u;
+  } else {  // ragged / unaligned rows, pad words: byte loads with bounds
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        int64_t e = e0 + 4 * q + rr;
+        if (e < k) x |= uint32_t(__ldg(src + 4 * q + rr)) << (8 * rr);
+      }
+      v[q] = x;
+    }
+  }
+  uint32_t* dst = out + r * kwp + j;
+  if constexpr (BITS > 0) {
+    store_planes<0, BITS>(dst, plane_stride, v);
+  } else {
+    for (int b = 0; b < bits; ++b) dst[b * plane_stride] = plane_word(v, b);
+  }
+}
+
 // POW2: kwp is a power of two (every ResNet channel count and the dense K of the
 // configs) -> the (row, word) split is a shift instead of a 64-bit division.
-template <int BITS, bool POW2>
+// FAST: k % 32 == 0 and 16-byte aligned rows — every task is two full 16-byte loads;
+// each thread keeps kBatch tasks (kBatch x 32 bytes) in flight, so the kernel reaches
+// HBM speed with few resident threads (it overlaps the tensor-core conv of another layer,
+// which leaves room for one 256-thread CTA per SM).
+template <int BITS, bool POW2, bool FAST>
 __global__ void __launch_bounds__(256) bitpack_kernel(const uint8_t* __restrict__ in, uint32_t* __restrict__ out,
                                                       int64_t rows, int64_t k, int64_t kwp, int kwp_shift,
                                                       int bits_rt, bool aligned16) {
   const int bits = BITS > 0 ? BITS : bits_rt;
   const int64_t tasks = rows * kwp;
   const int64_t plane_stride = rows * kwp;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tasks; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = POW2 ? (t >> kwp_shift) : t / kwp;
-    const int64_t j = t - r * kwp;
-    const int64_t e0 = 32 * j;  // first element of this word
-    uint32_t v[8];
-    const uint8_t* src = in + r * k + e0;
-    if (aligned16 && e0 + 32 <= k) {
-      uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
-      uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-      v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
-      v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
-    } else if (aligned16 && e0 + 16 == k) {  // k % 32 == 16: last word half full
-      uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
-      v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
-      v[4] = v[5] = v[6] = v[7] = 0u;
-    } else {  // ragged / unaligned rows, pad words: byte loads with bounds
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if constexpr (FAST && BITS > 0) {
+    constexpr int kBatch = 4;
+    for (; t + (kBatch - 1) * stride < tasks; t += kBatch * stride) {
+      uint4 lo[kBatch], hi[kBatch];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint32_t x = 0;
+      for (int u = 0; u < kBatch; ++u) {  // all loads first
+        const int64_t tt = t + u * stride;
+        const int64_t r = POW2 ? (tt >> kwp_shift) : tt / kwp;
+        const int64_t j = tt - r * kwp;
+        const uint4* src = reinterpret_cast<const uint4*>(in + r * k + 32 * j);
+        lo[u] = __ldg(src);
+        hi[u] = __ldg(src + 1);
+      }
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          int64_t e = e0 + 4 * q + rr;
-          if (e < k) x |= uint32_t(__ldg(src + 4 * q + rr)) << (8 * rr);
-        }
-        v[q] = x;
+      for (int u = 0; u < kBatch; ++u) {
+        const int64_t tt = t + u * stride;
+        const uint32_t v[8] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
+        store_planes<0, BITS>(out + tt, plane_stride, v);  // (row, word) = tt in [rows][kwp]
       }
     }
-    uint32_t* dst = out + r * kwp + j;
-    if constexpr (BITS > 0) {
-      store_planes<0, BITS>(dst, plane_stride, v);
-    } else {
-      for (int b = 0; b < bits; ++b) dst[b * plane_stride] = plane_word(v, b);
-    }
+  }
+  for (; t < tasks; t += stride) {
+    const int64_t r = POW2 ? (t >> kwp_shift) : t / kwp;
+    pack_word<BITS>(in, out, r, t - r * kwp, k, kwp, plane_stride, bits, aligned16);
   }
 }
 
 cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int64_t kwp, int bits,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, int max_ctas) {
   const int64_t tasks = rows * kwp;
   const int threads = 256;
   int64_t blocks = (tasks + threads - 1) / threads;
   const int64_t max_blocks = int64_t(kNumSMs) * 8 * 4;  // grid-stride beyond 4 waves of 8 CTAs/SM
   if (blocks > max_blocks) blocks = max_blocks;
+  if (max_ctas > 0 && blocks > max_ctas) blocks = max_ctas;  // leave SM room for a concurrent kernel
   const bool aligned16 = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (k % 16 == 0);
   const bool pow2 = (kwp & (kwp - 1)) == 0;
+  const bool fast = aligned16 && (k % 32) == 0 && kwp * 32 == k;  // every word full, no pad words
   int shift = 0;
   while ((int64_t(1) << shift) < kwp) ++shift;
-#define BS_PACK(BITS)                                                                                         \
-  if (pow2)                                                                                                   \
-    bitpack_kernel<BITS, true><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16); \
-  else                                                                                                        \
-    bitpack_kernel<BITS, false><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16);
+#define BS_PACK(BITS)                                                                                          \
+  if (fast && pow2)                                                                                            \
+    bitpack_kernel<BITS, true, true><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16); \
+  else if (pow2)                                                                                               \
+    bitpack_kernel<BITS, true, false><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16); \
+  else                                                                                                         \
+    bitpack_kernel<BITS, false, false><<<blocks, threads, 0, stream>>>(in, out, rows, k, kwp, shift, bits, aligned16);
   switch (bits) {
     case 1: BS_PACK(1) break;
     case 2: BS_PACK(2) break;

@@ -36,7 +36,7 @@ int64_t launch_count();
 enum class Algo : int { Auto = 0, Popc = 1, PopcLit = 2, Gemv = 3 };
 
 cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int64_t kwp, int bits,
-                           cudaStream_t stream);
+                           cudaStream_t stream, int max_ctas = 0);
 
 // Tiled AND+POPC implicit-GEMM kernel (conv and dense); returns cudaErrorNotSupported
 // when no instantiation covers (a_bits, w_bits, algo).

@@ -810,7 +810,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c) r[c] = c;
         } else {
+          PROF_BEGIN
           tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + cb * 32), r);
+          PROF_END(1)
           if constexpr (F4) {  // FP32 accumulator holding an exact integer |v| < 2^22 -> int32:
             // v + 1.5*2^23 puts v in the low mantissa bits (one FADD + one IADD instead of
             // the quarter-rate F2I)
@@ -842,8 +844,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else if (args.epi == kEpiTma) {
+          PROF_BEGIN
           if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // the store that last used `buf` has read it
           __syncwarp();
+          PROF_END(2)
+          PROF_BEGIN
           uint8_t* sb = ebuf + buf * kEpiBufBytes + lane * 128;
           const uint32_t swz = uint32_t(lane & 7);
 #pragma unroll
@@ -856,7 +861,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_2d(&tmap_out, n0 + cb * 32, int(m0) + q * 32, smem_u32(ebuf + buf * kEpiBufBytes));
             bulk_commit();
           }
-          buf ^= 1;
+          PROF_END(3)
+          buf = buf + 1 == kEpiBufs ? 0 : buf + 1;
         } else {  // OC % 4 != 0: plain bounded stores
           if (row < p.M) {
             int32_t* dst = p.out + row * p.oc;
@@ -883,8 +889,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 #ifdef BS_TC_PROFILE
   if (blockIdx.x == 0 && lane == 0)
-    printf("TCPROF warp %d total %lld w0 %lld w1 %lld w2 %lld\n", warp, clock64() - _t_start, _pacc[0], _pacc[1],
-           _pacc[2]);
+    printf("TCPROF warp %d total %lld w0 %lld w1 %lld w2 %lld w3 %lld\n", warp, clock64() - _t_start, _pacc[0],
+           _pacc[1], _pacc[2], _pacc[3]);
 #endif
   tc_fence_before();
   __syncthreads();

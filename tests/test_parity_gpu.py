@@ -433,3 +433,14 @@ def test_tc_accumulator_bound_extremes(fmt, a_bits, w_bits):
         got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=fmt)
         np.testing.assert_array_equal(got.cpu().numpy(), ref)
     assert int(np.abs(ref).max()) == k * ((1 << a_bits) - 1) * ((1 << w_bits) - 1)
+
+
+@pytest.mark.parametrize("max_ctas", [1, 7, 148])
+def test_bitpack_capped_grid(max_ctas):
+    """bs_bitpack_ex with a small grid (the batched fast path plus its tail) packs
+    exactly like the default launch."""
+    for rows, k, bits in ((3136 * 4, 64, 2), (1001, 96, 3), (513, 4096, 1), (77, 100, 2)):
+        g = inputs.gen(rows + k + bits + max_ctas)
+        x = inputs.codes((rows, k), bits, g)
+        got = bs.bitpack(x.to(DEV), bits, max_ctas=max_ctas).cpu().numpy().view(np.uint32)
+        np.testing.assert_array_equal(got, oracle.bitpack(x.numpy(), bits))
