@@ -582,6 +582,12 @@ def run_ours(args):
                                   f"({peaks['bf16_tflops']:.1f}, {peaks_src}); 1 binary MAC = 1 MMA MAC",
                     "peak_sustained": sustained, "frac_sustained": achieved / sustained,
                     "frac_of_int8_peak": achieved / (2.0 * peaks["bf16_tflops"]),
+                    # context: NVIDIA's nominal dense figure and the clock-derived MMA rate
+                    # measured with tools/mma_bench.cu (i8: 8189 MAC/clk/SM; mxf4: 2x) at f_max
+                    "peak_nominal": 9000.0 if f4 else 4500.0,
+                    "frac_of_nominal": achieved / (9000.0 if f4 else 4500.0),
+                    "peak_clock": (2 if f4 else 1) * 8189.0 * 2 * sms * f_max * 1e6 / 1e12,
+                    "frac_of_clock": achieved / ((2 if f4 else 1) * 8189.0 * 2 * sms * f_max * 1e6 / 1e12),
                     "r_popc": r_popc, "x_r_popc": achieved / r_popc}
     elif roof["kind"] == "alu":
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
