@@ -206,6 +206,8 @@ class ConvWorkload:
             self.side_stream = torch.cuda.Stream(device=dev)
             self.pack_events = [torch.cuda.Event() for _ in self.runs]
             self.pack_ctas = args.pack_ctas_per_sm * torch.cuda.get_device_properties(dev).multi_processor_count
+            self.conv_streams = args.conv_streams
+            self.conv2_stream = torch.cuda.Stream(device=dev)
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
             "layout": "NHWC/OHWI",
@@ -243,9 +245,19 @@ class ConvWorkload:
                 # the previous layer's persistent conv CTAs: a capped grid leaves them room
                 r.pack_only(0 if i == 0 else self.pack_ctas)
                 e.record(side)
-        for r, e in zip(self.runs, self.pack_events):
-            main.wait_event(e)
-            r.conv_only()
+        # the ten layers are independent problems (BASELINE configs[3]): convs alternate
+        # between two streams so one layer's persistent CTAs start on the SMs the previous
+        # layer's tail leaves idle (two conv CTAs never share an SM: smem + all of TMEM)
+        conv_streams = [main, self.conv2_stream] if self.conv_streams == 2 else [main]
+        for s in conv_streams[1:]:
+            s.wait_stream(main)
+        for i, (r, e) in enumerate(zip(self.runs, self.pack_events)):
+            cs = conv_streams[i % len(conv_streams)]
+            cs.wait_event(e)
+            with torch.cuda.stream(cs):
+                r.conv_only()
+        for s in conv_streams[1:]:
+            main.wait_stream(s)
         main.wait_stream(side)
 
     def roofline(self, reps):
@@ -722,6 +734,8 @@ def main():
     ap.add_argument("--unipolar", dest="bipolar", action="store_false")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="pack and conv of every layer in one stream")
+    ap.add_argument("--conv-streams", type=int, default=2, choices=[1, 2],
+                    help="overlapped step: convs of consecutive (independent) layers on 1 or 2 streams")
     ap.add_argument("--pack-ctas-per-sm", type=int, default=0,
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",

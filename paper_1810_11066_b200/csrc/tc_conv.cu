@@ -58,6 +58,9 @@ constexpr int kWordsPerStage = BKB / 32;  // 4 packed words per plane per row
 constexpr int kTeams = BS_TC_TEAMS;                    // producer teams (K chunks in flight)
 constexpr int kProducerWarps = 4 * kTeams;             // a team = 4 warps = one thread per row
 constexpr int kProducerThreads = kProducerWarps * 32;
+#ifndef BS_TC_MAX_STAGES
+#define BS_TC_MAX_STAGES 6
+#endif
 #ifndef BS_TC_EPI_WARPS
 #define BS_TC_EPI_WARPS 4
 #endif
@@ -74,7 +77,8 @@ constexpr int kEpiBufBytes = 32 * 128;  // one 32 x 32 int32 box
 constexpr int kEpiBufs = BS_TC_EPI_BUFS;  // staging buffers (TMA stores in flight) per epilogue warp
 constexpr int kEpiBytes = kEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kSmemLimit = 227 * 1024;
-constexpr int kMinSmem = 116 * 1024;  // > half the SM: guarantees one CTA per SM (TMEM)
+constexpr int kMinSmem = 116 * 1024;
+constexpr int kMaxTaps = 64;  // filter taps held in the shared-memory tap table  // > half the SM: guarantees one CTA per SM (TMEM)
 
 // BS_TC_PROFILE builds (tools only) count cycles spent in each role's waits and print
 // them per CTA 0 at exit; the product build compiles these to nothing.
@@ -448,7 +452,7 @@ struct Cfg {
   static constexpr int kACols = A_BITS * kAColsPlane;     // TMEM columns of one stage's A planes
   static constexpr int kBBytes = W_BITS * BN * kBRow;     // shared memory per stage (B only)
   static constexpr int kSFCols = F4 ? 32 : 0;             // SFA: 4 planes x 4 cols; SFB: 2 x 8
-  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + kEpiBytes;
+  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + 512 /*tap table*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
@@ -456,7 +460,7 @@ struct Cfg {
   // phase parity, and a team that could reach a stage two phases ahead of another team
   // would pass the wait early.  So the stage count is a multiple of the teams in use.
   static constexpr int kTeamsUsed = kFit < kTeams ? kFit : kTeams;
-  static constexpr int kStagesRaw = kFit > 6 ? 6 : kFit;
+  static constexpr int kStagesRaw = kFit > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFit;
   static constexpr int kStages = kTeamsUsed > 0 ? (kStagesRaw / kTeamsUsed) * kTeamsUsed : 0;
   static constexpr int kUsed = kFixed + kStages * kBBytes;
   static constexpr int kBytes = kUsed < kMinSmem ? kMinSmem : kUsed;
@@ -493,10 +497,12 @@ struct TcArgs {
   int b_bytes;      // bytes of the B region (resident: nchunks stages, else kStages)
   FastDiv div_hw, div_ow, div_kwid, div_ntn, div_kwa;  // n / (oh*ow), / ow, / kw, / ntn, / Cw
   int kwa_shift;    // log2(Cw) when Cw is a power of two, else -1
-  int debug;        // BS_TC_PROFILE builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
-                    // 2 skip accumulator tcgen05.ld (timing experiments; results are wrong)
+  int taps;         // kh * kw (the tap table is used when taps <= kMaxTaps)
+  int debug;        // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
+                    // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads
+                    // (timing experiments; results are wrong)
 };
-#ifdef BS_TC_PROFILE
+#if defined(BS_TC_PROFILE) || defined(BS_TC_KNOBS)
 #define DBG(bit) (args.debug & (1 << (bit)))
 #else
 #define DBG(bit) 0
@@ -521,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 3 * S;
   uint64_t* acc_empty = bars + 3 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [kMaxTaps] {offset, ky<<16|kx}
 
   const ConvProblem& p = args.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -530,6 +537,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   const int ntiles = args.ntiles, ntn = args.ntn, nchunks = args.nchunks;
 
+  // filter-tap table (implicit im2col): word offset of tap (ky, kx) from the row's
+  // receptive-field origin, and (ky, kx) for the bounds test
+  const bool tap_table = args.taps <= kMaxTaps;
+  if (tap_table && tid < args.taps) {
+    const int ky = tid / args.p.kwid, kx = tid - ky * args.p.kwid;
+    s_tap[tid] = make_int2((ky * args.p.w + kx) * args.p.kw_a, (ky << 16) | kx);
+  }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_u32(full_a + s), 4);  // the 4 warps of one team
@@ -601,6 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool rok = false;
     int iy0 = 0, ix0 = 0;
     const uint32_t* rbase = act;  // image base (pixel 0 of the row's image), word units
+    const uint32_t* rorg = act;   // receptive-field origin (iy0, ix0) of the row (may lie in the padding)
     auto set_tile = [&](int t) {
       const uint32_t mblk = args.div_ntn.div(uint32_t(t));
       const int64_t m = int64_t(mblk) * BM + arow;
@@ -611,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       iy0 = int(oy) * p.sh - p.ph;
       ix0 = int(ox) * p.sw - p.pw;
       rbase = act + int64_t(b) * p.h * p.w * kwa;
+      rorg = rbase + (int64_t(iy0) * p.w + ix0) * kwa;
     };
     // source of the 2- or 4-word piece starting at filter word kk (kk even)
     auto piece = [&](int kk, bool& ok) -> const uint32_t* {
@@ -622,12 +638,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         tap = int(args.div_kwa.div(uint32_t(kk)));
         cw = kk - tap * kwa;
       }
+      if (tap_table) {
+        const int2 e = s_tap[tap < kMaxTaps ? tap : 0];
+        const int iy = iy0 + (e.y >> 16), ix = ix0 + (e.y & 0xFFFF);
+        ok = rok && kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
+        return rorg + e.x + cw;
+      }
       const int ky = int(args.div_kwid.div(uint32_t(tap))), kx = tap - ky * p.kwid;
       const int iy = iy0 + ky, ix = ix0 + kx;
       ok = rok && kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
       return rbase + (int64_t(iy) * p.w + ix) * kwa + cw;
     };
     auto load = [&](int kc, uint4 (&v)[A_BITS]) {
+      if (DBG(3)) {  // timing experiment: no global loads
+#pragma unroll
+        for (int i = 0; i < A_BITS; ++i) v[i] = make_uint4(kc, i, arow, 7);
+        return;
+      }
       const int kk = kc * kWordsPerStage;
       bool ok0;
       const uint32_t* s0 = piece(kk, ok0);
@@ -971,6 +998,9 @@ cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cu
   a.div_kwid = make_fastdiv(uint32_t(p.kwid));
   a.div_ntn = make_fastdiv(uint32_t(a.ntn));
   a.div_kwa = make_fastdiv(uint32_t(p.kw_a));
+  a.taps = p.kh * p.kwid;
+  // the table's int32 word offsets: (ky*W + kx)*Cw must fit
+  if ((int64_t(p.kh) * p.w + p.kwid) * p.kw_a >= (int64_t(1) << 31)) a.taps = kMaxTaps + 1;
   a.kwa_shift = -1;
   for (int sh = 0; sh < 31; ++sh)
     if ((1 << sh) == p.kw_a) a.kwa_shift = sh;

@@ -6,6 +6,9 @@
 //   V1: lane 0 only, 64-bit descriptor precomputed per stage, + constant per MMA
 //   V2: whole warp runs the loop, one elect.sync per MMA, precomputed descriptors
 //   V3: whole warp, ONE asm block per stage: elect once, 8 MMAs with PTX adds inside
+//   V4: kind::mxf4 block-scaled, A from TMEM, whole warp, elect per 2 MMAs (K = 64 each):
+//       the FP4 conv kernel's issue shape (clk per 128x128x64 MMA)
+//   V5: V4 with A from shared memory (SS)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_issue_bench tools/mma_issue_bench.cu
 #include <cstdio>
 #include <cstdint>
@@ -60,6 +63,28 @@ __device__ __forceinline__ void mma_stage8(uint32_t d, uint32_t a, uint64_t b, u
       "r"(a), "l"(b), "r"(acc0), "n"(kIdesc));
 }
 
+constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
+__device__ __forceinline__ void mma2_f4_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
+      "elect.sync x|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
+      "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "}" ::"r"(d), "r"(a), "l"(b), "r"(acc), "n"(kIdescF4), "r"(sfa), "r"(sfb));
+}
+__device__ __forceinline__ void mma2_f4_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{.reg .pred p, e; .reg .b32 x; .reg .b64 a1, b1;\n"
+      "elect.sync x|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %3, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %4, [%5], [%6], p;\n"
+      "add.u64 a1, %1, 2; add.u64 b1, %2, 2;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], a1, b1, %4, [%5], [%6], 1;\n"
+      "}" ::"r"(d), "l"(a), "l"(b), "r"(acc), "n"(kIdescF4), "r"(sfa), "r"(sfb));
+}
+
 template <int V>
 __global__ void __launch_bounds__(128, 1) bench(int stages, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -104,8 +129,14 @@ __global__ void __launch_bounds__(128, 1) bench(int stages, unsigned long long* 
             else
               mma_ts_elect(acc, a0 + i * 32 + k * 8, bd + 2 * k, (st | i | k) & 15);
           }
-      } else {
+      } else if (V == 3) {
         mma_stage8(acc, a0, desc_sw128(b0), st & 15);
+      } else if (V == 4) {  // per stage: 2 planes x 2 K64 steps, SF regions at 448 / 480
+        mma2_f4_ts(acc, a0, desc_sw128(b0), tmem + 448, tmem + 480, st & 15);
+        mma2_f4_ts(acc, a0 + 16, desc_sw128(b0), tmem + 452, tmem + 480, 1);
+      } else {
+        mma2_f4_ss(acc, desc_sw128(b0 + 32768), desc_sw128(b0), tmem + 448, tmem + 480, st & 15);
+        mma2_f4_ss(acc, desc_sw128(b0 + 32768 + 64), desc_sw128(b0), tmem + 452, tmem + 480, 1);
       }
     }
     if (lane == 0)
@@ -136,8 +167,8 @@ void run(int sms) {
   cudaMemcpy(h, d, sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   double mx = 0;
   for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
-  printf("{\"variant\": %d, \"N\": %d, \"clk_per_mma\": %.2f, \"err\": \"%s\"}\n", V, N, mx / (stages * 8.0),
-         cudaGetErrorString(e));
+  printf("{\"variant\": %d, \"N\": %d, \"clk_per_mma\": %.2f, \"err\": \"%s\"}\n", V, N,
+         mx / (stages * (V >= 4 ? 4.0 : 8.0)), cudaGetErrorString(e));
   cudaFree(d);
 }
 
@@ -148,5 +179,7 @@ int main() {
   run<1>(sms);
   run<2>(sms);
   run<3>(sms);
+  run<4>(sms);
+  run<5>(sms);
   return 0;
 }
