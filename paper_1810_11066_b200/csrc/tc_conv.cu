@@ -59,13 +59,10 @@ constexpr int kTeams = BS_TC_TEAMS;                    // producer teams (K chun
 constexpr int kProducerWarps = 4 * kTeams;             // a team = 4 warps = one thread per row
 constexpr int kProducerThreads = kProducerWarps * 32;
 #ifndef BS_TC_MAX_STAGES
-#define BS_TC_MAX_STAGES 6
+#define BS_TC_MAX_STAGES 8
 #endif
 #ifndef BS_TC_EPI_WARPS
 #define BS_TC_EPI_WARPS 4
-#endif
-#ifndef BS_TC_EPI_BUFS
-#define BS_TC_EPI_BUFS 2
 #endif
 constexpr int kEpiWarps = BS_TC_EPI_WARPS;              // 4 or 8 (warp % 4 = lane quarter)
 constexpr int kEpiWarp0 = kProducerWarps;
@@ -74,7 +71,7 @@ constexpr int kTmaWarp = kProducerWarps + kEpiWarps;
 constexpr int kMmaWarp = kProducerWarps + kEpiWarps + 1;
 constexpr int kThreads = (kProducerWarps + kEpiWarps + 2) * 32;
 constexpr int kEpiBufBytes = 32 * 128;  // one 32 x 32 int32 box
-constexpr int kEpiBufs = BS_TC_EPI_BUFS;  // staging buffers (TMA stores in flight) per epilogue warp
+constexpr int kEpiBufs = 2;             // staging buffers (TMA stores in flight) per epilogue warp
 constexpr int kEpiBytes = kEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMinSmem = 116 * 1024;
@@ -456,12 +453,12 @@ struct Cfg {
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
-  // Every stage must always be filled by the same producer team: mbarrier waits are by
-  // phase parity, and a team that could reach a stage two phases ahead of another team
-  // would pass the wait early.  So the stage count is a multiple of the teams in use.
-  static constexpr int kTeamsUsed = kFit < kTeams ? kFit : kTeams;
-  static constexpr int kStagesRaw = kFit > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFit;
-  static constexpr int kStages = kTeamsUsed > 0 ? (kStagesRaw / kTeamsUsed) * kTeamsUsed : 0;
+  // Producers learn that a stage is free from a monotonic "chunks freed" counter that
+  // one warp publishes after waiting on each stage's empty barrier in chunk order (an
+  // mbarrier parity wait by a producer team could alias two phases when teams visit
+  // the same stage), so the stage count is independent of the team count.
+  static constexpr int kStages = kFit > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFit;
+  static constexpr int kTeamsUsed = kStages < kTeams ? kStages : kTeams;
   static constexpr int kUsed = kFixed + kStages * kBBytes;
   static constexpr int kBytes = kUsed < kMinSmem ? kMinSmem : kUsed;
   static constexpr int kTmemCols = 512;  // 2*BN accumulator columns + the A ring; one CTA per SM
@@ -499,7 +496,8 @@ struct TcArgs {
   int kwa_shift;    // log2(Cw) when Cw is a power of two, else -1
   int taps;         // kh * kw (the tap table is used when taps <= kMaxTaps)
   int debug;        // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
-                    // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads
+                    // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
+                    // 4 MMA warp ignores full_a
                     // (timing experiments; results are wrong)
 };
 #if defined(BS_TC_PROFILE) || defined(BS_TC_KNOBS)
@@ -519,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* s_stage = smem;                            // B: S ring stages, or nchunks resident
-  uint8_t* s_epi = smem + args.b_bytes;               // 4 warps x 2 x 4 KB (1024-aligned)
+  uint8_t* s_epi = smem + args.b_bytes;               // epilogue staging: warps x 2 x 4 KB (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_epi + kEpiBytes);
   uint64_t* full_a = bars;
   uint64_t* full_b = bars + S;
@@ -528,6 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_empty = bars + 3 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
   int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [kMaxTaps] {offset, ky<<16|kx}
+  int* s_freed = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 240);   // chunks whose stage is free
+  static_assert(8 * (3 * S + 4) + 4 <= 240, "barrier region");
 
   const ConvProblem& p = args.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(acc_full + a), 1);
       mbar_init(smem_u32(acc_empty + a), kEpiWarps);
     }
+    *s_freed = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -597,7 +598,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
   }
 
-  if (warp < 4 * C::kTeamsUsed) {
+  if (warp < 4 * C::kTeamsUsed && DBG(5)) {
+    // knob 5: producers idle (MMA-only timing with knob 4)
+  } else if (warp < 4 * C::kTeamsUsed) {
     // ================= expansion producers.  kTeams teams of 4 warps; team t expands the
     // chunks g = t, t+kTeams, ... of this CTA's (tile, K chunk) sequence, so kTeams chunks
     // are in flight.  Within a team, thread `arow` (warp % 4 == its TMEM lane quarter)
@@ -707,7 +710,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       advance_load();  // next step's words in flight during this step's expansion
       const int stage = g % S;
       PROF_BEGIN
-      mbar_wait(smem_u32(empty + stage), ((g / S) & 1) ^ 1u);
+      for (;;) {  // stage of chunk g free (published in chunk order by the TMA warp)
+        int freed;
+        asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(freed) : "r"(smem_u32(s_freed)) : "memory");
+        if (freed > g) break;
+        __nanosleep(20);
+      }
       PROF_END(1)
       tc_fence_after();
       const uint32_t ta = lane_base + uint32_t(C::kAcol0 + stage * C::kACols);
@@ -735,30 +743,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < kProducerWarps) {
     // producer warps of teams this configuration does not use: idle
   } else if (warp == kTmaWarp) {
-    // ================= weight tiles by TMA
-    if (lane == 0 && args.b_resident) {  // whole B once (one N block): every K chunk, W planes
-      const uint32_t fb = smem_u32(full_b);
-      mbar_expect_tx(fb, uint32_t(C::kBBytes) * uint32_t(nchunks));
-      for (int kc = 0; kc < nchunks; ++kc) {
-        const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
+    // ================= weight tiles by TMA, and the "chunks freed" counter: waits on each
+    // stage's empty barrier in chunk order, then publishes that chunk g may be written
+    if (lane == 0) {
+      const bool resident = args.b_resident;
+      if (resident) {  // whole B once (one N block): every K chunk, W planes
+        const uint32_t fb = smem_u32(full_b);
+        mbar_expect_tx(fb, uint32_t(C::kBBytes) * uint32_t(nchunks));
+        for (int kc = 0; kc < nchunks; ++kc) {
+          const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
 #pragma unroll
-        for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc, fb);
+          for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc, fb);
+        }
       }
-    } else if (lane == 0) {
-      int stage = 0;
+      int stage = 0, g = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int n0 = (tile % ntn) * BN;
-        for (int kc = 0; kc < nchunks; ++kc) {
+        for (int kc = 0; kc < nchunks; ++kc, ++g) {
           PROF_BEGIN
           mbar_wait(smem_u32(empty + stage), phase ^ 1u);
           PROF_END(0)
-          const uint32_t fb = smem_u32(full_b + stage);
-          mbar_expect_tx(fb, uint32_t(C::kBBytes));
-          const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
+          asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_freed)), "r"(g + 1) : "memory");
+          if (!resident) {
+            const uint32_t fb = smem_u32(full_b + stage);
+            mbar_expect_tx(fb, uint32_t(C::kBBytes));
+            const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
 #pragma unroll
-          for (int j = 0; j < W_BITS; ++j)
-            tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc + n0, fb);
+            for (int j = 0; j < W_BITS; ++j)
+              tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc + n0, fb);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1u;
@@ -783,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tacc = uint32_t(acc * BN);
       for (int kc = 0; kc < nchunks; ++kc) {
         PROF_BEGIN
-        mbar_wait(smem_u32(full_a + stage), phase);
+        if (!DBG(4)) mbar_wait(smem_u32(full_a + stage), phase);  // knob 4: MMA-only timing
         PROF_END(1)
         PROF_BEGIN
         if (!resident) mbar_wait(smem_u32(full_b + stage), phase);

@@ -9,6 +9,11 @@
 //   V4: kind::mxf4 block-scaled, A from TMEM, whole warp, elect per 2 MMAs (K = 64 each):
 //       the FP4 conv kernel's issue shape (clk per 128x128x64 MMA)
 //   V5: V4 with A from shared memory (SS)
+//   V6: V4 with B in 64-byte rows, SWIZZLE_64B (the FP4 conv kernel's B layout)
+//   V7: V6 + a tcgen05.commit to a stage mbarrier after every stage (4 MMAs), as the
+//       conv kernel does to release each stage; V8: commit every 2 stages
+//   V9: V7 + tcgen05.fence::after_thread_sync before each stage's MMAs (as after a wait)
+//   V10: V9 + the wait itself: mbarrier.try_wait.parity on an already-completed phase
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_issue_bench tools/mma_issue_bench.cu
 #include <cstdio>
 #include <cstdint>
@@ -63,6 +68,15 @@ __device__ __forceinline__ void mma_stage8(uint32_t d, uint32_t a, uint64_t b, u
       "r"(a), "l"(b), "r"(acc0), "n"(kIdesc));
 }
 
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
 constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
 __device__ __forceinline__ void mma2_f4_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t acc) {
   asm volatile(
@@ -90,11 +104,13 @@ __global__ void __launch_bounds__(128, 1) bench(int stages, unsigned long long* 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
+  __shared__ uint64_t sbar[4];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (i & 3);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&sbar[i])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -134,6 +150,20 @@ __global__ void __launch_bounds__(128, 1) bench(int stages, unsigned long long* 
       } else if (V == 4) {  // per stage: 2 planes x 2 K64 steps, SF regions at 448 / 480
         mma2_f4_ts(acc, a0, desc_sw128(b0), tmem + 448, tmem + 480, st & 15);
         mma2_f4_ts(acc, a0 + 16, desc_sw128(b0), tmem + 452, tmem + 480, 1);
+      } else if (V >= 6) {
+        if (V == 10) {
+          asm volatile("{.reg .pred p; W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 1; @!p bra W%=;}" ::"r"(
+                           su32(&bar))
+                       : "memory");
+        }
+        if (V >= 9) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        mma2_f4_ts(acc, a0, desc_sw64(b0), tmem + 448, tmem + 480, st & 15);
+        mma2_f4_ts(acc, a0 + 16, desc_sw64(b0), tmem + 452, tmem + 480, 1);
+        if (V == 7 || V >= 9 || (V == 8 && (st & 1)))
+          asm volatile(
+              "{.reg .pred e; .reg .b32 x; elect.sync x|e, 0xffffffff;\n"
+              "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];}" ::"r"(su32(&sbar[s]))
+              : "memory");
       } else {
         mma2_f4_ss(acc, desc_sw128(b0 + 32768), desc_sw128(b0), tmem + 448, tmem + 480, st & 15);
         mma2_f4_ss(acc, desc_sw128(b0 + 32768 + 64), desc_sw128(b0), tmem + 452, tmem + 480, 1);
@@ -181,5 +211,10 @@ int main() {
   run<3>(sms);
   run<4>(sms);
   run<5>(sms);
+  run<6>(sms);
+  run<7>(sms);
+  run<8>(sms);
+  run<9>(sms);
+  run<10>(sms);
   return 0;
 }
