@@ -275,9 +275,15 @@ class ConvWorkload:
         tc = self.args.path == "tc"
         kname = (f"tc_conv_kernel (tcgen05 kind::{'mxf4' if self.args.tc_format == 'f4' else 'i8'};" if tc else
                  "popc_conv_kernel (")
+        # algorithmic HBM bytes per conv launch: packed activations read once, weights
+        # (prepared form) read once, int32 outputs written once
+        conv_bytes = [r.packed.numel() * 4 + (r.w_tc.numel() if r.w_tc is not None else r.wp.numel() * 4)
+                      + r.out.numel() * 4 for r in self.runs]
         return {"kind": "tensor" if tc else "alu",
                 "kernel": f"{kname} sum over the {len(self.runs)} layer launches of one step, rank 0)",
-                "ops": ops, "ms": sum(conv_ms), "launches": len(self.runs),
+                "ops": ops, "ms": sum(conv_ms), "launches": len(self.runs), "bytes": sum(conv_bytes),
+                "per_layer": [{"layer": li, "binops": r.binops(), "bytes": b, "ms": t}
+                              for li, r, b, t in zip(self.layers, self.runs, conv_bytes, conv_ms)],
                 "breakdown": {"layers": list(self.layers), "conv_us": [1e3 * t for t in conv_ms],
                               "pack_us": [1e3 * t for t in pack_ms],
                               "conv_binary_tops": [r.binops() / (t / 1e3) / 1e12 for r, t in zip(self.runs, conv_ms)],
@@ -430,7 +436,10 @@ class DenseWorkload:
                 "kernel": (f"tc_conv_kernel (tcgen05 kind::{'mxf4' if self.args.tc_format == 'f4' else 'i8'}; dense = "
                            "1x1 implicit GEMM, rank 0 shard)" if self.tc else
                            "popc_conv_kernel (dense = 1x1 implicit GEMM, rank 0 shard)"), "ops": ops,
-                "ms": ms, "launches": 1, "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
+                "ms": ms, "launches": 1,
+                "bytes": self.packed.numel() * 4 + (self.w_tc.numel() if self.tc else self.wp.numel() * 4)
+                + self.out.numel() * 4,
+                "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
 
     def e2e(self, steps):
         a_host = self.a_cpu.pin_memory()
@@ -584,23 +593,44 @@ def run_ours(args):
         f4 = args.tc_format != "i8"
         ratio = 4.0 if f4 else 2.0
         peak = ratio * peaks["bf16_tflops"]
+        hbm = peaks["hbm_gbs"]
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
         sustained = ratio * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "binary TOPS",
-                    "frac": achieved / peak, "traffic": None, "kernel": roof["kernel"],
-                    "mma_kind": "kind::mxf4 (E2M1 bits, UE8M0 plane scales, FP32 accum)" if f4 else
-                                "kind::i8 (0/1 bytes, int32 accum)",
-                    "peak_basis": f"{'FP4' if f4 else 'INT8'} dense tensor peak = {ratio:.0f} x bf16_tflops "
-                                  f"({peaks['bf16_tflops']:.1f}, {peaks_src}); 1 binary MAC = 1 MMA MAC",
-                    "peak_sustained": sustained, "frac_sustained": achieved / sustained,
-                    "frac_of_int8_peak": achieved / (2.0 * peaks["bf16_tflops"]),
-                    # context: NVIDIA's nominal dense figure and the clock-derived MMA rate
-                    # measured with tools/mma_bench.cu (i8: 8189 MAC/clk/SM; mxf4: 2x) at f_max
-                    "peak_nominal": 9000.0 if f4 else 4500.0,
-                    "frac_of_nominal": achieved / (9000.0 if f4 else 4500.0),
-                    "peak_clock": (2 if f4 else 1) * 8189.0 * 2 * sms * f_max * 1e6 / 1e12,
-                    "frac_of_clock": achieved / ((2 if f4 else 1) * 8189.0 * 2 * sms * f_max * 1e6 / 1e12),
-                    "r_popc": r_popc, "x_r_popc": achieved / r_popc}
+        # time model: each launch is bound by max(tensor time, HBM time of its algorithmic
+        # bytes) — the int32 outputs (4 bytes per output) make the 1x1 and early layers
+        # HBM-bound; the primary "bound" is the one that dominates summed over the launches
+        t_tensor = roof["ops"] / (peak * 1e12) * 1e3
+        t_hbm = roof["bytes"] / (hbm * 1e9) * 1e3
+        per = roof.get("per_layer", [])
+        t_roof = sum(max(x["binops"] / (peak * 1e12), x["bytes"] / (hbm * 1e9)) * 1e3 for x in per) if per else \
+            max(t_tensor, t_hbm)
+        model = {"t_tensor_ms": t_tensor, "t_hbm_ms": t_hbm, "t_roof_ms": t_roof, "t_actual_ms": roof["ms"],
+                 "frac": t_roof / roof["ms"],
+                 "per_layer": [{"layer": x["layer"], "t_us": 1e3 * x["ms"],
+                                "t_tensor_us": 1e6 * x["binops"] / (peak * 1e12),
+                                "t_hbm_us": 1e6 * x["bytes"] / (hbm * 1e9)} for x in per]}
+        common = {"kernel": roof["kernel"], "traffic": None,
+                  "mma_kind": "kind::mxf4 (E2M1 bits, UE8M0 plane scales, FP32 accum)" if f4 else
+                              "kind::i8 (0/1 bytes, int32 accum)",
+                  "tensor": {"achieved": achieved, "peak": peak, "unit": "binary TOPS", "frac": achieved / peak,
+                             "peak_basis": f"{'FP4' if f4 else 'INT8'} dense tensor peak = {ratio:.0f} x bf16_tflops "
+                                           f"({peaks['bf16_tflops']:.1f}, {peaks_src}); 1 binary MAC = 1 MMA MAC",
+                             "peak_sustained": sustained, "frac_sustained": achieved / sustained,
+                             "frac_of_int8_peak": achieved / (2.0 * peaks["bf16_tflops"]),
+                             "peak_nominal": 9000.0 if f4 else 4500.0,
+                             "frac_of_nominal": achieved / (9000.0 if f4 else 4500.0),
+                             "peak_clock": (2 if f4 else 1) * 8189.0 * 2 * sms * f_max * 1e6 / 1e12,
+                             "frac_of_clock": achieved / ((2 if f4 else 1) * 8189.0 * 2 * sms * f_max * 1e6 / 1e12)},
+                  "hbm": {"achieved": roof["bytes"] / (roof["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                          "frac": roof["bytes"] / (roof["ms"] / 1e3) / 1e9 / hbm,
+                          "algorithmic_bytes": roof["bytes"]},
+                  "time_model": model, "r_popc": r_popc, "x_r_popc": achieved / r_popc}
+        if t_hbm >= t_tensor:  # HBM dominates summed over the step's launches
+            roofline = dict(common, bound="hbm", achieved=common["hbm"]["achieved"], peak=hbm, unit="GB/s",
+                            frac=common["hbm"]["frac"], peak_basis=f"HBM copy bandwidth, {peaks_src}")
+        else:
+            roofline = dict(common, bound="tensor", achieved=achieved, peak=peak, unit="binary TOPS",
+                            frac=achieved / peak, peak_basis=common["tensor"]["peak_basis"])
     elif roof["kind"] == "alu":
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": achieved, "peak": r_int, "unit": "binary TOPS",
