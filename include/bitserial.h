@@ -181,7 +181,7 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
  * every plane pair is one exact int8 x int8 -> int32 binary dot product on the tensor
  * cores: popcount(a_i AND w_j) = sum_k a_i[k] w_j[k] (Eq. 1), weighted
  * 2^(i+j) (Eq. 2); cost still grows with A*W.
- * Supported: a_bits in [1,4], w_bits in [1,2] (BS_ERR_UNSUPPORTED otherwise).
+ * Supported: a_bits in [1,4], w_bits in [1,4] (BS_ERR_UNSUPPORTED otherwise).
  * workspace: device, >= *_tc_workspace_bytes() (the larger, I8, size), 16-byte aligned,
  * overwritten.
  */

@@ -283,7 +283,7 @@ int bs_bitserial_conv2d_nhwc_tc(const uint32_t* act_packed, int a_bits, const ui
   const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
   if (int st = check_conv(g, a_bits, w_bits, w_enc, fn)) return st;
   if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, BS_TC_DEFAULT, fn)) return st;
-  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (!act_packed || !w_packed || !out || !workspace) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   const int64_t need = bs_conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits);
   if (workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
@@ -299,7 +299,7 @@ int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits, const uint32_t* 
   const char* fn = "bs_bitserial_dense_tc";
   if (int st = check_dense(a_packed, w_packed, out, a_bits, w_bits, w_enc, m, n, k, fn)) return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, BS_TC_DEFAULT, fn)) return st;
-  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   const int64_t need = bs_dense_tc_workspace_bytes(n, k, w_bits);
   if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
@@ -327,7 +327,7 @@ int bs_conv2d_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc
   if (int st = check_format(tc_format, fn)) return st;
   if (!w_packed || !w_tc) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   if (int st = check_bits(1, w_bits, w_enc, fn)) return st;
-  if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,2]", fn);
+  if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,4]", fn);
   if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0) return fail(BS_ERR_SHAPE, "%s: non-positive extent", fn);
   const int64_t need = bs_conv2d_tc_weight_bytes(oc, kh, kw, c, w_bits, tc_format);
   if (w_tc_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_tc needs %lld bytes", fn, (long long)need);
@@ -343,7 +343,7 @@ int bs_dense_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc,
   if (int st = check_format(tc_format, fn)) return st;
   if (!w_packed || !w_tc) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   if (int st = check_bits(1, w_bits, w_enc, fn)) return st;
-  if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,2]", fn);
+  if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,4]", fn);
   if (n <= 0 || k <= 0 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: bad n or k", fn);
   const int64_t need = bs_dense_tc_weight_bytes(n, k, w_bits, tc_format);
   if (w_tc_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_tc needs %lld bytes", fn, (long long)need);
@@ -360,7 +360,7 @@ int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits,
   const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
   if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
   if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, tc_format, fn)) return st;
-  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (!act_packed || !w_tc || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   if (!aligned16(act_packed) || !aligned16(w_tc) || !aligned16(out))
     return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
@@ -377,7 +377,7 @@ int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t*
   const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
   if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
   if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, tc_format, fn)) return st;
-  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (!act || !w_tc || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   const int64_t need = bs_conv2d_workspace_bytes(n, h, w, c, a_bits);
   if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
@@ -398,7 +398,7 @@ int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, const i
                            k, fn))
     return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn)) return st;
-  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
   bs::ConvProblem p = make_conv(a_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
@@ -412,7 +412,7 @@ int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, i
   if (int st = check_dense(a, reinterpret_cast<const uint32_t*>(w_tc), out, a_bits, w_bits, BS_UNIPOLAR, m, n, k, fn))
     return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn)) return st;
-  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   const int64_t need = bs_dense_workspace_bytes(m, k, a_bits);
   if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);

@@ -80,10 +80,22 @@ constexpr int kMaxTaps = 64;  // filter taps held in the shared-memory tap table
 // BS_TC_PROFILE builds (tools only) count cycles spent in each role's waits and print
 // them per CTA 0 at exit; the product build compiles these to nothing.
 #ifdef BS_TC_PROFILE
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define STAMP(name)                                                          \
+  do {                                                                       \
+    if (blockIdx.x == 0) printf("TCSTAMP %s warp %d t %llu\n", name, warp, gtime()); \
+  } while (0);
 #define PROF_DECL long long _pt = 0, _pacc[4] = {0, 0, 0, 0};
 #define PROF_BEGIN _pt = clock64();
 #define PROF_END(i) _pacc[i] += clock64() - _pt;
 #else
+#define STAMP(name) \
+  do {                \
+  } while (0);
 #define PROF_DECL
 #define PROF_BEGIN
 #define PROF_END(i)
@@ -448,7 +460,7 @@ struct Cfg {
   static constexpr int kAColsPlane = F4 ? 16 : BKB / 4;    // TMEM columns per plane per stage
   static constexpr int kACols = A_BITS * kAColsPlane;     // TMEM columns of one stage's A planes
   static constexpr int kBBytes = W_BITS * BN * kBRow;     // shared memory per stage (B only)
-  static constexpr int kSFCols = F4 ? 32 : 0;             // SFA: 4 planes x 4 cols; SFB: 2 x 8
+  static constexpr int kSFCols = F4 ? 16 + 8 * W_BITS : 0;  // SFA: 4 planes x 4 cols; SFB: W planes x 8
   static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + 512 /*tap table*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
@@ -531,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const ConvProblem& p = args.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (lane == 0 && (warp == 0 || warp == kMmaWarp)) STAMP("start")
   PROF_DECL
 #ifdef BS_TC_PROFILE
   const long long _t_start = clock64();
@@ -573,24 +586,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   // column 0, so TMEM addresses are compile-time constants
   if (*tmem_slot != 0u) asm volatile("trap;");
   constexpr uint32_t tmem = 0;
+  if (lane == 0 && warp == kMmaWarp) STAMP("prologue")
   if constexpr (F4) {
     // uniform UE8M0 scale factors: SFA plane i (4 columns) = 2^(i+1), SFB plane j (8
     // columns) = 2^(j+1); every byte of a region holds the plane's scale, so the MMA reads
     // the right value whatever its scale-factor layout (tools/mxf4_probe.cu: an M=128 /
     // N<=128 region spans 4 columns, N=256 8)
     if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-      uint32_t v[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) v[c] = 0x01010101u * uint32_t(c < 16 ? 128 + (c >> 2) : 128 + ((c - 16) >> 3));
-      asm volatile(
-          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-          "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-              tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::kSF0)),
-          "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-          "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
-          "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]),
-          "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-          : "memory");
+      for (int c0 = 0; c0 < C::kSFCols; c0 += 16) {  // 16 columns per store
+        uint32_t v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int col = c0 + c;
+          v[c] = 0x01010101u * uint32_t(col < 16 ? 128 + (col >> 2) : 128 + ((col - 16) >> 3));
+        }
+        tmem_st16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::kSF0 + c0), v);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     tc_fence_before();
@@ -789,6 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool resident = args.b_resident;
     const uint64_t bdesc0 = F4 ? smem_desc_sw64(smem_u32(s_stage)) : smem_desc_sw128(smem_u32(s_stage));
     if (resident) mbar_wait(smem_u32(full_b), 0);
+    if (lane == 0) STAMP("b_resident_ready")
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       PROF_BEGIN
       mbar_wait(smem_u32(acc_empty + acc), acc_phase ^ 1u);
@@ -823,6 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mma_commit_elect(smem_u32(acc_full + acc));
+      if (lane == 0 && tile == int(blockIdx.x)) STAMP("first_tile_issued")
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -843,6 +857,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_BEGIN
       mbar_wait(smem_u32(acc_full + acc), acc_phase);
       PROF_END(0)
+      if (lane == 0 && warp == kEpiWarp0 && tile == int(blockIdx.x)) STAMP("first_acc_full")
       tc_fence_after();
       bool released = false;
       for (int cb = cb0; cb < ncb; cb += kCbStep) {
@@ -925,7 +940,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1u;
       }
     }
+    if (lane == 0) STAMP("epilogue_loop_done")
     if (lane == 0) bulk_wait_all();
+    if (lane == 0) STAMP("stores_done")
   }
 
 #ifdef BS_TC_PROFILE
@@ -935,6 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   tc_fence_before();
   __syncthreads();
+  if (lane == 0 && warp == kMmaWarp) STAMP("end")
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::kTmemCols));
@@ -1080,7 +1098,7 @@ int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt) {
   return int64_t(w_bits) * n * tc_kpad(kp) * (tc_resolve_format(fmt) == kTcF4 ? 16 : 32);
 }
 
-bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 2; }
+bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 4; }
 
 cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int bipolar, int64_t n, int64_t kp,
                                      int8_t* wexp, int fmt, cudaStream_t stream) {
@@ -1107,6 +1125,7 @@ cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, in
     return f4 ? tc::launch_aw<A, W, true>(p, wexp, kpad, stream)                    \
               : tc::launch_aw<A, W, false>(p, wexp, kpad, stream);
   BS_TC(1, 1) BS_TC(2, 1) BS_TC(2, 2) BS_TC(1, 2) BS_TC(3, 1) BS_TC(3, 2) BS_TC(4, 1) BS_TC(4, 2)
+  BS_TC(1, 3) BS_TC(2, 3) BS_TC(3, 3) BS_TC(4, 3) BS_TC(1, 4) BS_TC(2, 4) BS_TC(3, 4) BS_TC(4, 4)
 #undef BS_TC
   return cudaErrorNotSupported;
 }

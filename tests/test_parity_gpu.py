@@ -265,7 +265,8 @@ def test_split_k_small_mn(case):
 
 
 # ------------------------------------------------------------ tensor-core path
-TC_PRECISIONS = [(1, 1), (2, 1), (2, 2), (1, 2), (3, 1), (3, 2), (4, 1), (4, 2)]
+TC_PRECISIONS = [(1, 1), (2, 1), (2, 2), (1, 2), (3, 1), (3, 2), (4, 1), (4, 2),
+                 (1, 3), (2, 3), (3, 3), (4, 3), (1, 4), (2, 4), (3, 4), (4, 4)]
 
 
 @pytest.mark.parametrize("a_bits,w_bits", TC_PRECISIONS)

@@ -5,8 +5,9 @@ and the time ratios the paper quotes ("W1A1 ... 14.4X faster than W4A4", "W2A2
 1.3x better" than W1A4; paper naming WxAy = our AyWx).  Parity of every cell is
 checked in tests/test_parity_gpu.py::test_limit_study_grid_parity.
 
-    python tools/limit_study.py > gpurun_out/limit_study.json
+    python tools/limit_study.py [--path tc|popc] > gpurun_out/limit_study.json
 """
+import argparse
 import json
 import os
 import sys
@@ -18,6 +19,9 @@ import paper_1810_11066_b200 as bs  # noqa: E402
 from paper_1810_11066_b200 import inputs  # noqa: E402
 
 
+PATH = "popc"
+
+
 def time_layer(L, batch, a_bits, w_bits, reps=20):
     g = inputs.gen(1000 * a_bits + w_bits + batch)
     act = inputs.codes((batch, L.h, L.w, L.ic), a_bits, g).cuda()
@@ -26,8 +30,16 @@ def time_layer(L, batch, a_bits, w_bits, reps=20):
     out = torch.empty((batch, L.h, L.w, L.oc), dtype=torch.int32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    def run():
-        bs.bitserial_conv2d_nhwc(ap, a_bits, wp, w_bits, bs.UNIPOLAR, batch, L.h, L.w, L.ic, L.oc, 3, 3, 1, 1, out=out)
+    if PATH == "tc":  # tensor-core path (FP4 format; prepared weights, untimed)
+        w_tc = bs.conv2d_tc_prepare_weights(wp, w_bits, bs.UNIPOLAR, L.oc, 3, 3, L.ic)
+
+        def run():
+            bs.bitserial_conv2d_nhwc_tc_prepared(ap, a_bits, w_tc, w_bits, batch, L.h, L.w, L.ic, L.oc, 3, 3, 1, 1,
+                                                 out=out)
+    else:
+        def run():
+            bs.bitserial_conv2d_nhwc(ap, a_bits, wp, w_bits, bs.UNIPOLAR, batch, L.h, L.w, L.ic, L.oc, 3, 3, 1, 1,
+                                     out=out)
     run()
     torch.cuda.synchronize()
     ts = []
@@ -45,8 +57,12 @@ def time_layer(L, batch, a_bits, w_bits, reps=20):
 
 
 def main():
+    global PATH
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--path", choices=["tc", "popc"], default="popc")
+    PATH = ap.parse_args().path
     L = inputs.TABLE1[9]
-    res = {}
+    res = {"path": PATH}
     for batch in (1, 256):
         cells = {}
         for a in range(1, 5):
