@@ -55,6 +55,12 @@ def _load():
         lib.oracle_bitpack.argtypes = [P, P, L, L, I]
         lib.oracle_bitpack.restype = I
         lib.oracle_num_threads.restype = I
+        lib.oracle_code_value.argtypes = [I, I, I]
+        lib.oracle_code_value.restype = L
+        lib.oracle_dense_enc.argtypes = [P, I, I, P, I, I, P, L, L, L]
+        lib.oracle_dense_enc.restype = I
+        lib.oracle_conv2d_nhwc_enc.argtypes = [P, I, I, P, I, I, P] + [I] * 11
+        lib.oracle_conv2d_nhwc_enc.restype = I
         _lib = lib
     return _lib
 
@@ -124,6 +130,50 @@ def conv2d_nhwc(act, a_bits: int, wt, w_bits: int, bipolar: bool,
                                     n, h, w, c, oc, kh, kw, sh, sw, ph, pw)
     if rc != 0:
         raise ValueError("oracle_conv2d_nhwc rejected its arguments")
+    return out
+
+
+UNSIGNED, BIPOLAR, SIGNED = 0, 1, 2  # operand encodings of the *_enc functions
+
+
+def code_value(code: int, bits: int, enc: int) -> int:
+    """Value of one code: 0 unsigned = code; 1 bipolar = sum_j 2^j (2 b_j - 1)
+    (PAPER.md:503); 2 signed two's complement, top plane -2^(bits-1)."""
+    return int(_load().oracle_code_value(int(code), int(bits), int(enc)))
+
+
+def dense_enc(a, a_bits: int, a_enc: int, w, w_bits: int, w_enc: int) -> np.ndarray:
+    """out[m][n] = sum_k value(a[m][k]) * value(w[n][k]) with an encoding per operand
+    (both-bipolar XNOR form PAPER.md:503, signed data PAPER.md:517)."""
+    a, w = _u8(a), _u8(w)
+    if a.ndim != 2 or w.ndim != 2 or a.shape[1] != w.shape[1]:
+        raise ValueError("dense_enc: a [M][K], w [N][K] with equal K")
+    m, k = a.shape
+    n = w.shape[0]
+    out = np.empty((m, n), dtype=np.int32)
+    if _load().oracle_dense_enc(_ptr(a), a_bits, a_enc, _ptr(w), w_bits, w_enc, _ptr(out), m, n, k) != 0:
+        raise ValueError("oracle_dense_enc rejected its arguments")
+    return out
+
+
+def conv2d_nhwc_enc(act, a_bits: int, a_enc: int, wt, w_bits: int, w_enc: int,
+                    stride=(1, 1), pad=(0, 0)) -> np.ndarray:
+    """conv2d_nhwc with an encoding per operand; padded positions contribute 0."""
+    act, wt = _u8(act), _u8(wt)
+    if act.ndim != 4 or wt.ndim != 4 or act.shape[3] != wt.shape[3]:
+        raise ValueError("conv2d_nhwc_enc: act [N][H][W][C], wt [OC][KH][KW][C]")
+    n, h, w, c = act.shape
+    oc, kh, kw, _ = wt.shape
+    sh, sw = stride
+    ph, pw = pad
+    oh, ow = conv_out_extent(h, kh, sh, ph), conv_out_extent(w, kw, sw, pw)
+    if oh <= 0 or ow <= 0:
+        raise ValueError("conv2d_nhwc_enc: empty output")
+    out = np.empty((n, oh, ow, oc), dtype=np.int32)
+    rc = _load().oracle_conv2d_nhwc_enc(_ptr(act), a_bits, a_enc, _ptr(wt), w_bits, w_enc, _ptr(out),
+                                        n, h, w, c, oc, kh, kw, sh, sw, ph, pw)
+    if rc != 0:
+        raise ValueError("oracle_conv2d_nhwc_enc rejected its arguments")
     return out
 
 

@@ -13,6 +13,11 @@
  *   oracle_weight_value  value of one weight code (unipolar / bipolar)
  *   oracle_dense         out[m][n] = sum_k a[m][k] * value(w[n][k])
  *   oracle_conv2d_nhwc   NHWC cross-correlation with zero padding, OHWI weights
+ *   oracle_code_value    value of one code in any encoding (unsigned / bipolar / signed)
+ *   oracle_dense_enc, oracle_conv2d_nhwc_enc
+ *                        the same products with an encoding for each operand
+ *                        (both-bipolar XNOR form; signed
+ *                        two's-complement data)
  *   oracle_bitpack       the packed bit-plane layout of the C ABI (defines it)
  *
  * No bit-planes, no popcount, no blocking or reordering: straight loops over the
@@ -123,6 +128,104 @@ int oracle_conv2d_nhwc(const uint8_t* act, int a_bits, const uint8_t* wt, int w_
       out[r * oc + o] = acc;
     }
   }
+  free(wv);
+  return 0;
+}
+
+/* Value of one code in encoding enc:
+ *   0 unsigned / unipolar : the code (Eq. 2);
+ *   1 bipolar             : every bit-plane a +/-1 digit, sum_j 2^j (2 b_j - 1)
+ *                           ("bipolar format (-1 and 1)");
+ *   2 signed              : two's complement, the top plane weighted -2^(bits-1)
+ *                           ("weighting binary dotproducts by their sign"). */
+int64_t oracle_code_value(int code, int bits, int enc) {
+  if (enc == 1) return oracle_weight_value(code, bits, 1);
+  if (enc == 2) return code >= (1 << (bits - 1)) ? (int64_t)code - ((int64_t)1 << bits) : code;
+  return code;
+}
+
+static int64_t max_abs_value(int bits, int enc) {
+  if (enc == 2) return (int64_t)1 << (bits - 1);
+  return ((int64_t)1 << bits) - 1;
+}
+
+static int enc_ok(int enc) { return enc >= 0 && enc <= 2; }
+
+/* out[m][n] = sum_k value(a[m][k]) * value(w[n][k]) with per-operand encodings. */
+int oracle_dense_enc(const uint8_t* a, int a_bits, int a_enc, const uint8_t* w, int w_bits, int w_enc,
+                     int32_t* out, int64_t m, int64_t n, int64_t k) {
+  if (m <= 0 || n <= 0 || k <= 0 || a_bits < 1 || a_bits > 8 || w_bits < 1 || w_bits > 8) return -1;
+  if (!enc_ok(a_enc) || !enc_ok(w_enc)) return -1;
+  if (!codes_in_range(a, m * k, a_bits) || !codes_in_range(w, n * k, w_bits)) return -1;
+  if ((double)k * (double)max_abs_value(a_bits, a_enc) * (double)max_abs_value(w_bits, w_enc) >= 2147483648.0)
+    return -1;
+  int32_t* av = (int32_t*)malloc(sizeof(int32_t) * (size_t)(m * k));
+  int32_t* wv = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n * k));
+  if (!av || !wv) {
+    free(av);
+    free(wv);
+    return -1;
+  }
+  for (int64_t i = 0; i < m * k; ++i) av[i] = (int32_t)oracle_code_value(a[i], a_bits, a_enc);
+  for (int64_t i = 0; i < n * k; ++i) wv[i] = (int32_t)oracle_code_value(w[i], w_bits, w_enc);
+#pragma omp parallel for schedule(static)
+  for (int64_t mi = 0; mi < m; ++mi) {
+    for (int64_t ni = 0; ni < n; ++ni) {
+      int32_t acc = 0;
+      for (int64_t ki = 0; ki < k; ++ki) acc += av[mi * k + ki] * wv[ni * k + ki];
+      out[mi * n + ni] = acc;
+    }
+  }
+  free(av);
+  free(wv);
+  return 0;
+}
+
+/* NHWC cross-correlation with per-operand encodings; zero padding: a padded position
+ * contributes 0 (value 0, whatever the activation encoding). */
+int oracle_conv2d_nhwc_enc(const uint8_t* act, int a_bits, int a_enc, const uint8_t* wt, int w_bits, int w_enc,
+                           int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                           int sh, int sw, int ph, int pw) {
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || oc <= 0 || kh <= 0 || kw <= 0) return -1;
+  if (sh < 1 || sw < 1 || ph < 0 || pw < 0) return -1;
+  if (a_bits < 1 || a_bits > 8 || w_bits < 1 || w_bits > 8 || !enc_ok(a_enc) || !enc_ok(w_enc)) return -1;
+  int64_t oh = oracle_conv_out_extent(h, kh, sh, ph), ow = oracle_conv_out_extent(w, kw, sw, pw);
+  if (oh <= 0 || ow <= 0) return -1;
+  int64_t K = (int64_t)kh * kw * c;
+  int64_t na = (int64_t)n * h * w * c;
+  if (!codes_in_range(act, na, a_bits) || !codes_in_range(wt, (int64_t)oc * K, w_bits)) return -1;
+  if ((double)K * (double)max_abs_value(a_bits, a_enc) * (double)max_abs_value(w_bits, w_enc) >= 2147483648.0)
+    return -1;
+  int32_t* av = (int32_t*)malloc(sizeof(int32_t) * (size_t)na);
+  int32_t* wv = (int32_t*)malloc(sizeof(int32_t) * (size_t)(oc * K));
+  if (!av || !wv) {
+    free(av);
+    free(wv);
+    return -1;
+  }
+  for (int64_t i = 0; i < na; ++i) av[i] = (int32_t)oracle_code_value(act[i], a_bits, a_enc);
+  for (int64_t i = 0; i < oc * K; ++i) wv[i] = (int32_t)oracle_code_value(wt[i], w_bits, w_enc);
+  int64_t rows = (int64_t)n * oh * ow;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r) {
+    int64_t b = r / (oh * ow), oy = (r / ow) % oh, ox = r % ow;
+    for (int o = 0; o < oc; ++o) {
+      int32_t acc = 0;
+      for (int ky = 0; ky < kh; ++ky) {
+        int64_t iy = oy * sh + ky - ph;
+        if (iy < 0 || iy >= h) continue; /* zero padding contributes 0 */
+        for (int kx = 0; kx < kw; ++kx) {
+          int64_t ix = ox * sw + kx - pw;
+          if (ix < 0 || ix >= w) continue;
+          const int32_t* ap = av + ((b * h + iy) * w + ix) * c;
+          const int32_t* wp = wv + (((int64_t)o * kh + ky) * kw + kx) * c;
+          for (int ci = 0; ci < c; ++ci) acc += ap[ci] * wp[ci];
+        }
+      }
+      out[r * oc + o] = acc;
+    }
+  }
+  free(av);
   free(wv);
   return 0;
 }

@@ -320,3 +320,97 @@ def test_rejections():
         oracle.conv2d_nhwc(np.zeros((1, 2, 2, 1), np.uint8), 1, np.zeros((1, 3, 3, 1), np.uint8), 1, False)  # empty
     with pytest.raises(ValueError):  # accumulator bound K*(2^8-1)^2 >= 2^31
         oracle.dense(np.zeros((1, 40000), np.uint8), 8, np.zeros((1, 40000), np.uint8), 8, False)
+
+
+# ----------------------------------------------------- encodings
+def eq2_signed_literal(a, a_bits, a_signed, w, w_bits, w_signed):
+    """PAPER.md:517 "Equation 2 can be modified to support signed data by weighting
+    binary dotproducts by their sign": two's complement, the top plane of a signed
+    operand carries sign -1, every plane pair popc(x_n & y_m) * s_n * s_m * 2^(n+m)."""
+    ap, wp = planes(a, a_bits), planes(w, w_bits)
+    sa = [(-1 if (a_signed and i == a_bits - 1) else 1) for i in range(a_bits)]
+    sw = [(-1 if (w_signed and j == w_bits - 1) else 1) for j in range(w_bits)]
+    return sum(sa[i] * sw[j] * (popcount(ap[i] & wp[j]) << (i + j)) for i in range(a_bits) for j in range(w_bits))
+
+
+def eq2_xnor_literal(a, a_bits, w, w_bits):
+    """PAPER.md:503: bipolar (-1/+1) data, "bitwise xnor replaces bitwise and": for
+    +/-1 digit vectors x_n, y_m of length K, x_n . y_m = 2 popc(~(x_n ^ y_m)) - K, and
+    the multi-bit value is sum_n sum_m 2^(n+m) x_n . y_m (Eq. 2 with that dot)."""
+    k = len(a)
+    mask = (1 << k) - 1
+    ap, wp = planes(a, a_bits), planes(w, w_bits)
+    return sum((2 * popcount(~(ap[i] ^ wp[j]) & mask) - k) << (i + j) for i in range(a_bits) for j in range(w_bits))
+
+
+def test_code_value_tables():
+    """Encodings: signed = two's complement; bipolar = 2 code - (2^bits - 1); unsigned."""
+    assert [oracle.code_value(c, 2, oracle.SIGNED) for c in range(4)] == [0, 1, -2, -1]
+    assert [oracle.code_value(c, 3, oracle.SIGNED) for c in range(8)] == [0, 1, 2, 3, -4, -3, -2, -1]
+    assert [oracle.code_value(c, 1, oracle.SIGNED) for c in range(2)] == [0, -1]
+    assert [oracle.code_value(c, 4, oracle.BIPOLAR) for c in range(16)] == [2 * c - 15 for c in range(16)]
+    assert [oracle.code_value(c, 3, oracle.UNSIGNED) for c in range(8)] == list(range(8))
+
+
+@pytest.mark.parametrize("a_bits,w_bits,k", [(2, 1, 3), (1, 2, 3), (2, 2, 2), (3, 1, 2), (1, 1, 4)])
+def test_encodings_exhaustive(a_bits, w_bits, k):
+    """Every code vector pair: the encoded oracle equals (1) the sign-weighted Eq. 2 for
+    each signed/unsigned combination, (2) the XNOR form for both operands bipolar,
+    (3) the literal bipolar-weight form and the plain oracle for unsigned activations."""
+    avs = list(itertools.product(range(1 << a_bits), repeat=k))
+    wvs = list(itertools.product(range(1 << w_bits), repeat=k))
+    A = np.array(avs, np.uint8)
+    W = np.array(wvs, np.uint8)
+    U, B, S = oracle.UNSIGNED, oracle.BIPOLAR, oracle.SIGNED
+    res = {(ae, we): oracle.dense_enc(A, a_bits, ae, W, w_bits, we) for ae in (U, B, S) for we in (U, B, S)}
+    np.testing.assert_array_equal(res[(U, U)], oracle.dense(A, a_bits, W, w_bits, False))
+    np.testing.assert_array_equal(res[(U, B)], oracle.dense(A, a_bits, W, w_bits, True))
+    for i, a in enumerate(avs):
+        for j, w in enumerate(wvs):
+            assert res[(S, S)][i, j] == eq2_signed_literal(a, a_bits, True, w, w_bits, True)
+            assert res[(S, U)][i, j] == eq2_signed_literal(a, a_bits, True, w, w_bits, False)
+            assert res[(U, S)][i, j] == eq2_signed_literal(a, a_bits, False, w, w_bits, True)
+            assert res[(B, B)][i, j] == eq2_xnor_literal(a, a_bits, w, w_bits)
+
+
+def _decode_enc(x, bits, enc):
+    x = x.astype(np.float64)
+    if enc == oracle.BIPOLAR:
+        return 2 * x - (2 ** bits - 1)
+    if enc == oracle.SIGNED:
+        return np.where(x >= 2 ** (bits - 1), x - 2 ** bits, x)
+    return x
+
+
+@pytest.mark.parametrize("a_enc,w_enc", [(1, 1), (2, 2), (2, 0), (0, 2), (1, 2), (2, 1), (1, 0)])
+def test_encoded_dense_and_conv_vs_torch(a_enc, w_enc):
+    """Library pin: float64 torch mm / conv2d (zero padding = value 0) on decoded values."""
+    rng = np.random.default_rng(7 * a_enc + w_enc)
+    for a_bits, w_bits in ((2, 1), (3, 2), (1, 1), (4, 3)):
+        a = rng.integers(0, 2 ** a_bits, (23, 131), dtype=np.uint8)
+        w = rng.integers(0, 2 ** w_bits, (17, 131), dtype=np.uint8)
+        got = oracle.dense_enc(a, a_bits, a_enc, w, w_bits, w_enc)
+        ref = torch.from_numpy(_decode_enc(a, a_bits, a_enc)) @ torch.from_numpy(_decode_enc(w, w_bits, w_enc)).T
+        np.testing.assert_array_equal(got, ref.numpy().astype(np.int64))
+        for case in CONV_CASES[:3]:
+            n, h, w_, c, oc, kh, kw, sh, sw, ph, pw = case
+            act = rng.integers(0, 2 ** a_bits, (n, h, w_, c), dtype=np.uint8)
+            wt = rng.integers(0, 2 ** w_bits, (oc, kh, kw, c), dtype=np.uint8)
+            got = oracle.conv2d_nhwc_enc(act, a_bits, a_enc, wt, w_bits, w_enc, stride=(sh, sw), pad=(ph, pw))
+            x = torch.from_numpy(_decode_enc(act, a_bits, a_enc)).permute(0, 3, 1, 2)
+            k_ = torch.from_numpy(_decode_enc(wt, w_bits, w_enc)).permute(0, 3, 1, 2)
+            ref = F.conv2d(x, k_, stride=(sh, sw), padding=(ph, pw)).permute(0, 2, 3, 1)
+            np.testing.assert_array_equal(got, ref.numpy().astype(np.int64))
+
+
+def test_encoded_closed_forms():
+    """Both bipolar, all codes max (every digit +1): each output = K (2^A-1)(2^W-1);
+    signed all-ones codes are -1: each output = K; signed min code x max."""
+    k = 77
+    a = np.full((3, k), 3, np.uint8)
+    w = np.full((2, k), 1, np.uint8)
+    assert (oracle.dense_enc(a, 2, 1, w, 1, 1) == k * 3 * 1).all()
+    assert (oracle.dense_enc(a, 2, 2, np.full((2, k), 3, np.uint8), 2, 2) == k).all()  # (-1)(-1)
+    assert (oracle.dense_enc(np.full((1, k), 2, np.uint8), 2, 2, np.full((1, k), 1, np.uint8), 2, 2) == -2 * k).all()
+    with pytest.raises(ValueError):
+        oracle.dense_enc(a, 2, 3, w, 1, 0)
