@@ -67,7 +67,16 @@ typedef enum {
   BS_ERR_WORKSPACE = 8      /* workspace missing or smaller than *_workspace_bytes() */
 } bs_status;
 
-typedef enum { BS_UNIPOLAR = 0, BS_BIPOLAR = 1 } bs_encoding;
+/* Weight encoding.  BS_SIGNED (two's complement, the top bit-plane weighs -2^(W-1):
+ * "weighting binary dotproducts by their sign") is accepted by the
+ * tensor-core entries only. */
+typedef enum { BS_UNIPOLAR = 0, BS_BIPOLAR = 1, BS_SIGNED = 2 } bs_encoding;
+
+/* Activation encoding (tensor-core entries, FP4 format).  BS_A_BIPOLAR: every plane a
+ * +/-1 digit (value 2 code - (2^A - 1)); with bipolar weights this is the XNOR form of
+ * PAPER.md:503.  BS_A_SIGNED: two's complement.  Zero padding and the
+ * reduction-axis tail contribute 0 in every encoding. */
+typedef enum { BS_A_UNSIGNED = 0, BS_A_BIPOLAR = 1, BS_A_SIGNED = 2 } bs_a_encoding;
 
 /* Kernel family for the *_ex entry points.  BS_ALGO_AUTO picks per shape.
  *   POPC     : AND + POPC per word pair (Eq. 1 inside Eq. 2) on the integer pipes;
@@ -223,28 +232,33 @@ typedef enum { BS_TC_DEFAULT = 0, BS_TC_I8 = 1, BS_TC_F4 = 2 } bs_tc_format;
 int64_t bs_conv2d_tc_weight_bytes(int oc, int kh, int kw, int c, int w_bits, int tc_format);
 int64_t bs_dense_tc_weight_bytes(int64_t n, int64_t k, int w_bits, int tc_format);
 int bs_conv2d_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
-                                 int tc_format, int8_t* w_tc, int64_t w_tc_bytes, void* stream);
+                                 int tc_format, int8_t* w_tc, int64_t w_tc_bytes, void* stream);  /* w_enc 0..2 */
 int bs_dense_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t k,
                                 int tc_format, int8_t* w_tc, int64_t w_tc_bytes, void* stream);
 
 /* Tensor-core conv / dense on prepared weights (one launch: the persistent tcgen05
- * kernel; out as in bs_bitserial_conv2d_nhwc / bs_bitserial_dense). */
-int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, const int8_t* w_tc, int w_bits,
-                                         int tc_format, int32_t* out, int n, int h, int w, int c, int oc, int kh,
-                                         int kw, int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
-int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, const int8_t* w_tc, int w_bits,
-                                   int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k, void* stream);
+ * kernel; out as in bs_bitserial_conv2d_nhwc / bs_bitserial_dense, with the value of
+ * each code given by a_enc (bs_a_encoding) and w_enc (bs_encoding, the encoding the
+ * weights were prepared with)).  a_enc != BS_A_UNSIGNED needs the FP4 format
+ * (BS_ERR_UNSUPPORTED on I8). */
+int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, int a_enc, const int8_t* w_tc,
+                                         int w_bits, int w_enc, int tc_format, int32_t* out, int n, int h, int w,
+                                         int c, int oc, int kh, int kw, int stride_h, int stride_w, int pad_h,
+                                         int pad_w, void* stream);
+int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,
+                                   int w_enc, int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k,
+                                   void* stream);
 
 /* The timed step of the paper on the tensor-core path: activation
  * bit-packing (raw uint8 codes -> workspace of *_workspace_bytes() bytes) followed by
  * the tensor-core conv / dense on prepared weights.  Two launches. */
-int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t* w_tc, int w_bits, int tc_format,
-                                   int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
-                                   int stride_h, int stride_w, int pad_h, int pad_w,
+int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,
+                                   int w_enc, int tc_format, int32_t* out, int n, int h, int w, int c, int oc,
+                                   int kh, int kw, int stride_h, int stride_w, int pad_h, int pad_w,
                                    void* workspace, int64_t workspace_bytes, void* stream);
-int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, int w_bits, int tc_format,
-                             int32_t* out, int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes,
-                             void* stream);
+int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, int a_enc, const int8_t* w_tc, int w_bits, int w_enc,
+                             int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k, void* workspace,
+                             int64_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * End-to-end entry with HOST activations and HOST output (used for the bench's
@@ -261,8 +275,8 @@ int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits,
                                   void* workspace, int64_t workspace_bytes, void* stream);
 
 /* As above on the tensor-core path with prepared weights (bs_bitserial_conv2d_nhwc_tc_i8). */
-int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, const int8_t* w_tc, int w_bits,
-                                     int tc_format, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,
+                                     int w_enc, int tc_format, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
                                      int stride_h, int stride_w, int pad_h, int pad_w,
                                      uint8_t* act_dev, int32_t* out_dev,
                                      void* workspace, int64_t workspace_bytes, void* stream);

@@ -18,7 +18,7 @@ import os
 import torch
 
 __all__ = [
-    "UNIPOLAR", "BIPOLAR", "ALGO_AUTO", "ALGO_POPC", "ALGO_POPC_LIT", "ALGO_GEMV",
+    "UNIPOLAR", "BIPOLAR", "SIGNED", "A_UNSIGNED", "A_BIPOLAR", "A_SIGNED", "ALGO_AUTO", "ALGO_POPC", "ALGO_POPC_LIT", "ALGO_GEMV",
     "BitserialError", "library_path", "abi_version", "kernel_launches", "packed_row_words", "bitpack",
     "bitserial_dense", "bitserial_dense_i8", "bitserial_conv2d_nhwc", "bitserial_conv2d_nhwc_i8",
     "bitserial_conv2d_nhwc_host", "conv2d_workspace_bytes", "dense_workspace_bytes", "conv_out_extent",
@@ -29,7 +29,8 @@ __all__ = [
     "TC_F4", "EXPORTED_SYMBOLS",
 ]
 
-UNIPOLAR, BIPOLAR = 0, 1
+UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
+A_UNSIGNED, A_BIPOLAR, A_SIGNED = 0, 1, 2    # activation encodings (bs_a_encoding)
 TC_DEFAULT, TC_I8, TC_F4 = 0, 1, 2  # bs_tc_format
 ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV = 0, 1, 2, 3
 
@@ -94,11 +95,11 @@ def _load():
         "bs_dense_tc_weight_bytes": ([L, L, I, I], L),
         "bs_conv2d_tc_prepare_weights": ([P, I, I, I, I, I, I, I, P, L, P], I),
         "bs_dense_tc_prepare_weights": ([P, I, I, L, L, I, P, L, P], I),
-        "bs_bitserial_conv2d_nhwc_tc_prepared": ([P, I, P, I, I, P] + [I] * 11 + [P], I),
-        "bs_bitserial_dense_tc_prepared": ([P, I, P, I, I, P, L, L, L, P], I),
-        "bs_bitserial_conv2d_nhwc_tc_i8": ([P, I, P, I, I, P] + [I] * 11 + [P, L, P], I),
-        "bs_bitserial_dense_tc_i8": ([P, I, P, I, I, P, L, L, L, P, L, P], I),
-        "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, P, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_prepared": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P], I),
+        "bs_bitserial_dense_tc_prepared": ([P, I, I, P, I, I, I, P, L, L, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_i8": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, L, P], I),
+        "bs_bitserial_dense_tc_i8": ([P, I, I, P, I, I, I, P, L, L, L, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -303,30 +304,32 @@ def dense_tc_prepare_weights(w_packed, w_bits, w_enc, n, k, tc_format=TC_DEFAULT
 
 
 def bitserial_conv2d_nhwc_tc_prepared(act_packed, a_bits, w_tc, w_bits, n, h, w, c, oc, kh, kw, stride=1, pad=0,
-                                      out=None, tc_format=TC_DEFAULT, stream=None):
-    """bs_bitserial_conv2d_nhwc_tc_prepared: packed activations x prepared weights -> int32 NHWC."""
+                                      out=None, tc_format=TC_DEFAULT, stream=None, a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
+    """bs_bitserial_conv2d_nhwc_tc_prepared: packed activations x prepared weights -> int32 NHWC
+    (a_enc: activation encoding; w_enc: the encoding the weights were prepared with)."""
     sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
     if out is None:
         out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act_packed.device)
     _check(_load().bs_bitserial_conv2d_nhwc_tc_prepared(
-        _dev(act_packed, "act_packed", torch.int32), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
+        _dev(act_packed, "act_packed", torch.int32), a_bits, int(a_enc), _dev(w_tc, "w_tc", torch.int8), w_bits,
+        int(w_enc), int(tc_format),
         _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _stream(stream)))
     return out
 
 
 def bitserial_dense_tc_prepared(a_packed, a_bits, w_tc, w_bits, m, n, k, out=None, tc_format=TC_DEFAULT,
-                                stream=None):
+                                stream=None, a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
     """bs_bitserial_dense_tc_prepared: packed activations x prepared weights -> int32 [m][n]."""
     if out is None:
         out = torch.empty((m, n), dtype=torch.int32, device=a_packed.device)
-    _check(_load().bs_bitserial_dense_tc_prepared(_dev(a_packed, "a_packed", torch.int32), a_bits,
-                                                  _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
+    _check(_load().bs_bitserial_dense_tc_prepared(_dev(a_packed, "a_packed", torch.int32), a_bits, int(a_enc),
+                                                  _dev(w_tc, "w_tc", torch.int8), w_bits, int(w_enc), int(tc_format),
                                                   _dev(out, "out", torch.int32), m, n, k, _stream(stream)))
     return out
 
 
 def bitserial_conv2d_nhwc_tc_i8(act, a_bits, w_tc, w_bits, oc, kh, kw, stride=1, pad=0, out=None, workspace=None,
-                                tc_format=TC_DEFAULT, stream=None):
+                                tc_format=TC_DEFAULT, stream=None, a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
     """bs_bitserial_conv2d_nhwc_tc_i8: raw uint8 NHWC activations packed inside the call,
     then the tensor-core conv on prepared weights (the timed step)."""
     n, h, w, c = act.shape
@@ -337,14 +340,15 @@ def bitserial_conv2d_nhwc_tc_i8(act, a_bits, w_tc, w_bits, oc, kh, kw, stride=1,
         workspace = torch.empty(max(conv2d_workspace_bytes(n, h, w, c, a_bits), 16), dtype=torch.uint8,
                                 device=act.device)
     _check(_load().bs_bitserial_conv2d_nhwc_tc_i8(
-        _dev(act, "act", torch.uint8), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
-        _dev(out, "out", torch.int32),
+        _dev(act, "act", torch.uint8), a_bits, int(a_enc), _dev(w_tc, "w_tc", torch.int8), w_bits, int(w_enc),
+        int(tc_format), _dev(out, "out", torch.int32),
         n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _dev(workspace, "workspace", torch.uint8), workspace.numel(),
         _stream(stream)))
     return out
 
 
-def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, tc_format=TC_DEFAULT, stream=None):
+def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, tc_format=TC_DEFAULT, stream=None,
+                          a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
     """bs_bitserial_dense_tc_i8: raw uint8 activations [m][k] packed inside the call, then
     the tensor-core dense product on prepared weights."""
     m, k = a.shape
@@ -352,7 +356,8 @@ def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, 
         out = torch.empty((m, n), dtype=torch.int32, device=a.device)
     if workspace is None:
         workspace = torch.empty(max(dense_workspace_bytes(m, k, a_bits), 16), dtype=torch.uint8, device=a.device)
-    _check(_load().bs_bitserial_dense_tc_i8(_dev(a, "a", torch.uint8), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits,
+    _check(_load().bs_bitserial_dense_tc_i8(_dev(a, "a", torch.uint8), a_bits, int(a_enc),
+                                            _dev(w_tc, "w_tc", torch.int8), w_bits, int(w_enc),
                                             int(tc_format), _dev(out, "out", torch.int32), m, n, k,
                                             _dev(workspace, "workspace", torch.uint8), workspace.numel(),
                                             _stream(stream)))
@@ -360,7 +365,7 @@ def bitserial_dense_tc_i8(a, a_bits, w_tc, w_bits, n, out=None, workspace=None, 
 
 
 def bitserial_conv2d_nhwc_tc_host(act_host, a_bits, w_tc, w_bits, oc, kh, kw, stride, pad, out_host, act_dev, out_dev,
-                                  workspace, tc_format=TC_DEFAULT, stream=None):
+                                  workspace, tc_format=TC_DEFAULT, stream=None, a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
     """bs_bitserial_conv2d_nhwc_tc_host: the e2e path (host in, host out) on the tensor-core kernel."""
     if act_host.device.type != "cpu" or out_host.device.type != "cpu":
         raise BitserialError("act_host/out_host must be CPU tensors")
@@ -369,7 +374,8 @@ def bitserial_conv2d_nhwc_tc_host(act_host, a_bits, w_tc, w_bits, oc, kh, kw, st
     n, h, w, c = act_host.shape
     sh, sw, ph, pw, _, _ = _conv_geom(n, h, w, kh, kw, stride, pad)
     _check(_load().bs_bitserial_conv2d_nhwc_tc_host(
-        ctypes.c_void_p(act_host.data_ptr()), a_bits, _dev(w_tc, "w_tc", torch.int8), w_bits, int(tc_format),
+        ctypes.c_void_p(act_host.data_ptr()), a_bits, int(a_enc), _dev(w_tc, "w_tc", torch.int8), w_bits, int(w_enc),
+        int(tc_format),
         ctypes.c_void_p(out_host.data_ptr()), n, h, w, c, oc, kh, kw, sh, sw, ph, pw,
         _dev(act_dev, "act_dev", torch.uint8), _dev(out_dev, "out_dev", torch.int32),
         _dev(workspace, "workspace", torch.uint8), workspace.numel(), _stream(stream)))

@@ -53,6 +53,21 @@ int check_bound(int64_t k, int a_bits, int w_bits, const char* fn) {
   return BS_OK;
 }
 
+// Tensor-core path encodings: weights unipolar / bipolar / signed (prepared offline);
+// activations unsigned / bipolar / signed on the FP4 format (the I8 format's A operand
+// is unsigned u8: unsigned activations only).
+int check_tc_enc(int a_enc, int w_enc, int tc_format, const char* fn) {
+  if (a_enc < BS_A_UNSIGNED || a_enc > BS_A_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad a_enc %d", fn, a_enc);
+  if (w_enc < BS_UNIPOLAR || w_enc > BS_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad w_enc %d", fn, w_enc);
+  if (a_enc != BS_A_UNSIGNED && bs::tc_resolve_format(tc_format) != bs::kTcF4)
+    return fail(BS_ERR_UNSUPPORTED, "%s: bipolar / signed activations need the FP4 tensor-core format", fn);
+  return BS_OK;
+}
+
+int64_t max_abs_code(int bits, int enc) {  // largest |value| of a code (signed: -2^(bits-1))
+  return enc == 2 ? (int64_t(1) << (bits - 1)) : (int64_t(1) << bits) - 1;
+}
+
 int check_format(int tc_format, const char* fn) {
   if (tc_format < BS_TC_DEFAULT || tc_format > BS_TC_F4)
     return fail(BS_ERR_INVALID_ARG, "%s: bad tensor-core format %d", fn, tc_format);
@@ -61,9 +76,9 @@ int check_format(int tc_format, const char* fn) {
 
 // The FP4 tensor-core format accumulates in FP32 and converts with the 1.5*2^23 trick:
 // exact while |out| < 2^22 (bound below); the I8 format is exact to the int32 bound.
-int check_tc_bound(int64_t k, int a_bits, int w_bits, int tc_format, const char* fn) {
+int check_tc_bound(int64_t k, int a_bits, int w_bits, int tc_format, const char* fn, int a_enc = 0, int w_enc = 0) {
   if (bs::tc_resolve_format(tc_format) != bs::kTcF4) return BS_OK;
-  const double bound = double(k) * double((1 << a_bits) - 1) * double((1 << w_bits) - 1);
+  const double bound = double(k) * double(max_abs_code(a_bits, a_enc)) * double(max_abs_code(w_bits, w_enc));
   if (bound >= 4194304.0)
     return fail(BS_ERR_OVERFLOW, "%s: K*(2^A-1)*(2^W-1) = %.0f >= 2^22 (FP4 format exactness bound; use BS_TC_I8)",
                 fn, bound);
@@ -106,6 +121,8 @@ bs::ConvProblem make_conv(const uint32_t* act, int a_bits, const uint32_t* wt, i
   p.sh = g.sh; p.sw = g.sw; p.ph = g.ph; p.pw = g.pw;
   p.oh = conv_out(g.h, g.kh, g.sh, g.ph); p.ow = conv_out(g.w, g.kw, g.sw, g.pw);
   p.a_bits = a_bits; p.w_bits = w_bits; p.bipolar = w_enc == BS_BIPOLAR;
+  p.a_enc = BS_A_UNSIGNED;
+  p.c_tap = g.c;
   p.act_plane = int64_t(g.n) * g.h * g.w * p.kw_a;
   p.M = int64_t(g.n) * p.oh * p.ow;
   p.kp = int64_t(g.kh) * g.kw * p.kw_a;
@@ -326,14 +343,15 @@ int bs_conv2d_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc
   const char* fn = "bs_conv2d_tc_prepare_weights";
   if (int st = check_format(tc_format, fn)) return st;
   if (!w_packed || !w_tc) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
-  if (int st = check_bits(1, w_bits, w_enc, fn)) return st;
+  if (int st = check_bits(1, w_bits, BS_UNIPOLAR, fn)) return st;
+  if (int st = check_tc_enc(BS_A_UNSIGNED, w_enc, tc_format, fn)) return st;
   if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,4]", fn);
   if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0) return fail(BS_ERR_SHAPE, "%s: non-positive extent", fn);
   const int64_t need = bs_conv2d_tc_weight_bytes(oc, kh, kw, c, w_bits, tc_format);
   if (w_tc_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_tc needs %lld bytes", fn, (long long)need);
   if (!aligned16(w_packed) || !aligned16(w_tc)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
-  return cuda_status(bs::launch_tc_expand_weights(w_packed, w_bits, w_enc == BS_BIPOLAR, oc,
-                                                  int64_t(kh) * kw * row_words(c), w_tc, tc_format,
+  return cuda_status(bs::launch_tc_expand_weights(w_packed, w_bits, w_enc, oc, int64_t(kh) * kw * row_words(c), c,
+                                                  int(row_words(c)), w_tc, tc_format,
                                                   static_cast<cudaStream_t>(stream)), fn);
 }
 
@@ -342,41 +360,48 @@ int bs_dense_tc_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc,
   const char* fn = "bs_dense_tc_prepare_weights";
   if (int st = check_format(tc_format, fn)) return st;
   if (!w_packed || !w_tc) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
-  if (int st = check_bits(1, w_bits, w_enc, fn)) return st;
+  if (int st = check_bits(1, w_bits, BS_UNIPOLAR, fn)) return st;
+  if (int st = check_tc_enc(BS_A_UNSIGNED, w_enc, tc_format, fn)) return st;
   if (!bs::tc_supported(1, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits in [1,4]", fn);
   if (n <= 0 || k <= 0 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: bad n or k", fn);
   const int64_t need = bs_dense_tc_weight_bytes(n, k, w_bits, tc_format);
   if (w_tc_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_tc needs %lld bytes", fn, (long long)need);
   if (!aligned16(w_packed) || !aligned16(w_tc)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
-  return cuda_status(bs::launch_tc_expand_weights(w_packed, w_bits, w_enc == BS_BIPOLAR, n, row_words(k), w_tc,
-                                                  tc_format, static_cast<cudaStream_t>(stream)), fn);
+  if (k > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: k too large", fn);
+  return cuda_status(bs::launch_tc_expand_weights(w_packed, w_bits, w_enc, n, row_words(k), int(k),
+                                                  int(row_words(k)), w_tc, tc_format,
+                                                  static_cast<cudaStream_t>(stream)), fn);
 }
 
-int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, const int8_t* w_tc, int w_bits,
-                                         int tc_format, int32_t* out, int n, int h, int w, int c, int oc, int kh,
-                                         int kw, int stride_h, int stride_w, int pad_h, int pad_w, void* stream) {
+int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits, int a_enc, const int8_t* w_tc,
+                                         int w_bits, int w_enc, int tc_format, int32_t* out, int n, int h, int w,
+                                         int c, int oc, int kh, int kw, int stride_h, int stride_w, int pad_h,
+                                         int pad_w, void* stream) {
   const char* fn = "bs_bitserial_conv2d_nhwc_tc_prepared";
   if (int st = check_format(tc_format, fn)) return st;
+  if (int st = check_tc_enc(a_enc, w_enc, tc_format, fn)) return st;
   const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
   if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
-  if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, tc_format, fn)) return st;
+  if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (!act_packed || !w_tc || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   if (!aligned16(act_packed) || !aligned16(w_tc) || !aligned16(out))
     return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
   bs::ConvProblem p = make_conv(act_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  p.a_enc = a_enc;
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream)), fn);
 }
 
-int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t* w_tc, int w_bits, int tc_format,
-                                   int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw, int stride_h,
-                                   int stride_w, int pad_h, int pad_w, void* workspace, int64_t workspace_bytes,
-                                   void* stream) {
+int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,
+                                   int w_enc, int tc_format, int32_t* out, int n, int h, int w, int c, int oc, int kh,
+                                   int kw, int stride_h, int stride_w, int pad_h, int pad_w, void* workspace,
+                                   int64_t workspace_bytes, void* stream) {
   const char* fn = "bs_bitserial_conv2d_nhwc_tc_i8";
   if (int st = check_format(tc_format, fn)) return st;
+  if (int st = check_tc_enc(a_enc, w_enc, tc_format, fn)) return st;
   const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
   if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
-  if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, tc_format, fn)) return st;
+  if (int st = check_tc_bound(int64_t(kh) * kw * c, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (!act || !w_tc || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
   const int64_t need = bs_conv2d_workspace_bytes(n, h, w, c, a_bits);
@@ -387,31 +412,37 @@ int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, const int8_t*
   uint32_t* ap = static_cast<uint32_t*>(workspace);
   if (int st = cuda_status(bs::launch_bitpack(act, ap, int64_t(n) * h * w, c, row_words(c), a_bits, s), fn)) return st;
   bs::ConvProblem p = make_conv(ap, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  p.a_enc = a_enc;
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, s), fn);
 }
 
-int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, const int8_t* w_tc, int w_bits, int tc_format,
-                                   int32_t* out, int64_t m, int64_t n, int64_t k, void* stream) {
+int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,
+                                   int w_enc, int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k,
+                                   void* stream) {
   const char* fn = "bs_bitserial_dense_tc_prepared";
   if (int st = check_format(tc_format, fn)) return st;
+  if (int st = check_tc_enc(a_enc, w_enc, tc_format, fn)) return st;
   if (int st = check_dense(a_packed, reinterpret_cast<const uint32_t*>(w_tc), out, a_bits, w_bits, BS_UNIPOLAR, m, n,
                            k, fn))
     return st;
-  if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn)) return st;
+  if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
   bs::ConvProblem p = make_conv(a_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  p.a_enc = a_enc;
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream)), fn);
 }
 
-int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, int w_bits, int tc_format, int32_t* out,
-                             int64_t m, int64_t n, int64_t k, void* workspace, int64_t workspace_bytes, void* stream) {
+int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, int a_enc, const int8_t* w_tc, int w_bits, int w_enc,
+                             int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
   const char* fn = "bs_bitserial_dense_tc_i8";
   if (int st = check_format(tc_format, fn)) return st;
+  if (int st = check_tc_enc(a_enc, w_enc, tc_format, fn)) return st;
   if (int st = check_dense(a, reinterpret_cast<const uint32_t*>(w_tc), out, a_bits, w_bits, BS_UNIPOLAR, m, n, k, fn))
     return st;
-  if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn)) return st;
+  if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
   if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   const int64_t need = bs_dense_workspace_bytes(m, k, a_bits);
@@ -422,11 +453,12 @@ int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, const int8_t* w_tc, i
   if (int st = cuda_status(bs::launch_bitpack(a, ap, m, k, row_words(k), a_bits, s), fn)) return st;
   ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
   bs::ConvProblem p = make_conv(ap, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  p.a_enc = a_enc;
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, s), fn);
 }
 
-int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, const int8_t* w_tc, int w_bits,
-                                     int tc_format, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
+int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,
+                                     int w_enc, int tc_format, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
                                      int stride_h, int stride_w, int pad_h, int pad_w, uint8_t* act_dev,
                                      int32_t* out_dev, void* workspace, int64_t workspace_bytes, void* stream) {
   const char* fn = "bs_bitserial_conv2d_nhwc_tc_host";
@@ -437,7 +469,7 @@ int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, const 
   const size_t in_bytes = size_t(n) * h * w * c;
   const size_t out_bytes = size_t(n) * conv_out(h, kh, stride_h, pad_h) * conv_out(w, kw, stride_w, pad_w) * oc * 4;
   if (int st = cuda_status(cudaMemcpyAsync(act_dev, act_host, in_bytes, cudaMemcpyHostToDevice, s), fn)) return st;
-  if (int st = bs_bitserial_conv2d_nhwc_tc_i8(act_dev, a_bits, w_tc, w_bits, tc_format, out_dev, n, h, w, c, oc, kh, kw,
+  if (int st = bs_bitserial_conv2d_nhwc_tc_i8(act_dev, a_bits, a_enc, w_tc, w_bits, w_enc, tc_format, out_dev, n, h, w, c, oc, kh, kw,
                                               stride_h, stride_w, pad_h, pad_w, workspace, workspace_bytes, stream))
     return st;
   if (int st = cuda_status(cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, s), fn)) return st;

@@ -21,7 +21,9 @@ struct ConvProblem {
   int sh, sw, ph, pw;       // stride, padding
   int oh, ow;               // output extent
   int a_bits, w_bits;
-  int bipolar;              // weight encoding
+  int bipolar;              // weight encoding (0 unipolar, 1 bipolar, 2 signed)
+  int a_enc;                // activation encoding (0 unsigned, 1 bipolar, 2 signed; tensor-core FP4 path)
+  int c_tap;                // channels (elements) per tap: c for conv, k for dense
   int64_t act_plane;        // rows_a * kw_a
   int64_t M;                // n*oh*ow
   int64_t kp;               // taps * kw_a
@@ -54,8 +56,9 @@ int64_t tc_kpad(int64_t kp);
 int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt);
 bool tc_supported(int a_bits, int w_bits);
 // expanded ("prepared") weights: [w_bits][n][tc_kpad(kp)*(32 | 16)] bytes, offline like packing
-cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int bipolar, int64_t n, int64_t kp,
-                                     int8_t* wexp, int fmt, cudaStream_t stream);
+// w_enc: 0 unipolar, 1 bipolar, 2 signed; c_tap elements in each kw_tap-word tap (padding -> 0)
+cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp,
+                                     int c_tap, int kw_tap, int8_t* wexp, int fmt, cudaStream_t stream);
 cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream);
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream);
 

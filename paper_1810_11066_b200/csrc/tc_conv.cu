@@ -355,6 +355,28 @@ __device__ __forceinline__ void expand_to_tmem_f4(uint32_t taddr, uint4 v) {
   tmem_st16(taddr, o);
 }
 
+// Activation encodings on the FP4 path: mode 0 unsigned (nibble 0.5*b),
+// 1 bipolar (every digit +-0.5: bit set 0b0001, clear 0b1001; words of a padding piece,
+// `valid` bit clear, are 0 so padding contributes nothing), 2 negative plane (the top
+// plane of two's-complement data: 0b1001 = -0.5 for a set bit).
+__device__ __forceinline__ void expand_to_tmem_f4_enc(uint32_t taddr, uint4 v, int mode, uint32_t valid) {
+  uint32_t o[16], t[4];
+  const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int wi = 0; wi < 4; ++wi) {
+    expand_word_f4(w4[wi], t);
+    const bool ok = (valid >> (wi >> 1)) & 1u;  // words 0-1: piece 0, words 2-3: piece 1
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t x = t[q];
+      if (mode == 1) x = ok ? (0x11111111u | ((x ^ 0x11111111u) << 3)) : 0u;
+      else if (mode == 2) x = x * 9u;  // 0/1 nibbles -> 0/9: no carries
+      o[4 * wi + q] = x;
+    }
+  }
+  tmem_st16(taddr, o);
+}
+
 // The 2 K-steps (64 elements = 8 TMEM columns / 32 bytes of B each) of one plane pair in
 // one 128-element chunk, kind::mxf4 with per-plane scale-factor regions in TMEM.
 template <uint32_t IDESC>
@@ -395,23 +417,44 @@ __device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
 // 4 words; bytes past kp*32 are 0), each 32-byte group in the transposed K order of
 // expand_word.  Plane j byte = 2^j b (unipolar) or 2^j (2b - 1)
 // (bipolar); zero padding of the activations makes the value of pad bytes irrelevant.
+// Valid-element mask of packed weight word kk: a filter row is KH*KW taps of kw_tap
+// words each holding c_tap elements (bits past c_tap in a tap's last word are padding);
+// padding expands to 0 so it contributes nothing whatever the activation encoding.
+__device__ __forceinline__ uint32_t tap_word_mask(int64_t kk, int64_t kp, int c_tap, int kw_tap) {
+  if (kk >= kp) return 0u;
+  const int wt = int(kk % kw_tap);
+  const int lo = wt * 32;
+  if (lo + 32 <= c_tap) return 0xFFFFFFFFu;
+  if (lo >= c_tap) return 0u;
+  return (1u << (c_tap - lo)) - 1u;
+}
+
+// Weight-plane value of a set / clear bit for encoding w_enc (0 unipolar, 1 bipolar,
+// 2 signed two's complement: the top plane weighs -2^(W-1)).
+__device__ __forceinline__ int plane_sign(int j, int w_bits, int w_enc) {
+  return (w_enc == 2 && j == w_bits - 1) ? -1 : 1;
+}
+
 __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __restrict__ w_packed,
                                                              int8_t* __restrict__ wexp, int w_bits, int n,
-                                                             int64_t kp, int64_t kpad, int bipolar) {
+                                                             int64_t kp, int64_t kpad, int w_enc, int c_tap,
+                                                             int kw_tap) {
   const int64_t words = int64_t(w_bits) * n * kpad;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < words; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t kk = t % kpad, rest = t / kpad;
     const int64_t row = rest % n, j = rest / n;
+    const uint32_t valid = tap_word_mask(kk, kp, c_tap, kw_tap);
     const uint32_t w = kk < kp ? w_packed[(j * n + row) * kp + kk] : 0u;
-    const int32_t mag = 1 << j;
+    const int32_t mag = (1 << j) * plane_sign(int(j), w_bits, w_enc);
     uint32_t out[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {  // byte r of expanded word q = element 8r + q (see expand_word)
       uint32_t v = 0;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int b = (w >> (8 * r + q)) & 1;
-        const int32_t val = bipolar ? (b ? mag : -mag) : (b ? mag : 0);
+        const int e = 8 * r + q;
+        const int b = (w >> e) & 1;
+        const int32_t val = !((valid >> e) & 1) ? 0 : (w_enc == 1 ? (b ? mag : -mag) : (b ? mag : 0));
         v |= (uint32_t(val) & 0xFFu) << (8 * r);
       }
       out[q] = v;
@@ -427,20 +470,25 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
 // = 0b0001 * b (unipolar) or b ? 0b0001 : 0b1001 (bipolar, +-0.5); scale 2^(j+1) at run time.
 __global__ void __launch_bounds__(256) expand_weights_f4_kernel(const uint32_t* __restrict__ w_packed,
                                                                 uint8_t* __restrict__ wexp, int w_bits, int n,
-                                                                int64_t kp, int64_t kpad, int bipolar) {
+                                                                int64_t kp, int64_t kpad, int w_enc, int c_tap,
+                                                                int kw_tap) {
   const int64_t words = int64_t(w_bits) * n * kpad;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < words; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t kk = t % kpad, rest = t / kpad;
     const int64_t row = rest % n, j = rest / n;
+    const uint32_t valid = tap_word_mask(kk, kp, c_tap, kw_tap);
     const uint32_t w = kk < kp ? w_packed[(j * n + row) * kp + kk] : 0u;
+    const bool neg_plane = plane_sign(int(j), w_bits, w_enc) < 0;
     uint32_t out[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // nibble r of expanded word q = element 4r + q
       uint32_t v = 0;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const uint32_t b = (w >> (4 * r + q)) & 1u;
-        const uint32_t nib = bipolar ? (b ? 0x1u : 0x9u) : b;
+        const int e = 4 * r + q;
+        const uint32_t b = (w >> e) & 1u;
+        // +0.5 = 0b0001, -0.5 = 0b1001; bipolar: every digit +-0.5; signed top plane: -0.5
+        const uint32_t nib = !((valid >> e) & 1u) ? 0u : (w_enc == 1 ? (b ? 0x1u : 0x9u) : (b ? (neg_plane ? 0x9u : 0x1u) : 0u));
         v |= nib << (4 * r);
       }
       out[q] = v;
@@ -664,15 +712,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ok = rok && kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
       return rbase + (int64_t(iy) * p.w + ix) * kwa + cw;
     };
-    auto load = [&](int kc, uint4 (&v)[A_BITS]) {
+    auto load = [&](int kc, uint4 (&v)[A_BITS], uint32_t& vm) {
       if (DBG(3)) {  // timing experiment: no global loads
 #pragma unroll
         for (int i = 0; i < A_BITS; ++i) v[i] = make_uint4(kc, i, arow, 7);
+        vm = 3u;
         return;
       }
       const int kk = kc * kWordsPerStage;
       bool ok0;
       const uint32_t* s0 = piece(kk, ok0);
+      vm = ok0 ? 3u : 0u;  // validity of the two 2-word pieces (padding / K tail -> 0)
       if (!split) {
 #pragma unroll
         for (int i = 0; i < A_BITS; ++i)
@@ -680,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         bool ok1;
         const uint32_t* s1 = piece(kk + 2, ok1);
+        vm = (ok0 ? 1u : 0u) | (ok1 ? 2u : 0u);
 #pragma unroll
         for (int i = 0; i < A_BITS; ++i) {
           const uint2 lo = ok0 ? ldg_nc_v2(s0 + i * plane) : make_uint2(0u, 0u);
@@ -698,6 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int cur_tile = -1;
     uint4 nxt[A_BITS];
+    uint32_t nvm = 0;
     auto advance_load = [&]() {
       if (lt < my_tiles) {
         const int t = int(blockIdx.x) + lt * int(gridDim.x);
@@ -705,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           set_tile(t);
           cur_tile = t;
         }
-        load(kc, nxt);
+        load(kc, nxt, nvm);
         kc += kTeams;
         while (kc >= nchunks) {
           kc -= nchunks;
@@ -719,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4 v[A_BITS];
 #pragma unroll
       for (int i = 0; i < A_BITS; ++i) v[i] = nxt[i];
+      const uint32_t vm = nvm;
       advance_load();  // next step's words in flight during this step's expansion
       const int stage = g % S;
       PROF_BEGIN
@@ -738,8 +791,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (x == 0x9e3779b9u) asm volatile("trap;");
       } else {
         if constexpr (F4) {
+          if (p.a_enc == 0) {
 #pragma unroll
-          for (int i = 0; i < A_BITS; ++i) expand_to_tmem_f4(ta + uint32_t(i * C::kAColsPlane), v[i]);
+            for (int i = 0; i < A_BITS; ++i) expand_to_tmem_f4(ta + uint32_t(i * C::kAColsPlane), v[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < A_BITS; ++i)
+              expand_to_tmem_f4_enc(ta + uint32_t(i * C::kAColsPlane), v[i],
+                                    p.a_enc == 1 ? 1 : (i == A_BITS - 1 ? 2 : 0), vm);
+          }
         } else {
           expand_to_tmem<0>(ta, v[0]);
           if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
@@ -1100,18 +1160,19 @@ int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt) {
 
 bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 4; }
 
-cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int bipolar, int64_t n, int64_t kp,
-                                     int8_t* wexp, int fmt, cudaStream_t stream) {
+cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp,
+                                     int c_tap, int kw_tap, int8_t* wexp, int fmt, cudaStream_t stream) {
   const int64_t kpad = tc_kpad(kp);
   const int64_t words = int64_t(w_bits) * n * kpad;
   int64_t blocks = (words + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   if (tc_resolve_format(fmt) == kTcF4)
     tc::expand_weights_f4_kernel<<<unsigned(blocks), 256, 0, stream>>>(w_packed, reinterpret_cast<uint8_t*>(wexp),
-                                                                       w_bits, int(n), kp, kpad, bipolar);
+                                                                       w_bits, int(n), kp, kpad, w_enc, c_tap,
+                                                                       kw_tap);
   else
     tc::expand_weights_kernel<<<unsigned(blocks), 256, 0, stream>>>(w_packed, wexp, w_bits, int(n), kp, kpad,
-                                                                    bipolar);
+                                                                    w_enc, c_tap, kw_tap);
   note_launch();
   return cudaPeekAtLastError();
 }
@@ -1132,7 +1193,8 @@ cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, in
 
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
-  cudaError_t e = launch_tc_expand_weights(p.wt, p.w_bits, p.bipolar, p.oc, p.kp, wexp_ws, fmt, stream);
+  const int c_tap = p.c_tap, kw_tap = p.kw_a;
+  cudaError_t e = launch_tc_expand_weights(p.wt, p.w_bits, p.bipolar, p.oc, p.kp, c_tap, kw_tap, wexp_ws, fmt, stream);
   if (e != cudaSuccess) return e;
   return launch_tc_conv_prepared(p, wexp_ws, fmt, stream);
 }

@@ -112,12 +112,16 @@ def test_product_package_does_not_import_oracle():
 
 def test_tc_validation_before_launch(lib):
     # bad tensor-core format
-    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 2, FAKE, 1, 7, FAKE, 16, 16, 64, NULL) == 2
+    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 2, 0, FAKE, 1, 0, 7, FAKE, 16, 16, 64, NULL) == 2
     # FP4 format exactness bound: K (2^4-1)(2^2-1) = 45 K >= 2^22 for K = 100000 (I8 accepts it)
-    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 4, FAKE, 2, bs.TC_F4, FAKE, 16, 16, 100000, NULL) == 6
+    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 4, 0, FAKE, 2, 0, bs.TC_F4, FAKE, 16, 16, 100000, NULL) == 6
     assert b"2^22" in lib.bs_last_error()
     # unsupported precision for the tensor-core path (A in [1,4], W in [1,2])
-    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 5, FAKE, 1, bs.TC_I8, FAKE, 16, 16, 64, NULL) == 3
+    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 5, 0, FAKE, 1, 0, bs.TC_I8, FAKE, 16, 16, 64, NULL) == 3
+    # encodings: bad a_enc; bipolar / signed activations need the FP4 format
+    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 2, 3, FAKE, 1, 0, bs.TC_F4, FAKE, 16, 16, 64, NULL) == 2
+    assert lib.bs_bitserial_dense_tc_prepared(FAKE, 2, 1, FAKE, 1, 1, bs.TC_I8, FAKE, 16, 16, 64, NULL) == 3
+    assert lib.bs_dense_tc_prepare_weights(FAKE, 1, 3, 64, 64, bs.TC_F4, FAKE, 1 << 20, NULL) == 2
     # prepared-weight buffer too small
     assert lib.bs_dense_tc_prepare_weights(FAKE, 1, 1, 64, 64, bs.TC_F4, FAKE, 16, NULL) == 8
     # weight bytes per format: I8 32 B, F4 16 B per packed word (K = 64 -> 2 words, padded to 4)

@@ -445,3 +445,56 @@ def test_bitpack_capped_grid(max_ctas):
         x = inputs.codes((rows, k), bits, g)
         got = bs.bitpack(x.to(DEV), bits, max_ctas=max_ctas).cpu().numpy().view(np.uint32)
         np.testing.assert_array_equal(got, oracle.bitpack(x.numpy(), bits))
+
+
+# --------------------------------------- encodings on the tensor-core path (8f3)
+ENC_PAIRS = [(a, w) for a in (bs.A_UNSIGNED, bs.A_BIPOLAR, bs.A_SIGNED) for w in (bs.UNIPOLAR, bs.BIPOLAR, bs.SIGNED)]
+
+
+@pytest.mark.parametrize("a_enc,w_enc", ENC_PAIRS)
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (3, 2), (4, 3), (1, 4)])
+def test_conv_tc_encodings(a_enc, w_enc, a_bits, w_bits):
+    """FP4 tensor-core conv with every (activation, weight) encoding — bipolar x bipolar
+    is the XNOR form of PAPER.md:503, signed the sign-weighted Eq. 2 of PAPER.md:517 —
+    on cases with zero padding (pad positions contribute 0 in every encoding), stride 2,
+    channel tails inside the packed words (C = 33, 96) and ragged M / OC."""
+    for (n, h, w, c, oc, kh, kw, sh, sw, ph, pw) in ((2, 9, 11, 33, 20, 3, 3, 1, 1, 1, 1),
+                                                    (1, 12, 10, 96, 100, 3, 3, 2, 2, 1, 1),
+                                                    (3, 7, 7, 64, 64, 1, 1, 1, 1, 0, 0)):
+        g = inputs.gen(n * 1000 + c + 7 * a_enc + 3 * w_enc + 11 * a_bits + w_bits)
+        act = inputs.codes((n, h, w, c), a_bits, g)
+        wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+        ref = oracle.conv2d_nhwc_enc(act.numpy(), a_bits, a_enc, wt.numpy(), w_bits, w_enc, stride=(sh, sw),
+                                     pad=(ph, pw))
+        wp = gpu_pack(wt.reshape(oc * kh * kw, c), w_bits)
+        w_tc = bs.conv2d_tc_prepare_weights(wp, w_bits, w_enc, oc, kh, kw, c, tc_format=bs.TC_F4)
+        got = bs.bitserial_conv2d_nhwc_tc_i8(act.to(DEV), a_bits, w_tc, w_bits, oc, kh, kw, (sh, sw), (ph, pw),
+                                             tc_format=bs.TC_F4, a_enc=a_enc, w_enc=w_enc)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"case c={c} a_enc={a_enc} w_enc={w_enc}")
+
+
+@pytest.mark.parametrize("a_enc,w_enc", ENC_PAIRS)
+def test_dense_tc_encodings(a_enc, w_enc):
+    """Dense products with every encoding pair, K tails (k = 100, 1000) and a multi-tile
+    shape, both entry points (packed / in-call packing)."""
+    for (m, n, k, a_bits, w_bits) in ((130, 72, 100, 2, 1), (257, 132, 1000, 3, 2), (64, 256, 4096, 1, 1)):
+        a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=a_enc * 100 + w_enc * 10 + a_bits + k)
+        ref = oracle.dense_enc(a.numpy(), a_bits, a_enc, w.numpy(), w_bits, w_enc)
+        w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, w_enc, n, k, tc_format=bs.TC_F4)
+        got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=bs.TC_F4, a_enc=a_enc,
+                                       w_enc=w_enc)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+        got2 = bs.bitserial_dense_tc_prepared(gpu_pack(a, a_bits), a_bits, w_tc, w_bits, m, n, k,
+                                              tc_format=bs.TC_F4, a_enc=a_enc, w_enc=w_enc)
+        assert torch.equal(got, got2)
+
+
+@pytest.mark.parametrize("w_bits", [1, 2, 3])
+def test_i8_signed_weights(w_bits):
+    """The I8 format takes signed weights (top plane byte -2^(W-1)); activations unsigned."""
+    m, n, k, a_bits = 200, 96, 333, 2
+    a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=w_bits + 5)
+    ref = oracle.dense_enc(a.numpy(), a_bits, 0, w.numpy(), w_bits, 2)
+    w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, bs.SIGNED, n, k, tc_format=bs.TC_I8)
+    got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=bs.TC_I8, w_enc=bs.SIGNED)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
