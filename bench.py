@@ -207,7 +207,8 @@ class ConvWorkload:
             self.pack_events = [torch.cuda.Event() for _ in self.runs]
             self.pack_ctas = args.pack_ctas_per_sm * torch.cuda.get_device_properties(dev).multi_processor_count
             self.conv_streams = args.conv_streams
-            self.conv2_stream = torch.cuda.Stream(device=dev)
+            self.extra_conv_streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+            self.packs_first = args.packs_first
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
             "layout": "NHWC/OHWI",
@@ -248,7 +249,10 @@ class ConvWorkload:
         # the ten layers are independent problems (BASELINE configs[3]): convs alternate
         # between two streams so one layer's persistent CTAs start on the SMs the previous
         # layer's tail leaves idle (two conv CTAs never share an SM: smem + all of TMEM)
-        conv_streams = [main, self.conv2_stream] if self.conv_streams == 2 else [main]
+        conv_streams = [main] + self.extra_conv_streams[:self.conv_streams - 1]
+        if self.packs_first:  # experiment: every pack before any conv
+            for e in self.pack_events:
+                main.wait_event(e)
         for s in conv_streams[1:]:
             s.wait_stream(main)
         for i, (r, e) in enumerate(zip(self.runs, self.pack_events)):
@@ -764,7 +768,8 @@ def main():
     ap.add_argument("--unipolar", dest="bipolar", action="store_false")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="pack and conv of every layer in one stream")
-    ap.add_argument("--conv-streams", type=int, default=2, choices=[1, 2],
+    ap.add_argument("--packs-first", action="store_true", help="overlapped step variant: all packs before any conv")
+    ap.add_argument("--conv-streams", type=int, default=2, choices=[1, 2, 3],
                     help="overlapped step: convs of consecutive (independent) layers on 1 or 2 streams")
     ap.add_argument("--pack-ctas-per-sm", type=int, default=0,
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")

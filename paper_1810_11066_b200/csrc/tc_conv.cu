@@ -62,7 +62,7 @@ constexpr int kProducerThreads = kProducerWarps * 32;
 #define BS_TC_MAX_STAGES 8
 #endif
 #ifndef BS_TC_EPI_WARPS
-#define BS_TC_EPI_WARPS 4
+#define BS_TC_EPI_WARPS 8
 #endif
 constexpr int kEpiWarps = BS_TC_EPI_WARPS;              // 4 or 8 (warp % 4 = lane quarter)
 constexpr int kEpiWarp0 = kProducerWarps;
@@ -71,7 +71,10 @@ constexpr int kTmaWarp = kProducerWarps + kEpiWarps;
 constexpr int kMmaWarp = kProducerWarps + kEpiWarps + 1;
 constexpr int kThreads = (kProducerWarps + kEpiWarps + 2) * 32;
 constexpr int kEpiBufBytes = 32 * 128;  // one 32 x 32 int32 box
-constexpr int kEpiBufs = 2;             // staging buffers (TMA stores in flight) per epilogue warp
+#ifndef BS_TC_EPI_BUFS
+#define BS_TC_EPI_BUFS 2
+#endif
+constexpr int kEpiBufs = BS_TC_EPI_BUFS;  // staging buffers (TMA stores in flight) per epilogue warp
 constexpr int kEpiBytes = kEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMinSmem = 116 * 1024;
@@ -772,7 +775,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int i = 0; i < A_BITS; ++i) v[i] = nxt[i];
       const uint32_t vm = nvm;
+#ifndef BS_TC_LOAD_AFTER_ST
       advance_load();  // next step's words in flight during this step's expansion
+#endif
       const int stage = g % S;
       PROF_BEGIN
       for (;;) {  // stage of chunk g free (published in chunk order by the TMA warp)
@@ -807,6 +812,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
         }
       }
+#ifdef BS_TC_LOAD_AFTER_ST
+      advance_load();  // next step's gathers overlap the tensor-memory store latency
+#endif
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
