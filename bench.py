@@ -163,6 +163,11 @@ class ConvLayerRun:
             self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h,
                                           L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
 
+    def group_item(self):
+        L = self.L
+        return dict(act_packed=self.packed, w_tc=self.w_tc, out=self.out, n=self.n, h=L.h, w=L.w, c=L.ic, oc=L.oc,
+                    kh=L.k, kw=L.k, stride=L.s, pad=L.pad, w_enc=self.enc)
+
     def host_buffers(self):
         return (self.act_cpu.contiguous().pin_memory(), torch.empty(self.out.shape, dtype=torch.int32).pin_memory(),
                 torch.empty_like(self.act), torch.empty_like(self.out))
@@ -209,6 +214,12 @@ class ConvWorkload:
             self.conv_streams = args.conv_streams
             self.extra_conv_streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
             self.packs_first = args.packs_first
+            # grouped convs: the layers split into `conv_groups` contiguous groups, each one
+            # bs_bitserial_conv2d_nhwc_tc_group launch (0: one launch per layer)
+            ng = min(args.conv_groups, len(self.runs))
+            self.groups = ([list(range(len(self.runs)))[g * len(self.runs) // ng:(g + 1) * len(self.runs) // ng]
+                            for g in range(ng)] if ng > 0 else [])
+            self.group_items = [[self.runs[i].group_item() for i in grp] for grp in self.groups]
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
             "layout": "NHWC/OHWI",
@@ -223,6 +234,7 @@ class ConvWorkload:
                      "prepacked, untimed)"),
             "path": args.path,
             "tc_format": args.tc_format if args.path == "tc" else None,
+            "conv_groups": (args.conv_groups if self.overlap else 0),
         }
 
     def step(self):
@@ -255,7 +267,17 @@ class ConvWorkload:
                 main.wait_event(e)
         for s in conv_streams[1:]:
             s.wait_stream(main)
+        if self.groups:  # one grouped tensor-core launch per group of layers
+            for gi, (grp, items) in enumerate(zip(self.groups, self.group_items)):
+                cs = conv_streams[gi % len(conv_streams)]
+                for i in grp:
+                    cs.wait_event(self.pack_events[i])
+                with torch.cuda.stream(cs):
+                    self.runs[0].bs.bitserial_conv2d_nhwc_tc_group(items, self.args.a_bits, self.args.w_bits,
+                                                                   tc_format=tc_fmt(self.args))
         for i, (r, e) in enumerate(zip(self.runs, self.pack_events)):
+            if self.groups:
+                break
             cs = conv_streams[i % len(conv_streams)]
             cs.wait_event(e)
             with torch.cuda.stream(cs):
@@ -771,6 +793,8 @@ def main():
     ap.add_argument("--packs-first", action="store_true", help="overlapped step variant: all packs before any conv")
     ap.add_argument("--conv-streams", type=int, default=2, choices=[1, 2, 3],
                     help="overlapped step: convs of consecutive (independent) layers on 1 or 2 streams")
+    ap.add_argument("--conv-groups", type=int, default=0,
+                    help="tensor-core path: layers per step in this many grouped launches (0: one launch per layer)")
     ap.add_argument("--pack-ctas-per-sm", type=int, default=0,
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",

@@ -249,6 +249,26 @@ int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, int a_e
                                    int w_enc, int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k,
                                    void* stream);
 
+/* Several tensor-core convolutions of one precision in ONE persistent launch (per 16
+ * problems): the tiles of all problems form one sequence that the SM-resident CTAs walk,
+ * so the per-launch prologue, the pipeline fill and the last-wave tail are paid once
+ * for the group instead of once per layer (the paper times each layer of ResNet-18,
+ * PAPER.md:715-731, Table 1; a network runs them back to back).  Each descriptor is one
+ * bs_bitserial_conv2d_nhwc_tc_prepared call (same meaning, layout and ownership of
+ * act_packed / w_tc / out; a dense layer is n = 1, h = m, w = 1, c = k, kh = kw = 1).
+ * All members share a_bits, w_bits and tc_format; outputs must not overlap inputs or
+ * each other.  Every descriptor is validated before anything is launched (the first
+ * failing one is reported; nothing runs).  count = 0 is a no-op. */
+typedef struct bs_tc_conv_desc {
+  const uint32_t* act_packed; /* [a_bits][n*h*w][bs_packed_row_words(c)] (bs_bitpack) */
+  const int8_t* w_tc;         /* prepared weights (bs_conv2d_tc_prepare_weights) */
+  int32_t* out;               /* [n][oh][ow][oc] */
+  int a_enc, w_enc;           /* bs_a_encoding, bs_encoding */
+  int n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w;
+} bs_tc_conv_desc;
+int bs_bitserial_conv2d_nhwc_tc_group(const bs_tc_conv_desc* descs, int count, int a_bits, int w_bits,
+                                      int tc_format, void* stream);
+
 /* The timed step of the paper on the tensor-core path: activation
  * bit-packing (raw uint8 codes -> workspace of *_workspace_bytes() bytes) followed by
  * the tensor-core conv / dense on prepared weights.  Two launches. */

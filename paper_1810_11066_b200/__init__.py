@@ -26,7 +26,7 @@ __all__ = [
     "conv2d_tc_prepare_weights", "dense_tc_prepare_weights", "bitserial_conv2d_nhwc_tc_prepared",
     "bitserial_dense_tc_prepared", "bitserial_conv2d_nhwc_tc_i8", "bitserial_dense_tc_i8",
     "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
-    "TC_F4", "EXPORTED_SYMBOLS",
+    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "bs_conv2d_tc_prepare_weights", "bs_dense_tc_prepare_weights", "bs_bitserial_conv2d_nhwc_tc_prepared",
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
+    "bs_bitserial_conv2d_nhwc_tc_group",
 )
 
 
@@ -100,8 +101,11 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tc_i8": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, L, P], I),
         "bs_bitserial_dense_tc_i8": ([P, I, I, P, I, I, I, P, L, L, L, P, L, P], I),
         "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_group": ([P, I, I, I, I, P], I),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("BITSERIAL_LIB") and not hasattr(lib, name):
+            continue  # an older experimental build (A/B timing) may lack newer entry points
         f = getattr(lib, name)
         f.argtypes, f.restype = args, res
     _lib = lib
@@ -315,6 +319,39 @@ def bitserial_conv2d_nhwc_tc_prepared(act_packed, a_bits, w_tc, w_bits, n, h, w,
         int(w_enc), int(tc_format),
         _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _stream(stream)))
     return out
+
+
+class TcConvDesc(ctypes.Structure):
+    """bs_tc_conv_desc (include/bitserial.h): one member of a grouped tensor-core launch."""
+    _fields_ = [("act_packed", ctypes.c_void_p), ("w_tc", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("a_enc", ctypes.c_int), ("w_enc", ctypes.c_int)] + \
+        [(f, ctypes.c_int) for f in ("n", "h", "w", "c", "oc", "kh", "kw", "stride_h", "stride_w", "pad_h", "pad_w")]
+
+
+def bitserial_conv2d_nhwc_tc_group(convs, a_bits, w_bits, tc_format=TC_DEFAULT, stream=None):
+    """bs_bitserial_conv2d_nhwc_tc_group: several prepared-weight convolutions of one
+    precision in one persistent launch.  `convs` is a sequence of dicts with the keys of
+    bitserial_conv2d_nhwc_tc_prepared (act_packed, w_tc, n, h, w, c, oc, kh, kw and
+    optional stride, pad, out, a_enc, w_enc).  Returns the output tensors in order."""
+    descs = (TcConvDesc * max(len(convs), 1))()
+    outs = []
+    for i, cv in enumerate(convs):
+        n, h, w, c, oc, kh, kw = (cv[k] for k in ("n", "h", "w", "c", "oc", "kh", "kw"))
+        sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, cv.get("stride", 1), cv.get("pad", 0))
+        out = cv.get("out")
+        if out is None:
+            out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=cv["act_packed"].device)
+        d = descs[i]
+        d.act_packed = _dev(cv["act_packed"], "act_packed", torch.int32).value
+        d.w_tc = _dev(cv["w_tc"], "w_tc", torch.int8).value
+        d.out = _dev(out, "out", torch.int32).value
+        d.a_enc, d.w_enc = int(cv.get("a_enc", A_UNSIGNED)), int(cv.get("w_enc", UNIPOLAR))
+        d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw = n, h, w, c, oc, kh, kw
+        d.stride_h, d.stride_w, d.pad_h, d.pad_w = sh, sw, ph, pw
+        outs.append(out)
+    _check(_load().bs_bitserial_conv2d_nhwc_tc_group(ctypes.cast(descs, ctypes.c_void_p), len(convs), a_bits,
+                                                     w_bits, int(tc_format), _stream(stream)))
+    return outs
 
 
 def bitserial_dense_tc_prepared(a_packed, a_bits, w_tc, w_bits, m, n, k, out=None, tc_format=TC_DEFAULT,

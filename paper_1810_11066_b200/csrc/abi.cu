@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "../../include/bitserial.h"
 #include "kernels.h"
@@ -390,6 +391,34 @@ int bs_bitserial_conv2d_nhwc_tc_prepared(const uint32_t* act_packed, int a_bits,
   bs::ConvProblem p = make_conv(act_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
   p.a_enc = a_enc;
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tc_group(const bs_tc_conv_desc* descs, int count, int a_bits, int w_bits,
+                                      int tc_format, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tc_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  if (int st = check_format(tc_format, fn)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  std::vector<bs::ConvProblem> ps(static_cast<size_t>(count));
+  std::vector<const int8_t*> ws(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_tc_conv_desc& d = descs[q];
+    if (int st = check_tc_enc(d.a_enc, d.w_enc, tc_format, fn)) return st;
+    const ConvArgs g{d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw, d.stride_h, d.stride_w, d.pad_h, d.pad_w};
+    if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+    if (int st = check_tc_bound(int64_t(d.kh) * d.kw * d.c, a_bits, w_bits, tc_format, fn, d.a_enc, d.w_enc))
+      return st;
+    if (!d.act_packed || !d.w_tc || !d.out) return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    if (!aligned16(d.act_packed) || !aligned16(d.w_tc) || !aligned16(d.out))
+      return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
+    ps[q] = make_conv(d.act_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, d.out, g);
+    ps[q].a_enc = d.a_enc;
+    ws[q] = d.w_tc;
+  }
+  return cuda_status(bs::launch_tc_conv_group(ps.data(), ws.data(), count, tc_format,
+                                              static_cast<cudaStream_t>(stream)), fn);
 }
 
 int bs_bitserial_conv2d_nhwc_tc_i8(const uint8_t* act, int a_bits, int a_enc, const int8_t* w_tc, int w_bits,

@@ -61,6 +61,9 @@ cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w
                                      int c_tap, int kw_tap, int8_t* wexp, int fmt, cudaStream_t stream);
 cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream);
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream);
+// Several problems of one (a_bits, w_bits) in one persistent launch per 16 problems.
+cudaError_t launch_tc_conv_group(const ConvProblem* ps, const int8_t* const* wexps, int count, int fmt,
+                                 cudaStream_t stream);
 
 // Matrix-vector kernel for m <= 8 dense products.
 //   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)

@@ -40,8 +40,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -77,8 +79,9 @@ constexpr int kEpiBufBytes = 32 * 128;  // one 32 x 32 int32 box
 constexpr int kEpiBufs = BS_TC_EPI_BUFS;  // staging buffers (TMA stores in flight) per epilogue warp
 constexpr int kEpiBytes = kEpiWarps * kEpiBufs * kEpiBufBytes;
 constexpr int kSmemLimit = 227 * 1024;
-constexpr int kMinSmem = 116 * 1024;
-constexpr int kMaxTaps = 64;  // filter taps held in the shared-memory tap table  // > half the SM: guarantees one CTA per SM (TMEM)
+constexpr int kMinSmem = 116 * 1024;  // > half the SM: guarantees one CTA per SM (TMEM)
+constexpr int kMaxTaps = 64;          // filter taps held in the shared-memory tap table
+constexpr int kGroupMax = 16;         // problems in one grouped launch
 
 // BS_TC_PROFILE builds (tools only) count cycles spent in each role's waits and print
 // them per CTA 0 at exit; the product build compiles these to nothing.
@@ -184,9 +187,8 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 
 // Instruction descriptor, kind::i8: D = S32, A = u8 (activation planes, 0 or 2^i),
 // B = s8 (weight planes, +/-2^j or 0/2^j), both K-major, M = 128, N = BN.
-template <int BN>
-constexpr uint32_t idesc_i8() {
-  return (2u << 4) | (0u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+inline uint32_t idesc_i8(int n) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -218,8 +220,7 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint
 // operand warp-uniform (uniform registers, no per-MMA R2UR / waterfall) — the MMA warp
 // shares its SM sub-partition with ALU-bound producer warps, so its instruction count
 // per MMA sets the tensor-core feed rate.
-template <uint32_t IDESC>
-__device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
       "elect.sync x|e, 0xffffffff;\n"
@@ -232,7 +233,7 @@ __device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint
       "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
       "}" ::"r"(d),
-      "r"(a), "l"(b), "r"(accumulate), "n"(IDESC));
+      "r"(a), "l"(b), "r"(accumulate), "r"(idesc));
 }
 
 // tcgen05.commit from the elected lane (the lane that issued the MMAs).
@@ -382,8 +383,7 @@ __device__ __forceinline__ void expand_to_tmem_f4_enc(uint32_t taddr, uint4 v, i
 
 // The 2 K-steps (64 elements = 8 TMEM columns / 32 bytes of B each) of one plane pair in
 // one 128-element chunk, kind::mxf4 with per-plane scale-factor regions in TMEM.
-template <uint32_t IDESC>
-__device__ __forceinline__ void mma2_f4(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb,
+__device__ __forceinline__ void mma2_f4(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
@@ -393,14 +393,13 @@ __device__ __forceinline__ void mma2_f4(uint32_t d, uint32_t a, uint64_t b, uint
       "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
       "}" ::"r"(d),
-      "r"(a), "l"(b), "r"(accumulate), "n"(IDESC), "r"(sfa), "r"(sfb));
+      "r"(a), "l"(b), "r"(accumulate), "r"(idesc), "r"(sfa), "r"(sfb));
 }
 
 // Block-scaled instruction descriptor, kind::mxf4: A, B = E2M1, scales UE8M0, K = 64,
 // K-major, M = 128, N = BN (D is always F32).
-template <int BN>
-constexpr uint32_t idesc_mxf4() {
-  return (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
+inline uint32_t idesc_mxf4(int n) {
+  return (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
 }
 
 // 64B-swizzled K-major UMMA descriptor (FP4 B tiles: 64-byte rows of 128 elements):
@@ -505,14 +504,14 @@ __global__ void __launch_bounds__(256) expand_weights_f4_kernel(const uint32_t* 
 // F4 = false: kind::i8 (bytes, 128-byte B rows, SWIZZLE_128B); F4 = true: kind::mxf4
 // (packed E2M1, 64-byte B rows, SWIZZLE_64B, scale-factor regions in TMEM).  A chunk is
 // 128 K elements (4 packed words per plane per row) in both formats.
-template <int A_BITS, int W_BITS, int BN, bool F4>
+template <int A_BITS, int W_BITS, int BN, bool F4, int NP = 1>
 struct Cfg {
   static constexpr int kBRow = F4 ? 64 : BKB;             // B bytes per row per plane per stage
   static constexpr int kAColsPlane = F4 ? 16 : BKB / 4;    // TMEM columns per plane per stage
   static constexpr int kACols = A_BITS * kAColsPlane;     // TMEM columns of one stage's A planes
   static constexpr int kBBytes = W_BITS * BN * kBRow;     // shared memory per stage (B only)
   static constexpr int kSFCols = F4 ? 16 + 8 * W_BITS : 0;  // SFA: 4 planes x 4 cols; SFB: W planes x 8
-  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + 512 /*tap table*/ + kEpiBytes;
+  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + NP * 512 /*tap tables*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
@@ -548,20 +547,36 @@ inline FastDiv make_fastdiv(uint32_t d) {
   return f;
 }
 
-struct TcArgs {
+// One problem of a launch (a single conv / dense, or one member of a group).
+struct TcProb {
   ConvProblem p;
-  int ntiles, ntn;  // tiles, N-tiles per M block
+  int ntn;          // N-tiles per M block
   int nchunks;      // K chunks (of 4 words) per tile
+  int tile0;        // first tile of this problem in the launch's tile sequence
   int epi;          // EpiMode: direct 16-byte stores (OC % 4 == 0), TMA stores, or scalar
-  int b_resident;   // ntn == 1 and the whole expanded B fits: loaded once, kept in smem
-  int b_bytes;      // bytes of the B region (resident: nchunks stages, else kStages)
+  uint32_t idesc;   // MMA instruction descriptor (N = 64 for OC <= 64 inside a BN = 128 group)
   FastDiv div_hw, div_ow, div_kwid, div_ntn, div_kwa;  // n / (oh*ow), / ow, / kw, / ntn, / Cw
   int kwa_shift;    // log2(Cw) when Cw is a power of two, else -1
   int taps;         // kh * kw (the tap table is used when taps <= kMaxTaps)
-  int debug;        // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
-                    // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
-                    // 4 MMA warp ignores full_a
-                    // (timing experiments; results are wrong)
+};
+
+// Launch arguments: NP problems whose tiles are concatenated (problem q owns tiles
+// [tile0_q, tile0_{q+1})); CTAs walk the whole sequence with a grid stride, so every
+// role sees its problem index only grow.  NP = 1 is the single-problem launch.
+template <int NP>
+struct TcArgs {
+  int nprob, ntiles;  // problems, tiles of all problems
+  int b_resident;     // single problem, ntn == 1 and the whole expanded B fits: loaded once
+  int b_bytes;        // bytes of the B region (resident: nchunks stages, else kStages)
+  int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
+                      // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
+                      // 4 MMA warp ignores full_a, 5 producers idle (timing experiments; results are wrong)
+  TcProb prob[NP];
+};
+template <int NP>
+struct TcMaps {
+  CUtensorMap w[NP];    // prepared weights [W][oc][kpad bytes]
+  CUtensorMap out[NP];  // int32 output [M][oc] (TMA-store epilogue)
 };
 #if defined(BS_TC_PROFILE) || defined(BS_TC_KNOBS)
 #define DBG(bit) (args.debug & (1 << (bit)))
@@ -569,18 +584,17 @@ struct TcArgs {
 #define DBG(bit) 0
 #endif
 
-template <int A_BITS, int W_BITS, int BN, bool F4>
+template <int A_BITS, int W_BITS, int BN, bool F4, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_conv_kernel(const TcArgs args, const __grid_constant__ CUtensorMap tmap_w,
-                   const __grid_constant__ CUtensorMap tmap_out) {
-  using C = Cfg<A_BITS, W_BITS, BN, F4>;
+    tc_conv_kernel(const __grid_constant__ TcArgs<NP> args, const __grid_constant__ TcMaps<NP> maps) {
+  using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
   constexpr int S = C::kStages;
   static_assert(S >= 2, "tensor-core tile does not fit two stages of shared memory");
   static_assert(C::kBytes <= kSmemLimit, "shared memory");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* s_stage = smem;                            // B: S ring stages, or nchunks resident
-  uint8_t* s_epi = smem + args.b_bytes;               // epilogue staging: warps x 2 x 4 KB (1024-aligned)
+  uint8_t* s_epi = smem + args.b_bytes;               // epilogue staging: warps x bufs x 4 KB (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_epi + kEpiBytes);
   uint64_t* full_a = bars;
   uint64_t* full_b = bars + S;
@@ -588,25 +602,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 3 * S;
   uint64_t* acc_empty = bars + 3 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
-  int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [kMaxTaps] {offset, ky<<16|kx}
+  int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [NP][kMaxTaps] {offset, ky<<16|kx}
   int* s_freed = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 240);   // chunks whose stage is free
   static_assert(8 * (3 * S + 4) + 4 <= 240, "barrier region");
 
-  const ConvProblem& p = args.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (lane == 0 && (warp == 0 || warp == kMmaWarp)) STAMP("start")
   PROF_DECL
 #ifdef BS_TC_PROFILE
   const long long _t_start = clock64();
 #endif
-  const int ntiles = args.ntiles, ntn = args.ntn, nchunks = args.nchunks;
+  const int ntiles = args.ntiles;
+  // problem of tile t: pi only grows along a CTA's tile sequence
+  auto track = [&](int t, int& pi) {
+    if constexpr (NP > 1)
+      while (pi + 1 < args.nprob && t >= args.prob[pi + 1].tile0) ++pi;
+  };
 
-  // filter-tap table (implicit im2col): word offset of tap (ky, kx) from the row's
+  // filter-tap tables (implicit im2col): word offset of tap (ky, kx) from the row's
   // receptive-field origin, and (ky, kx) for the bounds test
-  const bool tap_table = args.taps <= kMaxTaps;
-  if (tap_table && tid < args.taps) {
-    const int ky = tid / args.p.kwid, kx = tid - ky * args.p.kwid;
-    s_tap[tid] = make_int2((ky * args.p.w + kx) * args.p.kw_a, (ky << 16) | kx);
+  for (int q = 0; q < args.nprob; ++q) {
+    const TcProb& P = args.prob[q];
+    if (P.taps <= kMaxTaps && tid < P.taps) {
+      const int ky = tid / P.p.kwid, kx = tid - ky * P.p.kwid;
+      s_tap[q * kMaxTaps + tid] = make_int2((ky * P.p.w + kx) * P.p.kw_a, (ky << 16) | kx);
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -626,9 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "r"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (warp == kTmaWarp && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_out)) : "memory");
+  if (warp == kTmaWarp && lane < args.nprob) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w[lane])) : "memory");
+    if (args.prob[lane].epi == kEpiTma)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.out[lane])) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -673,47 +694,72 @@ __global__ void __launch_bounds__(kThreads, 1)
     // precomputed fast divisions (a team changes tile almost every step when K is short).
     constexpr int kTeams = C::kTeamsUsed;
     const int team = warp >> 2, arow = tid & (BM - 1);
-    const int kp = int(p.kp), kwa = p.kw_a;
-    const bool split = (kwa & 3) != 0;  // a 4-word group spans two taps (Cw = 2 mod 4)
-    const uint32_t* __restrict__ act = p.act;
-    const int64_t plane = p.act_plane;
+    int pi = 0;  // problem of the chunk being loaded
+#define LP args.prob[pi].p
+    // the loaded problem's per-chunk fields in registers, refreshed when the problem
+    // changes (grouped launches: a parameter indexed by a run-time problem number costs an
+    // LDC per use; with NP = 1 these fold back into constant-bank operands)
+    struct Hot {
+      int64_t plane;
+      int kp, kwa, kwa_shift, h, w, a_enc, nchunks, next_tile0;
+      bool tap;
+    };
+    auto hot_of = [&](int q) {
+      const TcProb& P = args.prob[q];
+      Hot r;
+      r.plane = P.p.act_plane;
+      r.kp = int(P.p.kp);
+      r.kwa = P.p.kw_a;
+      r.kwa_shift = P.kwa_shift;
+      r.h = P.p.h;
+      r.w = P.p.w;
+      r.a_enc = P.p.a_enc;
+      r.nchunks = P.nchunks;
+      r.next_tile0 = q + 1 < args.nprob ? args.prob[q + 1].tile0 : 0x7FFFFFFF;
+      r.tap = P.taps <= kMaxTaps;
+      return r;
+    };
+    Hot H = hot_of(0);
     // geometry of this thread's row in tile `t`
     bool rok = false;
     int iy0 = 0, ix0 = 0;
-    const uint32_t* rbase = act;  // image base (pixel 0 of the row's image), word units
-    const uint32_t* rorg = act;   // receptive-field origin (iy0, ix0) of the row (may lie in the padding)
+    const uint32_t* rbase = LP.act;  // image base (pixel 0 of the row's image), word units
+    const uint32_t* rorg = LP.act;   // receptive-field origin (iy0, ix0) of the row (may lie in the padding)
     auto set_tile = [&](int t) {
-      const uint32_t mblk = args.div_ntn.div(uint32_t(t));
+      const TcProb& P = args.prob[pi];
+      const uint32_t mblk = P.div_ntn.div(uint32_t(t - P.tile0));
       const int64_t m = int64_t(mblk) * BM + arow;
-      rok = m < p.M;
+      rok = m < P.p.M;
       const uint32_t mm = rok ? uint32_t(m) : 0u;
-      const uint32_t b = args.div_hw.div(mm), rem = mm - b * args.div_hw.d;
-      const uint32_t oy = args.div_ow.div(rem), ox = rem - oy * args.div_ow.d;
-      iy0 = int(oy) * p.sh - p.ph;
-      ix0 = int(ox) * p.sw - p.pw;
-      rbase = act + int64_t(b) * p.h * p.w * kwa;
-      rorg = rbase + (int64_t(iy0) * p.w + ix0) * kwa;
+      const uint32_t b = P.div_hw.div(mm), rem = mm - b * P.div_hw.d;
+      const uint32_t oy = P.div_ow.div(rem), ox = rem - oy * P.div_ow.d;
+      iy0 = int(oy) * P.p.sh - P.p.ph;
+      ix0 = int(ox) * P.p.sw - P.p.pw;
+      rbase = P.p.act + int64_t(b) * P.p.h * P.p.w * P.p.kw_a;
+      rorg = rbase + (int64_t(iy0) * P.p.w + ix0) * P.p.kw_a;
     };
     // source of the 2- or 4-word piece starting at filter word kk (kk even)
     auto piece = [&](int kk, bool& ok) -> const uint32_t* {
+      const int kwa = H.kwa;
       int tap, cw;
-      if (args.kwa_shift >= 0) {
-        tap = kk >> args.kwa_shift;
+      if (H.kwa_shift >= 0) {
+        tap = kk >> H.kwa_shift;
         cw = kk & (kwa - 1);
       } else {
-        tap = int(args.div_kwa.div(uint32_t(kk)));
+        tap = int(args.prob[pi].div_kwa.div(uint32_t(kk)));
         cw = kk - tap * kwa;
       }
-      if (tap_table) {
-        const int2 e = s_tap[tap < kMaxTaps ? tap : 0];
+      if (H.tap) {
+        const int2 e = s_tap[pi * kMaxTaps + (tap < kMaxTaps ? tap : 0)];
         const int iy = iy0 + (e.y >> 16), ix = ix0 + (e.y & 0xFFFF);
-        ok = rok && kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
+        ok = rok && kk < H.kp && unsigned(iy) < unsigned(H.h) && unsigned(ix) < unsigned(H.w);
         return rorg + e.x + cw;
       }
-      const int ky = int(args.div_kwid.div(uint32_t(tap))), kx = tap - ky * p.kwid;
+      const TcProb& P = args.prob[pi];
+      const int ky = int(P.div_kwid.div(uint32_t(tap))), kx = tap - ky * P.p.kwid;
       const int iy = iy0 + ky, ix = ix0 + kx;
-      ok = rok && kk < kp && unsigned(iy) < unsigned(p.h) && unsigned(ix) < unsigned(p.w);
-      return rbase + (int64_t(iy) * p.w + ix) * kwa + cw;
+      ok = rok && kk < H.kp && unsigned(iy) < unsigned(H.h) && unsigned(ix) < unsigned(H.w);
+      return rbase + (int64_t(iy) * H.w + ix) * kwa + cw;
     };
     auto load = [&](int kc, uint4 (&v)[A_BITS], uint32_t& vm) {
       if (DBG(3)) {  // timing experiment: no global loads
@@ -722,15 +768,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         vm = 3u;
         return;
       }
+      const int64_t plane = H.plane;
       const int kk = kc * kWordsPerStage;
       bool ok0;
       const uint32_t* s0 = piece(kk, ok0);
       vm = ok0 ? 3u : 0u;  // validity of the two 2-word pieces (padding / K tail -> 0)
-      if (!split) {
+      if ((H.kwa & 3) == 0) {
 #pragma unroll
         for (int i = 0; i < A_BITS; ++i)
           v[i] = ok0 ? ldg_nc_v4(s0 + i * plane) : make_uint4(0u, 0u, 0u, 0u);
-      } else {
+      } else {  // a 4-word group spans two taps (Cw = 2 mod 4)
         bool ok1;
         const uint32_t* s1 = piece(kk + 2, ok1);
         vm = (ok0 ? 1u : 0u) | (ok1 ? 2u : 0u);
@@ -742,42 +789,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
-    const int my_tiles = ntiles > int(blockIdx.x) ? (ntiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
-    const int total = my_tiles * nchunks;
-    // iterator of the next chunk to load: (local tile lt, kc)
-    int lt = 0, kc = team;
-    while (kc >= nchunks && lt < my_tiles) {
-      kc -= nchunks;
-      ++lt;
-    }
-    int cur_tile = -1;
-    uint4 nxt[A_BITS];
-    uint32_t nvm = 0;
-    auto advance_load = [&]() {
-      if (lt < my_tiles) {
-        const int t = int(blockIdx.x) + lt * int(gridDim.x);
-        if (t != cur_tile) {
-          set_tile(t);
-          cur_tile = t;
+    // iterator of the next chunk to load: tile t (of problem pi), chunk kc
+    int t = int(blockIdx.x), kc = team, cur_tile = -1;
+    auto carry = [&]() {  // move kc past the ends of tiles
+      for (;;) {
+        if (t >= ntiles) return;
+        if constexpr (NP > 1) {
+          while (t >= H.next_tile0) H = hot_of(++pi);
         }
-        load(kc, nxt, nvm);
-        kc += kTeams;
-        while (kc >= nchunks) {
-          kc -= nchunks;
-          ++lt;
-        }
+        if (kc < H.nchunks) return;
+        kc -= H.nchunks;
+        t += int(gridDim.x);
       }
     };
-    advance_load();
+    uint4 nxt[A_BITS];
+    uint32_t nvm = 0;
+    int nenc = 0;
+    auto advance_load = [&]() -> bool {
+      if (t >= ntiles) return false;
+      if (t != cur_tile) {
+        set_tile(t);
+        cur_tile = t;
+      }
+      load(kc, nxt, nvm);
+      nenc = H.a_enc;
+      kc += kTeams;
+      carry();
+      return true;
+    };
+#undef LP
+    carry();
+    bool have = advance_load();
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
-    for (int g = team; g < total; g += kTeams) {
+    for (int g = team; have; g += kTeams) {
       uint4 v[A_BITS];
 #pragma unroll
       for (int i = 0; i < A_BITS; ++i) v[i] = nxt[i];
       const uint32_t vm = nvm;
-#ifndef BS_TC_LOAD_AFTER_ST
-      advance_load();  // next step's words in flight during this step's expansion
-#endif
+      const int enc = nenc;
+      have = advance_load();  // next step's words in flight during this step's expansion
       const int stage = g % S;
       PROF_BEGIN
       for (;;) {  // stage of chunk g free (published in chunk order by the TMA warp)
@@ -796,14 +846,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (x == 0x9e3779b9u) asm volatile("trap;");
       } else {
         if constexpr (F4) {
-          if (p.a_enc == 0) {
+          if (enc == 0) {
 #pragma unroll
             for (int i = 0; i < A_BITS; ++i) expand_to_tmem_f4(ta + uint32_t(i * C::kAColsPlane), v[i]);
           } else {
 #pragma unroll
             for (int i = 0; i < A_BITS; ++i)
               expand_to_tmem_f4_enc(ta + uint32_t(i * C::kAColsPlane), v[i],
-                                    p.a_enc == 1 ? 1 : (i == A_BITS - 1 ? 2 : 0), vm);
+                                    enc == 1 ? 1 : (i == A_BITS - 1 ? 2 : 0), vm);
           }
         } else {
           expand_to_tmem<0>(ta, v[0]);
@@ -812,9 +862,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
         }
       }
-#ifdef BS_TC_LOAD_AFTER_ST
-      advance_load();  // next step's gathers overlap the tensor-memory store latency
-#endif
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -826,20 +873,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= weight tiles by TMA, and the "chunks freed" counter: waits on each
     // stage's empty barrier in chunk order, then publishes that chunk g may be written
     if (lane == 0) {
-      const bool resident = args.b_resident;
+      const bool resident = args.b_resident;  // single-problem launches only
       if (resident) {  // whole B once (one N block): every K chunk, W planes
         const uint32_t fb = smem_u32(full_b);
+        const int nchunks = args.prob[0].nchunks;
         mbar_expect_tx(fb, uint32_t(C::kBBytes) * uint32_t(nchunks));
         for (int kc = 0; kc < nchunks; ++kc) {
           const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
 #pragma unroll
-          for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc, fb);
+          for (int j = 0; j < W_BITS; ++j)
+            tma_load_2d(sB + j * BN * C::kBRow, &maps.w[0], kc * C::kBRow, j * args.prob[0].p.oc, fb);
         }
       }
-      int stage = 0, g = 0;
+      int stage = 0, g = 0, pi = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int n0 = (tile % ntn) * BN;
+        track(tile, pi);
+        const TcProb& P = args.prob[pi];
+        const int n0 = ((tile - P.tile0) % P.ntn) * BN, nchunks = P.nchunks, oc = P.p.oc;
+        const CUtensorMap* tw = &maps.w[pi];
         for (int kc = 0; kc < nchunks; ++kc, ++g) {
           PROF_BEGIN
           mbar_wait(smem_u32(empty + stage), phase ^ 1u);
@@ -850,8 +902,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(fb, uint32_t(C::kBBytes));
             const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
 #pragma unroll
-            for (int j = 0; j < W_BITS; ++j)
-              tma_load_2d(sB + j * BN * C::kBRow, &tmap_w, kc * C::kBRow, j * p.oc + n0, fb);
+            for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * C::kBRow, tw, kc * C::kBRow, j * oc + n0, fb);
           }
           if (++stage == S) {
             stage = 0;
@@ -863,14 +914,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer: the whole warp walks the loop (uniform values); one
     // elected lane issues.  TMEM base is column 0 (all 512 columns are this CTA's).
-    constexpr uint32_t kIdesc = F4 ? idesc_mxf4<BN>() : idesc_i8<BN>();
-    int stage = 0, acc = 0;
+    int stage = 0, acc = 0, pi = 0;
     uint32_t phase = 0, acc_phase = 0;
     const bool resident = args.b_resident;
     const uint64_t bdesc0 = F4 ? smem_desc_sw64(smem_u32(s_stage)) : smem_desc_sw128(smem_u32(s_stage));
     if (resident) mbar_wait(smem_u32(full_b), 0);
     if (lane == 0) STAMP("b_resident_ready")
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      track(tile, pi);
+      const uint32_t idesc = args.prob[pi].idesc;
+      const int nchunks = args.prob[pi].nchunks;
       PROF_BEGIN
       mbar_wait(smem_u32(acc_empty + acc), acc_phase ^ 1u);
       PROF_END(0)
@@ -891,11 +944,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < W_BITS; ++j) {
             if constexpr (F4)
-              mma2_f4<kIdesc>(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
-                              uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), (kc | i | j) != 0);
+              mma2_f4(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
+                      uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), idesc, (kc | i | j) != 0);
             else
-              mma4_ts<kIdesc>(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4),
-                              (kc | i | j) != 0);
+              mma4_ts(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4), idesc,
+                      (kc | i | j) != 0);
           }
         mma_commit_elect(smem_u32(empty + stage));
         if (++stage == S) {
@@ -916,12 +969,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - kEpiWarp0, cb0 = ew >> 2;  // with 8 warps, two per lane quarter split the columns
     constexpr int kCbStep = kEpiWarps / 4;
     uint8_t* ebuf = s_epi + ew * (kEpiBufs * kEpiBufBytes);
-    int acc = 0, buf = 0;
+    int acc = 0, buf = 0, pi = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int64_t m0 = int64_t(tile / ntn) * BM;
-      const int n0 = (tile % ntn) * BN;
-      const int ncb = min(BN, p.oc - n0 + 31) / 32;  // 32-column blocks holding valid columns
+      track(tile, pi);
+      const TcProb& P = args.prob[pi];
+      const int tl = tile - P.tile0;
+      const int64_t m0 = int64_t(tl / P.ntn) * BM;
+      const int n0 = (tl % P.ntn) * BN;
+      const int oc = P.p.oc, epi = P.epi;
+      const int64_t M = P.p.M;
+      int32_t* const out = P.p.out;
+      const int ncb = min(BN, oc - n0 + 31) / 32;  // 32-column blocks holding valid columns
       PROF_BEGIN
       mbar_wait(smem_u32(acc_full + acc), acc_phase);
       PROF_END(0)
@@ -954,20 +1013,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t row = m0 + q * 32 + lane;
         if (DBG(0)) {
           if (r[0] == 0x9e3779b9u) asm volatile("trap;");
-        } else if (args.epi == kEpiDirect) {  // this lane's row segment: 128 contiguous bytes, 8 x 16-byte stores
-          if (row < p.M && n0 + cb * 32 + 32 <= p.oc) {
-            uint4* dst = reinterpret_cast<uint4*>(p.out + row * p.oc + n0 + cb * 32);
+        } else if (epi == kEpiDirect) {  // this lane's row segment: 128 contiguous bytes, 8 x 16-byte stores
+          if (row < M && n0 + cb * 32 + 32 <= oc) {
+            uint4* dst = reinterpret_cast<uint4*>(out + row * oc + n0 + cb * 32);
 #pragma unroll
             for (int c = 0; c < 8; ++c) dst[c] = make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
-          } else if (row < p.M) {
-            int32_t* dst = p.out + row * p.oc;
+          } else if (row < M) {
+            int32_t* dst = out + row * oc;
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
               const int col = n0 + cb * 32 + c;
-              if (col < p.oc) dst[col] = int32_t(r[c]);
+              if (col < oc) dst[col] = int32_t(r[c]);
             }
           }
-        } else if (args.epi == kEpiTma) {
+        } else if (epi == kEpiTma) {
           PROF_BEGIN
           if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // the store that last used `buf` has read it
           __syncwarp();
@@ -982,18 +1041,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmap_out, n0 + cb * 32, int(m0) + q * 32, smem_u32(ebuf + buf * kEpiBufBytes));
+            tma_store_2d(&maps.out[pi], n0 + cb * 32, int(m0) + q * 32, smem_u32(ebuf + buf * kEpiBufBytes));
             bulk_commit();
           }
           PROF_END(3)
           buf = buf + 1 == kEpiBufs ? 0 : buf + 1;
         } else {  // OC % 4 != 0: plain bounded stores
-          if (row < p.M) {
-            int32_t* dst = p.out + row * p.oc;
+          if (row < M) {
+            int32_t* dst = out + row * oc;
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
               const int col = n0 + cb * 32 + c;
-              if (col < p.oc) dst[col] = int32_t(r[c]);
+              if (col < oc) dst[col] = int32_t(r[c]);
             }
           }
         }
@@ -1065,71 +1124,90 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int A_BITS, int W_BITS, int BN, bool F4>
-cudaError_t launch_bn(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
-  using C = Cfg<A_BITS, W_BITS, BN, F4>;
-  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4>;
+// Fill one problem's launch record and tensor maps for tile width BN (the MMA uses N = 64
+// when the problem's filters fit it).  Returns false when a tensor map cannot be encoded.
+bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p, const int8_t* wexp, int tile0,
+               int bn, bool f4, int64_t& tiles) {
+  P.p = p;
+  P.ntn = (p.oc + bn - 1) / bn;
+  tiles = (p.M + BM - 1) / BM * P.ntn;
+  const int64_t kpad = tc_kpad(p.kp);
+  P.nchunks = int(kpad / kWordsPerStage);
+  P.tile0 = tile0;
+  // TMA-store epilogue by default (direct 16-byte stores of one row segment per lane
+  // measured 1.4-1.8x slower on the output-bound layers); BS_TC_EPI=direct selects them.
+  const char* epi_env = getenv("BS_TC_EPI");
+  const bool want_direct = epi_env && epi_env[0] == 'd';
+  P.epi = (p.oc % 4) != 0 ? kEpiScalar : (want_direct ? kEpiDirect : kEpiTma);
+  const int mma_n = p.oc <= 64 ? 64 : bn;
+  P.idesc = f4 ? idesc_mxf4(mma_n) : idesc_i8(mma_n);
+  P.div_hw = make_fastdiv(uint32_t(p.oh) * uint32_t(p.ow));
+  P.div_ow = make_fastdiv(uint32_t(p.ow));
+  P.div_kwid = make_fastdiv(uint32_t(p.kwid));
+  P.div_ntn = make_fastdiv(uint32_t(P.ntn));
+  P.div_kwa = make_fastdiv(uint32_t(p.kw_a));
+  P.taps = p.kh * p.kwid;
+  // the table's int32 word offsets: (ky*W + kx)*Cw must fit
+  if ((int64_t(p.kh) * p.w + p.kwid) * p.kw_a >= (int64_t(1) << 31)) P.taps = kMaxTaps + 1;
+  P.kwa_shift = -1;
+  for (int sh = 0; sh < 31; ++sh)
+    if ((1 << sh) == p.kw_a) P.kwa_shift = sh;
+  const int brow = f4 ? 64 : BKB;
+  const uint64_t wrow = uint64_t(kpad) * (f4 ? 16 : 32);  // prepared-weight row bytes
+  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, wrow, uint64_t(p.w_bits) * p.oc, wrow, brow, bn,
+                 f4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  if (P.epi == kEpiTma)
+    return encode_2d(&to, CU_TENSOR_MAP_DATA_TYPE_INT32, p.out, uint64_t(p.oc), uint64_t(p.M), uint64_t(p.oc) * 4, 32,
+                     32, CU_TENSOR_MAP_SWIZZLE_128B);
+  to = tw;  // unused
+  return true;
+}
+
+template <int A_BITS, int W_BITS, int BN, bool F4, int NP>
+cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int count, cudaStream_t stream) {
+  using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
+  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4, NP>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  TcArgs a;
-  a.p = p;
-  a.ntn = (p.oc + BN - 1) / BN;
-  const int64_t mtiles = (p.M + BM - 1) / BM;
-  if (mtiles * a.ntn > (int64_t(1) << 31) - 1) return cudaErrorInvalidValue;
-  a.ntiles = int(mtiles * a.ntn);
-  a.nchunks = int(kpad / kWordsPerStage);
-  // TMA-store epilogue by default (direct 16-byte stores of one row segment per lane
-  // measured 1.4-1.8x slower on the output-bound layers); BS_TC_EPI=direct selects them.
-  const char* epi_env = getenv("BS_TC_EPI");
-  const bool want_direct = epi_env && epi_env[0] == 'd';
-  a.epi = (p.oc % 4) != 0 ? kEpiScalar : (want_direct ? kEpiDirect : kEpiTma);
+  if (count < 1 || count > NP) return cudaErrorInvalidValue;
+  TcArgs<NP> a;
+  TcMaps<NP> maps;
+  memset(&a, 0, sizeof(a));
+  memset(&maps, 0, sizeof(maps));
+  a.nprob = count;
+  int64_t total = 0;
+  for (int q = 0; q < count; ++q) {
+    int64_t tiles = 0;
+    if (!make_prob(a.prob[q], maps.w[q], maps.out[q], ps[q], wexps[q], int(total), BN, F4, tiles))
+      return cudaErrorInvalidValue;
+    total += tiles;
+    if (total > (int64_t(1) << 31) - 1) return cudaErrorInvalidValue;
+  }
+  if (total == 0) return cudaSuccess;
+  a.ntiles = int(total);
   const char* res_env = getenv("BS_TC_RESIDENT");
   const bool allow_res = !(res_env && res_env[0] == '0');
-  const int64_t fixed = C::kFixed;
-  const int64_t res_bytes = int64_t(a.nchunks) * C::kBBytes;
-  a.b_resident = allow_res && a.ntn == 1 && fixed + res_bytes <= kSmemLimit;
+  const int64_t res_bytes = int64_t(a.prob[0].nchunks) * C::kBBytes;
+  a.b_resident = NP == 1 && allow_res && a.prob[0].ntn == 1 && C::kFixed + res_bytes <= kSmemLimit;
   a.b_bytes = int(a.b_resident ? res_bytes : int64_t(C::kStages) * C::kBBytes);
-  a.div_hw = make_fastdiv(uint32_t(p.oh) * uint32_t(p.ow));
-  a.div_ow = make_fastdiv(uint32_t(p.ow));
-  a.div_kwid = make_fastdiv(uint32_t(p.kwid));
-  a.div_ntn = make_fastdiv(uint32_t(a.ntn));
-  a.div_kwa = make_fastdiv(uint32_t(p.kw_a));
-  a.taps = p.kh * p.kwid;
-  // the table's int32 word offsets: (ky*W + kx)*Cw must fit
-  if ((int64_t(p.kh) * p.w + p.kwid) * p.kw_a >= (int64_t(1) << 31)) a.taps = kMaxTaps + 1;
-  a.kwa_shift = -1;
-  for (int sh = 0; sh < 31; ++sh)
-    if ((1 << sh) == p.kw_a) a.kwa_shift = sh;
   const char* dbg_env = getenv("BS_TC_DEBUG");
   a.debug = dbg_env ? atoi(dbg_env) : 0;
-  int smem_bytes = int(fixed) + a.b_bytes;
+  int smem_bytes = C::kFixed + a.b_bytes;
   if (smem_bytes < kMinSmem) smem_bytes = kMinSmem;
-  CUtensorMap tw, to;
-  const uint64_t wrow = uint64_t(kpad) * (F4 ? 16 : 32);  // prepared-weight row bytes
-  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, wrow, uint64_t(W_BITS) * p.oc, wrow, C::kBRow, BN,
-                 F4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  if (a.epi == kEpiTma) {
-    if (!encode_2d(&to, CU_TENSOR_MAP_DATA_TYPE_INT32, p.out, uint64_t(p.oc), uint64_t(p.M), uint64_t(p.oc) * 4, 32,
-                   32, CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
-  } else {
-    to = tw;  // unused
-  }
   const int grid = a.ntiles < num_sms() ? a.ntiles : num_sms();
-  kern<<<grid, kThreads, smem_bytes, stream>>>(a, tw, to);
+  kern<<<grid, kThreads, smem_bytes, stream>>>(a, maps);
   note_launch();
   return cudaPeekAtLastError();
 }
 
 // Tile width: BN = 64 when the filters fit it, else 128 (the widest tile whose double-
 // buffered accumulators leave TMEM room for the A ring).  BS_TC_BN overrides (tests).
-template <int A_BITS, int W_BITS>
-int pick_bn(const ConvProblem& p, int64_t) {
+inline int pick_bn(const ConvProblem& p) {
   if (const char* e = getenv("BS_TC_BN")) {
     const int v = atoi(e);
     if (v == 64 || v == 128) return v;
@@ -1138,14 +1216,39 @@ int pick_bn(const ConvProblem& p, int64_t) {
 }
 
 template <int A_BITS, int W_BITS, bool F4>
-cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, int64_t kpad, cudaStream_t stream) {
-  switch (pick_bn<A_BITS, W_BITS>(p, kpad)) {
+cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream) {
+  switch (pick_bn(p)) {
     case 128:
       if constexpr (Cfg<A_BITS, W_BITS, 128, F4>::kFit >= 2)
-        return launch_bn<A_BITS, W_BITS, 128, F4>(p, wexp, kpad, stream);
+        return launch_bn<A_BITS, W_BITS, 128, F4, 1>(&p, &wexp, 1, stream);
       [[fallthrough]];
     default:
-      return launch_bn<A_BITS, W_BITS, 64, F4>(p, wexp, kpad, stream);
+      return launch_bn<A_BITS, W_BITS, 64, F4, 1>(&p, &wexp, 1, stream);
+  }
+}
+
+// Group launch: up to kGroupMax problems of one (A, W) precision in one persistent
+// kernel with BN-wide tiles (N = 64 MMAs for OC <= 64 members of a BN = 128 group).
+// Problems are ordered by decreasing K so the cheapest tiles form the tail of every
+// CTA's sequence.
+template <int A_BITS, int W_BITS, int BN, bool F4>
+cudaError_t launch_group_aw(const ConvProblem* ps, const int8_t* const* wexps, int count, cudaStream_t stream) {
+  if (count == 1) return launch_aw<A_BITS, W_BITS, F4>(ps[0], wexps[0], stream);
+  if constexpr (Cfg<A_BITS, W_BITS, BN, F4, kGroupMax>::kFit >= 2) {
+    ConvProblem sp[kGroupMax];
+    const int8_t* sw[kGroupMax];
+    int order[kGroupMax];
+    for (int q = 0; q < count; ++q) order[q] = q;
+    std::stable_sort(order, order + count, [&](int x, int y) { return ps[x].kp > ps[y].kp; });
+    for (int q = 0; q < count; ++q) {
+      sp[q] = ps[order[q]];
+      sw[q] = wexps[order[q]];
+    }
+    return launch_bn<A_BITS, W_BITS, BN, F4, kGroupMax>(sp, sw, count, stream);
+  } else {
+    for (int q = 0; q < count; ++q)
+      if (cudaError_t e = launch_aw<A_BITS, W_BITS, F4>(ps[q], wexps[q], stream)) return e;
+    return cudaSuccess;
   }
 }
 
@@ -1185,19 +1288,60 @@ cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w
   return cudaPeekAtLastError();
 }
 
+#define BS_TC_DISPATCH(CALL)                                                                          \
+  BS_TC(1, 1, CALL) BS_TC(2, 1, CALL) BS_TC(2, 2, CALL) BS_TC(1, 2, CALL) BS_TC(3, 1, CALL)           \
+  BS_TC(3, 2, CALL) BS_TC(4, 1, CALL) BS_TC(4, 2, CALL) BS_TC(1, 3, CALL) BS_TC(2, 3, CALL)           \
+  BS_TC(3, 3, CALL) BS_TC(4, 3, CALL) BS_TC(1, 4, CALL) BS_TC(2, 4, CALL) BS_TC(3, 4, CALL)           \
+  BS_TC(4, 4, CALL)
+
 cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
-  const int64_t kpad = tc_kpad(p.kp);
   const bool f4 = tc_resolve_format(fmt) == kTcF4;
-#define BS_TC(A, W)                                                                 \
-  if (p.a_bits == A && p.w_bits == W)                                               \
-    return f4 ? tc::launch_aw<A, W, true>(p, wexp, kpad, stream)                    \
-              : tc::launch_aw<A, W, false>(p, wexp, kpad, stream);
-  BS_TC(1, 1) BS_TC(2, 1) BS_TC(2, 2) BS_TC(1, 2) BS_TC(3, 1) BS_TC(3, 2) BS_TC(4, 1) BS_TC(4, 2)
-  BS_TC(1, 3) BS_TC(2, 3) BS_TC(3, 3) BS_TC(4, 3) BS_TC(1, 4) BS_TC(2, 4) BS_TC(3, 4) BS_TC(4, 4)
+#define BS_TC(A, W, CALL)                                                   \
+  if (p.a_bits == A && p.w_bits == W)                                       \
+    return f4 ? tc::launch_aw<A, W, true>(p, wexp, stream) : tc::launch_aw<A, W, false>(p, wexp, stream);
+  BS_TC_DISPATCH(0)
 #undef BS_TC
   return cudaErrorNotSupported;
 }
+
+cudaError_t launch_tc_conv_group(const ConvProblem* ps, const int8_t* const* wexps, int count, int fmt,
+                                 cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  const int a_bits = ps[0].a_bits, w_bits = ps[0].w_bits;
+  if (!tc_supported(a_bits, w_bits)) return cudaErrorNotSupported;
+  for (int q = 1; q < count; ++q)
+    if (ps[q].a_bits != a_bits || ps[q].w_bits != w_bits) return cudaErrorInvalidValue;
+  const bool f4 = tc_resolve_format(fmt) == kTcF4;
+  // members whose filters fit a 64-wide tile run in BN = 64 groups, the rest in BN = 128
+  // groups (the tile width pick_bn makes for a single launch)
+  for (int wide = 1; wide >= 0; --wide) {
+    ConvProblem gp[tc::kGroupMax];
+    const int8_t* gw[tc::kGroupMax];
+    int cnt = 0;
+    for (int q = 0; q <= count; ++q) {
+      if (q < count && (tc::pick_bn(ps[q]) == 128) == bool(wide)) {
+        gp[cnt] = ps[q];
+        gw[cnt++] = wexps[q];
+      }
+      if (cnt == tc::kGroupMax || (q == count && cnt > 0)) {
+        cudaError_t e = cudaErrorNotSupported;
+#define BS_TC(A, W, CALL)                                                                          \
+  if (a_bits == A && w_bits == W)                                                                  \
+    e = wide ? (f4 ? tc::launch_group_aw<A, W, 128, true>(gp, gw, cnt, stream)                     \
+                   : tc::launch_group_aw<A, W, 128, false>(gp, gw, cnt, stream))                   \
+             : (f4 ? tc::launch_group_aw<A, W, 64, true>(gp, gw, cnt, stream)                      \
+                   : tc::launch_group_aw<A, W, 64, false>(gp, gw, cnt, stream));
+        BS_TC_DISPATCH(0)
+#undef BS_TC
+        if (e != cudaSuccess) return e;
+        cnt = 0;
+      }
+    }
+  }
+  return cudaSuccess;
+}
+#undef BS_TC_DISPATCH
 
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;

@@ -128,3 +128,33 @@ def test_tc_validation_before_launch(lib):
     assert lib.bs_dense_tc_weight_bytes(64, 64, 1, bs.TC_I8) == 64 * 4 * 32
     assert lib.bs_dense_tc_weight_bytes(64, 64, 2, bs.TC_F4) == 2 * 64 * 4 * 16
     assert lib.bs_dense_tc_weight_bytes(64, 64, 1, 9) == 0
+
+
+def _desc(**kw):
+    d = bs.TcConvDesc()
+    d.act_packed = d.w_tc = d.out = 1 << 20  # fake, 16-byte aligned device pointers (never dereferenced)
+    d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw, d.stride_h, d.stride_w, d.pad_h, d.pad_w = 1, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1
+    for k, v in kw.items():
+        setattr(d, k, v)
+    return d
+
+
+def test_tc_group_validation_before_launch(lib):
+    """bs_bitserial_conv2d_nhwc_tc_group validates every descriptor before launching
+    anything (no GPU here: a launch would fail with a CUDA error, not these codes)."""
+    import ctypes
+    arr = (bs.TcConvDesc * 3)(_desc(), _desc(oc=0), _desc())
+    p = ctypes.cast(arr, ctypes.c_void_p)
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 0, 2, 1, bs.TC_F4, NULL) == 0  # empty: no-op
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(NULL, 2, 2, 1, bs.TC_F4, NULL) == 1  # NULL array
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 2, 1, bs.TC_F4, NULL) == 4  # member 1: oc = 0
+    arr[1] = _desc(out=0)
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 2, 1, bs.TC_F4, NULL) == 1  # NULL out
+    arr[1] = _desc(w_tc=(1 << 20) + 4)
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 2, 1, bs.TC_F4, NULL) == 5  # misaligned
+    arr[1] = _desc(a_enc=bs.A_BIPOLAR)
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 2, 1, bs.TC_I8, NULL) == 3  # bipolar A needs FP4
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 5, 1, bs.TC_F4, NULL) == 3  # A5 unsupported
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 2, 1, 7, NULL) == 2  # bad format
+    arr[1] = _desc(c=100000, kh=1, kw=1, pad_h=0, pad_w=0)
+    assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 4, 2, bs.TC_F4, NULL) == 6  # FP4 bound 2^22

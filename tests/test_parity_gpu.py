@@ -498,3 +498,89 @@ def test_i8_signed_weights(w_bits):
     w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, bs.SIGNED, n, k, tc_format=bs.TC_I8)
     got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=bs.TC_I8, w_enc=bs.SIGNED)
     np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+# ------------------------------- grouped launch: several convolutions, one persistent kernel
+GROUP_CASES = [  # (n, h, w, c, oc, kh, kw, sh, sw, ph, pw): OC <= 64 (N = 64 MMAs), ragged OC
+    (2, 9, 11, 33, 20, 3, 3, 1, 1, 1, 1),      # and M tails, stride 2, 1x1, a dense layer
+    (1, 12, 10, 96, 100, 3, 3, 2, 2, 1, 1),    # (n = 1, w = 1, 1x1), K from 1 to 36 chunks
+    (3, 7, 7, 64, 64, 1, 1, 1, 1, 0, 0),
+    (1, 14, 14, 128, 300, 3, 3, 1, 1, 1, 1),
+    (1, 130, 1, 1000, 72, 1, 1, 1, 1, 0, 0),
+    (2, 5, 5, 7, 4, 3, 3, 1, 1, 2, 2),
+]
+
+
+def _group_run(cases, a_bits, w_bits, fmt, encs, seed):
+    items, refs = [], []
+    for i, (n, h, w, c, oc, kh, kw, sh, sw, ph, pw) in enumerate(cases):
+        a_enc, w_enc = encs[i % len(encs)]
+        g = inputs.gen(seed + 31 * i)
+        act = inputs.codes((n, h, w, c), a_bits, g)
+        wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+        refs.append(oracle.conv2d_nhwc_enc(act.numpy(), a_bits, a_enc, wt.numpy(), w_bits, w_enc, stride=(sh, sw),
+                                           pad=(ph, pw)))
+        w_tc = bs.conv2d_tc_prepare_weights(gpu_pack(wt.reshape(oc * kh * kw, c), w_bits), w_bits, w_enc, oc, kh,
+                                            kw, c, tc_format=fmt)
+        items.append(dict(act_packed=gpu_pack(act.reshape(-1, c), a_bits), w_tc=w_tc, n=n, h=h, w=w, c=c, oc=oc,
+                          kh=kh, kw=kw, stride=(sh, sw), pad=(ph, pw), a_enc=a_enc, w_enc=w_enc))
+    return bs.bitserial_conv2d_nhwc_tc_group(items, a_bits, w_bits, tc_format=fmt), refs
+
+
+@pytest.mark.parametrize("bn", ["", "64", "128"])
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+@pytest.mark.parametrize("a_bits,w_bits", TC_PRECISIONS)
+def test_conv_tc_group_mixed(monkeypatch, bn, fmt, a_bits, w_bits):
+    """bs_bitserial_conv2d_nhwc_tc_group on six problems of different geometry (problems
+    reordered by K inside; tiles of all problems interleaved across CTAs): every output
+    equals the oracle's.  Default tile widths (OC <= 64 members in a BN = 64 group, the
+    rest in a BN = 128 group) and every member forced into one BN = 64 or BN = 128
+    launch (N = 64 MMAs for the narrow members).  FP4 mixes the encodings per member."""
+    if bn:
+        monkeypatch.setenv("BS_TC_BN", bn)
+    encs = [(bs.A_UNSIGNED, bs.UNIPOLAR), (bs.A_UNSIGNED, bs.BIPOLAR)]
+    if fmt == bs.TC_F4:
+        encs += [(bs.A_BIPOLAR, bs.BIPOLAR), (bs.A_SIGNED, bs.SIGNED), (bs.A_UNSIGNED, bs.SIGNED)]
+    outs, refs = _group_run(GROUP_CASES, a_bits, w_bits, fmt, encs, seed=1000 * fmt + 10 * a_bits + w_bits)
+    for i, (o, r) in enumerate(zip(outs, refs)):
+        np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"member {i} {GROUP_CASES[i]}")
+
+
+def test_conv_tc_group_more_than_one_launch():
+    """More members than one launch holds (16): split into launches of <= 16, all exact;
+    a group of one and an empty group."""
+    cases = [(1, 4 + i % 5, 5, 16 + 8 * (i % 3), 8 + 12 * (i % 4), 3, 3, 1 + i % 2, 1, 1, 1) for i in range(21)]
+    outs, refs = _group_run(cases, 2, 1, bs.TC_F4, [(bs.A_UNSIGNED, bs.BIPOLAR)], seed=5)
+    for i, (o, r) in enumerate(zip(outs, refs)):
+        np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"member {i}")
+    outs, refs = _group_run(cases[:1], 2, 1, bs.TC_I8, [(bs.A_UNSIGNED, bs.BIPOLAR)], seed=6)
+    np.testing.assert_array_equal(outs[0].cpu().numpy(), refs[0])
+    assert bs.bitserial_conv2d_nhwc_tc_group([], 2, 1) == []
+
+
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+def test_config4_batch256_tc_group(fmt):
+    """BASELINE configs[3] as the bench's grouped step runs it: the ten ResNet-18 layers
+    at batch 256, A2W1 bipolar, in ONE grouped launch; each layer equals the single-layer
+    launch bit for bit, and the oracle checks images 0 and 255 of every layer."""
+    items, acts, wts = [], [], []
+    for layer in inputs.BASELINE_LAYERS:
+        L = inputs.TABLE1[layer]
+        act, wt = inputs.conv_operands(L, 256, 2, 1, inputs.seed_for(4, 2, 1, "bipolar", layer))
+        w_tc = bs.conv2d_tc_prepare_weights(gpu_pack(wt.view(L.oc * L.k * L.k, L.ic), 1), 1, bs.BIPOLAR, L.oc, L.k,
+                                            L.k, L.ic, tc_format=fmt)
+        items.append(dict(act_packed=gpu_pack(act.reshape(-1, L.ic), 2), w_tc=w_tc, n=256, h=L.h, w=L.w, c=L.ic,
+                          oc=L.oc, kh=L.k, kw=L.k, stride=L.s, pad=L.pad, w_enc=bs.BIPOLAR))
+        acts.append(act)
+        wts.append(wt)
+    outs = bs.bitserial_conv2d_nhwc_tc_group(items, 2, 1, tc_format=fmt)
+    for layer, it, o, act, wt in zip(inputs.BASELINE_LAYERS, items, outs, acts, wts):
+        L = inputs.TABLE1[layer]
+        single = bs.bitserial_conv2d_nhwc_tc_prepared(it["act_packed"], 2, it["w_tc"], 1, 256, L.h, L.w, L.ic, L.oc,
+                                                      L.k, L.k, L.s, L.pad, tc_format=fmt, w_enc=bs.BIPOLAR)
+        assert torch.equal(o, single), f"L{layer}"
+        o = o.cpu().numpy()
+        for img in (0, 255):
+            ref = oracle.conv2d_nhwc(act[img:img + 1].numpy(), 2, wt.numpy(), 1, True, stride=(L.s, L.s),
+                                     pad=(L.pad, L.pad))
+            np.testing.assert_array_equal(o[img:img + 1], ref, err_msg=f"L{layer} image {img}")

@@ -25,36 +25,19 @@ ap.add_argument("--layers", default=",".join(map(str, inputs.BASELINE_LAYERS)))
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--tc", action="store_true", help="tensor-core path on prepared weights")
 ap.add_argument("--fused", action="store_true", help="include activation packing (the *_i8 entry)")
+ap.add_argument("--group", action="store_true",
+                help="tensor-core path through bs_bitserial_conv2d_nhwc_tc_group: each layer as a group of one, "
+                     "then all layers in one group")
 args = ap.parse_args()
 dev = torch.device("cuda")
 enc = bs.UNIPOLAR if args.unipolar else bs.BIPOLAR
 res = {}
 tot_ops, tot_ms = 0, 0.0
 stream = torch.cuda.Stream()
-for li in map(int, args.layers.split(",")):
-    L = inputs.TABLE1[li]
-    g = inputs.gen(li)
-    act = inputs.codes((args.batch, L.h, L.w, L.ic), args.a, g).to(dev)
-    wt = inputs.codes((L.oc * L.k * L.k, L.ic), args.w, g).to(dev)
-    ap_ = bs.bitpack(act, args.a)
-    wp = bs.bitpack(wt, args.w)
-    oh = bs.conv_out_extent(L.h, L.k, L.s, L.pad)
-    out = torch.empty((args.batch, oh, oh, L.oc), dtype=torch.int32, device=dev)
-    ws = torch.empty(max(16, bs.conv2d_workspace_bytes(args.batch, L.h, L.w, L.ic, args.a)), dtype=torch.uint8,
-                     device=dev)
-    w_tc = bs.conv2d_tc_prepare_weights(wp, args.w, enc, L.oc, L.k, L.k, L.ic) if args.tc else None
-    if args.tc and args.fused:
-        run = lambda s: bs.bitserial_conv2d_nhwc_tc_i8(act, args.a, w_tc, args.w, L.oc, L.k, L.k, L.s, L.pad,  # noqa
-                                                       out=out, workspace=ws, stream=s)
-    elif args.tc:
-        run = lambda s: bs.bitserial_conv2d_nhwc_tc_prepared(ap_, args.a, w_tc, args.w, args.batch, L.h, L.w,  # noqa
-                                                             L.ic, L.oc, L.k, L.k, L.s, L.pad, out=out, stream=s)
-    elif args.fused:
-        run = lambda s: bs.bitserial_conv2d_nhwc_i8(act, args.a, wp, args.w, enc, L.oc, L.k, L.k, L.s, L.pad,  # noqa
-                                                    out=out, workspace=ws, stream=s)
-    else:
-        run = lambda s: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc,  # noqa
-                                                 L.k, L.k, L.s, L.pad, out=out, algo=args.algo, stream=s)
+items = []
+
+
+def time_graph(run):
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         run(stream)
@@ -75,13 +58,49 @@ for li in map(int, args.layers.split(",")):
             e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / args.reps)
-    ms = sorted(ts)[len(ts) // 2]
+    del graph
+    return sorted(ts)[len(ts) // 2]
+
+
+for li in map(int, args.layers.split(",")):
+    L = inputs.TABLE1[li]
+    g = inputs.gen(li)
+    act = inputs.codes((args.batch, L.h, L.w, L.ic), args.a, g).to(dev)
+    wt = inputs.codes((L.oc * L.k * L.k, L.ic), args.w, g).to(dev)
+    ap_ = bs.bitpack(act, args.a)
+    wp = bs.bitpack(wt, args.w)
+    oh = bs.conv_out_extent(L.h, L.k, L.s, L.pad)
+    out = torch.empty((args.batch, oh, oh, L.oc), dtype=torch.int32, device=dev)
+    ws = torch.empty(max(16, bs.conv2d_workspace_bytes(args.batch, L.h, L.w, L.ic, args.a)), dtype=torch.uint8,
+                     device=dev)
+    w_tc = bs.conv2d_tc_prepare_weights(wp, args.w, enc, L.oc, L.k, L.k, L.ic) if args.tc else None
+    if args.group:
+        item = dict(act_packed=ap_, w_tc=w_tc, out=out, n=args.batch, h=L.h, w=L.w, c=L.ic, oc=L.oc, kh=L.k, kw=L.k,
+                    stride=L.s, pad=L.pad, w_enc=enc)
+        items.append(item)
+        run = lambda s, it=item: bs.bitserial_conv2d_nhwc_tc_group([it], args.a, args.w, stream=s)  # noqa
+    elif args.tc and args.fused:
+        run = lambda s: bs.bitserial_conv2d_nhwc_tc_i8(act, args.a, w_tc, args.w, L.oc, L.k, L.k, L.s, L.pad,  # noqa
+                                                       out=out, workspace=ws, stream=s)
+    elif args.tc:
+        run = lambda s: bs.bitserial_conv2d_nhwc_tc_prepared(ap_, args.a, w_tc, args.w, args.batch, L.h, L.w,  # noqa
+                                                             L.ic, L.oc, L.k, L.k, L.s, L.pad, out=out, stream=s)
+    elif args.fused:
+        run = lambda s: bs.bitserial_conv2d_nhwc_i8(act, args.a, wp, args.w, enc, L.oc, L.k, L.k, L.s, L.pad,  # noqa
+                                                    out=out, workspace=ws, stream=s)
+    else:
+        run = lambda s: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc,  # noqa
+                                                 L.k, L.k, L.s, L.pad, out=out, algo=args.algo, stream=s)
+    ms = time_graph(run)
     ops = 2 * args.batch * oh * oh * L.oc * L.k * L.k * L.ic * args.a * args.w
     out_gb = out.numel() * 4 / 1e9
     res[li] = {"us": round(ms * 1e3, 2), "tops": round(ops / ms / 1e9, 1), "out_gbs": round(out_gb / ms * 1e3, 1)}
     tot_ops += ops
     tot_ms += ms
-    del graph
+extra = {}
+if args.group:
+    extra["all_in_one_group_us"] = round(1e3 * time_graph(lambda s: bs.bitserial_conv2d_nhwc_tc_group(
+        items, args.a, args.w, stream=s)), 2)
 print(json.dumps({"lib": bs.library_path(), "tc": args.tc, "fused": args.fused, "a": args.a, "w": args.w,
                   "batch": args.batch, "bn": os.environ.get("BS_TC_BN"), "layers": res,
-                  "total_us": round(tot_ms * 1e3, 1), "total_tops": round(tot_ops / tot_ms / 1e9, 1)}))
+                  "total_us": round(tot_ms * 1e3, 1), "total_tops": round(tot_ops / tot_ms / 1e9, 1), **extra}))
