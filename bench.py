@@ -226,16 +226,27 @@ class ConvWorkload:
             "parallelism": (f"{world} independent replicas (batch 1 does not shard)" if self.replicas > 1 else
                             f"batch-sharded dp{world} (no collective)"),
             "rank0_images": [lo, hi],
-            "step": (("per layer: bitpack(act) [side stream, overlapping earlier layers' convs] + tensor-core "
-                      "bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_prepared" if not args.no_overlap else
-                      "per layer: bitpack(act) + tensor-core bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_i8")
-                     + " (weights packed + plane-expanded once, untimed)" if args.path == "tc" else
-                     "per layer: bitpack(act) + AND/POPC bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights "
-                     "prepacked, untimed)"),
+            "step": self.describe_step(args),
             "path": args.path,
             "tc_format": args.tc_format if args.path == "tc" else None,
             "conv_groups": (args.conv_groups if self.overlap else 0),
+            "pack_group": bool(self.overlap and args.pack_group),
         }
+
+    def describe_step(self, args):
+        if args.path != "tc":
+            return ("per layer: bitpack(act) + AND/POPC bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights "
+                    "prepacked, untimed)")
+        if args.no_overlap:
+            return ("per layer: bitpack(act) + tensor-core bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_i8 "
+                    "(weights packed + plane-expanded once, untimed)")
+        packs = ("every layer's activations packed by ONE bs_bitpack_group launch [side stream]" if args.pack_group
+                 else "per layer bs_bitpack [side stream]")
+        convs = (f"the layers' tensor-core convs in {len(self.groups)} bs_bitserial_conv2d_nhwc_tc_group calls "
+                 f"{[[self.layers[i] for i in g] for g in self.groups]} on alternating streams (each waits for its "
+                 "members' packs)" if self.groups else
+                 "per layer bs_bitserial_conv2d_nhwc_tc_prepared on alternating streams (each waits for its pack)")
+        return f"{packs}; {convs} (weights packed + plane-expanded once, untimed)"
 
     def step(self):
         if self.overlap:
@@ -253,7 +264,14 @@ class ConvWorkload:
         side = self.side_stream
         side.wait_stream(main)
         with torch.cuda.stream(side):
+            if self.args.pack_group:  # every layer's activations packed by one launch
+                self.runs[0].bs.bitpack_group([r.act for r in self.runs], self.args.a_bits,
+                                              outs=[r.packed for r in self.runs])
+                for e in self.pack_events:
+                    e.record(side)
             for i, (r, e) in enumerate(zip(self.runs, self.pack_events)):
+                if self.args.pack_group:
+                    break
                 # the first layer's pack has nothing to overlap: full grid; later packs run beside
                 # the previous layer's persistent conv CTAs: a capped grid leaves them room
                 r.pack_only(0 if i == 0 else self.pack_ctas)
@@ -305,16 +323,41 @@ class ConvWorkload:
         # (prepared form) read once, int32 outputs written once
         conv_bytes = [r.packed.numel() * 4 + (r.w_tc.numel() if r.w_tc is not None else r.wp.numel() * 4)
                       + r.out.numel() * 4 for r in self.runs]
-        return {"kind": "tensor" if tc else "alu",
-                "kernel": f"{kname} sum over the {len(self.runs)} layer launches of one step, rank 0)",
-                "ops": ops, "ms": sum(conv_ms), "launches": len(self.runs), "bytes": sum(conv_bytes),
-                "per_layer": [{"layer": li, "binops": r.binops(), "bytes": b, "ms": t}
-                              for li, r, b, t in zip(self.layers, self.runs, conv_bytes, conv_ms)],
-                "breakdown": {"layers": list(self.layers), "conv_us": [1e3 * t for t in conv_ms],
-                              "pack_us": [1e3 * t for t in pack_ms],
-                              "conv_binary_tops": [r.binops() / (t / 1e3) / 1e12 for r, t in zip(self.runs, conv_ms)],
-                              "pack_gbs": pack_bytes / (sum(pack_ms) / 1e3) / 1e9,
-                              "out_gbs": sum(r.out.numel() * 4 for r in self.runs) / (sum(conv_ms) / 1e3) / 1e9}}
+        res = {"kind": "tensor" if tc else "alu",
+               "kernel": f"{kname} sum over the {len(self.runs)} layer launches of one step, rank 0)",
+               "ops": ops, "ms": sum(conv_ms), "launches": len(self.runs), "bytes": sum(conv_bytes),
+               "per_layer": [{"layer": li, "binops": r.binops(), "bytes": b, "ms": t}
+                             for li, r, b, t in zip(self.layers, self.runs, conv_bytes, conv_ms)],
+               "breakdown": {"layers": list(self.layers), "conv_us": [1e3 * t for t in conv_ms],
+                             "pack_us": [1e3 * t for t in pack_ms],
+                             "conv_binary_tops": [r.binops() / (t / 1e3) / 1e12 for r, t in zip(self.runs, conv_ms)],
+                             "pack_gbs": pack_bytes / (sum(pack_ms) / 1e3) / 1e9,
+                             "out_gbs": sum(r.out.numel() * 4 for r in self.runs) / (sum(conv_ms) / 1e3) / 1e9}}
+        if tc and self.overlap and self.groups:
+            # the step's launch configuration: one bs_bitserial_conv2d_nhwc_tc_group call per
+            # group (a BN = 64 launch for OC <= 64 members, one persistent BN = 128 launch for
+            # the rest), each timed as a whole (its members run concurrently inside it)
+            bs, fmt = self.runs[0].bs, tc_fmt(self.args)
+            fns = [lambda items=items: bs.bitserial_conv2d_nhwc_tc_group(items, self.args.a_bits, self.args.w_bits,
+                                                                          tc_format=fmt) for items in self.group_items]
+            n0 = bs.kernel_launches()
+            for f in fns:
+                f()
+            launches = bs.kernel_launches() - n0
+            torch.cuda.synchronize()
+            gms = [graph_launch_ms(f, reps) for f in fns]
+            per = [{"layers": [self.layers[i] for i in grp], "binops": sum(self.runs[i].binops() for i in grp),
+                    "bytes": sum(conv_bytes[i] for i in grp), "ms": t} for grp, t in zip(self.groups, gms)]
+            res.update(kernel=f"{kname} the step's {len(fns)} grouped calls ({launches} launches), rank 0)",
+                       ms=sum(gms), launches=launches, per_layer=per)
+            res["breakdown"]["group_us"] = [1e3 * t for t in gms]
+            res["breakdown"]["groups"] = [[self.layers[i] for i in grp] for grp in self.groups]
+        if tc and self.overlap and self.args.pack_group:
+            pms = graph_launch_ms(lambda: self.runs[0].bs.bitpack_group(
+                [r.act for r in self.runs], self.args.a_bits, outs=[r.packed for r in self.runs]), reps)
+            res["breakdown"]["pack_group_us"] = 1e3 * pms
+            res["breakdown"]["pack_group_gbs"] = pack_bytes / (pms / 1e3) / 1e9
+        return res
 
     def e2e(self, steps):
         bufs = [r.host_buffers() for r in self.runs]
@@ -632,7 +675,7 @@ def run_ours(args):
             max(t_tensor, t_hbm)
         model = {"t_tensor_ms": t_tensor, "t_hbm_ms": t_hbm, "t_roof_ms": t_roof, "t_actual_ms": roof["ms"],
                  "frac": t_roof / roof["ms"],
-                 "per_layer": [{"layer": x["layer"], "t_us": 1e3 * x["ms"],
+                 "per_layer": [{"layer": x.get("layer", x.get("layers")), "t_us": 1e3 * x["ms"],
                                 "t_tensor_us": 1e6 * x["binops"] / (peak * 1e12),
                                 "t_hbm_us": 1e6 * x["bytes"] / (hbm * 1e9)} for x in per]}
         common = {"kernel": roof["kernel"], "traffic": None,
@@ -793,7 +836,9 @@ def main():
     ap.add_argument("--packs-first", action="store_true", help="overlapped step variant: all packs before any conv")
     ap.add_argument("--conv-streams", type=int, default=2, choices=[1, 2, 3],
                     help="overlapped step: convs of consecutive (independent) layers on 1 or 2 streams")
-    ap.add_argument("--conv-groups", type=int, default=0,
+    ap.add_argument("--no-pack-group", dest="pack_group", action="store_false",
+                    help="tensor-core path: one bs_bitpack launch per layer instead of one bs_bitpack_group launch")
+    ap.add_argument("--conv-groups", type=int, default=2,
                     help="tensor-core path: layers per step in this many grouped launches (0: one launch per layer)")
     ap.add_argument("--pack-ctas-per-sm", type=int, default=0,
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")

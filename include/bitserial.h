@@ -123,6 +123,18 @@ int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bi
  * each thread keeps several 32-byte groups in flight, so the pack stays near HBM speed. */
 int bs_bitpack_ex(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, int max_ctas, void* stream);
 
+/* Several bs_bitpack problems of one bit width in ONE launch (per 16 descriptors): the
+ * activation packing of every layer of a network step (PAPER.md:715 times activation
+ * packing per layer) without a launch per tensor.  Each descriptor means exactly what
+ * the bs_bitpack arguments mean; outputs must not overlap any input or each other.  All
+ * descriptors are validated before anything is launched; count = 0 is a no-op. */
+typedef struct bs_pack_desc {
+  const uint8_t* in; /* [rows][k] uint8 codes */
+  uint32_t* out;     /* [bits][rows][bs_packed_row_words(k)] */
+  int64_t rows, k;
+} bs_pack_desc;
+int bs_bitpack_group(const bs_pack_desc* descs, int count, int bits, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Bitserial dense / matrix multiply (Sec. 3.2 and 6.2.1).
  *   out[m][n] = sum_{k<K} a[m][k] * value(w[n][k])          (int32 [m][n] row-major)

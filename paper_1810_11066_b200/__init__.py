@@ -26,7 +26,7 @@ __all__ = [
     "conv2d_tc_prepare_weights", "dense_tc_prepare_weights", "bitserial_conv2d_nhwc_tc_prepared",
     "bitserial_dense_tc_prepared", "bitserial_conv2d_nhwc_tc_i8", "bitserial_dense_tc_i8",
     "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
-    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group",
+    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
@@ -50,7 +50,7 @@ EXPORTED_SYMBOLS = (
     "bs_conv2d_tc_prepare_weights", "bs_dense_tc_prepare_weights", "bs_bitserial_conv2d_nhwc_tc_prepared",
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
-    "bs_bitserial_conv2d_nhwc_tc_group",
+    "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group",
 )
 
 
@@ -102,6 +102,7 @@ def _load():
         "bs_bitserial_dense_tc_i8": ([P, I, I, P, I, I, I, P, L, L, L, P, L, P], I),
         "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
         "bs_bitserial_conv2d_nhwc_tc_group": ([P, I, I, I, I, P], I),
+        "bs_bitpack_group": ([P, I, I, P], I),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("BITSERIAL_LIB") and not hasattr(lib, name):
@@ -170,6 +171,30 @@ def bitpack(x: torch.Tensor, bits: int, out: torch.Tensor | None = None, stream=
     _check(_load().bs_bitpack_ex(_dev(x, "x", torch.uint8), _dev(out, "out", torch.int32), rows, k, bits,
                                  int(max_ctas), _stream(stream)))
     return out
+
+
+class PackDesc(ctypes.Structure):
+    """bs_pack_desc (include/bitserial.h): one member of a grouped pack."""
+    _fields_ = [("in_", ctypes.c_void_p), ("out", ctypes.c_void_p), ("rows", ctypes.c_int64), ("k", ctypes.c_int64)]
+
+
+def bitpack_group(xs, bits, outs=None, stream=None):
+    """bs_bitpack_group: bitpack every tensor of `xs` (uint8 codes, reduction axis last)
+    at `bits` in one launch; returns the packed tensors (or fills `outs`)."""
+    descs = (PackDesc * max(len(xs), 1))()
+    res = []
+    for i, x in enumerate(xs):
+        k = x.shape[-1]
+        rows = x.numel() // k
+        out = outs[i] if outs is not None else torch.empty((bits, rows, packed_row_words(k)), dtype=torch.int32,
+                                                            device=x.device)
+        d = descs[i]
+        d.in_ = _dev(x, "x", torch.uint8).value
+        d.out = _dev(out, "out", torch.int32).value
+        d.rows, d.k = rows, k
+        res.append(out)
+    _check(_load().bs_bitpack_group(ctypes.cast(descs, ctypes.c_void_p), len(xs), bits, _stream(stream)))
+    return res
 
 
 def bitserial_dense(a_packed, a_bits, w_packed, w_bits, w_enc, m, n, k, out=None, algo=ALGO_AUTO, stream=None):

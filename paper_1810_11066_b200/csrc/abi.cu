@@ -204,6 +204,24 @@ int bs_bitpack_ex(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int
                                         max_ctas), fn);
 }
 
+int bs_bitpack_group(const bs_pack_desc* descs, int count, int bits, void* stream) {
+  const char* fn = "bs_bitpack_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  if (bits < 1 || bits > 8) return fail(BS_ERR_INVALID_ARG, "%s: bits=%d not in [1,8]", fn, bits);
+  std::vector<bs::PackSeg> segs(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_pack_desc& d = descs[q];
+    if (!d.in || !d.out) return fail(BS_ERR_NULL, "%s: NULL tensor pointer in descriptor %d", fn, q);
+    if (d.rows <= 0 || d.k <= 0) return fail(BS_ERR_SHAPE, "%s: descriptor %d: rows and k must be >= 1", fn, q);
+    if (!aligned16(d.in) || !aligned16(d.out))
+      return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
+    segs[q] = bs::PackSeg{d.in, d.out, d.rows, d.k, row_words(d.k), 0, -1, 0};
+  }
+  return cuda_status(bs::launch_bitpack_group(segs.data(), count, bits, static_cast<cudaStream_t>(stream)), fn);
+}
+
 int bs_bitserial_dense_ex(const uint32_t* a_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,
                           int32_t* out, int64_t m, int64_t n, int64_t k, int algo, void* stream) {
   const char* fn = "bs_bitserial_dense";

@@ -40,6 +40,22 @@ enum class Algo : int { Auto = 0, Popc = 1, PopcLit = 2, Gemv = 3 };
 cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int64_t kwp, int bits,
                            cudaStream_t stream, int max_ctas = 0);
 
+// One segment of a grouped pack (in/out/rows/k/kwp set by the caller; the rest by the launcher).
+struct PackSeg {
+  const uint8_t* in;
+  uint32_t* out;
+  int64_t rows, k, kwp, task0;
+  int shift;      // log2(kwp) or -1
+  int aligned16;  // 16-byte aligned rows
+};
+constexpr int kPackGroupMax = 16;
+struct PackGroupArgs {
+  int nseg;
+  int64_t tasks;
+  PackSeg seg[kPackGroupMax];
+};
+cudaError_t launch_bitpack_group(const PackSeg* segs, int count, int bits, cudaStream_t stream);
+
 // Tiled AND+POPC implicit-GEMM kernel (conv and dense); returns cudaErrorNotSupported
 // when no instantiation covers (a_bits, w_bits, algo).
 cudaError_t launch_popc_conv(const ConvProblem& p, Algo algo, cudaStream_t stream);

@@ -158,3 +158,18 @@ def test_tc_group_validation_before_launch(lib):
     assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 2, 1, 7, NULL) == 2  # bad format
     arr[1] = _desc(c=100000, kh=1, kw=1, pad_h=0, pad_w=0)
     assert lib.bs_bitserial_conv2d_nhwc_tc_group(p, 3, 4, 2, bs.TC_F4, NULL) == 6  # FP4 bound 2^22
+
+
+def test_bitpack_group_validation(lib):
+    import ctypes
+    arr = (bs.PackDesc * 2)()
+    for d in arr:
+        d.in_, d.out, d.rows, d.k = 1 << 20, 1 << 21, 10, 64
+    p = ctypes.cast(arr, ctypes.c_void_p)
+    assert lib.bs_bitpack_group(p, 0, 2, NULL) == 0
+    assert lib.bs_bitpack_group(NULL, 2, 2, NULL) == 1
+    assert lib.bs_bitpack_group(p, 2, 9, NULL) == 2
+    arr[1].k = 0
+    assert lib.bs_bitpack_group(p, 2, 2, NULL) == 4
+    arr[1].k, arr[1].out = 64, (1 << 21) + 4
+    assert lib.bs_bitpack_group(p, 2, 2, NULL) == 5

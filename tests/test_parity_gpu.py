@@ -584,3 +584,16 @@ def test_config4_batch256_tc_group(fmt):
             ref = oracle.conv2d_nhwc(act[img:img + 1].numpy(), 2, wt.numpy(), 1, True, stride=(L.s, L.s),
                                      pad=(L.pad, L.pad))
             np.testing.assert_array_equal(o[img:img + 1], ref, err_msg=f"L{layer} image {img}")
+
+
+def test_bitpack_group_parity():
+    """bs_bitpack_group: ragged, unaligned-K, pad-word and multi-launch (> 16 members)
+    segments packed in one launch each equal the oracle's packing."""
+    shapes = [(3136 * 2, 64), (1001, 96), (513, 4096), (77, 100), (5, 1), (33, 33), (7, 48)] * 3
+    for bits in (1, 2, 3, 4, 8):
+        g = inputs.gen(bits)
+        xs = [inputs.codes(s, bits, g) for s in shapes]
+        outs = bs.bitpack_group([x.to(DEV) for x in xs], bits)
+        for x, o in zip(xs, outs):
+            np.testing.assert_array_equal(o.cpu().numpy().view(np.uint32), oracle.bitpack(x.numpy(), bits))
+    assert bs.bitpack_group([], 2) == []

@@ -34,6 +34,10 @@ def packs(s):
         bs.bitpack(act, A, out=packed, stream=s)
 
 
+def packgroup(s):
+    bs.bitpack_group([r[1] for r in runs], A, outs=[r[2] for r in runs], stream=s)
+
+
 def convs(s):
     for L, act, packed, it in runs:
         bs.bitserial_conv2d_nhwc_tc_prepared(it["act_packed"], A, it["w_tc"], W, B, L.h, L.w, L.ic, L.oc, L.k, L.k,
@@ -83,5 +87,7 @@ res = {
     "packs+group_serial": t(lambda s: (packs(s), group(s))),
     "interleaved_pack_conv": t(interleaved),
     "groups_5_5": t(lambda s: (group(s, set(range(5))), group(s, set(range(5, 10))))),
+    "packgroup": t(packgroup),
+    "packgroup+group_serial": t(lambda s: (packgroup(s), group(s))),
 }
 print(json.dumps(res))
