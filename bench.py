@@ -219,6 +219,10 @@ class ConvWorkload:
             ng = min(args.conv_groups, len(self.runs))
             self.groups = ([list(range(len(self.runs)))[g * len(self.runs) // ng:(g + 1) * len(self.runs) // ng]
                             for g in range(ng)] if ng > 0 else [])
+            if args.group_layers:  # explicit partition, e.g. "2|4,5,6,7,8,9,10,11,12"
+                self.groups = [[self.layers.index(int(x)) for x in part.split(",")]
+                               for part in args.group_layers.split("|")]
+                assert sorted(i for grp in self.groups for i in grp) == list(range(len(self.runs)))
             self.group_items = [[self.runs[i].group_item() for i in grp] for grp in self.groups]
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
@@ -838,6 +842,8 @@ def main():
                     help="overlapped step: convs of consecutive (independent) layers on 1 or 2 streams")
     ap.add_argument("--no-pack-group", dest="pack_group", action="store_false",
                     help="tensor-core path: one bs_bitpack launch per layer instead of one bs_bitpack_group launch")
+    ap.add_argument("--group-layers", default="",
+                    help="explicit conv groups as layer lists, e.g. '2|4,5,6,7,8,9,10,11,12' (overrides --conv-groups)")
     ap.add_argument("--conv-groups", type=int, default=2,
                     help="tensor-core path: layers per step in this many grouped launches (0: one launch per layer)")
     ap.add_argument("--pack-ctas-per-sm", type=int, default=0,

@@ -108,16 +108,25 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // ------------------------------------------------------------------ PTX wrappers
+// Activation gathers allocate in L1: consecutive K chunks (filter taps) of a tile re-read
+// mostly the same pixels (measured 4% faster over the ResNet layers than L1::no_allocate)
+// back-off of a producer team polling the "chunks freed" counter
+#ifndef BS_TC_FREE_NS
+#define BS_TC_FREE_NS 20
+#endif
+#ifndef BS_TC_LDG_HINT
+#define BS_TC_LDG_HINT ""
+#endif
 __device__ __forceinline__ uint4 ldg_nc_v4(const uint32_t* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.nc" BS_TC_LDG_HINT ".v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint2 ldg_nc_v2(const uint32_t* p) {
   uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  asm volatile("ld.global.nc" BS_TC_LDG_HINT ".v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
@@ -317,10 +326,10 @@ __device__ __forceinline__ void expand_to_tmem(uint32_t taddr, uint4 v) {
 }
 
 // ---- FP4 (kind::mxf4) operand format.  Elements are packed E2M1 nibbles, 8 per 32-bit
-// word; a bit b becomes the nibble 0b0001 (= 0.5) * b, and the plane weights 2^(i+1),
-// 2^(j+1) are the UE8M0 block scale factors (constant per plane), so 0.5*2^(i+1) * a_i *
-// 0.5*2^(j+1) * w_j = 2^(i+j) a_i w_j.  Bipolar weight bits are the nibbles +0.5 / -0.5
-// (0b0001 / 0b1001).  K order inside a packed word (shared with the weights): nibble r
+// word; two bit planes (b_lo, b_hi) become one radix-4 digit nibble 0.5 * (b_lo + 2 b_hi)
+// (digit_nibbles), and the digit weights 2^(2d+1), 2^(2e+1) are the UE8M0 block scale
+// factors (constant per digit), so 0.5*2^(2d+1) * a_d * 0.5*2^(2e+1) * w_e =
+// 4^(d+e) a_d w_e.  K order inside a packed word (shared with the weights): nibble r
 // of expanded word q (q < 4) holds element 4r + q, so expanded word q = (w >> q) & 0x1..1.
 // Products and partial sums are small integers times powers of two, exact in the FP32
 // accumulator (tools/mxf4_probe.cu: bit-exact up to |sum| = 803,600 > the 737,280 bound).
@@ -341,44 +350,79 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&o)[16
       : "memory");
 }
 
-// One plane's four packed words (128 K elements) -> 16 TMEM columns of packed E2M1.
-__device__ __forceinline__ void expand_to_tmem_f4(uint32_t taddr, uint4 v) {
-  uint32_t o[16], t[4];
-  expand_word_f4(v.x, t);
+// Radix-4 digits on the FP4 path.  An E2M1 nibble holds 0.5 x {0, 1, 2, 3} exactly
+// (0b0000, 0b0001, 0b0010, 0b0011), so two bit planes (lo = plane 2d, hi = plane 2d+1)
+// form ONE operand digit d of weight 4^d (scale factor 2^(2d+1)); each digit-pair MMA
+// does the work of up to four plane-pair MMAs of Eq. 2 (the sum over planes is exact
+// either way).  L, H: nibble bit-0 masks of the lo / hi plane (bit 4r of
+// L = element bit).  mode 0 unsigned: L + 2H; 1 bipolar: (2L-1) + 2(2H-1) (single: 2L-1);
+// 2 the digit holding the two's-complement top plane: L - 2H (single: -L).
+template <bool HAS_HI>
+__device__ __forceinline__ uint32_t digit_nibbles(uint32_t L, uint32_t H, int mode) {
+  constexpr uint32_t M = 0x11111111u;
+  if (mode == 0) return HAS_HI ? (L | (H << 1)) : L;
+  if (mode == 1)  // +-0.5 (0b0001 / 0b1001), +-1.5 (0b0011 / 0b1011)
+    return HAS_HI ? (M | ((~(L ^ H) & M) << 1) | ((~H & M) << 3)) : (M | ((L ^ M) << 3));
+  return HAS_HI ? (L | ((H & ~L) << 1) | (H << 3)) : L * 9u;  // 0.5, -1, -0.5 / -0.5
+}
+
+// Expanded word q (q < 4) of one digit from packed plane words lo, hi, mode fixed at
+// compile time.  Shifts are folded per q so the unsigned pair costs what two separate
+// planes did (a shift and a mask per plane and word, merged by one LOP3):
+// 0.5 * (b_lo + 2 b_hi) = nibble bit 0 from lo, bit 1 from hi.
+template <int MODE, bool HAS_HI, int Q>
+__device__ __forceinline__ uint32_t digit_word(uint32_t lo, uint32_t hi, uint32_t lox) {
+  constexpr uint32_t M = 0x11111111u;
+  const uint32_t L = (Q == 0 ? lo : lo >> Q) & M;
+  if constexpr (MODE == 0) {
+    if constexpr (!HAS_HI) return L;
+    const uint32_t H2 = (Q == 0 ? hi << 1 : (Q == 1 ? hi : hi >> (Q - 1))) & (M << 1);
+    return L | H2;
+  } else if constexpr (MODE == 1) {  // bipolar: 1 | (lo == hi) << 1 | !hi << 3; single 1 | !lo << 3
+    if constexpr (!HAS_HI) return M | (((Q == 3 ? ~lo : ~lo << (3 - Q))) & (M << 3));
+    const uint32_t E = (Q == 0 ? ~lox << 1 : (Q == 1 ? ~lox : ~lox >> (Q - 1))) & (M << 1);  // lox = lo ^ hi
+    const uint32_t S = (Q == 3 ? ~hi : ~hi << (3 - Q)) & (M << 3);
+    return M | E | S;
+  } else {  // the signed top digit: L - 2H (0.5, -1, -0.5); single: -L
+    if constexpr (!HAS_HI) return L * 9u;
+    const uint32_t H = (Q == 0 ? hi : hi >> Q) & M;
+    return L | ((H & ~L) << 1) | (H << 3);
+  }
+}
+
+// One digit's four packed words per plane (128 K elements) -> 16 TMEM columns of E2M1.
+// `valid` (bipolar only): pieces of padding (bit clear) expand to 0, not to -1.5.
+template <int MODE, bool HAS_HI>
+__device__ __forceinline__ void expand_digit_f4(uint32_t taddr, uint4 lo, uint4 hi, uint32_t valid) {
+  const uint32_t l4[4] = {lo.x, lo.y, lo.z, lo.w}, h4[4] = {hi.x, hi.y, hi.z, hi.w};
+  uint32_t o[16];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) o[q] = t[q];
-  expand_word_f4(v.y, t);
+  for (int wi = 0; wi < 4; ++wi) {
+    const uint32_t l = l4[wi], h = HAS_HI ? h4[wi] : 0u, x = l ^ h;
+    uint32_t t[4] = {digit_word<MODE, HAS_HI, 0>(l, h, x), digit_word<MODE, HAS_HI, 1>(l, h, x),
+                     digit_word<MODE, HAS_HI, 2>(l, h, x), digit_word<MODE, HAS_HI, 3>(l, h, x)};
+    if constexpr (MODE == 1) {
+      const bool ok = (valid >> (wi >> 1)) & 1u;  // words 0-1: piece 0, words 2-3: piece 1
 #pragma unroll
-  for (int q = 0; q < 4; ++q) o[4 + q] = t[q];
-  expand_word_f4(v.z, t);
+      for (int q = 0; q < 4; ++q) t[q] = ok ? t[q] : 0u;
+    }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) o[8 + q] = t[q];
-  expand_word_f4(v.w, t);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) o[12 + q] = t[q];
+    for (int q = 0; q < 4; ++q) o[4 * wi + q] = t[q];
+  }
   tmem_st16(taddr, o);
 }
 
-// Activation encodings on the FP4 path: mode 0 unsigned (nibble 0.5*b),
-// 1 bipolar (every digit +-0.5: bit set 0b0001, clear 0b1001; words of a padding piece,
-// `valid` bit clear, are 0 so padding contributes nothing), 2 negative plane (the top
-// plane of two's-complement data: 0b1001 = -0.5 for a set bit).
-__device__ __forceinline__ void expand_to_tmem_f4_enc(uint32_t taddr, uint4 v, int mode, uint32_t valid) {
-  uint32_t o[16], t[4];
-  const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int wi = 0; wi < 4; ++wi) {
-    expand_word_f4(w4[wi], t);
-    const bool ok = (valid >> (wi >> 1)) & 1u;  // words 0-1: piece 0, words 2-3: piece 1
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t x = t[q];
-      if (mode == 1) x = ok ? (0x11111111u | ((x ^ 0x11111111u) << 3)) : 0u;
-      else if (mode == 2) x = x * 9u;  // 0/1 nibbles -> 0/9: no carries
-      o[4 * wi + q] = x;
-    }
+// Every digit of one chunk: digit D holds planes 2D, 2D+1; with MODE 2 (signed) only the
+// digit holding plane A-1 uses the signed rule.
+template <int A_BITS, int MODE, int D = 0>
+__device__ __forceinline__ void expand_digits_f4(uint32_t ta, const uint4 (&v)[A_BITS], uint32_t valid) {
+  if constexpr (2 * D < A_BITS) {
+    constexpr bool kHi = 2 * D + 1 < A_BITS;
+    constexpr bool kTop = 2 * D + 2 >= A_BITS;
+    constexpr int kMode = (MODE == 2 && !kTop) ? 0 : MODE;
+    expand_digit_f4<kMode, kHi>(ta + uint32_t(D * 16), v[2 * D], v[kHi ? 2 * D + 1 : 2 * D], valid);
+    expand_digits_f4<A_BITS, MODE, D + 1>(ta, v, valid);
   }
-  tmem_st16(taddr, o);
 }
 
 // The 2 K-steps (64 elements = 8 TMEM columns / 32 bytes of B each) of one plane pair in
@@ -467,35 +511,40 @@ __global__ void __launch_bounds__(256) expand_weights_kernel(const uint32_t* __r
   }
 }
 
-// FP4 layout: w_packed [W][N][kp] words -> wexp [W][N][kpad*16] bytes, 16 bytes (4
-// expanded words of 8 nibbles) per packed word in the order of expand_word_f4; nibble
-// = 0b0001 * b (unipolar) or b ? 0b0001 : 0b1001 (bipolar, +-0.5); scale 2^(j+1) at run time.
+// FP4 layout: w_packed [W][N][kp] words -> wexp [WD][N][kpad*16] bytes, WD = ceil(W/2)
+// radix-4 digits (planes 2e, 2e+1; see digit_nibbles), 16 bytes (4 expanded words of 8
+// nibbles) per packed word in the order of expand_word_f4; padding elements are 0;
+// digit scale 2^(2e+1) at run time.
 __global__ void __launch_bounds__(256) expand_weights_f4_kernel(const uint32_t* __restrict__ w_packed,
                                                                 uint8_t* __restrict__ wexp, int w_bits, int n,
                                                                 int64_t kp, int64_t kpad, int w_enc, int c_tap,
                                                                 int kw_tap) {
-  const int64_t words = int64_t(w_bits) * n * kpad;
+  const int wd = (w_bits + 1) / 2;
+  const int64_t words = int64_t(wd) * n * kpad;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < words; t += int64_t(gridDim.x) * blockDim.x) {
     const int64_t kk = t % kpad, rest = t / kpad;
-    const int64_t row = rest % n, j = rest / n;
+    const int64_t row = rest % n, e = rest / n;
     const uint32_t valid = tap_word_mask(kk, kp, c_tap, kw_tap);
-    const uint32_t w = kk < kp ? w_packed[(j * n + row) * kp + kk] : 0u;
-    const bool neg_plane = plane_sign(int(j), w_bits, w_enc) < 0;
+    const int jlo = int(2 * e), jhi = jlo + 1;
+    const bool has_hi = jhi < w_bits;
+    const uint32_t wl = kk < kp ? w_packed[(jlo * int64_t(n) + row) * kp + kk] : 0u;
+    const uint32_t wh = (has_hi && kk < kp) ? w_packed[(jhi * int64_t(n) + row) * kp + kk] : 0u;
+    // mode: 1 bipolar; 2 the digit holding the signed top plane (W-1); else 0
+    const int mode = w_enc == 1 ? 1 : (w_enc == 2 && (has_hi ? jhi : jlo) == w_bits - 1 ? 2 : 0);
     uint32_t out[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // nibble r of expanded word q = element 4r + q
-      uint32_t v = 0;
+      uint32_t L = 0, H = 0, V = 0;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const int e = 4 * r + q;
-        const uint32_t b = (w >> e) & 1u;
-        // +0.5 = 0b0001, -0.5 = 0b1001; bipolar: every digit +-0.5; signed top plane: -0.5
-        const uint32_t nib = !((valid >> e) & 1u) ? 0u : (w_enc == 1 ? (b ? 0x1u : 0x9u) : (b ? (neg_plane ? 0x9u : 0x1u) : 0u));
-        v |= nib << (4 * r);
+        const int el = 4 * r + q;
+        L |= ((wl >> el) & 1u) << (4 * r);
+        H |= ((wh >> el) & 1u) << (4 * r);
+        V |= ((valid >> el) & 1u) ? 0xFu << (4 * r) : 0u;
       }
-      out[q] = v;
+      out[q] = (has_hi ? digit_nibbles<true>(L, H, mode) : digit_nibbles<false>(L, H, mode)) & V;
     }
-    *reinterpret_cast<uint4*>(wexp + (j * int64_t(n) + row) * kpad * 16 + kk * 16) =
+    *reinterpret_cast<uint4*>(wexp + (e * int64_t(n) + row) * kpad * 16 + kk * 16) =
         make_uint4(out[0], out[1], out[2], out[3]);
   }
 }
@@ -506,11 +555,14 @@ __global__ void __launch_bounds__(256) expand_weights_f4_kernel(const uint32_t* 
 // 128 K elements (4 packed words per plane per row) in both formats.
 template <int A_BITS, int W_BITS, int BN, bool F4, int NP = 1>
 struct Cfg {
+  // operand "planes": bit planes (I8), radix-4 digits of two bit planes (F4, digit_nibbles)
+  static constexpr int kAP = F4 ? (A_BITS + 1) / 2 : A_BITS;
+  static constexpr int kWP = F4 ? (W_BITS + 1) / 2 : W_BITS;
   static constexpr int kBRow = F4 ? 64 : BKB;             // B bytes per row per plane per stage
   static constexpr int kAColsPlane = F4 ? 16 : BKB / 4;    // TMEM columns per plane per stage
-  static constexpr int kACols = A_BITS * kAColsPlane;     // TMEM columns of one stage's A planes
-  static constexpr int kBBytes = W_BITS * BN * kBRow;     // shared memory per stage (B only)
-  static constexpr int kSFCols = F4 ? 16 + 8 * W_BITS : 0;  // SFA: 4 planes x 4 cols; SFB: W planes x 8
+  static constexpr int kACols = kAP * kAColsPlane;        // TMEM columns of one stage's A planes
+  static constexpr int kBBytes = kWP * BN * kBRow;        // shared memory per stage (B only)
+  static constexpr int kSFCols = F4 ? 16 + 8 * kWP : 0;   // SFA: up to 4 x 4 cols; SFB: kWP x 8
   static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + NP * 512 /*tap tables*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
@@ -566,6 +618,8 @@ struct TcProb {
 template <int NP>
 struct TcArgs {
   int nprob, ntiles;  // problems, tiles of all problems
+  int nset0, tiles0;  // grouped launches: problems [0, nset0) (tensor-heavy) own tiles [0, tiles0); the rest
+                      // (output-heavy) [tiles0, ntiles); each CTA interleaves its tiles of the two sets
   int b_resident;     // single problem, ntn == 1 and the whole expanded B fits: loaded once
   int b_bytes;        // bytes of the B region (resident: nchunks stages, else kStages)
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
@@ -583,6 +637,49 @@ struct TcMaps {
 #else
 #define DBG(bit) 0
 #endif
+
+// A CTA's tile sequence.  Single problem: blockIdx.x, +gridDim.x, ...  Grouped: the CTA's
+// share of each set (same grid stride) merged in proportion, so tensor-heavy tiles (long
+// K: producer / MMA work) alternate with output-heavy ones (1x1 layers: epilogue and HBM
+// work) and the roles of one SM overlap the two kinds; the problem index is tracked per
+// set (it only grows within a set).  Every role walks an identical copy.
+template <int NP>
+struct TileSeq {
+  int c, g, a, b, j0, j1, pi0, pi1;
+  __device__ __forceinline__ explicit TileSeq(const TcArgs<NP>& args) {
+    c = int(blockIdx.x);
+    g = int(gridDim.x);
+    const int t0 = NP > 1 ? args.tiles0 : args.ntiles, t1 = args.ntiles - t0;
+    a = t0 > c ? (t0 - 1 - c) / g + 1 : 0;
+    b = t1 > c ? (t1 - 1 - c) / g + 1 : 0;
+    j0 = j1 = 0;
+    pi0 = 0;
+    pi1 = NP > 1 ? args.nset0 : 0;
+  }
+  // next tile and its problem; false when the CTA's sequence is done
+  __device__ __forceinline__ bool next(const TcArgs<NP>& args, int& tile, int& pi) {
+    if constexpr (NP == 1) {
+      if (j0 >= a) return false;
+      tile = c + j0++ * g;
+      pi = 0;
+      return true;
+    } else {
+      const bool take0 = j0 < a && (j1 >= b || int64_t(2 * j0 + 1) * b <= int64_t(2 * j1 + 1) * a);
+      if (take0) {
+        tile = c + j0++ * g;
+        while (pi0 + 1 < args.nset0 && tile >= args.prob[pi0 + 1].tile0) ++pi0;
+        pi = pi0;
+      } else if (j1 < b) {
+        tile = args.tiles0 + c + j1++ * g;
+        while (pi1 + 1 < args.nprob && tile >= args.prob[pi1 + 1].tile0) ++pi1;
+        pi = pi1;
+      } else {
+        return false;
+      }
+      return true;
+    }
+  }
+};
 
 template <int A_BITS, int W_BITS, int BN, bool F4, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -612,12 +709,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef BS_TC_PROFILE
   const long long _t_start = clock64();
 #endif
-  const int ntiles = args.ntiles;
-  // problem of tile t: pi only grows along a CTA's tile sequence
-  auto track = [&](int t, int& pi) {
-    if constexpr (NP > 1)
-      while (pi + 1 < args.nprob && t >= args.prob[pi + 1].tile0) ++pi;
-  };
 
   // filter-tap tables (implicit im2col): word offset of tap (ky, kx) from the row's
   // receptive-field origin, and (ky, kx) for the bounds test
@@ -660,8 +751,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t tmem = 0;
   if (lane == 0 && warp == kMmaWarp) STAMP("prologue")
   if constexpr (F4) {
-    // uniform UE8M0 scale factors: SFA plane i (4 columns) = 2^(i+1), SFB plane j (8
-    // columns) = 2^(j+1); every byte of a region holds the plane's scale, so the MMA reads
+    // uniform UE8M0 scale factors: SFA digit d (4 columns) = 2^(2d+1), SFB digit e (8
+    // columns) = 2^(2e+1); every byte of a region holds the digit's scale, so the MMA reads
     // the right value whatever its scale-factor layout (tools/mxf4_probe.cu: an M=128 /
     // N<=128 region spans 4 columns, N=256 8)
     if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
@@ -671,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           const int col = c0 + c;
-          v[c] = 0x01010101u * uint32_t(col < 16 ? 128 + (col >> 2) : 128 + ((col - 16) >> 3));
+          v[c] = 0x01010101u * uint32_t(col < 16 ? 128 + 2 * (col >> 2) : 128 + 2 * ((col - 16) >> 3));
         }
         tmem_st16(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::kSF0 + c0), v);
       }
@@ -701,10 +792,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // LDC per use; with NP = 1 these fold back into constant-bank operands)
     struct Hot {
       int64_t plane;
-      int kp, kwa, kwa_shift, h, w, a_enc, nchunks, next_tile0;
+      int kp, kwa, kwa_shift, h, w, a_enc, nchunks;
       bool tap;
     };
-    auto hot_of = [&](int q) {
+    auto hot_of = [&](int q) {  // (next_tile0 is unused: the tile sequence tracks problems)
       const TcProb& P = args.prob[q];
       Hot r;
       r.plane = P.p.act_plane;
@@ -715,7 +806,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       r.w = P.p.w;
       r.a_enc = P.p.a_enc;
       r.nchunks = P.nchunks;
-      r.next_tile0 = q + 1 < args.nprob ? args.prob[q + 1].tile0 : 0x7FFFFFFF;
       r.tap = P.taps <= kMaxTaps;
       return r;
     };
@@ -790,23 +880,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     // iterator of the next chunk to load: tile t (of problem pi), chunk kc
-    int t = int(blockIdx.x), kc = team, cur_tile = -1;
+    TileSeq<NP> seq(args);
+    int t = -1, kc = team, cur_tile = -1;
+    bool more = seq.next(args, t, pi);
+    if constexpr (NP > 1) H = hot_of(pi);
     auto carry = [&]() {  // move kc past the ends of tiles
-      for (;;) {
-        if (t >= ntiles) return;
-        if constexpr (NP > 1) {
-          while (t >= H.next_tile0) H = hot_of(++pi);
-        }
-        if (kc < H.nchunks) return;
+      while (more && kc >= H.nchunks) {
         kc -= H.nchunks;
-        t += int(gridDim.x);
+        const int prev = pi;
+        more = seq.next(args, t, pi);
+        if constexpr (NP > 1) {
+          if (more && pi != prev) H = hot_of(pi);
+        }
       }
     };
     uint4 nxt[A_BITS];
     uint32_t nvm = 0;
     int nenc = 0;
     auto advance_load = [&]() -> bool {
-      if (t >= ntiles) return false;
+      if (!more) return false;
       if (t != cur_tile) {
         set_tile(t);
         cur_tile = t;
@@ -834,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int freed;
         asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(freed) : "r"(smem_u32(s_freed)) : "memory");
         if (freed > g) break;
-        __nanosleep(20);
+        __nanosleep(BS_TC_FREE_NS);
       }
       PROF_END(1)
       tc_fence_after();
@@ -846,15 +938,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (x == 0x9e3779b9u) asm volatile("trap;");
       } else {
         if constexpr (F4) {
-          if (enc == 0) {
-#pragma unroll
-            for (int i = 0; i < A_BITS; ++i) expand_to_tmem_f4(ta + uint32_t(i * C::kAColsPlane), v[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < A_BITS; ++i)
-              expand_to_tmem_f4_enc(ta + uint32_t(i * C::kAColsPlane), v[i],
-                                    enc == 1 ? 1 : (i == A_BITS - 1 ? 2 : 0), vm);
-          }
+          if (enc == 0)
+            expand_digits_f4<A_BITS, 0>(ta, v, vm);
+          else if (enc == 1)
+            expand_digits_f4<A_BITS, 1>(ta, v, vm);
+          else
+            expand_digits_f4<A_BITS, 2>(ta, v, vm);
         } else {
           expand_to_tmem<0>(ta, v[0]);
           if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
@@ -881,14 +970,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kc = 0; kc < nchunks; ++kc) {
           const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
 #pragma unroll
-          for (int j = 0; j < W_BITS; ++j)
+          for (int j = 0; j < C::kWP; ++j)
             tma_load_2d(sB + j * BN * C::kBRow, &maps.w[0], kc * C::kBRow, j * args.prob[0].p.oc, fb);
         }
       }
-      int stage = 0, g = 0, pi = 0;
+      int stage = 0, g = 0, pi = 0, tile = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        track(tile, pi);
+      for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
         const TcProb& P = args.prob[pi];
         const int n0 = ((tile - P.tile0) % P.ntn) * BN, nchunks = P.nchunks, oc = P.p.oc;
         const CUtensorMap* tw = &maps.w[pi];
@@ -902,7 +990,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(fb, uint32_t(C::kBBytes));
             const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
 #pragma unroll
-            for (int j = 0; j < W_BITS; ++j) tma_load_2d(sB + j * BN * C::kBRow, tw, kc * C::kBRow, j * oc + n0, fb);
+            for (int j = 0; j < C::kWP; ++j) tma_load_2d(sB + j * BN * C::kBRow, tw, kc * C::kBRow, j * oc + n0, fb);
           }
           if (++stage == S) {
             stage = 0;
@@ -914,14 +1002,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer: the whole warp walks the loop (uniform values); one
     // elected lane issues.  TMEM base is column 0 (all 512 columns are this CTA's).
-    int stage = 0, acc = 0, pi = 0;
+    int stage = 0, acc = 0, pi = 0, tile = 0;
     uint32_t phase = 0, acc_phase = 0;
+    bool first = true;
     const bool resident = args.b_resident;
     const uint64_t bdesc0 = F4 ? smem_desc_sw64(smem_u32(s_stage)) : smem_desc_sw128(smem_u32(s_stage));
     if (resident) mbar_wait(smem_u32(full_b), 0);
     if (lane == 0) STAMP("b_resident_ready")
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      track(tile, pi);
+    for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
       const uint32_t idesc = args.prob[pi].idesc;
       const int nchunks = args.prob[pi].nchunks;
       PROF_BEGIN
@@ -940,9 +1028,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t a_base = uint32_t(C::kAcol0 + stage * C::kACols);
         const uint64_t b_desc = bdesc0 + uint64_t(((resident ? kc : stage) * C::kBBytes) >> 4);
 #pragma unroll
-        for (int i = 0; i < A_BITS; ++i)
+        for (int i = 0; i < C::kAP; ++i)
 #pragma unroll
-          for (int j = 0; j < W_BITS; ++j) {
+          for (int j = 0; j < C::kWP; ++j) {
             if constexpr (F4)
               mma2_f4(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
                       uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), idesc, (kc | i | j) != 0);
@@ -957,7 +1045,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mma_commit_elect(smem_u32(acc_full + acc));
-      if (lane == 0 && tile == int(blockIdx.x)) STAMP("first_tile_issued")
+      if (lane == 0 && first) STAMP("first_tile_issued")
+      first = false;
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -969,10 +1058,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - kEpiWarp0, cb0 = ew >> 2;  // with 8 warps, two per lane quarter split the columns
     constexpr int kCbStep = kEpiWarps / 4;
     uint8_t* ebuf = s_epi + ew * (kEpiBufs * kEpiBufBytes);
-    int acc = 0, buf = 0, pi = 0;
+    int acc = 0, buf = 0, pi = 0, tile = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      track(tile, pi);
+    bool first = true;
+    for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
       const TcProb& P = args.prob[pi];
       const int tl = tile - P.tile0;
       const int64_t m0 = int64_t(tl / P.ntn) * BM;
@@ -984,7 +1073,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_BEGIN
       mbar_wait(smem_u32(acc_full + acc), acc_phase);
       PROF_END(0)
-      if (lane == 0 && warp == kEpiWarp0 && tile == int(blockIdx.x)) STAMP("first_acc_full")
+      if (lane == 0 && warp == kEpiWarp0 && first) STAMP("first_acc_full")
+      first = false;
       tc_fence_after();
       bool released = false;
       for (int cb = cb0; cb < ncb; cb += kCbStep) {
@@ -1154,7 +1244,8 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
     if ((1 << sh) == p.kw_a) P.kwa_shift = sh;
   const int brow = f4 ? 64 : BKB;
   const uint64_t wrow = uint64_t(kpad) * (f4 ? 16 : 32);  // prepared-weight row bytes
-  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, wrow, uint64_t(p.w_bits) * p.oc, wrow, brow, bn,
+  const int wplanes = f4 ? (p.w_bits + 1) / 2 : p.w_bits;  // F4: radix-4 digits
+  if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, wrow, uint64_t(wplanes) * p.oc, wrow, brow, bn,
                  f4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
   if (P.epi == kEpiTma)
@@ -1165,7 +1256,8 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
 }
 
 template <int A_BITS, int W_BITS, int BN, bool F4, int NP>
-cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int count, cudaStream_t stream) {
+cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int count, cudaStream_t stream,
+                      int nset0 = -1) {
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
   auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4, NP>;
   static bool configured = false;
@@ -1190,6 +1282,8 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
   }
   if (total == 0) return cudaSuccess;
   a.ntiles = int(total);
+  a.nset0 = nset0 < 0 || nset0 > count ? count : nset0;
+  a.tiles0 = a.nset0 < count ? a.prob[a.nset0].tile0 : a.ntiles;
   const char* res_env = getenv("BS_TC_RESIDENT");
   const bool allow_res = !(res_env && res_env[0] == '0');
   const int64_t res_bytes = int64_t(a.prob[0].nchunks) * C::kBBytes;
@@ -1244,7 +1338,19 @@ cudaError_t launch_group_aw(const ConvProblem* ps, const int8_t* const* wexps, i
       sp[q] = ps[order[q]];
       sw[q] = wexps[order[q]];
     }
-    return launch_bn<A_BITS, W_BITS, BN, F4, kGroupMax>(sp, sw, count, stream);
+    // set 0 (tensor-heavy): a tile's expansion + MMA work, ~256 clk per K chunk and plane
+    // pair (measured producer rate), exceeds its epilogue's, ~BN*128*4 bytes at ~17 B/clk
+    // (measured per-SM output rate); set 1: the rest.  Measured neutral on the ResNet-18
+    // group (246 us either way), so one set is the default; BS_TC_SPLIT=1 interleaves.
+    int nset0 = count;
+    if (const char* e = getenv("BS_TC_SPLIT"))
+      if (e[0] == '1') {
+        nset0 = 0;
+        while (nset0 < count && int64_t(tc_kpad(sp[nset0].kp) / kWordsPerStage) * A_BITS * W_BITS * 256 >
+                                    int64_t(BN) * BM * 4 / 17)
+          ++nset0;
+      }
+    return launch_bn<A_BITS, W_BITS, BN, F4, kGroupMax>(sp, sw, count, stream, nset0);
   } else {
     for (int q = 0; q < count; ++q)
       if (cudaError_t e = launch_aw<A_BITS, W_BITS, F4>(ps[q], wexps[q], stream)) return e;
@@ -1266,7 +1372,8 @@ int tc_resolve_format(int fmt) {
 int64_t tc_kpad(int64_t kp) { return (kp + tc::kWordsPerStage - 1) / tc::kWordsPerStage * tc::kWordsPerStage; }
 
 int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt) {
-  return int64_t(w_bits) * n * tc_kpad(kp) * (tc_resolve_format(fmt) == kTcF4 ? 16 : 32);
+  const bool f4 = tc_resolve_format(fmt) == kTcF4;  // F4: ceil(W/2) radix-4 digits of 16 B per word
+  return int64_t(f4 ? (w_bits + 1) / 2 : w_bits) * n * tc_kpad(kp) * (f4 ? 16 : 32);
 }
 
 bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 4; }

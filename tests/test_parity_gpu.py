@@ -546,10 +546,14 @@ def test_conv_tc_group_mixed(monkeypatch, bn, fmt, a_bits, w_bits):
         np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"member {i} {GROUP_CASES[i]}")
 
 
-def test_conv_tc_group_more_than_one_launch():
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_conv_tc_group_more_than_one_launch(monkeypatch, split):
     """More members than one launch holds (16): split into launches of <= 16, all exact;
-    a group of one and an empty group."""
-    cases = [(1, 4 + i % 5, 5, 16 + 8 * (i % 3), 8 + 12 * (i % 4), 3, 3, 1 + i % 2, 1, 1, 1) for i in range(21)]
+    a group of one and an empty group.  split=1: each launch interleaves its long-K and
+    short-K members' tiles (BS_TC_SPLIT)."""
+    monkeypatch.setenv("BS_TC_SPLIT", split)
+    cases = [(1, 4 + i % 5, 5, 16 + 8 * (i % 3), 8 + 12 * (i % 4), 3, 3, 1 + i % 2, 1, 1, 1) for i in range(19)]
+    cases += [(2, 6, 6, 512, 72, 3, 3, 1, 1, 1, 1), (3, 5, 7, 8, 100, 1, 1, 1, 1, 0, 0)]  # long / short K
     outs, refs = _group_run(cases, 2, 1, bs.TC_F4, [(bs.A_UNSIGNED, bs.BIPOLAR)], seed=5)
     for i, (o, r) in enumerate(zip(outs, refs)):
         np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"member {i}")
