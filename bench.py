@@ -437,6 +437,11 @@ class DenseWorkload:
         kwp = bs.packed_row_words(k)
         self.packed = self.ws[:args.a_bits * (hi - lo) * kwp * 4].view(torch.int32).view(args.a_bits, hi - lo, kwp)
         self.replicas = 1 if gather else world
+        # fused all-gather epilogue: C lives in symmetric memory; each rank's
+        # tensor-core kernel stores its row block into every rank's copy over NVLink
+        self.fused = None
+        if gather and self.tc and args.fused_gather:
+            self.fused = bsdist.FusedGather(m, n, lo, hi, dev)
         self.total_binops = 2 * m * n * k * args.a_bits * args.w_bits * self.replicas
         self.config_id, self.name = config_id, name
         self.graph_ok = not (gather and world > 1)
@@ -450,8 +455,21 @@ class DenseWorkload:
                     + (" + NCCL all-gather of C" if gather else ""),
             "path": "tc" if self.tc else ("gemv" if (hi - lo) <= 8 else "popc"),
         }
+        if self.fused is not None:
+            self.config["parallelism"] = (f"row-sharded tp{world}; all-gather fused into the tensor-core epilogue "
+                                          f"({self.fused.describe()})")
+            self.config["step"] = ("bitpack(A shard) + bs_bitserial_dense_tc_prepared_gather (C row block stored to "
+                                   "every rank's symmetric-memory C) + device barrier")
 
     def step(self):
+        if self.fused is not None:
+            rows = self.rows[1] - self.rows[0]
+            self.bs.bitpack(self.a, self.a_bits, out=self.packed)
+            self.bs.bitserial_dense_tc_gather(self.packed, self.a_bits, self.w_tc, self.w_bits, rows, self.n, self.k,
+                                              self.fused.local_block(), self.fused.peer_blocks(), tc_format=self.fmt,
+                                              w_enc=self.enc)
+            self.fused.barrier()
+            return
         if self.tc:
             self.bs.bitserial_dense_tc_i8(self.a, self.a_bits, self.w_tc, self.w_bits, self.n, out=self.out,
                                           workspace=self.ws, tc_format=self.fmt)
@@ -749,8 +767,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "vs_baseline": None,
-            "dtype": (("u8 codes -> packed u32 bit-planes -> e2m1 0/0.5 planes x ue8m0 2^i scales on tcgen05 "
-                       "kind::mxf4 (fp32 accum, exact) -> i32" if args.tc_format == "f4" else
+            "dtype": (("u8 codes -> packed u32 bit-planes -> radix-4 e2m1 digits (two planes per nibble, 0.5 x {0..3}) x "
+                       "ue8m0 4^d scales on tcgen05 kind::mxf4 (fp32 accum, exact) -> i32" if args.tc_format == "f4" else
                        "u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32")
                       if args.path == "tc" else "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32"),
             "scaling": "weak" if getattr(wl, "replicas", 1) > 1 else "strong",
@@ -852,6 +870,8 @@ def main():
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
     ap.add_argument("--path", choices=["tc", "popc"], default="tc",
                     help="conv/GEMM kernel: tensor-core bitserial (default) or the AND/POPC integer-pipe kernel")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="gemm, N>1: all-gather fused into the tensor-core epilogue over symmetric memory (SURVEY 8 f2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

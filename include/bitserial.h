@@ -261,6 +261,21 @@ int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, int a_e
                                    int w_enc, int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k,
                                    void* stream);
 
+/* Row-sharded dense with the all-gather FUSED into the epilogue (the
+ * multi-GPU GEMM of BASELINE configs[4]): this rank computes its [m][n] row block of C
+ * (as bs_bitserial_dense_tc_prepared) and every staged 32x32 output box is stored to
+ * `out` AND to each out_peers[d] — device pointers, valid in this process, to this
+ * rank's row block inside the other ranks' gathered C buffers (peer memory mapped over
+ * NVLink, e.g. torch symmetric memory or CUDA IPC handles).  The transfer overlaps the
+ * math tile by tile; no separate collective runs.  The caller orders the exchange: all
+ * ranks' launches must complete (a barrier on every rank after the call) before C is
+ * read.  npeers in [0, 8]; npeers > 0 needs n % 4 == 0.  npeers = 0 is exactly
+ * bs_bitserial_dense_tc_prepared. */
+int bs_bitserial_dense_tc_prepared_gather(const uint32_t* a_packed, int a_bits, int a_enc, const int8_t* w_tc,
+                                          int w_bits, int w_enc, int tc_format, int32_t* out,
+                                          int32_t* const* out_peers, int npeers, int64_t m, int64_t n, int64_t k,
+                                          void* stream);
+
 /* Several tensor-core convolutions of one precision in ONE persistent launch (per 16
  * problems): the tiles of all problems form one sequence that the SM-resident CTAs walk,
  * so the per-launch prologue, the pipeline fill and the last-wave tail are paid once

@@ -26,7 +26,7 @@ __all__ = [
     "conv2d_tc_prepare_weights", "dense_tc_prepare_weights", "bitserial_conv2d_nhwc_tc_prepared",
     "bitserial_dense_tc_prepared", "bitserial_conv2d_nhwc_tc_i8", "bitserial_dense_tc_i8",
     "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
-    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group",
+    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group", "bitserial_dense_tc_gather",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
@@ -50,7 +50,7 @@ EXPORTED_SYMBOLS = (
     "bs_conv2d_tc_prepare_weights", "bs_dense_tc_prepare_weights", "bs_bitserial_conv2d_nhwc_tc_prepared",
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
-    "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group",
+    "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitserial_dense_tc_prepared_gather",
 )
 
 
@@ -103,6 +103,7 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
         "bs_bitserial_conv2d_nhwc_tc_group": ([P, I, I, I, I, P], I),
         "bs_bitpack_group": ([P, I, I, P], I),
+        "bs_bitserial_dense_tc_prepared_gather": ([P, I, I, P, I, I, I, P, P, I, L, L, L, P], I),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("BITSERIAL_LIB") and not hasattr(lib, name):
@@ -387,6 +388,21 @@ def bitserial_dense_tc_prepared(a_packed, a_bits, w_tc, w_bits, m, n, k, out=Non
     _check(_load().bs_bitserial_dense_tc_prepared(_dev(a_packed, "a_packed", torch.int32), a_bits, int(a_enc),
                                                   _dev(w_tc, "w_tc", torch.int8), w_bits, int(w_enc), int(tc_format),
                                                   _dev(out, "out", torch.int32), m, n, k, _stream(stream)))
+    return out
+
+
+def bitserial_dense_tc_gather(a_packed, a_bits, w_tc, w_bits, m, n, k, out, peers, tc_format=TC_DEFAULT,
+                              stream=None, a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
+    """bs_bitserial_dense_tc_prepared_gather: this rank's [m][n] row block of C written to
+    `out` and, from the same staged tiles, to every peer block in `peers` (CUDA tensors —
+    e.g. other ranks' symmetric-memory buffers — or raw device addresses)."""
+    ptrs = (ctypes.c_void_p * max(len(peers), 1))()
+    for i, p in enumerate(peers):
+        ptrs[i] = _dev(p, "peer", torch.int32).value if isinstance(p, torch.Tensor) else int(p)
+    _check(_load().bs_bitserial_dense_tc_prepared_gather(
+        _dev(a_packed, "a_packed", torch.int32), a_bits, int(a_enc), _dev(w_tc, "w_tc", torch.int8), w_bits,
+        int(w_enc), int(tc_format), _dev(out, "out", torch.int32), ctypes.cast(ptrs, ctypes.c_void_p), len(peers),
+        m, n, k, _stream(stream)))
     return out
 
 

@@ -481,6 +481,33 @@ int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, int a_e
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream)), fn);
 }
 
+int bs_bitserial_dense_tc_prepared_gather(const uint32_t* a_packed, int a_bits, int a_enc, const int8_t* w_tc,
+                                          int w_bits, int w_enc, int tc_format, int32_t* out,
+                                          int32_t* const* out_peers, int npeers, int64_t m, int64_t n, int64_t k,
+                                          void* stream) {
+  const char* fn = "bs_bitserial_dense_tc_prepared_gather";
+  if (int st = check_format(tc_format, fn)) return st;
+  if (int st = check_tc_enc(a_enc, w_enc, tc_format, fn)) return st;
+  if (int st = check_dense(a_packed, reinterpret_cast<const uint32_t*>(w_tc), out, a_bits, w_bits, BS_UNIPOLAR, m, n,
+                           k, fn))
+    return st;
+  if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (npeers < 0 || npeers > 8) return fail(BS_ERR_INVALID_ARG, "%s: npeers=%d not in [0,8]", fn, npeers);
+  if (npeers > 0 && !out_peers) return fail(BS_ERR_NULL, "%s: NULL out_peers", fn);
+  if (npeers > 0 && n % 4 != 0) return fail(BS_ERR_UNSUPPORTED, "%s: the fused gather needs n %% 4 == 0", fn);
+  for (int d = 0; d < npeers; ++d) {
+    if (!out_peers[d]) return fail(BS_ERR_NULL, "%s: NULL out_peers[%d]", fn, d);
+    if (!aligned16(out_peers[d])) return fail(BS_ERR_ALIGN, "%s: out_peers[%d] must be 16-byte aligned", fn, d);
+  }
+  ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
+  bs::ConvProblem p = make_conv(a_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
+  p.a_enc = a_enc;
+  return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream), out_peers,
+                                                 npeers), fn);
+}
+
 int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, int a_enc, const int8_t* w_tc, int w_bits, int w_enc,
                              int tc_format, int32_t* out, int64_t m, int64_t n, int64_t k, void* workspace,
                              int64_t workspace_bytes, void* stream) {

@@ -75,7 +75,10 @@ bool tc_supported(int a_bits, int w_bits);
 // w_enc: 0 unipolar, 1 bipolar, 2 signed; c_tap elements in each kw_tap-word tap (padding -> 0)
 cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp,
                                      int c_tap, int kw_tap, int8_t* wexp, int fmt, cudaStream_t stream);
-cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream);
+// peers (npeer <= 8): the output is also stored, box by box from the same staged tile, to
+// these [M][oc] blocks (other ranks' gathered buffers mapped over NVLink): a fused all-gather.
+cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream,
+                                    int32_t* const* peers = nullptr, int npeer = 0);
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream);
 // Several problems of one (a_bits, w_bits) in one persistent launch per 16 problems.
 cudaError_t launch_tc_conv_group(const ConvProblem* ps, const int8_t* const* wexps, int count, int fmt,

@@ -82,6 +82,7 @@ constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMinSmem = 116 * 1024;  // > half the SM: guarantees one CTA per SM (TMEM)
 constexpr int kMaxTaps = 64;          // filter taps held in the shared-memory tap table
 constexpr int kGroupMax = 16;         // problems in one grouped launch
+constexpr int kMaxPeers = 8;          // extra destinations of a fused all-gather epilogue
 
 // BS_TC_PROFILE builds (tools only) count cycles spent in each role's waits and print
 // them per CTA 0 at exit; the product build compiles these to nothing.
@@ -622,6 +623,7 @@ struct TcArgs {
                       // (output-heavy) [tiles0, ntiles); each CTA interleaves its tiles of the two sets
   int b_resident;     // single problem, ntn == 1 and the whole expanded B fits: loaded once
   int b_bytes;        // bytes of the B region (resident: nchunks stages, else kStages)
+  int npeer;          // single-problem launches: every output box is also stored through peer[0..npeer)
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                       // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
                       // 4 MMA warp ignores full_a, 5 producers idle (timing experiments; results are wrong)
@@ -631,6 +633,7 @@ template <int NP>
 struct TcMaps {
   CUtensorMap w[NP];    // prepared weights [W][oc][kpad bytes]
   CUtensorMap out[NP];  // int32 output [M][oc] (TMA-store epilogue)
+  CUtensorMap peer[NP == 1 ? kMaxPeers : 1];  // fused all-gather: the same [M][oc] block in other ranks' buffers
 };
 #if defined(BS_TC_PROFILE) || defined(BS_TC_KNOBS)
 #define DBG(bit) (args.debug & (1 << (bit)))
@@ -1131,7 +1134,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&maps.out[pi], n0 + cb * 32, int(m0) + q * 32, smem_u32(ebuf + buf * kEpiBufBytes));
+            const uint32_t sbox = smem_u32(ebuf + buf * kEpiBufBytes);
+            tma_store_2d(&maps.out[pi], n0 + cb * 32, int(m0) + q * 32, sbox);
+            if constexpr (NP == 1)  // fused all-gather: the same staged box to every peer copy (NVLink)
+              for (int d = 0; d < args.npeer; ++d) tma_store_2d(&maps.peer[d], n0 + cb * 32, int(m0) + q * 32, sbox);
             bulk_commit();
           }
           PROF_END(3)
@@ -1257,7 +1263,7 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
 
 template <int A_BITS, int W_BITS, int BN, bool F4, int NP>
 cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int count, cudaStream_t stream,
-                      int nset0 = -1) {
+                      int nset0 = -1, int32_t* const* peers = nullptr, int npeer = 0) {
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
   auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4, NP>;
   static bool configured = false;
@@ -1283,6 +1289,15 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
   if (total == 0) return cudaSuccess;
   a.ntiles = int(total);
   a.nset0 = nset0 < 0 || nset0 > count ? count : nset0;
+  if (npeer > 0) {  // fused all-gather (single problem, TMA-store epilogue)
+    if (NP != 1 || npeer > kMaxPeers || a.prob[0].epi != kEpiTma) return cudaErrorNotSupported;
+    const ConvProblem& p = ps[0];
+    for (int d = 0; d < npeer; ++d)
+      if (!encode_2d(&maps.peer[d], CU_TENSOR_MAP_DATA_TYPE_INT32, peers[d], uint64_t(p.oc), uint64_t(p.M),
+                     uint64_t(p.oc) * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+  }
+  a.npeer = npeer;
   a.tiles0 = a.nset0 < count ? a.prob[a.nset0].tile0 : a.ntiles;
   const char* res_env = getenv("BS_TC_RESIDENT");
   const bool allow_res = !(res_env && res_env[0] == '0');
@@ -1310,14 +1325,15 @@ inline int pick_bn(const ConvProblem& p) {
 }
 
 template <int A_BITS, int W_BITS, bool F4>
-cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream) {
+cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream, int32_t* const* peers = nullptr,
+                      int npeer = 0) {
   switch (pick_bn(p)) {
     case 128:
       if constexpr (Cfg<A_BITS, W_BITS, 128, F4>::kFit >= 2)
-        return launch_bn<A_BITS, W_BITS, 128, F4, 1>(&p, &wexp, 1, stream);
+        return launch_bn<A_BITS, W_BITS, 128, F4, 1>(&p, &wexp, 1, stream, -1, peers, npeer);
       [[fallthrough]];
     default:
-      return launch_bn<A_BITS, W_BITS, 64, F4, 1>(&p, &wexp, 1, stream);
+      return launch_bn<A_BITS, W_BITS, 64, F4, 1>(&p, &wexp, 1, stream, -1, peers, npeer);
   }
 }
 
@@ -1401,12 +1417,14 @@ cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w
   BS_TC(3, 3, CALL) BS_TC(4, 3, CALL) BS_TC(1, 4, CALL) BS_TC(2, 4, CALL) BS_TC(3, 4, CALL)           \
   BS_TC(4, 4, CALL)
 
-cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream) {
+cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream,
+                                    int32_t* const* peers, int npeer) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
   const bool f4 = tc_resolve_format(fmt) == kTcF4;
-#define BS_TC(A, W, CALL)                                                   \
-  if (p.a_bits == A && p.w_bits == W)                                       \
-    return f4 ? tc::launch_aw<A, W, true>(p, wexp, stream) : tc::launch_aw<A, W, false>(p, wexp, stream);
+#define BS_TC(A, W, CALL)                                                                 \
+  if (p.a_bits == A && p.w_bits == W)                                                     \
+    return f4 ? tc::launch_aw<A, W, true>(p, wexp, stream, peers, npeer)                  \
+              : tc::launch_aw<A, W, false>(p, wexp, stream, peers, npeer);
   BS_TC_DISPATCH(0)
 #undef BS_TC
   return cudaErrorNotSupported;

@@ -73,3 +73,44 @@ def gather_rows(out_full: torch.Tensor, shard: torch.Tensor):
         parts = list(out_full.chunk(world, dim=0))
         dist.all_gather(parts, shard)
     return out_full
+
+
+class FusedGather:
+    """Buffers of the fused all-gather epilogue: the gathered C [m][n] in
+    torch symmetric memory on every rank; this rank's kernel stores its row block
+    [lo, hi) into its own copy (local_block) and, over NVLink, into every peer's copy
+    (peer_blocks: peer memory mapped into this process); barrier() orders the exchange
+    (a device-side barrier on the current stream).  With one process there are no peers
+    and C is an ordinary tensor."""
+
+    def __init__(self, m: int, n: int, lo: int, hi: int, device):
+        self.lo, self.hi, self.peers, self.handle = lo, hi, [], None
+        world = dist.get_world_size() if dist.is_initialized() else 1
+        if world == 1:
+            self.full = torch.empty((m, n), dtype=torch.int32, device=device)
+            return
+        import torch.distributed._symmetric_memory as symm_mem
+        self.full = symm_mem.empty((m, n), dtype=torch.int32, device=device)
+        self.handle = symm_mem.rendezvous(self.full, dist.group.WORLD.group_name)
+        rank = dist.get_rank()
+        self.peers = [self.handle.get_buffer(p, (m, n), torch.int32)[lo:hi] for p in peer_ranks(rank, world)]
+
+    def local_block(self):
+        return self.full[self.lo:self.hi]
+
+    def peer_blocks(self):
+        return self.peers
+
+    def barrier(self):
+        if self.handle is not None:
+            self.handle.barrier(channel=0)
+
+    def describe(self):
+        return (f"torch symmetric memory, {len(self.peers)} peer copies written by the kernel"
+                if self.handle is not None else "one process: no peers")
+
+
+def peer_ranks(rank: int, world: int):
+    """The ranks whose C copies this rank writes besides its own (all others, in ring
+    order starting after `rank` so the ranks' NVLink stores spread over destinations)."""
+    return [(rank + d) % world for d in range(1, world)]

@@ -176,3 +176,17 @@ def test_bitpack_group_validation(lib):
     assert lib.bs_bitpack_group(p, 2, 2, NULL) == 4
     arr[1].k, arr[1].out = 64, (1 << 21) + 4
     assert lib.bs_bitpack_group(p, 2, 2, NULL) == 5
+
+
+def test_dense_gather_validation(lib):
+    import ctypes
+    peers = (ctypes.c_void_p * 9)(*([1 << 20] * 9))
+    pp = ctypes.cast(peers, ctypes.c_void_p)
+    f = lib.bs_bitserial_dense_tc_prepared_gather
+    assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, pp, 9, 16, 16, 64, NULL) == 2   # npeers > 8
+    assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, NULL, 2, 16, 16, 64, NULL) == 1  # NULL peer list
+    assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, pp, 2, 16, 18, 64, NULL) == 3   # n % 4 != 0
+    peers[1] = (1 << 20) + 4
+    assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, pp, 2, 16, 16, 64, NULL) == 5   # misaligned peer
+    peers[1] = 0
+    assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, pp, 2, 16, 16, 64, NULL) == 1   # NULL peer

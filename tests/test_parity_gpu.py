@@ -601,3 +601,26 @@ def test_bitpack_group_parity():
         for x, o in zip(xs, outs):
             np.testing.assert_array_equal(o.cpu().numpy().view(np.uint32), oracle.bitpack(x.numpy(), bits))
     assert bs.bitpack_group([], 2) == []
+
+
+# ------------------------------- fused all-gather epilogue, one GPU
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+@pytest.mark.parametrize("m,n,k,npeers", [(300, 256, 1000, 2), (128, 64, 64, 1), (257, 132, 4096, 7)])
+def test_dense_tc_fused_gather(fmt, m, n, k, npeers):
+    """bs_bitserial_dense_tc_prepared_gather as rank 1 of npeers+1 ranks simulated on one
+    GPU: the rank's row block of C lands in its own gathered buffer and, from the same
+    staged tiles, in every peer's buffer at the same rows; other rows are untouched."""
+    world, rank = npeers + 1, 1
+    a, w = inputs.dense_operands(m, n, k, 2, 1, seed=m + n + k + npeers)
+    ref = oracle.dense(a.numpy(), 2, w.numpy(), 1, True)
+    w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, 1), 1, bs.BIPOLAR, n, k, tc_format=fmt)
+    fulls = [torch.full((world * m, n), -7, dtype=torch.int32, device=DEV) for _ in range(world)]
+    blk = slice(rank * m, (rank + 1) * m)
+    peers = [fulls[r][blk] for r in range(world) if r != rank]
+    bs.bitserial_dense_tc_gather(gpu_pack(a, 2), 2, w_tc, 1, m, n, k, fulls[rank][blk], peers, tc_format=fmt,
+                                 w_enc=bs.BIPOLAR)
+    torch.cuda.synchronize()
+    for r, f in enumerate(fulls):
+        f = f.cpu().numpy()
+        np.testing.assert_array_equal(f[blk], ref, err_msg=f"buffer of rank {r}")
+        assert (f[:rank * m] == -7).all() and (f[(rank + 1) * m:] == -7).all()
