@@ -676,36 +676,43 @@ def run_ours(args):
     r_popc = 64.0 * POPC_PER_CLK_PER_SM * sms * f_max * 1e6 / 1e12
     r_int = 2.0 * r_popc
     if roof["kind"] == "tensor":
-        # binary dot products on the tensor cores: one binary MAC = one MAC of the MMA kind
-        # in use.  FP4 (kind::mxf4, the default format): peak = 4 x the measured bf16 peak
-        # (B200_PROFILING.md nominal 9 vs 2.25 PFLOP/s); I8 (kind::i8): 2 x (measured with
-        # tools/mma_bench.cu: kind::i8 sustains exactly 2x the kind::f16 MACs per clock).
-        # Burst figure (each kernel timed alone).
+        # binary dot products on the tensor cores.  I8 (kind::i8): one binary MAC per MMA MAC
+        # (bit planes), peak = 2 x the measured bf16 peak (tools/mma_bench.cu: kind::i8
+        # sustains exactly 2x the kind::f16 MACs per clock).  FP4 (kind::mxf4, default):
+        # peak = 4 x bf16 (B200_PROFILING.md nominal 9 vs 2.25 PFLOP/s) and one MMA MAC
+        # multiplies two radix-4 digits, i.e. A*W / (ceil(A/2)*ceil(W/2)) binary MACs, so the
+        # tensor roofline is stated in MMA ops (= binary ops x digits/planes).  Burst figure.
         f4 = args.tc_format != "i8"
         ratio = 4.0 if f4 else 2.0
         peak = ratio * peaks["bf16_tflops"]
         hbm = peaks["hbm_gbs"]
-        achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
+        mma_per_bin = (((args.a_bits + 1) // 2) * ((args.w_bits + 1) // 2) / (args.a_bits * args.w_bits)) if f4 else 1.0
+        achieved = roof["ops"] * mma_per_bin / (roof["ms"] / 1e3) / 1e12
         sustained = ratio * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         # time model: each launch is bound by max(tensor time, HBM time of its algorithmic
         # bytes) — the int32 outputs (4 bytes per output) make the 1x1 and early layers
         # HBM-bound; the primary "bound" is the one that dominates summed over the launches
-        t_tensor = roof["ops"] / (peak * 1e12) * 1e3
+        t_tensor = roof["ops"] * mma_per_bin / (peak * 1e12) * 1e3
         t_hbm = roof["bytes"] / (hbm * 1e9) * 1e3
         per = roof.get("per_layer", [])
-        t_roof = sum(max(x["binops"] / (peak * 1e12), x["bytes"] / (hbm * 1e9)) * 1e3 for x in per) if per else \
+        t_roof = sum(max(x["binops"] * mma_per_bin / (peak * 1e12), x["bytes"] / (hbm * 1e9)) * 1e3 for x in per) \
+            if per else \
             max(t_tensor, t_hbm)
         model = {"t_tensor_ms": t_tensor, "t_hbm_ms": t_hbm, "t_roof_ms": t_roof, "t_actual_ms": roof["ms"],
                  "frac": t_roof / roof["ms"],
                  "per_layer": [{"layer": x.get("layer", x.get("layers")), "t_us": 1e3 * x["ms"],
-                                "t_tensor_us": 1e6 * x["binops"] / (peak * 1e12),
+                                "t_tensor_us": 1e6 * x["binops"] * mma_per_bin / (peak * 1e12),
                                 "t_hbm_us": 1e6 * x["bytes"] / (hbm * 1e9)} for x in per]}
         common = {"kernel": roof["kernel"], "traffic": None,
-                  "mma_kind": "kind::mxf4 (E2M1 bits, UE8M0 plane scales, FP32 accum)" if f4 else
+                  "mma_kind": "kind::mxf4 (E2M1 radix-4 digits, UE8M0 digit scales, FP32 accum)" if f4 else
                               "kind::i8 (0/1 bytes, int32 accum)",
-                  "tensor": {"achieved": achieved, "peak": peak, "unit": "binary TOPS", "frac": achieved / peak,
+                  "tensor": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "unit_note": "MMA ops (2 x FP4 or I8 MACs)", "frac": achieved / peak,
+                             "binary_tops": roof["ops"] / (roof["ms"] / 1e3) / 1e12,
+                             "mma_ops_per_binary_op": mma_per_bin,
                              "peak_basis": f"{'FP4' if f4 else 'INT8'} dense tensor peak = {ratio:.0f} x bf16_tflops "
-                                           f"({peaks['bf16_tflops']:.1f}, {peaks_src}); 1 binary MAC = 1 MMA MAC",
+                                           f"({peaks['bf16_tflops']:.1f}, {peaks_src}); "
+                                           + ("1 MMA MAC = 1 radix-4 digit pair = A*W/(ceil(A/2)*ceil(W/2)) binary MACs"
+                                              if f4 else "1 binary MAC = 1 MMA MAC"),
                              "peak_sustained": sustained, "frac_sustained": achieved / sustained,
                              "frac_of_int8_peak": achieved / (2.0 * peaks["bf16_tflops"]),
                              "peak_nominal": 9000.0 if f4 else 4500.0,
@@ -720,7 +727,7 @@ def run_ours(args):
             roofline = dict(common, bound="hbm", achieved=common["hbm"]["achieved"], peak=hbm, unit="GB/s",
                             frac=common["hbm"]["frac"], peak_basis=f"HBM copy bandwidth, {peaks_src}")
         else:
-            roofline = dict(common, bound="tensor", achieved=achieved, peak=peak, unit="binary TOPS",
+            roofline = dict(common, bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
                             frac=achieved / peak, peak_basis=common["tensor"]["peak_basis"])
     elif roof["kind"] == "alu":
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
