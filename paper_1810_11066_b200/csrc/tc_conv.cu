@@ -789,6 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kTeams = C::kTeamsUsed;
     const int team = warp >> 2, arow = tid & (BM - 1);
     int pi = 0;  // problem of the chunk being loaded
+    const uint32_t s_tap_u32 = smem_u32(s_tap);
 #define LP args.prob[pi].p
     // the loaded problem's per-chunk fields in registers, refreshed when the problem
     // changes (grouped launches: a parameter indexed by a run-time problem number costs an
@@ -828,8 +829,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t oy = P.div_ow.div(rem), ox = rem - oy * P.div_ow.d;
       iy0 = int(oy) * P.p.sh - P.p.ph;
       ix0 = int(ox) * P.p.sw - P.p.pw;
-      rbase = P.p.act + int64_t(b) * P.p.h * P.p.w * P.p.kw_a;
-      rorg = rbase + (int64_t(iy0) * P.p.w + ix0) * P.p.kw_a;
+      // pixel index of the receptive-field origin in 32-bit arithmetic (N*H*W < 2^31,
+      // ABI-checked; the origin may lie in the padding, i.e. slightly negative)
+      const int img = int(b) * H.h;
+      rbase = P.p.act + int64_t(img * H.w) * H.kwa;
+      rorg = P.p.act + int64_t((img + iy0) * H.w + ix0) * H.kwa;
     };
     // source of the 2- or 4-word piece starting at filter word kk (kk even)
     auto piece = [&](int kk, bool& ok) -> const uint32_t* {
@@ -843,7 +847,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         cw = kk - tap * kwa;
       }
       if (H.tap) {
-        const int2 e = s_tap[pi * kMaxTaps + (tap < kMaxTaps ? tap : 0)];
+        int2 e;  // explicit shared-space load (a generic load would take the long-scoreboard path)
+        asm("ld.shared.v2.s32 {%0, %1}, [%2];"
+                     : "=r"(e.x), "=r"(e.y)
+                     : "r"(s_tap_u32 + uint32_t(8 * (pi * kMaxTaps + (tap < kMaxTaps ? tap : 0)))));
         const int iy = iy0 + (e.y >> 16), ix = ix0 + (e.y & 0xFFFF);
         ok = rok && kk < H.kp && unsigned(iy) < unsigned(H.h) && unsigned(ix) < unsigned(H.w);
         return rorg + e.x + cw;
