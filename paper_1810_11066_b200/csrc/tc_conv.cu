@@ -60,6 +60,7 @@ constexpr int kWordsPerStage = BKB / 32;  // 4 packed words per plane per row
 constexpr int kTeams = BS_TC_TEAMS;                    // producer teams (K chunks in flight)
 constexpr int kProducerWarps = 4 * kTeams;             // a team = 4 warps = one thread per row
 constexpr int kProducerThreads = kProducerWarps * 32;
+constexpr int kBarBytes = 512;  // mbarriers (3 per stage + 4), the "chunks freed" counter
 #ifndef BS_TC_MAX_STAGES
 #define BS_TC_MAX_STAGES 8
 #endif
@@ -564,7 +565,7 @@ struct Cfg {
   static constexpr int kACols = kAP * kAColsPlane;        // TMEM columns of one stage's A planes
   static constexpr int kBBytes = kWP * BN * kBRow;        // shared memory per stage (B only)
   static constexpr int kSFCols = F4 ? 16 + 8 * kWP : 0;   // SFA: up to 4 x 4 cols; SFB: kWP x 8
-  static constexpr int kFixed = 1024 /*align slack*/ + 256 /*barriers*/ + NP * 512 /*tap tables*/ + kEpiBytes;
+  static constexpr int kFixed = 1024 /*align slack*/ + kBarBytes + NP * 512 /*tap tables*/ + kEpiBytes;
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
@@ -702,9 +703,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 3 * S;
   uint64_t* acc_empty = bars + 3 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
-  int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [NP][kMaxTaps] {offset, ky<<16|kx}
-  int* s_freed = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 240);   // chunks whose stage is free
-  static_assert(8 * (3 * S + 4) + 4 <= 240, "barrier region");
+  int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // [NP][kMaxTaps] {offset, ky<<16|kx}
+  int* s_freed = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes - 16);  // chunks whose stage is free
+  static_assert(8 * (3 * S + 4) + 4 <= kBarBytes - 16, "barrier region");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (lane == 0 && (warp == 0 || warp == kMmaWarp)) STAMP("start")
@@ -924,12 +925,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool have = advance_load();
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
     for (int g = team; have; g += kTeams) {
+      PROF_BEGIN  // slot 0: this step's words landed (copy) + next step's address math and loads
       uint4 v[A_BITS];
 #pragma unroll
       for (int i = 0; i < A_BITS; ++i) v[i] = nxt[i];
       const uint32_t vm = nvm;
       const int enc = nenc;
       have = advance_load();  // next step's words in flight during this step's expansion
+#ifdef BS_TC_PROFILE
+      if (v[0].x == 0x9e3779b9u && v[0].y == 0x7f4a7c15u) _pacc[0] += 1;  // first use of the loaded words
+#endif
+      PROF_END(0)
       const int stage = g % S;
       PROF_BEGIN
       for (;;) {  // stage of chunk g free (published in chunk order by the TMA warp)
@@ -940,6 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       PROF_END(1)
       tc_fence_after();
+      PROF_BEGIN  // slot 2: digit formation + tcgen05.st issue
       const uint32_t ta = lane_base + uint32_t(C::kAcol0 + stage * C::kACols);
       if (DBG(1)) {
         uint32_t x = 0;
@@ -961,7 +968,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
         }
       }
+      PROF_END(2)
+      PROF_BEGIN  // slot 3: tensor-memory store completion
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      PROF_END(3)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(full_a + stage));
