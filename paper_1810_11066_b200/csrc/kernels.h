@@ -68,7 +68,7 @@ cudaError_t launch_popc_conv(const ConvProblem& p, Algo algo, cudaStream_t strea
 constexpr int kTcI8 = 1, kTcF4 = 2;
 constexpr int kTcDefault = kTcF4;
 int tc_resolve_format(int fmt);
-int64_t tc_kpad(int64_t kp);
+int64_t tc_kpad(int64_t kp, int fmt);  // K words rounded to the format's chunk (I8 4, FP4 8)
 int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt);
 bool tc_supported(int a_bits, int w_bits);
 // expanded ("prepared") weights: [w_bits][n][tc_kpad(kp)*(32 | 16)] bytes, offline like packing

@@ -52,8 +52,11 @@ namespace bs {
 namespace tc {
 
 constexpr int BM = 128;                   // UMMA M (cta_group::1): output rows per tile
-constexpr int BKB = 128;                  // K bytes per stage = one 128B swizzle row
-constexpr int kWordsPerStage = BKB / 32;  // 4 packed words per plane per row
+constexpr int BKB = 128;                  // B bytes per row per plane per stage = one 128B swizzle row
+// packed words per plane per row in one stage (K chunk): I8 4 (32 bytes per word),
+// FP4 8 (16 bytes per word: a 256-element chunk, so each stage's fixed producer / MMA-issue
+// cost is spread over four K=64 MMAs per digit pair)
+constexpr int chunk_words(bool f4) { return f4 ? 8 : 4; }
 #ifndef BS_TC_TEAMS
 #define BS_TC_TEAMS 4
 #endif
@@ -416,20 +419,23 @@ __device__ __forceinline__ void expand_digit_f4(uint32_t taddr, uint4 lo, uint4 
 
 // Every digit of one chunk: digit D holds planes 2D, 2D+1; with MODE 2 (signed) only the
 // digit holding plane A-1 uses the signed rule.
-template <int A_BITS, int MODE, int D = 0>
-__device__ __forceinline__ void expand_digits_f4(uint32_t ta, const uint4 (&v)[A_BITS], uint32_t valid) {
+template <int A_BITS, int MODE, int KQ, int D = 0>
+__device__ __forceinline__ void expand_digits_f4(uint32_t ta, const uint4 (&v)[A_BITS][KQ], uint32_t valid) {
   if constexpr (2 * D < A_BITS) {
     constexpr bool kHi = 2 * D + 1 < A_BITS;
     constexpr bool kTop = 2 * D + 2 >= A_BITS;
     constexpr int kMode = (MODE == 2 && !kTop) ? 0 : MODE;
-    expand_digit_f4<kMode, kHi>(ta + uint32_t(D * 16), v[2 * D], v[kHi ? 2 * D + 1 : 2 * D], valid);
-    expand_digits_f4<A_BITS, MODE, D + 1>(ta, v, valid);
+#pragma unroll
+    for (int q = 0; q < KQ; ++q)  // digit D's 32 columns per stage: 16 per 4-word group
+      expand_digit_f4<kMode, kHi>(ta + uint32_t(D * 32 + q * 16), v[2 * D][q], v[kHi ? 2 * D + 1 : 2 * D][q],
+                                  valid >> (2 * q));
+    expand_digits_f4<A_BITS, MODE, KQ, D + 1>(ta, v, valid);
   }
 }
 
-// The 2 K-steps (64 elements = 8 TMEM columns / 32 bytes of B each) of one plane pair in
-// one 128-element chunk, kind::mxf4 with per-plane scale-factor regions in TMEM.
-__device__ __forceinline__ void mma2_f4(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t idesc,
+// The 4 K-steps (64 elements = 8 TMEM columns / 32 bytes of a 128B-swizzled B row each)
+// of one digit pair in one 256-element FP4 chunk.
+__device__ __forceinline__ void mma4_f4(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
@@ -437,6 +443,10 @@ __device__ __forceinline__ void mma2_f4(uint32_t d, uint32_t a, uint64_t b, uint
       "setp.ne.b32 p, %3, 0;\n"
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
       "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
       "}" ::"r"(d),
       "r"(a), "l"(b), "r"(accumulate), "r"(idesc), "r"(sfa), "r"(sfb));
@@ -448,17 +458,6 @@ inline uint32_t idesc_mxf4(int n) {
   return (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
 }
 
-// 64B-swizzled K-major UMMA descriptor (FP4 B tiles: 64-byte rows of 128 elements):
-// SBO = 8 rows x 64 B = 512 B, layout type 4 = SWIZZLE_64B; base 512-byte aligned.
-__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= uint64_t((saddr >> 4) & 0x3FFF);
-  d |= uint64_t(1) << 16;
-  d |= uint64_t(512 >> 4) << 32;
-  d |= uint64_t(1) << 46;
-  d |= uint64_t(4) << 61;
-  return d;
-}
 
 // ------------------------------------------------------------------ weight expansion
 // w_packed [W][N][kp] words -> wexp [W][N][kpad*32] bytes (kpad = kp rounded up to
@@ -552,16 +551,19 @@ __global__ void __launch_bounds__(256) expand_weights_f4_kernel(const uint32_t* 
 }
 
 // ----------------------------------------------------------------------- main kernel
-// F4 = false: kind::i8 (bytes, 128-byte B rows, SWIZZLE_128B); F4 = true: kind::mxf4
-// (packed E2M1, 64-byte B rows, SWIZZLE_64B, scale-factor regions in TMEM).  A chunk is
-// 128 K elements (4 packed words per plane per row) in both formats.
+// F4 = false: kind::i8 (bytes; a chunk = 128 K elements = 4 packed words per plane and
+// row); F4 = true: kind::mxf4 (packed E2M1 radix-4 digits, scale-factor regions in TMEM;
+// a chunk = 256 K elements = 8 packed words).  Both: 128-byte B rows, SWIZZLE_128B, 32
+// TMEM columns per plane / digit per stage, four K-steps per plane / digit pair.
 template <int A_BITS, int W_BITS, int BN, bool F4, int NP = 1>
 struct Cfg {
   // operand "planes": bit planes (I8), radix-4 digits of two bit planes (F4, digit_nibbles)
   static constexpr int kAP = F4 ? (A_BITS + 1) / 2 : A_BITS;
   static constexpr int kWP = F4 ? (W_BITS + 1) / 2 : W_BITS;
-  static constexpr int kBRow = F4 ? 64 : BKB;             // B bytes per row per plane per stage
-  static constexpr int kAColsPlane = F4 ? 16 : BKB / 4;    // TMEM columns per plane per stage
+  static constexpr int kCW = chunk_words(F4);             // packed words per plane per row per stage
+  static constexpr int kQ = kCW / 4;                      // 4-word groups per stage
+  static constexpr int kBRow = BKB;                       // B bytes per row per plane per stage (128B swizzle)
+  static constexpr int kAColsPlane = 32;                  // TMEM columns per plane / digit per stage
   static constexpr int kACols = kAP * kAColsPlane;        // TMEM columns of one stage's A planes
   static constexpr int kBBytes = kWP * BN * kBRow;        // shared memory per stage (B only)
   static constexpr int kSFCols = F4 ? 16 + 8 * kWP : 0;   // SFA: up to 4 x 4 cols; SFB: kWP x 8
@@ -862,31 +864,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       ok = rok && kk < H.kp && unsigned(iy) < unsigned(H.h) && unsigned(ix) < unsigned(H.w);
       return rbase + (int64_t(iy) * H.w + ix) * kwa + cw;
     };
-    auto load = [&](int kc, uint4 (&v)[A_BITS], uint32_t& vm) {
+    // one chunk's kCW words per plane of this thread's row, as kQ uint4 groups; vm bit p =
+    // 2-word piece p valid (padding / K tail pieces load as 0)
+    constexpr int kQ = C::kQ;
+    auto load = [&](int kc, uint4 (&v)[A_BITS][kQ], uint32_t& vm) {
       if (DBG(3)) {  // timing experiment: no global loads
 #pragma unroll
-        for (int i = 0; i < A_BITS; ++i) v[i] = make_uint4(kc, i, arow, 7);
-        vm = 3u;
+        for (int i = 0; i < A_BITS; ++i)
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) v[i][q] = make_uint4(kc, i, arow, q);
+        vm = 0xFu;
         return;
       }
       const int64_t plane = H.plane;
-      const int kk = kc * kWordsPerStage;
-      bool ok0;
-      const uint32_t* s0 = piece(kk, ok0);
-      vm = ok0 ? 3u : 0u;  // validity of the two 2-word pieces (padding / K tail -> 0)
-      if ((H.kwa & 3) == 0) {
+      const int kk0 = kc * C::kCW;
+      vm = 0u;
+      if (kQ == 2 && (H.kwa & 7) == 0) {  // the 8 words lie in one tap
+        bool ok;
+        const uint32_t* s0 = piece(kk0, ok);
+        vm = ok ? 0xFu : 0u;
 #pragma unroll
         for (int i = 0; i < A_BITS; ++i)
-          v[i] = ok0 ? ldg_nc_v4(s0 + i * plane) : make_uint4(0u, 0u, 0u, 0u);
-      } else {  // a 4-word group spans two taps (Cw = 2 mod 4)
-        bool ok1;
-        const uint32_t* s1 = piece(kk + 2, ok1);
-        vm = (ok0 ? 1u : 0u) | (ok1 ? 2u : 0u);
 #pragma unroll
-        for (int i = 0; i < A_BITS; ++i) {
-          const uint2 lo = ok0 ? ldg_nc_v2(s0 + i * plane) : make_uint2(0u, 0u);
-          const uint2 hi = ok1 ? ldg_nc_v2(s1 + i * plane) : make_uint2(0u, 0u);
-          v[i] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+          for (int q = 0; q < kQ; ++q)
+            v[i][q] = ok ? ldg_nc_v4(s0 + i * plane + 4 * q) : make_uint4(0u, 0u, 0u, 0u);
+      } else if ((H.kwa & 3) == 0) {  // 4-word groups, each in one tap
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          bool ok;
+          const uint32_t* s0 = piece(kk0 + 4 * q, ok);
+          vm |= ok ? 3u << (2 * q) : 0u;
+#pragma unroll
+          for (int i = 0; i < A_BITS; ++i) v[i][q] = ok ? ldg_nc_v4(s0 + i * plane) : make_uint4(0u, 0u, 0u, 0u);
+        }
+      } else {  // Cw = 2 mod 4: 2-word pieces, a tap boundary inside every 4-word group
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          bool ok0, ok1;
+          const uint32_t* s0 = piece(kk0 + 4 * q, ok0);
+          const uint32_t* s1 = piece(kk0 + 4 * q + 2, ok1);
+          vm |= ((ok0 ? 1u : 0u) | (ok1 ? 2u : 0u)) << (2 * q);
+#pragma unroll
+          for (int i = 0; i < A_BITS; ++i) {
+            const uint2 lo = ok0 ? ldg_nc_v2(s0 + i * plane) : make_uint2(0u, 0u);
+            const uint2 hi = ok1 ? ldg_nc_v2(s1 + i * plane) : make_uint2(0u, 0u);
+            v[i][q] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+          }
         }
       }
     };
@@ -905,7 +928,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
-    uint4 nxt[A_BITS];
+    uint4 nxt[A_BITS][kQ];
     uint32_t nvm = 0;
     int nenc = 0;
     auto advance_load = [&]() -> bool {
@@ -925,17 +948,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool have = advance_load();
     const uint32_t lane_base = tmem + (uint32_t((warp & 3) * 32) << 16);
     for (int g = team; have; g += kTeams) {
-      PROF_BEGIN  // slot 0: this step's words landed (copy) + next step's address math and loads
-      uint4 v[A_BITS];
-#pragma unroll
-      for (int i = 0; i < A_BITS; ++i) v[i] = nxt[i];
+      // one register buffer: this step expands nxt, then reloads it with the next step's
+      // words, whose latency is covered by the tensor-memory store wait, the barrier
+      // arrive and the next stage-free wait (two buffers would spill at 8 words per plane)
+      uint4 (&v)[A_BITS][kQ] = nxt;
       const uint32_t vm = nvm;
       const int enc = nenc;
-      have = advance_load();  // next step's words in flight during this step's expansion
-#ifdef BS_TC_PROFILE
-      if (v[0].x == 0x9e3779b9u && v[0].y == 0x7f4a7c15u) _pacc[0] += 1;  // first use of the loaded words
-#endif
-      PROF_END(0)
       const int stage = g % S;
       PROF_BEGIN
       for (;;) {  // stage of chunk g free (published in chunk order by the TMA warp)
@@ -951,24 +969,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (DBG(1)) {
         uint32_t x = 0;
 #pragma unroll
-        for (int i = 0; i < A_BITS; ++i) x ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
+        for (int i = 0; i < A_BITS; ++i) x ^= v[i][0].x ^ v[i][0].y ^ v[i][kQ - 1].z ^ v[i][kQ - 1].w;
         if (x == 0x9e3779b9u) asm volatile("trap;");
       } else {
         if constexpr (F4) {
           if (enc == 0)
-            expand_digits_f4<A_BITS, 0>(ta, v, vm);
+            expand_digits_f4<A_BITS, 0, kQ>(ta, v, vm);
           else if (enc == 1)
-            expand_digits_f4<A_BITS, 1>(ta, v, vm);
+            expand_digits_f4<A_BITS, 1, kQ>(ta, v, vm);
           else
-            expand_digits_f4<A_BITS, 2>(ta, v, vm);
+            expand_digits_f4<A_BITS, 2, kQ>(ta, v, vm);
         } else {
-          expand_to_tmem<0>(ta, v[0]);
-          if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1]);
-          if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2]);
-          if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3]);
+          expand_to_tmem<0>(ta, v[0][0]);
+          if constexpr (A_BITS > 1) expand_to_tmem<1>(ta + 1 * (BKB / 4), v[1][0]);
+          if constexpr (A_BITS > 2) expand_to_tmem<2>(ta + 2 * (BKB / 4), v[2][0]);
+          if constexpr (A_BITS > 3) expand_to_tmem<3>(ta + 3 * (BKB / 4), v[3][0]);
         }
       }
       PROF_END(2)
+      PROF_BEGIN  // slot 0: next step's address math and load issue
+      have = advance_load();
+      PROF_END(0)
       PROF_BEGIN  // slot 3: tensor-memory store completion
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       PROF_END(3)
@@ -1026,7 +1047,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0, acc_phase = 0;
     bool first = true;
     const bool resident = args.b_resident;
-    const uint64_t bdesc0 = F4 ? smem_desc_sw64(smem_u32(s_stage)) : smem_desc_sw128(smem_u32(s_stage));
+    const uint64_t bdesc0 = smem_desc_sw128(smem_u32(s_stage));
     if (resident) mbar_wait(smem_u32(full_b), 0);
     if (lane == 0) STAMP("b_resident_ready")
     for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
@@ -1052,7 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < C::kWP; ++j) {
             if constexpr (F4)
-              mma2_f4(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
+              mma4_f4(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
                       uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), idesc, (kc | i | j) != 0);
             else
               mma4_ts(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4), idesc,
@@ -1244,8 +1265,8 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
   P.p = p;
   P.ntn = (p.oc + bn - 1) / bn;
   tiles = (p.M + BM - 1) / BM * P.ntn;
-  const int64_t kpad = tc_kpad(p.kp);
-  P.nchunks = int(kpad / kWordsPerStage);
+  const int64_t kpad = tc_kpad(p.kp, f4 ? kTcF4 : kTcI8);
+  P.nchunks = int(kpad / chunk_words(f4));
   P.tile0 = tile0;
   // TMA-store epilogue by default (direct 16-byte stores of one row segment per lane
   // measured 1.4-1.8x slower on the output-bound layers); BS_TC_EPI=direct selects them.
@@ -1265,11 +1286,11 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
   P.kwa_shift = -1;
   for (int sh = 0; sh < 31; ++sh)
     if ((1 << sh) == p.kw_a) P.kwa_shift = sh;
-  const int brow = f4 ? 64 : BKB;
+  const int brow = BKB;
   const uint64_t wrow = uint64_t(kpad) * (f4 ? 16 : 32);  // prepared-weight row bytes
   const int wplanes = f4 ? (p.w_bits + 1) / 2 : p.w_bits;  // F4: radix-4 digits
   if (!encode_2d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, wexp, wrow, uint64_t(wplanes) * p.oc, wrow, brow, bn,
-                 f4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+                 CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
   if (P.epi == kEpiTma)
     return encode_2d(&to, CU_TENSOR_MAP_DATA_TYPE_INT32, p.out, uint64_t(p.oc), uint64_t(p.M), uint64_t(p.oc) * 4, 32,
@@ -1379,7 +1400,7 @@ cudaError_t launch_group_aw(const ConvProblem* ps, const int8_t* const* wexps, i
     if (const char* e = getenv("BS_TC_SPLIT"))
       if (e[0] == '1') {
         nset0 = 0;
-        while (nset0 < count && int64_t(tc_kpad(sp[nset0].kp) / kWordsPerStage) * A_BITS * W_BITS * 256 >
+        while (nset0 < count && int64_t(tc_kpad(sp[nset0].kp, F4 ? kTcF4 : kTcI8) / 4) * A_BITS * W_BITS * 256 >
                                     int64_t(BN) * BM * 4 / 17)
           ++nset0;
       }
@@ -1402,18 +1423,21 @@ int tc_resolve_format(int fmt) {
   return kTcDefault;
 }
 
-int64_t tc_kpad(int64_t kp) { return (kp + tc::kWordsPerStage - 1) / tc::kWordsPerStage * tc::kWordsPerStage; }
+int64_t tc_kpad(int64_t kp, int fmt) {
+  const int64_t cw = tc::chunk_words(tc_resolve_format(fmt) == kTcF4);
+  return (kp + cw - 1) / cw * cw;
+}
 
 int64_t tc_weight_bytes(int64_t n, int64_t kp, int w_bits, int fmt) {
   const bool f4 = tc_resolve_format(fmt) == kTcF4;  // F4: ceil(W/2) radix-4 digits of 16 B per word
-  return int64_t(f4 ? (w_bits + 1) / 2 : w_bits) * n * tc_kpad(kp) * (f4 ? 16 : 32);
+  return int64_t(f4 ? (w_bits + 1) / 2 : w_bits) * n * tc_kpad(kp, fmt) * (f4 ? 16 : 32);
 }
 
 bool tc_supported(int a_bits, int w_bits) { return a_bits >= 1 && a_bits <= 4 && w_bits >= 1 && w_bits <= 4; }
 
 cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp,
                                      int c_tap, int kw_tap, int8_t* wexp, int fmt, cudaStream_t stream) {
-  const int64_t kpad = tc_kpad(kp);
+  const int64_t kpad = tc_kpad(kp, fmt);
   const int64_t words = int64_t(w_bits) * n * kpad;
   int64_t blocks = (words + 255) / 256;
   if (blocks > 4096) blocks = 4096;

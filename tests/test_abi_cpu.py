@@ -124,12 +124,14 @@ def test_tc_validation_before_launch(lib):
     assert lib.bs_dense_tc_prepare_weights(FAKE, 1, 3, 64, 64, bs.TC_F4, FAKE, 1 << 20, NULL) == 2
     # prepared-weight buffer too small
     assert lib.bs_dense_tc_prepare_weights(FAKE, 1, 1, 64, 64, bs.TC_F4, FAKE, 16, NULL) == 8
-    # weight bytes per format: I8 32 B per packed word and plane; F4 16 B per packed word and
-    # radix-4 digit (ceil(W/2) digits); K = 64 -> 2 words, padded to 4
+    # weight bytes per format: I8 32 B per packed word and plane, K words padded to 4; F4 16 B
+    # per packed word and radix-4 digit (ceil(W/2) digits), K words padded to 8 (256-element
+    # chunks); K = 64 -> 2 words
     assert lib.bs_dense_tc_weight_bytes(64, 64, 1, bs.TC_I8) == 64 * 4 * 32
     assert lib.bs_dense_tc_weight_bytes(64, 64, 2, bs.TC_I8) == 2 * 64 * 4 * 32
-    assert lib.bs_dense_tc_weight_bytes(64, 64, 2, bs.TC_F4) == 1 * 64 * 4 * 16
-    assert lib.bs_dense_tc_weight_bytes(64, 64, 3, bs.TC_F4) == 2 * 64 * 4 * 16
+    assert lib.bs_dense_tc_weight_bytes(64, 64, 2, bs.TC_F4) == 1 * 64 * 8 * 16
+    assert lib.bs_dense_tc_weight_bytes(64, 64, 3, bs.TC_F4) == 2 * 64 * 8 * 16
+    assert lib.bs_dense_tc_weight_bytes(64, 300, 1, bs.TC_F4) == 1 * 64 * 16 * 16  # 10 words -> 16
     assert lib.bs_dense_tc_weight_bytes(64, 64, 1, 9) == 0
 
 
