@@ -629,7 +629,8 @@ struct TcArgs {
   int npeer;          // single-problem launches: every output box is also stored through peer[0..npeer)
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                       // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
-                      // 4 MMA warp ignores full_a, 5 producers idle (timing experiments; results are wrong)
+                      // 4 MMA warp ignores full_a, 5 producers idle, 6 producers keep their first tile's
+                    // row geometry (timing experiments; results are wrong)
   TcProb prob[NP];
 };
 template <int NP>
@@ -933,7 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int nenc = 0;
     auto advance_load = [&]() -> bool {
       if (!more) return false;
-      if (t != cur_tile) {
+      if (t != cur_tile && !(DBG(6) && cur_tile >= 0)) {  // knob 6: geometry of the first tile only
         set_tile(t);
         cur_tile = t;
       }
