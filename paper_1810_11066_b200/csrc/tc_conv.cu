@@ -201,7 +201,7 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 
 // Instruction descriptor, kind::i8: D = S32, A = u8 (activation planes, 0 or 2^i),
 // B = s8 (weight planes, +/-2^j or 0/2^j), both K-major, M = 128, N = BN.
-inline uint32_t idesc_i8(int n) {
+constexpr uint32_t idesc_i8(int n) {
   return (2u << 4) | (0u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
@@ -234,7 +234,24 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint
 // operand warp-uniform (uniform registers, no per-MMA R2UR / waterfall) — the MMA warp
 // shares its SM sub-partition with ALU-bound producer warps, so its instruction count
 // per MMA sets the tensor-core feed rate.
+template <uint32_t IDESC = 0>  // IDESC != 0: compile-time instruction descriptor (single-problem launches)
 __device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (IDESC != 0) {
+    asm volatile(
+        "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
+        "elect.sync x|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %3, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n"
+        "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "}" ::"r"(d),
+        "r"(a), "l"(b), "r"(accumulate), "n"(IDESC));
+    return;
+  }
   asm volatile(
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
       "elect.sync x|e, 0xffffffff;\n"
@@ -435,8 +452,25 @@ __device__ __forceinline__ void expand_digits_f4(uint32_t ta, const uint4 (&v)[A
 
 // The 4 K-steps (64 elements = 8 TMEM columns / 32 bytes of a 128B-swizzled B row each)
 // of one digit pair in one 256-element FP4 chunk.
+template <uint32_t IDESC = 0>  // IDESC != 0: compile-time instruction descriptor (single-problem launches)
 __device__ __forceinline__ void mma4_f4(uint32_t d, uint32_t a, uint64_t b, uint32_t sfa, uint32_t sfb, uint32_t idesc,
                                         uint32_t accumulate) {
+  if constexpr (IDESC != 0) {
+    asm volatile(
+        "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
+        "elect.sync x|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %3, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
+        "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "}" ::"r"(d),
+        "r"(a), "l"(b), "r"(accumulate), "n"(IDESC), "r"(sfa), "r"(sfb));
+    return;
+  }
   asm volatile(
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
       "elect.sync x|e, 0xffffffff;\n"
@@ -454,7 +488,7 @@ __device__ __forceinline__ void mma4_f4(uint32_t d, uint32_t a, uint64_t b, uint
 
 // Block-scaled instruction descriptor, kind::mxf4: A, B = E2M1, scales UE8M0, K = 64,
 // K-major, M = 128, N = BN (D is always F32).
-inline uint32_t idesc_mxf4(int n) {
+constexpr uint32_t idesc_mxf4(int n) {
   return (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
 }
 
@@ -1052,6 +1086,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (resident) mbar_wait(smem_u32(full_b), 0);
     if (lane == 0) STAMP("b_resident_ready")
     for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
+      // single-problem launches: N = BN is known at compile time (an immediate descriptor
+      // saves a constant-bank reload per MMA); groups: the member's N (64 or BN)
+      constexpr uint32_t kIdesc = NP == 1 ? (F4 ? idesc_mxf4(BN) : idesc_i8(BN)) : 0u;
       const uint32_t idesc = args.prob[pi].idesc;
       const int nchunks = args.prob[pi].nchunks;
       PROF_BEGIN
@@ -1074,10 +1111,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < C::kWP; ++j) {
             if constexpr (F4)
-              mma4_f4(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
+              mma4_f4<kIdesc>(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
                       uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), idesc, (kc | i | j) != 0);
             else
-              mma4_ts(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4), idesc,
+              mma4_ts<kIdesc>(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4), idesc,
                       (kc | i | j) != 0);
           }
         mma_commit_elect(smem_u32(empty + stage));
