@@ -664,7 +664,7 @@ struct TcArgs {
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                       // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
                       // 4 MMA warp ignores full_a, 5 producers idle, 6 producers keep their first tile's
-                    // row geometry (timing experiments; results are wrong)
+                    // row geometry, 7 no MMAs issued (timing experiments; results are wrong)
   TcProb prob[NP];
 };
 template <int NP>
@@ -1110,6 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < C::kAP; ++i)
 #pragma unroll
           for (int j = 0; j < C::kWP; ++j) {
+            if (DBG(7)) continue;  // knob 7: no MMAs (issue-path timing)
             if constexpr (F4)
               mma4_f4<kIdesc>(tacc, a_base + uint32_t(i * C::kAColsPlane), b_desc + uint64_t((j * BN * C::kBRow) >> 4),
                       uint32_t(C::kSF0 + 4 * i), uint32_t(C::kSF0 + 16 + 8 * j), idesc, (kc | i | j) != 0);
