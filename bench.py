@@ -365,10 +365,18 @@ class ConvWorkload:
 
     def e2e(self, steps):
         bufs = [r.host_buffers() for r in self.runs]
+        if self.overlap:  # tensor-core path: one pipelined host-buffer call for all layers
+            layers = [dict(act_host=b[0], out_host=b[1], act_dev=b[2], packed_dev=r.packed, out_dev=b[3], w_tc=r.w_tc,
+                           oc=r.L.oc, kh=r.L.k, kw=r.L.k, stride=r.L.s, pad=r.L.pad, w_enc=r.enc)
+                      for r, b in zip(self.runs, bufs)]
+            bs, fmt = self.runs[0].bs, tc_fmt(self.args)
 
-        def step():
-            for r, b in zip(self.runs, bufs):
-                r.host_step(b)
+            def step():
+                bs.bitserial_conv2d_nhwc_tc_host_group(layers, self.args.a_bits, self.args.w_bits, tc_format=fmt)
+        else:
+            def step():
+                for r, b in zip(self.runs, bufs):
+                    r.host_step(b)
         step()
         bsdist.barrier()
         torch.cuda.synchronize()

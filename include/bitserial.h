@@ -296,6 +296,27 @@ typedef struct bs_tc_conv_desc {
 int bs_bitserial_conv2d_nhwc_tc_group(const bs_tc_conv_desc* descs, int count, int a_bits, int w_bits,
                                       int tc_format, void* stream);
 
+/* End-to-end from HOST buffers for several layers, pipelined: per layer the upload of
+ * the uint8 NHWC activations (act_host -> act_dev), bit-packing (act_dev -> packed_dev,
+ * bs_conv2d_workspace_bytes bytes), the tensor-core conv on prepared weights (-> out_dev)
+ * and the download of the int32 output (out_dev -> out_host) — uploads, compute and
+ * downloads run on three streams so a layer's download overlaps the next layers'
+ * uploads and compute (PCIe is full duplex).  Host buffers should be pinned for the
+ * copies to overlap.  Every buffer is the caller's and distinct per layer.  Returns when
+ * every output is on the host; validation of all descriptors precedes any copy. */
+typedef struct bs_tc_host_desc {
+  const uint8_t* act_host; /* [n][h][w][c] uint8 codes (host, pinned) */
+  int32_t* out_host;       /* [n][oh][ow][oc] (host, pinned) */
+  uint8_t* act_dev;        /* device copy of act_host */
+  uint32_t* packed_dev;    /* device workspace for the packed activations */
+  int32_t* out_dev;        /* device output */
+  const int8_t* w_tc;      /* prepared weights (bs_conv2d_tc_prepare_weights) */
+  int a_enc, w_enc;
+  int n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w;
+} bs_tc_host_desc;
+int bs_bitserial_conv2d_nhwc_tc_host_group(const bs_tc_host_desc* descs, int count, int a_bits, int w_bits,
+                                           int tc_format, void* stream);
+
 /* The timed step of the paper on the tensor-core path: activation
  * bit-packing (raw uint8 codes -> workspace of *_workspace_bytes() bytes) followed by
  * the tensor-core conv / dense on prepared weights.  Two launches. */

@@ -26,7 +26,8 @@ __all__ = [
     "conv2d_tc_prepare_weights", "dense_tc_prepare_weights", "bitserial_conv2d_nhwc_tc_prepared",
     "bitserial_dense_tc_prepared", "bitserial_conv2d_nhwc_tc_i8", "bitserial_dense_tc_i8",
     "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
-    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group", "bitserial_dense_tc_gather",
+    "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group",
+    "bitserial_dense_tc_gather", "TcHostDesc", "bitserial_conv2d_nhwc_tc_host_group",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
@@ -51,6 +52,7 @@ EXPORTED_SYMBOLS = (
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
     "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitserial_dense_tc_prepared_gather",
+    "bs_bitserial_conv2d_nhwc_tc_host_group",
 )
 
 
@@ -103,6 +105,7 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
         "bs_bitserial_conv2d_nhwc_tc_group": ([P, I, I, I, I, P], I),
         "bs_bitpack_group": ([P, I, I, P], I),
+        "bs_bitserial_conv2d_nhwc_tc_host_group": ([P, I, I, I, I, P], I),
         "bs_bitserial_dense_tc_prepared_gather": ([P, I, I, P, I, I, I, P, P, I, L, L, L, P], I),
     }
     for name, (args, res) in sig.items():
@@ -389,6 +392,44 @@ def bitserial_dense_tc_prepared(a_packed, a_bits, w_tc, w_bits, m, n, k, out=Non
                                                   _dev(w_tc, "w_tc", torch.int8), w_bits, int(w_enc), int(tc_format),
                                                   _dev(out, "out", torch.int32), m, n, k, _stream(stream)))
     return out
+
+
+class TcHostDesc(ctypes.Structure):
+    """bs_tc_host_desc (include/bitserial.h): one layer of a pipelined host-buffer call."""
+    _fields_ = [("act_host", ctypes.c_void_p), ("out_host", ctypes.c_void_p), ("act_dev", ctypes.c_void_p),
+                ("packed_dev", ctypes.c_void_p), ("out_dev", ctypes.c_void_p), ("w_tc", ctypes.c_void_p),
+                ("a_enc", ctypes.c_int), ("w_enc", ctypes.c_int)] + \
+        [(f, ctypes.c_int) for f in ("n", "h", "w", "c", "oc", "kh", "kw", "stride_h", "stride_w", "pad_h", "pad_w")]
+
+
+def _host_ptr(t: torch.Tensor, name: str, dtype):
+    if not isinstance(t, torch.Tensor) or t.device.type != "cpu" or t.dtype != dtype or not t.is_contiguous():
+        raise BitserialError(f"{name} must be a contiguous CPU {dtype} tensor")
+    return t.data_ptr()
+
+
+def bitserial_conv2d_nhwc_tc_host_group(layers, a_bits, w_bits, tc_format=TC_DEFAULT, stream=None):
+    """bs_bitserial_conv2d_nhwc_tc_host_group: every layer host -> device -> pack -> conv ->
+    host, pipelined over three streams.  `layers`: dicts with act_host (uint8 NHWC, pinned),
+    out_host (int32, pinned), act_dev, packed_dev (int32 workspace), out_dev, w_tc, oc, kh,
+    kw and optional stride, pad, a_enc, w_enc.  Returns the out_host tensors."""
+    descs = (TcHostDesc * max(len(layers), 1))()
+    for i, ly in enumerate(layers):
+        n, h, w, c = ly["act_host"].shape
+        sh, sw, ph, pw, _, _ = _conv_geom(n, h, w, ly["kh"], ly["kw"], ly.get("stride", 1), ly.get("pad", 0))
+        d = descs[i]
+        d.act_host = _host_ptr(ly["act_host"], "act_host", torch.uint8)
+        d.out_host = _host_ptr(ly["out_host"], "out_host", torch.int32)
+        d.act_dev = _dev(ly["act_dev"], "act_dev", torch.uint8).value
+        d.packed_dev = _dev(ly["packed_dev"], "packed_dev", ly["packed_dev"].dtype).value
+        d.out_dev = _dev(ly["out_dev"], "out_dev", torch.int32).value
+        d.w_tc = _dev(ly["w_tc"], "w_tc", torch.int8).value
+        d.a_enc, d.w_enc = int(ly.get("a_enc", A_UNSIGNED)), int(ly.get("w_enc", UNIPOLAR))
+        d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw = n, h, w, c, ly["oc"], ly["kh"], ly["kw"]
+        d.stride_h, d.stride_w, d.pad_h, d.pad_w = sh, sw, ph, pw
+    _check(_load().bs_bitserial_conv2d_nhwc_tc_host_group(ctypes.cast(descs, ctypes.c_void_p), len(layers), a_bits,
+                                                          w_bits, int(tc_format), _stream(stream)))
+    return [ly["out_host"] for ly in layers]
 
 
 def bitserial_dense_tc_gather(a_packed, a_bits, w_tc, w_bits, m, n, k, out, peers, tc_format=TC_DEFAULT,

@@ -550,6 +550,69 @@ int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, int a_
   return cuda_status(cudaStreamSynchronize(s), fn);
 }
 
+int bs_bitserial_conv2d_nhwc_tc_host_group(const bs_tc_host_desc* descs, int count, int a_bits, int w_bits,
+                                           int tc_format, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tc_host_group";
+  if (count < 0 || count > (1 << 16)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  if (int st = check_format(tc_format, fn)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  std::vector<bs::ConvProblem> ps(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_tc_host_desc& d = descs[q];
+    if (int st = check_tc_enc(d.a_enc, d.w_enc, tc_format, fn)) return st;
+    const ConvArgs g{d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw, d.stride_h, d.stride_w, d.pad_h, d.pad_w};
+    if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+    if (int st = check_tc_bound(int64_t(d.kh) * d.kw * d.c, a_bits, w_bits, tc_format, fn, d.a_enc, d.w_enc))
+      return st;
+    if (!d.act_host || !d.out_host || !d.act_dev || !d.packed_dev || !d.out_dev || !d.w_tc)
+      return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    if (!aligned16(d.act_dev) || !aligned16(d.packed_dev) || !aligned16(d.out_dev) || !aligned16(d.w_tc))
+      return fail(BS_ERR_ALIGN, "%s: descriptor %d: device pointers must be 16-byte aligned", fn, q);
+    ps[q] = make_conv(d.packed_dev, a_bits, nullptr, w_bits, BS_UNIPOLAR, d.out_dev, g);
+    ps[q].a_enc = d.a_enc;
+  }
+  // three-stage pipeline: uploads on one stream, pack + conv on the caller's stream,
+  // downloads on a third; layer q's download overlaps layer q+1's upload and compute
+  cudaStream_t s = static_cast<cudaStream_t>(stream), s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(count) + 2, nullptr);
+  cudaError_t e = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
+  for (auto& x : ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  cudaEvent_t start = ev[0], end = ev[1];
+  if (e == cudaSuccess) e = cudaEventRecord(start, s);  // nothing starts before the caller's prior work
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s_in, start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, start, 0);
+  for (int q = 0; q < count && e == cudaSuccess; ++q) {
+    const bs_tc_host_desc& d = descs[q];
+    const bs::ConvProblem& p = ps[q];
+    cudaEvent_t in = ev[2 + 2 * q], done = ev[3 + 2 * q];
+    const size_t in_bytes = size_t(d.n) * d.h * d.w * d.c;
+    const size_t out_bytes = size_t(p.M) * d.oc * 4;
+    e = cudaMemcpyAsync(d.act_dev, d.act_host, in_bytes, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(in, s_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, in, 0);
+    if (e == cudaSuccess) e = bs::launch_bitpack(d.act_dev, d.packed_dev, int64_t(d.n) * d.h * d.w, d.c, row_words(d.c),
+                                               a_bits, s);
+    if (e == cudaSuccess) e = bs::launch_tc_conv_prepared(p, d.w_tc, tc_format, s);
+    if (e == cudaSuccess) e = cudaEventRecord(done, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, done, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d.out_host, d.out_dev, out_bytes, cudaMemcpyDeviceToHost, s_out);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(end, s_out);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, end, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (s_in) cudaStreamSynchronize(s_in);
+  if (s_out) cudaStreamSynchronize(s_out);
+  for (auto& x : ev)
+    if (x) cudaEventDestroy(x);
+  if (s_in) cudaStreamDestroy(s_in);
+  if (s_out) cudaStreamDestroy(s_out);
+  return cuda_status(e, fn);
+}
+
 int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits, const uint32_t* w_packed, int w_bits,
                                   int w_enc, int32_t* out_host, int n, int h, int w, int c, int oc, int kh, int kw,
                                   int stride_h, int stride_w, int pad_h, int pad_w, uint8_t* act_dev,

@@ -192,3 +192,23 @@ def test_dense_gather_validation(lib):
     assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, pp, 2, 16, 16, 64, NULL) == 5   # misaligned peer
     peers[1] = 0
     assert f(FAKE, 2, 0, FAKE, 1, 1, bs.TC_F4, FAKE, pp, 2, 16, 16, 64, NULL) == 1   # NULL peer
+
+
+def test_tc_host_group_validation(lib):
+    import ctypes
+    d = (bs.TcHostDesc * 1)()
+    x = d[0]
+    x.act_host = x.out_host = 1 << 20
+    x.act_dev = x.packed_dev = x.out_dev = x.w_tc = 1 << 21
+    x.n, x.h, x.w, x.c, x.oc, x.kh, x.kw, x.stride_h, x.stride_w, x.pad_h, x.pad_w = 1, 8, 8, 64, 64, 3, 3, 1, 1, 1, 1
+    p = ctypes.cast(d, ctypes.c_void_p)
+    f = lib.bs_bitserial_conv2d_nhwc_tc_host_group
+    assert f(p, 0, 2, 1, bs.TC_F4, NULL) == 0
+    assert f(NULL, 1, 2, 1, bs.TC_F4, NULL) == 1
+    assert f(p, 1, 2, 1, 7, NULL) == 2
+    x.out_dev = 0
+    assert f(p, 1, 2, 1, bs.TC_F4, NULL) == 1
+    x.out_dev = (1 << 21) + 8
+    assert f(p, 1, 2, 1, bs.TC_F4, NULL) == 5
+    x.out_dev, x.oc = 1 << 21, 0
+    assert f(p, 1, 2, 1, bs.TC_F4, NULL) == 4

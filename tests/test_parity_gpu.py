@@ -624,3 +624,30 @@ def test_dense_tc_fused_gather(fmt, m, n, k, npeers):
         f = f.cpu().numpy()
         np.testing.assert_array_equal(f[blk], ref, err_msg=f"buffer of rank {r}")
         assert (f[:rank * m] == -7).all() and (f[(rank + 1) * m:] == -7).all()
+
+
+def test_conv_tc_host_group_pipelined():
+    """bs_bitserial_conv2d_nhwc_tc_host_group: pinned host activations -> device -> pack ->
+    tensor-core conv -> pinned host outputs for several layers on three streams; every
+    output equals the oracle (and the call returns only when all are on the host)."""
+    cases = [(2, 9, 11, 33, 20, 3, 3, 1, 1), (1, 14, 14, 128, 136, 3, 3, 2, 1), (3, 7, 7, 64, 64, 1, 1, 1, 0)]
+    layers, refs = [], []
+    for i, (n, h, w, c, oc, kh, kw, st, pd) in enumerate(cases):
+        g = inputs.gen(900 + i)
+        act = inputs.codes((n, h, w, c), 2, g)
+        wt = inputs.codes((oc, kh, kw, c), 1, g)
+        refs.append(oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(st, st), pad=(pd, pd)))
+        w_tc = bs.conv2d_tc_prepare_weights(gpu_pack(wt.reshape(oc * kh * kw, c), 1), 1, bs.BIPOLAR, oc, kh, kw, c)
+        oh = bs.conv_out_extent(h, kh, st, pd)
+        ow = bs.conv_out_extent(w, kw, st, pd)
+        layers.append(dict(act_host=act.contiguous().pin_memory(),
+                           out_host=torch.full((n, oh, ow, oc), -9, dtype=torch.int32).pin_memory(),
+                           act_dev=torch.empty((n, h, w, c), dtype=torch.uint8, device=DEV),
+                           packed_dev=torch.empty(bs.conv2d_workspace_bytes(n, h, w, c, 2) // 4, dtype=torch.int32,
+                                                  device=DEV),
+                           out_dev=torch.empty((n, oh, ow, oc), dtype=torch.int32, device=DEV), w_tc=w_tc, oc=oc,
+                           kh=kh, kw=kw, stride=st, pad=pd, w_enc=bs.BIPOLAR))
+    for _ in range(2):  # repeated calls reuse the buffers
+        outs = bs.bitserial_conv2d_nhwc_tc_host_group(layers, 2, 1)
+        for o, r in zip(outs, refs):
+            np.testing.assert_array_equal(o.numpy(), r)
