@@ -369,6 +369,8 @@ class ConvWorkload:
             layers = [dict(act_host=b[0], out_host=b[1], act_dev=b[2], packed_dev=r.packed, out_dev=b[3], w_tc=r.w_tc,
                            oc=r.L.oc, kh=r.L.k, kw=r.L.k, stride=r.L.s, pad=r.L.pad, w_enc=r.enc)
                       for r, b in zip(self.runs, bufs)]
+            # smallest upload first: the download stream (745 MB, the PCIe-bound part) starts sooner
+            layers.sort(key=lambda d: d["act_host"].numel())
             bs, fmt = self.runs[0].bs, tc_fmt(self.args)
 
             def step():
