@@ -196,12 +196,12 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
 
 /* ---------------------------------------------------------------------------
  * Tensor-core bitserial (tcgen05.mma on sm_100a, format BS_TC_DEFAULT).  Same operation and
- * operands as bs_bitserial_conv2d_nhwc / bs_bitserial_dense.  Each activation plane i
- * and weight plane j is expanded inside the kernel (weights: by a first kernel into
- * `workspace`) to bytes 2^i*a_i and 2^j*b_j (unipolar) or 2^j*(2b_j-1) (bipolar), and
- * every plane pair is one exact int8 x int8 -> int32 binary dot product on the tensor
- * cores: popcount(a_i AND w_j) = sum_k a_i[k] w_j[k] (Eq. 1), weighted
- * 2^(i+j) (Eq. 2); cost still grows with A*W.
+ * operands as bs_bitserial_conv2d_nhwc / bs_bitserial_dense.  The packed activation and
+ * weight planes are expanded inside the kernel (weights: by a first kernel into
+ * `workspace`) into tensor-core operands whose exact products are the binary dot products
+ * popcount(a_i AND w_j) = sum_k a_i[k] w_j[k] (Eq. 1) weighted 2^(i+j)
+ * (Eq. 2): per plane pair (BS_TC_I8) or per pair of radix-4 digits of two
+ * planes each (BS_TC_F4, see bs_tc_format).
  * Supported: a_bits in [1,4], w_bits in [1,4] (BS_ERR_UNSUPPORTED otherwise).
  * workspace: device, >= *_tc_workspace_bytes() (the larger, I8, size), 16-byte aligned,
  * overwritten.
@@ -220,13 +220,15 @@ int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits,
 
 /* Operand format of the tensor-core path (same results, bit-exact; different speed):
  *   BS_TC_I8  : every plane pair as tcgen05.mma.kind::i8 on bytes 2^i*a_i (u8) and
- *               2^j*b_j or 2^j*(2b_j-1) (s8), int32 accumulation.
- *   BS_TC_F4  : tcgen05.mma.kind::mxf4 (block-scaled FP4): bits as packed E2M1 nibbles
- *               0.5*b (weights +-0.5 when bipolar), the plane weights 2^(i+1), 2^(j+1) as
- *               UE8M0 block scales, FP32 accumulation.  Every product and partial sum is
- *               an integer (times 2^-2) far below 2^24, so the FP32 result is exact and is
+ *               2^j*b_j or 2^j*(2b_j-1) (s8), int32 accumulation; 128-element K chunks.
+ *   BS_TC_F4  : tcgen05.mma.kind::mxf4 (block-scaled FP4): planes (2d, 2d+1) form one
+ *               radix-4 digit, an E2M1 nibble 0.5 * {0..3} (bipolar +-0.5 / +-1.5, the
+ *               signed top digit b_lo - 2 b_hi), the digit weights 4^d as UE8M0 block
+ *               scales 2^(2d+1): ceil(A/2)*ceil(W/2) MMAs per K step instead of A*W;
+ *               FP32 accumulation; 256-element K chunks.  Every product and partial sum
+ *               is an integer far below 2^24, so the FP32 result is exact and is
  *               converted to int32 (tools/mxf4_probe.cu checks exactness up to |sum| >
- *               the 737,280 accumulator bound of the configs).  Twice the MAC rate of i8.
+ *               the 737,280 accumulator bound of the configs).
  *   BS_TC_DEFAULT (0): the library's choice (BS_TC_F4).
  * Prepared weights are format-specific: prepare and run with the same format. */
 typedef enum { BS_TC_DEFAULT = 0, BS_TC_I8 = 1, BS_TC_F4 = 2 } bs_tc_format;
@@ -234,10 +236,11 @@ typedef enum { BS_TC_DEFAULT = 0, BS_TC_I8 = 1, BS_TC_F4 = 2 } bs_tc_format;
 /* Prepared weights for the tensor-core path.  Weight packing is done ahead of time
  * and is not timed; the expansion of the packed weight planes into the
  * tensor-core operand layout is part of that offline step:
- *   w_tc : device [w_bits][oc][Kpad*B] bytes (dense: [w_bits][n][Kpad*B]), B = 32 (I8)
- *          or 16 (F4) bytes per packed word, Kpad = K words (kh*kw*bs_packed_row_words(c),
- *          dense bs_packed_row_words(k)) rounded up to a multiple of 4; the encoding
- *          (unipolar / bipolar) is baked into w_tc.
+ *   w_tc : device [P][oc][Kpad*B] bytes (dense: [P][n][Kpad*B]); I8: P = w_bits planes,
+ *          B = 32 bytes per packed word, Kpad = K words (kh*kw*bs_packed_row_words(c),
+ *          dense bs_packed_row_words(k)) rounded up to a multiple of 4; F4: P = ceil(w_bits/2)
+ *          radix-4 digits, B = 16, Kpad rounded up to a multiple of 8; the encoding
+ *          (unipolar / bipolar / signed) is baked into w_tc.
  *   w_tc_bytes >= bs_conv2d_tc_weight_bytes() / bs_dense_tc_weight_bytes() (0 on bad
  *   arguments).
  */
