@@ -303,12 +303,16 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits, const uint32_t* 
 
 int64_t bs_conv2d_tc_workspace_bytes(int oc, int kh, int kw, int c, int w_bits) {
   if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0 || w_bits < 1 || w_bits > 8) return 0;
-  return bs::tc_weight_bytes(oc, int64_t(kh) * kw * row_words(c), w_bits, bs::kTcI8);  // the larger format
+  const int64_t kp = int64_t(kh) * kw * row_words(c);  // either format fits
+  const int64_t i8 = bs::tc_weight_bytes(oc, kp, w_bits, bs::kTcI8), f4 = bs::tc_weight_bytes(oc, kp, w_bits, bs::kTcF4);
+  return i8 > f4 ? i8 : f4;
 }
 
 int64_t bs_dense_tc_workspace_bytes(int64_t n, int64_t k, int w_bits) {
   if (n <= 0 || k <= 0 || w_bits < 1 || w_bits > 8) return 0;
-  return bs::tc_weight_bytes(n, row_words(k), w_bits, bs::kTcI8);
+  const int64_t i8 = bs::tc_weight_bytes(n, row_words(k), w_bits, bs::kTcI8);
+  const int64_t f4 = bs::tc_weight_bytes(n, row_words(k), w_bits, bs::kTcF4);
+  return i8 > f4 ? i8 : f4;  // either format fits
 }
 
 int bs_bitserial_conv2d_nhwc_tc(const uint32_t* act_packed, int a_bits, const uint32_t* w_packed, int w_bits,
