@@ -651,3 +651,21 @@ def test_conv_tc_host_group_pipelined():
         outs = bs.bitserial_conv2d_nhwc_tc_host_group(layers, 2, 1)
         for o, r in zip(outs, refs):
             np.testing.assert_array_equal(o.numpy(), r)
+
+
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+@pytest.mark.parametrize("size", [4096, 8192, 16384])
+@pytest.mark.parametrize("a_bits,w_bits,bipolar", [(1, 1, False), (2, 1, True), (4, 2, True)])
+def test_config5_gemm_tc_sampled_rows(fmt, size, a_bits, w_bits, bipolar):
+    """BASELINE configs[4] on the tensor-core path in the bench's launch configuration
+    (bs_bitserial_dense_tc_i8: activation pack + one persistent launch over the whole
+    M = N = K product); the oracle checks rows at both ends and the middle, every column."""
+    e = "bipolar" if bipolar else "unipolar"
+    a, w = inputs.dense_operands(size, size, size, a_bits, w_bits, inputs.seed_for(5, a_bits, w_bits, e))
+    w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, enc(bipolar), size, size, tc_format=fmt)
+    got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, size, tc_format=fmt, w_enc=enc(bipolar))
+    rows = [0, 127, 128, size // 2 + 3, size - 1]
+    ref = oracle.dense(a[rows].numpy(), a_bits, w.numpy(), w_bits, bipolar)
+    np.testing.assert_array_equal(got[rows].cpu().numpy(), ref)
+    del got
+    torch.cuda.empty_cache()
