@@ -669,3 +669,40 @@ def test_config5_gemm_tc_sampled_rows(fmt, size, a_bits, w_bits, bipolar):
     np.testing.assert_array_equal(got[rows].cpu().numpy(), ref)
     del got
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+def test_tc_group_writes_stay_in_bounds(fmt):
+    """Every grouped-launch output lives inside one flat buffer between sentinel guard
+    bands (ragged M / OC, OC % 4 != 0 scalar epilogue, OC <= 64 and wide members): the
+    outputs equal the oracle and no byte outside them changes."""
+    cases = [(1, 9, 11, 33, 20, 3, 3, 1, 1), (2, 5, 7, 64, 130, 3, 3, 2, 1), (1, 6, 6, 96, 18, 1, 1, 1, 0),
+             (3, 7, 5, 40, 64, 3, 3, 1, 1)]
+    guard = 4096
+    sizes = []
+    for (n, h, w, c, oc, kh, kw, st, pd) in cases:
+        oh, ow = bs.conv_out_extent(h, kh, st, pd), bs.conv_out_extent(w, kw, st, pd)
+        sizes.append((n, oh, ow, oc))
+    total = guard + sum(int(np.prod(s_)) + guard for s_ in sizes)
+    flat = torch.full((total,), 0x5A5A5A5A, dtype=torch.int32, device=DEV)
+    items, refs, spans, off = [], [], [], guard
+    for i, ((n, h, w, c, oc, kh, kw, st, pd), shp) in enumerate(zip(cases, sizes)):
+        g = inputs.gen(700 + i)
+        act = inputs.codes((n, h, w, c), 2, g)
+        wt = inputs.codes((oc, kh, kw, c), 1, g)
+        refs.append(oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 1, True, stride=(st, st), pad=(pd, pd)))
+        cnt = int(np.prod(shp))
+        out = flat[off:off + cnt].view(shp)
+        spans.append((off, cnt))
+        off += cnt + guard
+        w_tc = bs.conv2d_tc_prepare_weights(gpu_pack(wt.reshape(oc * kh * kw, c), 1), 1, bs.BIPOLAR, oc, kh, kw, c,
+                                            tc_format=fmt)
+        items.append(dict(act_packed=gpu_pack(act.reshape(-1, c), 2), w_tc=w_tc, out=out, n=n, h=h, w=w, c=c, oc=oc,
+                          kh=kh, kw=kw, stride=st, pad=pd, w_enc=bs.BIPOLAR))
+    bs.bitserial_conv2d_nhwc_tc_group(items, 2, 1, tc_format=fmt)
+    host = flat.cpu().numpy()
+    mask = np.ones(total, dtype=bool)
+    for (o, cnt), shp, r in zip(spans, sizes, refs):
+        np.testing.assert_array_equal(host[o:o + cnt].reshape(shp), r)
+        mask[o:o + cnt] = False
+    assert (host[mask] == 0x5A5A5A5A).all()
