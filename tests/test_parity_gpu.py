@@ -706,3 +706,27 @@ def test_tc_group_writes_stay_in_bounds(fmt):
         np.testing.assert_array_equal(host[o:o + cnt].reshape(shp), r)
         mask[o:o + cnt] = False
     assert (host[mask] == 0x5A5A5A5A).all()
+
+
+@pytest.mark.parametrize("fmt", TC_FORMATS)
+@pytest.mark.parametrize("bn", ["64", "128"])
+@pytest.mark.parametrize("a_bits,w_bits", [(2, 1), (4, 3), (1, 4)])
+def test_tc_single_launch_writes_stay_in_bounds(monkeypatch, fmt, bn, a_bits, w_bits):
+    """A single tensor-core launch (ragged M and OC, each tile width) writes exactly its
+    output: sentinel guard bands before and after stay intact."""
+    monkeypatch.setenv("BS_TC_BN", bn)
+    n, h, w, c, oc = 2, 11, 9, 72, 100
+    g = inputs.gen(31 * a_bits + w_bits + int(bn))
+    act = inputs.codes((n, h, w, c), a_bits, g)
+    wt = inputs.codes((oc, 3, 3, c), w_bits, g)
+    ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, True, stride=(1, 1), pad=(1, 1))
+    guard, cnt = 4096, ref.size
+    flat = torch.full((2 * guard + cnt,), 0x3C3C3C3C, dtype=torch.int32, device=DEV)
+    out = flat[guard:guard + cnt].view(ref.shape)
+    w_tc = bs.conv2d_tc_prepare_weights(gpu_pack(wt.reshape(oc * 9, c), w_bits), w_bits, bs.BIPOLAR, oc, 3, 3, c,
+                                        tc_format=fmt)
+    bs.bitserial_conv2d_nhwc_tc_prepared(gpu_pack(act.reshape(-1, c), a_bits), a_bits, w_tc, w_bits, n, h, w, c, oc,
+                                         3, 3, 1, 1, out=out, tc_format=fmt, w_enc=bs.BIPOLAR)
+    host = flat.cpu().numpy()
+    np.testing.assert_array_equal(host[guard:guard + cnt].reshape(ref.shape), ref)
+    assert (host[:guard] == 0x3C3C3C3C).all() and (host[guard + cnt:] == 0x3C3C3C3C).all()
