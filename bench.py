@@ -126,7 +126,7 @@ class ConvLayerRun:
         self.bs, self.L, self.path = bs, L, path
         self.a_bits, self.w_bits, self.enc = a_bits, w_bits, (bs.BIPOLAR if bipolar else bs.UNIPOLAR)
         self.n = act_cpu.shape[0]
-        self.act_cpu = act_cpu
+        self.act_cpu, self.wt_cpu = act_cpu, wt_cpu
         self.act = act_cpu.to(dev)
         self.wp = bs.bitpack(wt_cpu.reshape(L.oc * L.k * L.k, L.ic).to(dev), w_bits)  # untimed
         self.oh = bs.conv_out_extent(L.h, L.k, L.s, L.pad)
@@ -393,6 +393,28 @@ class ConvWorkload:
         ms = e0.elapsed_time(e1) / steps
         return ms, sum(b[0].numel() for b in bufs), sum(b[1].numel() * 4 for b in bufs)
 
+    def parity_check(self, rank, world):
+        """Outputs of the TIMED step (what the graph replays left in HBM) against the
+        oracle on the same inputs: this rank's first image, every layer at N = 1 (the
+        layers round-robin across ranks at N > 1, so the CPU work stays bounded)."""
+        import numpy as np
+
+        import oracle
+        a = self.args
+        checked = mism = 0
+        done = []
+        for i, (li, r) in enumerate(zip(self.layers, self.runs)):
+            if world > 1 and i % world != rank % world:
+                continue
+            L = r.L
+            got = r.out[0:1].cpu().numpy()
+            ref = oracle.conv2d_nhwc(r.act_cpu[0:1].numpy(), a.a_bits, r.wt_cpu.numpy(), a.w_bits, a.bipolar,
+                                     stride=(L.s, L.s), pad=(L.pad, L.pad))
+            checked += ref.size
+            mism += int(np.count_nonzero(got != ref))
+            done.append(li)
+        return checked, mism, f"image {self.images[0]} (this rank's first) of layers {done}"
+
     def oracle_sample(self, images):
         """The oracle on `images` images of every layer (same seeds as the GPU arm)."""
         import oracle
@@ -563,6 +585,26 @@ class DenseWorkload:
         bsdist.barrier()
         return e0.elapsed_time(e1) / steps, a_host.numel(), c_host.numel() * 4
 
+    def parity_check(self, rank, world):
+        """Rows of the timed step's C against the oracle: every row of the GEMV; for the
+        row-sharded GEMM the first row of EVERY rank's block (and the last row) of this
+        rank's gathered C, so the exchange step is checked too."""
+        import numpy as np
+
+        import oracle
+        enc = "bipolar" if self.args.bipolar else "unipolar"
+        a, w = inputs.dense_operands(self.m, self.n, self.k, self.a_bits, self.w_bits,
+                                     inputs.seed_for(self.config_id, self.a_bits, self.w_bits, enc))
+        if self.gather:
+            pick = sorted({bsdist.shard_range(self.m, r, self.world)[0] for r in range(self.world)} | {self.m - 1})
+            full = self.fused.full if self.fused is not None else self.full
+            got = full[pick].cpu().numpy()
+        else:
+            pick = list(range(self.m)) if self.m <= 8 else sorted({0, self.m // 3, (2 * self.m) // 3, self.m - 1})
+            got = self.out[pick].cpu().numpy()
+        ref = oracle.dense(a[pick].numpy(), self.a_bits, w.numpy(), self.w_bits, self.args.bipolar)
+        return ref.size, int(np.count_nonzero(got != ref)), f"rows {pick} of C"
+
     def oracle_sample(self, rows):
         import oracle
         a = self.args
@@ -680,6 +722,20 @@ def run_ours(args):
     clocks = clk.summary()
     value = wl.total_binops / (ms / 1e3) / 1e12
 
+    # self-check: the outputs the timed step left in HBM against the oracle (same inputs)
+    parity = None
+    if not args.no_parity:
+        if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+            os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // world))
+        n_chk, n_bad, what = wl.parity_check(rank, world)
+        tot = torch.tensor([n_chk, n_bad], dtype=torch.int64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(tot)
+        n_chk, n_bad = int(tot[0]), int(tot[1])
+        parity = {"result": "bit-exact" if n_bad == 0 else f"MISMATCH n={n_bad}", "outputs_checked": n_chk,
+                  "ranks": world, "rank0_sample": what + " of the timed step's outputs vs the CPU oracle"}
+
     roof = wl.roofline(10)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or MAX_MHZ_FALLBACK
@@ -774,7 +830,7 @@ def run_ours(args):
         ops, t, sample = wl.oracle_sample(units)
         cpu = {"value": ops / t / 1e12, "unit": "binary TOPS", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": sample + " (bounded sample of the same workload, same seeds), OpenMP C oracle",
-               "seconds": t}
+               "seconds": t, "cpu_model": cpu_model()}
 
     if rank == 0:
         cfg = dict(wl.config)
@@ -793,7 +849,7 @@ def run_ours(args):
             "config": cfg, "roofline": roofline,
             "breakdown": dict(roof.get("breakdown", {}), hbm_peak_gbs=peaks["hbm_gbs"], peaks_source=peaks_src),
             "clocks": clocks, "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -802,12 +858,26 @@ def run_ours(args):
     return 0
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args):
     """The reference arm of this tier: the CPU oracle, as it stands, on the host
     cores, each step a bounded sample of the same workload (rank 0 only)."""
     world, rank, _ = bsdist.env()
+    if world > 1:  # under torchrun: a gloo group only to keep the ranks' exits together
+        bsdist.init("gloo")
     if rank != 0:
-        return 0
+        bsdist.barrier()
+        return 0  # rank 0 alone runs the CPU oracle and prints
     import oracle
     oracle.build()
     wl = make_workload_cpu(args)
@@ -821,15 +891,17 @@ def run_reference(args):
     ms = 1e3 * sum(ts) / len(ts)
     value = ops / (ms / 1e3) / 1e12
     line = {
-        "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": args.gpus, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": max(world, args.gpus), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u8 codes -> i32 (plain integer loops)", "data": "synthetic (seeded uniform codes)",
         "impl": "reference", "config": dict(wl.config, sample_per_step=sample),
         "cpu_baseline": {"value": value, "unit": "binary TOPS", "cores": oracle.num_threads(), "kind": "oracle",
-                         "sample": sample + " per step (bounded sample of the workload; OpenMP C oracle)"},
+                         "sample": sample + " per step (bounded sample of the workload; OpenMP C oracle)",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "binary TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    bsdist.barrier()
     return 0
 
 
@@ -857,6 +929,24 @@ def make_workload_cpu(args):
     if args.workload == "gemv":
         return Dense(1, 4096, 4096, 2, "gemv")
     return Dense(args.size, args.size, args.size, 5, "gemm")
+
+
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(n, argv=None):
+    """`bench.py --gpus N` without torchrun: re-run this script as N ranks on one node
+    (torch.distributed.run, rendezvous on 127.0.0.1), exactly as the driver launches it;
+    rank 0 prints the JSON line.  Returns torchrun's exit status."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + \
+        list(sys.argv[1:] if argv is None else argv)
+    return subprocess.call(cmd)
 
 
 def main():
@@ -891,7 +981,13 @@ def main():
                     help="gemm, N>1: all-gather fused into the tensor-core epilogue over symmetric memory (SURVEY 8 f2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step's outputs")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:  # not launched by torchrun: launch N ranks (one per GPU) ourselves
+        return relaunch(args.gpus)
+    if world and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with --nproc-per-node {args.gpus}")
     if args.impl == "ours" and args.warmup < 3:
         args.warmup = 3
     return run_reference(args) if args.impl == "reference" else run_ours(args)

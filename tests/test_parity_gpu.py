@@ -436,6 +436,66 @@ def test_tc_accumulator_bound_extremes(fmt, a_bits, w_bits):
     assert int(np.abs(ref).max()) == k * ((1 << a_bits) - 1) * ((1 << w_bits) - 1)
 
 
+def _near_max_codes(rows, k, bits, g, base, alts, p_alt=0.002):
+    """Codes equal to `base` except a sparse random sprinkle of the codes in `alts`
+    (so sums sit just under the bound with odd, row-dependent low bits)."""
+    x = torch.full((rows, k), base, dtype=torch.uint8)
+    sel = torch.rand((rows, k), generator=g) < p_alt
+    pick = torch.randint(0, len(alts), (rows, k), generator=g)
+    alt = torch.tensor(alts, dtype=torch.uint8)[pick]
+    return torch.where(sel, alt, x)
+
+
+# (a_bits, a_enc, w_bits, w_enc, K): K * max|a| * max|w| just under the FP4 ABI bound
+# 2^22 = 4,194,304 (abi.cu check_tc_bound) for every encoding family.
+FP4_BOUND_CASES = [
+    (1, 0, 1, 0, 4_194_303),   # A1W1: +1 increments on a running sum at 2^22 (FP32 ulp 0.5)
+    (1, 0, 1, 1, 4_194_303),   # W1 bipolar: +-1
+    (4, 0, 4, 0, 18_641),      # A4W4 unsigned x unipolar: 18,641 * 225 = 4,194,225
+    (4, 0, 4, 1, 18_641),      # bipolar weights +-15
+    (4, 2, 4, 2, 65_535),      # both signed: (-8)(-8) = 64 -> 4,194,240; signed-digit partials up to (11/8)^2 more
+    (2, 1, 2, 1, 466_033),     # both bipolar (XNOR form): 466,033 * 9 = 4,194,297
+]
+
+
+@pytest.mark.parametrize("a_bits,a_enc,w_bits,w_enc,k", FP4_BOUND_CASES)
+def test_tc_fp4_at_abi_bound(a_bits, a_enc, w_bits, w_enc, k):
+    """The FP4 (kind::mxf4) format's exactness at its ABI bound: the dense product with
+    K * max|a| * max|w| just below 2^22 (the largest magnitude check_tc_bound admits),
+    near-max codes with a sparse sprinkle of other codes (odd low bits on a large running
+    sum), against the oracle element by element.  The FP32 accumulator holds integers
+    exactly below 2^24 (every digit product and partial sum is an integer,
+    DESIGN.md R17/R21); this pins that the hardware's internal accumulation keeps them."""
+    m, n = 5, 9
+    g = inputs.gen(k * 31 + a_bits * 7 + w_bits + 100 * a_enc + 1000 * w_enc)
+    a_max = (1 << a_bits) - 1 if a_enc != 2 else 1 << (a_bits - 1)      # code of the largest |value|
+    w_max = (1 << w_bits) - 1 if w_enc != 2 else 1 << (w_bits - 1)
+    a_alts = [0, 1, (1 << a_bits) - 1] + ([9, 11, 15] if a_enc == 2 else [])
+    w_alts = [0, 1] + ([9, 11, 15] if w_enc == 2 else [])
+    a = _near_max_codes(m, k, a_bits, g, a_max, a_alts)
+    w = _near_max_codes(n, k, w_bits, g, w_max, w_alts)
+    w[n - 1] = 0 if w_enc == 1 else w_max  # one weight row of constant sign: |sum| at its largest
+    ref = oracle.dense_enc(a.numpy(), a_bits, a_enc, w.numpy(), w_bits, w_enc)
+    bound = k * (a_max if a_enc != 1 else (1 << a_bits) - 1) * (w_max if w_enc != 1 else (1 << w_bits) - 1)
+    assert bound < 1 << 22
+    assert int(np.abs(ref).max()) > 0.99 * bound  # the case really sits at the bound
+    w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, w_enc, n, k, tc_format=bs.TC_F4)
+    got = bs.bitserial_dense_tc_i8(a.to(DEV), a_bits, w_tc, w_bits, n, tc_format=bs.TC_F4, a_enc=a_enc, w_enc=w_enc)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+def test_tc_fp4_bound_rejects_past_2p22():
+    """One past the bound is refused before launch (BS_ERR_OVERFLOW), nothing written."""
+    k = 18_642  # 18,642 * 225 = 4,194,450 >= 2^22
+    a = torch.full((2, k), 15, dtype=torch.uint8, device=DEV)
+    w_tc = bs.dense_tc_prepare_weights(bs.bitpack(torch.full((3, k), 15, dtype=torch.uint8, device=DEV), 4), 4,
+                                       bs.UNIPOLAR, 3, k, tc_format=bs.TC_F4)
+    out = torch.full((2, 3), -7, dtype=torch.int32, device=DEV)
+    with pytest.raises(bs.BitserialError, match="2\\^22"):
+        bs.bitserial_dense_tc_i8(a, 4, w_tc, 4, 3, out=out, tc_format=bs.TC_F4)
+    assert bool((out == -7).all())
+
+
 @pytest.mark.parametrize("max_ctas", [1, 7, 148])
 def test_bitpack_capped_grid(max_ctas):
     """bs_bitpack_ex with a small grid (the batched fast path plus its tail) packs
