@@ -63,7 +63,7 @@ constexpr int chunk_words(bool f4) { return f4 ? 8 : 4; }
 constexpr int kTeams = BS_TC_TEAMS;                    // producer teams (K chunks in flight)
 constexpr int kProducerWarps = 4 * kTeams;             // a team = 4 warps = one thread per row
 constexpr int kProducerThreads = kProducerWarps * 32;
-constexpr int kBarBytes = 512;  // mbarriers (3 per stage + 4), the "chunks freed" counter
+constexpr int kBarBytes = 1024;  // mbarriers (2 per A stage, 2 per B slot, 4), the "chunks freed" counter
 #ifndef BS_TC_MAX_STAGES
 #define BS_TC_MAX_STAGES 8
 #endif
@@ -82,7 +82,7 @@ constexpr int kEpiBufBytes = 32 * 128;  // one 32 x 32 int32 box
 #endif
 constexpr int kEpiBufs = BS_TC_EPI_BUFS;  // staging buffers (TMA stores in flight) per epilogue warp
 constexpr int kEpiBytes = kEpiWarps * kEpiBufs * kEpiBufBytes;
-constexpr int kSmemLimit = 227 * 1024;
+constexpr int kSmemLimit = 226 * 1024;  // dynamic shared memory (the kernel also has 1 KB static)
 constexpr int kMinSmem = 116 * 1024;  // > half the SM: guarantees one CTA per SM (TMEM)
 constexpr int kMaxTaps = 64;          // filter taps held in the shared-memory tap table
 constexpr int kGroupMax = 16;         // problems in one grouped launch
@@ -602,16 +602,22 @@ struct Cfg {
   static constexpr int kBBytes = kWP * BN * kBRow;        // shared memory per stage (B only)
   static constexpr int kSFCols = F4 ? 16 + 8 * kWP : 0;   // SFA: up to 4 x 4 cols; SFB: kWP x 8
   static constexpr int kFixed = 1024 /*align slack*/ + kBarBytes + NP * 512 /*tap tables*/ + kEpiBytes;
-  static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;
+  static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;   // B chunk slots that fit
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
-  // Producers learn that a stage is free from a monotonic "chunks freed" counter that
-  // one warp publishes after waiting on each stage's empty barrier in chunk order (an
-  // mbarrier parity wait by a producer team could alias two phases when teams visit
-  // the same stage), so the stage count is independent of the team count.
-  static constexpr int kStages = kFit > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFit;
+  // A operand ring (tensor memory): kStages stages.  Producers learn that a stage is free
+  // from a monotonic "chunks freed" counter that one warp publishes after waiting on each
+  // stage's empty barrier in chunk order (an mbarrier parity wait by a producer team could
+  // alias two phases when teams visit the same stage), so the stage count is independent
+  // of the team count.
+  static constexpr int kStages = kFitTmem > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFitTmem;
+  // B operand (shared memory): kBSlots chunk slots, decoupled from the A ring.  A tile whose
+  // K chunks all fit keeps its weights RESIDENT (chunk kc in slot kc) and the next tile of
+  // the same (problem, N block) reuses them without a reload; longer K streams through the
+  // slots as a ring (BPlan).
+  static constexpr int kBSlots = kFitSmem > 32 ? 32 : kFitSmem;
   static constexpr int kTeamsUsed = kStages < kTeams ? kStages : kTeams;
-  static constexpr int kUsed = kFixed + kStages * kBBytes;
+  static constexpr int kUsed = kFixed + kBSlots * kBBytes;
   static constexpr int kBytes = kUsed < kMinSmem ? kMinSmem : kUsed;
   static constexpr int kTmemCols = 512;  // 2*BN accumulator columns + the A ring; one CTA per SM
   static constexpr int kSF0 = 2 * BN;               // first scale-factor column (F4)
@@ -640,12 +646,14 @@ inline FastDiv make_fastdiv(uint32_t d) {
 // One problem of a launch (a single conv / dense, or one member of a group).
 struct TcProb {
   ConvProblem p;
-  int ntn;          // N-tiles per M block
+  int ntn;          // N blocks
+  int nmb;          // M blocks (tiles are N-major: tile = nblk * nmb + mblk, so a CTA's consecutive
+                    // tiles share an N block and its resident weights)
   int nchunks;      // K chunks (of 4 words) per tile
   int tile0;        // first tile of this problem in the launch's tile sequence
   int epi;          // EpiMode: direct 16-byte stores (OC % 4 == 0), TMA stores, or scalar
   uint32_t idesc;   // MMA instruction descriptor (N = 64 for OC <= 64 inside a BN = 128 group)
-  FastDiv div_hw, div_ow, div_kwid, div_ntn, div_kwa;  // n / (oh*ow), / ow, / kw, / ntn, / Cw
+  FastDiv div_hw, div_ow, div_kwid, div_nm, div_kwa;  // n / (oh*ow), / ow, / kw, / nmb, / Cw
   int kwa_shift;    // log2(Cw) when Cw is a power of two, else -1
   int taps;         // kh * kw (the tap table is used when taps <= kMaxTaps)
 };
@@ -658,8 +666,7 @@ struct TcArgs {
   int nprob, ntiles;  // problems, tiles of all problems
   int nset0, tiles0;  // grouped launches: problems [0, nset0) (tensor-heavy) own tiles [0, tiles0); the rest
                       // (output-heavy) [tiles0, ntiles); each CTA interleaves its tiles of the two sets
-  int b_resident;     // single problem, ntn == 1 and the whole expanded B fits: loaded once
-  int b_bytes;        // bytes of the B region (resident: nchunks stages, else kStages)
+  int b_bytes;        // bytes of the B region (kBSlots chunk slots)
   int npeer;          // single-problem launches: every output box is also stored through peer[0..npeer)
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                       // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
@@ -678,6 +685,36 @@ struct TcMaps {
 #else
 #define DBG(bit) 0
 #endif
+
+// (M block, N block) of a problem's tile (N-major order).
+__device__ __forceinline__ void tile_mn(const TcProb& P, int tile, uint32_t& mblk, uint32_t& nblk) {
+  const uint32_t tl = uint32_t(tile - P.tile0);
+  nblk = P.div_nm.div(tl);
+  mblk = tl - nblk * P.div_nm.d;
+}
+
+// Where each K chunk's weights live in the B slots, decided identically by the TMA warp
+// (which loads) and the MMA warp (which waits / releases) as both walk the tile sequence.
+// Resident (nchunks <= slots): chunk kc in slot kc, loaded only when the (problem, N block)
+// differs from the previous tile's; streaming: ring slots, always loaded.
+struct BPlan {
+  int key_pi = -1, key_nb = -1, ring = 0;
+  __device__ __forceinline__ void next(int pi, int nb, int nchunks, int nslots, bool& res, bool& reload,
+                                       int& slot0) {
+    res = nchunks <= nslots;
+    if (res) {
+      reload = !(pi == key_pi && nb == key_nb);
+      key_pi = pi;
+      key_nb = nb;
+      slot0 = 0;
+    } else {
+      reload = true;
+      key_pi = -1;
+      slot0 = ring;
+      ring = (ring + nchunks) % nslots;
+    }
+  }
+};
 
 // A CTA's tile sequence.  Single problem: blockIdx.x, +gridDim.x, ...  Grouped: the CTA's
 // share of each set (same grid stride) merged in proportion, so tensor-heavy tiles (long
@@ -726,23 +763,25 @@ template <int A_BITS, int W_BITS, int BN, bool F4, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_conv_kernel(const __grid_constant__ TcArgs<NP> args, const __grid_constant__ TcMaps<NP> maps) {
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
-  constexpr int S = C::kStages;
-  static_assert(S >= 2, "tensor-core tile does not fit two stages of shared memory");
+  constexpr int S = C::kStages;   // A ring stages (tensor memory)
+  constexpr int NB = C::kBSlots;  // B chunk slots (shared memory)
+  static_assert(S >= 2 && NB >= 2, "tensor-core tile does not fit two stages");
   static_assert(C::kBytes <= kSmemLimit, "shared memory");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* s_stage = smem;                            // B: S ring stages, or nchunks resident
+  uint8_t* s_stage = smem;                            // B: NB chunk slots
   uint8_t* s_epi = smem + args.b_bytes;               // epilogue staging: warps x bufs x 4 KB (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_epi + kEpiBytes);
   uint64_t* full_a = bars;
-  uint64_t* full_b = bars + S;
-  uint64_t* empty = bars + 2 * S;
-  uint64_t* acc_full = bars + 3 * S;
-  uint64_t* acc_empty = bars + 3 * S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* empty = bars + S;           // A stage consumed (MMA commit)
+  uint64_t* full_b = bars + 2 * S;      // B slot loaded (TMA transaction bytes)
+  uint64_t* empty_b = bars + 2 * S + NB;  // B slot released before a reload (MMA commit)
+  uint64_t* acc_full = bars + 2 * S + 2 * NB;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 4);
   int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // [NP][kMaxTaps] {offset, ky<<16|kx}
   int* s_freed = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes - 16);  // chunks whose stage is free
-  static_assert(8 * (3 * S + 4) + 4 <= kBarBytes - 16, "barrier region");
+  static_assert(8 * (2 * S + 2 * NB + 4) + 4 <= kBarBytes - 16, "barrier region");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (lane == 0 && (warp == 0 || warp == kMmaWarp)) STAMP("start")
@@ -763,8 +802,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_u32(full_a + s), 4);  // the 4 warps of one team
-      mbar_init(smem_u32(full_b + s), 1);
       mbar_init(smem_u32(empty + s), 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(smem_u32(full_b + b), 1);
+      mbar_init(smem_u32(empty_b + b), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(acc_full + a), 1);
@@ -859,7 +901,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t* rorg = LP.act;   // receptive-field origin (iy0, ix0) of the row (may lie in the padding)
     auto set_tile = [&](int t) {
       const TcProb& P = args.prob[pi];
-      const uint32_t mblk = P.div_ntn.div(uint32_t(t - P.tile0));
+      uint32_t mblk, nblk;
+      tile_mn(P, t, mblk, nblk);
       const int64_t m = int64_t(mblk) * BM + arow;
       rok = m < P.p.M;
       const uint32_t mm = rok ? uint32_t(m) : 0u;
@@ -1036,35 +1079,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     // producer warps of teams this configuration does not use: idle
   } else if (warp == kTmaWarp) {
     // ================= weight tiles by TMA, and the "chunks freed" counter: waits on each
-    // stage's empty barrier in chunk order, then publishes that chunk g may be written
+    // A stage's empty barrier in chunk order, then publishes that chunk g may be written;
+    // loads the chunk's weights into its B slot unless they are resident (BPlan)
     if (lane == 0) {
-      const bool resident = args.b_resident;  // single-problem launches only
-      if (resident) {  // whole B once (one N block): every K chunk, W planes
-        const uint32_t fb = smem_u32(full_b);
-        const int nchunks = args.prob[0].nchunks;
-        mbar_expect_tx(fb, uint32_t(C::kBBytes) * uint32_t(nchunks));
-        for (int kc = 0; kc < nchunks; ++kc) {
-          const uint32_t sB = smem_u32(s_stage + kc * C::kBBytes);
-#pragma unroll
-          for (int j = 0; j < C::kWP; ++j)
-            tma_load_2d(sB + j * BN * C::kBRow, &maps.w[0], kc * C::kBRow, j * args.prob[0].p.oc, fb);
-        }
-      }
       int stage = 0, g = 0, pi = 0, tile = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, ldpar = 0;  // ldpar bit b: parity of the loads issued into B slot b
+      BPlan plan;
       for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
         const TcProb& P = args.prob[pi];
-        const int n0 = ((tile - P.tile0) % P.ntn) * BN, nchunks = P.nchunks, oc = P.p.oc;
+        uint32_t mb, nb;
+        tile_mn(P, tile, mb, nb);
+        const int n0 = int(nb) * BN, nchunks = P.nchunks, oc = P.p.oc;
         const CUtensorMap* tw = &maps.w[pi];
+        bool res, reload;
+        int slot;
+        plan.next(pi, int(nb), nchunks, NB, res, reload, slot);
         for (int kc = 0; kc < nchunks; ++kc, ++g) {
           PROF_BEGIN
           mbar_wait(smem_u32(empty + stage), phase ^ 1u);
           PROF_END(0)
           asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_freed)), "r"(g + 1) : "memory");
-          if (!resident) {
-            const uint32_t fb = smem_u32(full_b + stage);
+          if (reload) {
+            const uint32_t bit = 1u << slot;
+            mbar_wait(smem_u32(empty_b + slot), (ldpar & bit) ? 0u : 1u);  // the slot's previous use released
+            ldpar ^= bit;
+            const uint32_t fb = smem_u32(full_b + slot);
             mbar_expect_tx(fb, uint32_t(C::kBBytes));
-            const uint32_t sB = smem_u32(s_stage + stage * C::kBBytes);
+            const uint32_t sB = smem_u32(s_stage + slot * C::kBBytes);
 #pragma unroll
             for (int j = 0; j < C::kWP; ++j) tma_load_2d(sB + j * BN * C::kBRow, tw, kc * C::kBRow, j * oc + n0, fb);
           }
@@ -1072,6 +1113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage = 0;
             phase ^= 1u;
           }
+          slot = (res || slot + 1 < NB) ? slot + 1 : 0;
         }
       }
     }
@@ -1079,18 +1121,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= MMA issuer: the whole warp walks the loop (uniform values); one
     // elected lane issues.  TMEM base is column 0 (all 512 columns are this CTA's).
     int stage = 0, acc = 0, pi = 0, tile = 0;
-    uint32_t phase = 0, acc_phase = 0;
+    uint32_t phase = 0, acc_phase = 0, fpar = 0;  // fpar bit b: parity of the loads consumed from B slot b
     bool first = true;
-    const bool resident = args.b_resident;
     const uint64_t bdesc0 = smem_desc_sw128(smem_u32(s_stage));
-    if (resident) mbar_wait(smem_u32(full_b), 0);
-    if (lane == 0) STAMP("b_resident_ready")
-    for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
+    BPlan plan;
+    TileSeq<NP> seq(args);
+    bool have = seq.next(args, tile, pi);
+    while (have) {
+      int ntile = 0, npi = 0;
+      const bool nhave = seq.next(args, ntile, npi);
       // single-problem launches: N = BN is known at compile time (an immediate descriptor
       // saves a constant-bank reload per MMA); groups: the member's N (64 or BN)
       constexpr uint32_t kIdesc = NP == 1 ? (F4 ? idesc_mxf4(BN) : idesc_i8(BN)) : 0u;
-      const uint32_t idesc = args.prob[pi].idesc;
-      const int nchunks = args.prob[pi].nchunks;
+      const TcProb& P = args.prob[pi];
+      const uint32_t idesc = P.idesc;
+      const int nchunks = P.nchunks;
+      uint32_t mb, nb;
+      tile_mn(P, tile, mb, nb);
+      bool res, reload;
+      int slot;
+      plan.next(pi, int(nb), nchunks, NB, res, reload, slot);
+      bool keep = false;  // the next tile reuses this tile's resident weights: no release
+      if (res && nhave && npi == pi) {
+        uint32_t mb2, nb2;
+        tile_mn(args.prob[npi], ntile, mb2, nb2);
+        keep = nb2 == nb;
+      }
       PROF_BEGIN
       mbar_wait(smem_u32(acc_empty + acc), acc_phase ^ 1u);
       PROF_END(0)
@@ -1101,11 +1157,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!DBG(4)) mbar_wait(smem_u32(full_a + stage), phase);  // knob 4: MMA-only timing
         PROF_END(1)
         PROF_BEGIN
-        if (!resident) mbar_wait(smem_u32(full_b + stage), phase);
+        if (reload) {
+          mbar_wait(smem_u32(full_b + slot), (fpar >> slot) & 1u);
+          fpar ^= 1u << slot;
+        }
         PROF_END(2)
         tc_fence_after();
         const uint32_t a_base = uint32_t(C::kAcol0 + stage * C::kACols);
-        const uint64_t b_desc = bdesc0 + uint64_t(((resident ? kc : stage) * C::kBBytes) >> 4);
+        const uint64_t b_desc = bdesc0 + uint64_t((slot * C::kBBytes) >> 4);
 #pragma unroll
         for (int i = 0; i < C::kAP; ++i)
 #pragma unroll
@@ -1119,10 +1178,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                       (kc | i | j) != 0);
           }
         mma_commit_elect(smem_u32(empty + stage));
+        if (!keep) mma_commit_elect(smem_u32(empty_b + slot));
         if (++stage == S) {
           stage = 0;
           phase ^= 1u;
         }
+        slot = (res || slot + 1 < NB) ? slot + 1 : 0;
       }
       mma_commit_elect(smem_u32(acc_full + acc));
       if (lane == 0 && first) STAMP("first_tile_issued")
@@ -1131,6 +1192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc = 0;
         acc_phase ^= 1u;
       }
+      tile = ntile;
+      pi = npi;
+      have = nhave;
     }
   } else {
     // ================= epilogue: warp q = warp % 4 owns TMEM lanes / tile rows 32q..32q+31
@@ -1143,9 +1207,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool first = true;
     for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
       const TcProb& P = args.prob[pi];
-      const int tl = tile - P.tile0;
-      const int64_t m0 = int64_t(tl / P.ntn) * BM;
-      const int n0 = (tl % P.ntn) * BN;
+      uint32_t mb, nb;
+      tile_mn(P, tile, mb, nb);
+      const int64_t m0 = int64_t(mb) * BM;
+      const int n0 = int(nb) * BN;
       const int oc = P.p.oc, epi = P.epi;
       const int64_t M = P.p.M;
       int32_t* const out = P.p.out;
@@ -1303,7 +1368,8 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
                int bn, bool f4, int64_t& tiles) {
   P.p = p;
   P.ntn = (p.oc + bn - 1) / bn;
-  tiles = (p.M + BM - 1) / BM * P.ntn;
+  P.nmb = int((p.M + BM - 1) / BM);
+  tiles = int64_t(P.nmb) * P.ntn;
   const int64_t kpad = tc_kpad(p.kp, f4 ? kTcF4 : kTcI8);
   P.nchunks = int(kpad / chunk_words(f4));
   P.tile0 = tile0;
@@ -1317,7 +1383,7 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
   P.div_hw = make_fastdiv(uint32_t(p.oh) * uint32_t(p.ow));
   P.div_ow = make_fastdiv(uint32_t(p.ow));
   P.div_kwid = make_fastdiv(uint32_t(p.kwid));
-  P.div_ntn = make_fastdiv(uint32_t(P.ntn));
+  P.div_nm = make_fastdiv(uint32_t(P.nmb));
   P.div_kwa = make_fastdiv(uint32_t(p.kw_a));
   P.taps = p.kh * p.kwid;
   // the table's int32 word offsets: (ky*W + kx)*Cw must fit
@@ -1376,11 +1442,7 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
   }
   a.npeer = npeer;
   a.tiles0 = a.nset0 < count ? a.prob[a.nset0].tile0 : a.ntiles;
-  const char* res_env = getenv("BS_TC_RESIDENT");
-  const bool allow_res = !(res_env && res_env[0] == '0');
-  const int64_t res_bytes = int64_t(a.prob[0].nchunks) * C::kBBytes;
-  a.b_resident = NP == 1 && allow_res && a.prob[0].ntn == 1 && C::kFixed + res_bytes <= kSmemLimit;
-  a.b_bytes = int(a.b_resident ? res_bytes : int64_t(C::kStages) * C::kBBytes);
+  a.b_bytes = C::kBSlots * C::kBBytes;
   const char* dbg_env = getenv("BS_TC_DEBUG");
   a.debug = dbg_env ? atoi(dbg_env) : 0;
   int smem_bytes = C::kFixed + a.b_bytes;
