@@ -102,6 +102,26 @@ const char* bs_last_error(void);
  * Used by bench.py to report how many of the library's kernels a step runs. */
 int64_t bs_kernel_launches(void);
 
+/* Tuning knobs of the tensor-core path, process-wide (atomic; every later launch on any
+ * thread sees the new value).  They never change results, only the launch configuration;
+ * 0 is the library's choice.  For tests and experiments:
+ *   BS_TUNE_TC_TILE_N      : output tile width 64 or 128 (default: 64 when oc <= 64, else 128)
+ *   BS_TUNE_TC_EPILOGUE    : 1 = direct 16-byte global stores instead of TMA stores
+ *   BS_TUNE_TC_GROUP_SPLIT : 1 = grouped launches interleave long-K and short-K members' tiles
+ *   BS_TUNE_TC_B_SLOTS     : cap on the weight chunk slots in shared memory (2..32): fewer slots
+ *                            than a tile's K chunks make its weights stream instead of staying
+ *                            resident
+ * bs_set_tuning returns BS_ERR_INVALID_ARG for an unknown knob or value; bs_get_tuning returns
+ * the current value (0 for an unknown knob). */
+typedef enum {
+  BS_TUNE_TC_TILE_N = 0,
+  BS_TUNE_TC_EPILOGUE = 1,
+  BS_TUNE_TC_GROUP_SPLIT = 2,
+  BS_TUNE_TC_B_SLOTS = 3
+} bs_tune_knob;
+int bs_set_tuning(int knob, int value);
+int bs_get_tuning(int knob);
+
 /* Words per packed row for reduction length k: ceil(k/32) rounded up to an even
  * number (8-byte rows).  Returns 0 for k <= 0. */
 int64_t bs_packed_row_words(int64_t k);

@@ -27,18 +27,26 @@ __all__ = [
     "bitserial_dense_tc_prepared", "bitserial_conv2d_nhwc_tc_i8", "bitserial_dense_tc_i8",
     "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
     "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group",
-    "bitserial_dense_tc_gather", "TcHostDesc", "bitserial_conv2d_nhwc_tc_host_group",
+    "bitserial_dense_tc_gather", "TcHostDesc", "bitserial_conv2d_nhwc_tc_host_group", "set_tuning", "get_tuning",
+    "TUNE_TC_TILE_N", "TUNE_TC_EPILOGUE", "TUNE_TC_GROUP_SPLIT", "TUNE_TC_B_SLOTS",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
 A_UNSIGNED, A_BIPOLAR, A_SIGNED = 0, 1, 2    # activation encodings (bs_a_encoding)
 TC_DEFAULT, TC_I8, TC_F4 = 0, 1, 2  # bs_tc_format
 ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV = 0, 1, 2, 3
+TUNE_TC_TILE_N, TUNE_TC_EPILOGUE, TUNE_TC_GROUP_SPLIT, TUNE_TC_B_SLOTS = 0, 1, 2, 3  # bs_tune_knob
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# BITSERIAL_LIB selects an alternative build of the same library (A/B timing of
-# compile-time variants in tools/); default is the in-tree product library.
-_LIB_PATH = os.environ.get("BITSERIAL_LIB") or os.path.join(_HERE, "libbitserial.so")
+# BITSERIAL_LIB selects an experiment build of the same library (A/B timing of compile-time
+# variants in tools/); it must live under the repository's build/ directory.  Default: the
+# in-tree product library.
+_LIB_PATH = os.path.join(_HERE, "libbitserial.so")
+if os.environ.get("BITSERIAL_LIB"):
+    _alt = os.path.realpath(os.environ["BITSERIAL_LIB"])
+    if not _alt.startswith(os.path.join(os.path.dirname(_HERE), "build") + os.sep):
+        raise ImportError(f"BITSERIAL_LIB={_alt}: experiment builds must be under the repository's build/ directory")
+    _LIB_PATH = _alt
 _lib = None
 
 EXPORTED_SYMBOLS = (
@@ -52,7 +60,7 @@ EXPORTED_SYMBOLS = (
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
     "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitserial_dense_tc_prepared_gather",
-    "bs_bitserial_conv2d_nhwc_tc_host_group",
+    "bs_bitserial_conv2d_nhwc_tc_host_group", "bs_set_tuning", "bs_get_tuning",
 )
 
 
@@ -107,6 +115,8 @@ def _load():
         "bs_bitpack_group": ([P, I, I, P], I),
         "bs_bitserial_conv2d_nhwc_tc_host_group": ([P, I, I, I, I, P], I),
         "bs_bitserial_dense_tc_prepared_gather": ([P, I, I, P, I, I, I, P, P, I, L, L, L, P], I),
+        "bs_set_tuning": ([I, I], I),
+        "bs_get_tuning": ([I], I),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("BITSERIAL_LIB") and not hasattr(lib, name):
@@ -146,6 +156,15 @@ def abi_version() -> int:
 def kernel_launches() -> int:
     """Kernels launched by libbitserial.so so far in this process (bs_kernel_launches)."""
     return int(_load().bs_kernel_launches())
+
+
+def set_tuning(knob: int, value: int) -> None:
+    """bs_set_tuning: a process-wide launch-configuration knob (TUNE_*; 0 = library choice)."""
+    _check(_load().bs_set_tuning(int(knob), int(value)))
+
+
+def get_tuning(knob: int) -> int:
+    return int(_load().bs_get_tuning(int(knob)))
 
 
 def packed_row_words(k: int) -> int:

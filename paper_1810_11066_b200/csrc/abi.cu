@@ -13,6 +13,22 @@ namespace bs {
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+std::atomic<int> g_tune[kTuneCount];
+int tuning(int knob) { return knob >= 0 && knob < kTuneCount ? g_tune[knob].load(std::memory_order_relaxed) : 0; }
+
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+int device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  if (dev < kMaxDevices)
+    if (int n = g_sms[dev].load(std::memory_order_relaxed)) return n;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;  // B200
+  if (dev < kMaxDevices) g_sms[dev].store(n, std::memory_order_relaxed);
+  return n;
+}
 }  // namespace bs
 
 namespace {
@@ -91,6 +107,8 @@ int check_algo(int algo, const char* fn) {
   return BS_OK;
 }
 
+constexpr int64_t kMaxRows = (int64_t(1) << 31) - 257;  // output rows (M) a launch may index
+
 struct ConvArgs {
   int n, h, w, c, oc, kh, kw, sh, sw, ph, pw;
 };
@@ -109,6 +127,10 @@ int check_conv(const ConvArgs& g, int a_bits, int w_bits, int w_enc, const char*
   if (conv_out(g.h, g.kh, g.sh, g.ph) <= 0 || conv_out(g.w, g.kw, g.sw, g.pw) <= 0)
     return fail(BS_ERR_SHAPE, "%s: empty output (kernel larger than padded input)", fn);
   if (int64_t(g.n) * g.h * g.w > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: too many pixels", fn);
+  // output rows M = n*oh*ow index the kernels' 32-bit row arithmetic (fast division, TMA
+  // coordinates) up to a tile past the end; oh, ow can exceed h, w when padded
+  if (int64_t(g.n) * conv_out(g.h, g.kh, g.sh, g.ph) * conv_out(g.w, g.kw, g.sw, g.pw) > kMaxRows)
+    return fail(BS_ERR_SHAPE, "%s: more than 2^31 - 257 output pixels", fn);
   if (int64_t(g.kh) * g.kw * row_words(g.c) > (int64_t(1) << 30)) return fail(BS_ERR_SHAPE, "%s: reduction too long", fn);
   return check_bound(int64_t(g.kh) * g.kw * g.c, a_bits, w_bits, fn);
 }
@@ -147,7 +169,7 @@ int dense_core(const uint32_t* a_packed, const uint8_t* a_codes, int a_bits, con
     return cuda_status(bs::launch_gemv(a_packed, a_codes, a_bits, w_packed, w_bits, w_enc == BS_BIPOLAR, out, m, n, k,
                                        kwp, s), fn);
   if (a_codes) return fail(BS_ERR_UNSUPPORTED, "%s: internal: codes path needs GEMV", fn);
-  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};  // dense = 1x1 conv over m "pixels"
   bs::ConvProblem p = make_conv(a_packed, a_bits, w_packed, w_bits, w_enc, out, g);
   return launch_conv(p, algo, s, fn);
@@ -160,6 +182,45 @@ int check_dense(const void* a, const uint32_t* w, const int32_t* out, int a_bits
   if (m <= 0 || n <= 0 || k <= 0) return fail(BS_ERR_SHAPE, "%s: m, n, k must be >= 1", fn);
   if (!aligned16(a) || !aligned16(w) || !aligned16(out)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
   return check_bound(k, a_bits, w_bits, fn);
+}
+
+// Side streams and events of the pipelined host-buffer entry, kept per thread (created on
+// first use, re-created when the thread's current device changes, grown to the largest
+// event count seen) instead of being created and destroyed on every call.
+struct HostPipe {
+  int dev = -1;
+  cudaStream_t in = nullptr, out = nullptr;
+  std::vector<cudaEvent_t> ev;
+  void release() {
+    for (auto& x : ev)
+      if (x) cudaEventDestroy(x);
+    ev.clear();
+    if (in) cudaStreamDestroy(in);
+    if (out) cudaStreamDestroy(out);
+    in = out = nullptr;
+    dev = -1;
+  }
+  cudaError_t prepare(size_t events) {
+    int d = 0;
+    if (cudaError_t e = cudaGetDevice(&d)) return e;
+    if (d != dev) {
+      release();
+      if (cudaError_t e = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking)) return e;
+      if (cudaError_t e = cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking)) return e;
+      dev = d;
+    }
+    while (ev.size() < events) {
+      cudaEvent_t x = nullptr;
+      if (cudaError_t e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) return e;
+      ev.push_back(x);
+    }
+    return cudaSuccess;
+  }
+  ~HostPipe() { release(); }
+};
+HostPipe& host_pipe() {
+  thread_local HostPipe p;
+  return p;
 }
 
 }  // namespace
@@ -188,6 +249,28 @@ const char* bs_last_error(void) { return g_last_error; }
 int64_t bs_packed_row_words(int64_t k) { return row_words(k); }
 
 int64_t bs_kernel_launches(void) { return bs::launch_count(); }
+
+int bs_set_tuning(int knob, int value) {
+  const char* fn = "bs_set_tuning";
+  switch (knob) {
+    case BS_TUNE_TC_TILE_N:
+      if (value != 0 && value != 64 && value != 128) return fail(BS_ERR_INVALID_ARG, "%s: tile width %d", fn, value);
+      break;
+    case BS_TUNE_TC_EPILOGUE:
+    case BS_TUNE_TC_GROUP_SPLIT:
+      if (value != 0 && value != 1) return fail(BS_ERR_INVALID_ARG, "%s: value %d not 0 or 1", fn, value);
+      break;
+    case BS_TUNE_TC_B_SLOTS:
+      if (value != 0 && (value < 2 || value > 32)) return fail(BS_ERR_INVALID_ARG, "%s: B slots %d", fn, value);
+      break;
+    default:
+      return fail(BS_ERR_INVALID_ARG, "%s: unknown knob %d", fn, knob);
+  }
+  bs::g_tune[knob].store(value, std::memory_order_relaxed);
+  return BS_OK;
+}
+
+int bs_get_tuning(int knob) { return bs::tuning(knob); }
 
 int bs_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int bits, void* stream) {
   return bs_bitpack_ex(in, out, rows, k, bits, 0, stream);
@@ -340,7 +423,7 @@ int bs_bitserial_dense_tc(const uint32_t* a_packed, int a_bits, const uint32_t* 
   if (int st = check_dense(a_packed, w_packed, out, a_bits, w_bits, w_enc, m, n, k, fn)) return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, BS_TC_DEFAULT, fn)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
-  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   const int64_t need = bs_dense_tc_workspace_bytes(n, k, w_bits);
   if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
   if (!aligned16(workspace)) return fail(BS_ERR_ALIGN, "%s: workspace must be 16-byte aligned", fn);
@@ -478,7 +561,7 @@ int bs_bitserial_dense_tc_prepared(const uint32_t* a_packed, int a_bits, int a_e
     return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
-  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
   bs::ConvProblem p = make_conv(a_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out, g);
   p.a_enc = a_enc;
@@ -497,7 +580,7 @@ int bs_bitserial_dense_tc_prepared_gather(const uint32_t* a_packed, int a_bits, 
     return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
-  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   if (npeers < 0 || npeers > 8) return fail(BS_ERR_INVALID_ARG, "%s: npeers=%d not in [0,8]", fn, npeers);
   if (npeers > 0 && !out_peers) return fail(BS_ERR_NULL, "%s: NULL out_peers", fn);
   if (npeers > 0 && n % 4 != 0) return fail(BS_ERR_UNSUPPORTED, "%s: the fused gather needs n %% 4 == 0", fn);
@@ -522,7 +605,7 @@ int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, int a_enc, const int8
     return st;
   if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
   if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
-  if (m > (int64_t(1) << 31) - 1 || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
   const int64_t need = bs_dense_workspace_bytes(m, k, a_bits);
   if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
   if (!aligned16(workspace)) return fail(BS_ERR_ALIGN, "%s: workspace must be 16-byte aligned", fn);
@@ -578,14 +661,14 @@ int bs_bitserial_conv2d_nhwc_tc_host_group(const bs_tc_host_desc* descs, int cou
     ps[q].a_enc = d.a_enc;
   }
   // three-stage pipeline: uploads on one stream, pack + conv on the caller's stream,
-  // downloads on a third; layer q's download overlaps layer q+1's upload and compute
-  cudaStream_t s = static_cast<cudaStream_t>(stream), s_in = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(count) + 2, nullptr);
-  cudaError_t e = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
-  for (auto& x : ev)
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
-  cudaEvent_t start = ev[0], end = ev[1];
+  // downloads on a third; layer q's download overlaps layer q+1's upload and compute.
+  // The side streams and events are this thread's, created once per device (HostPipe).
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HostPipe& hp = host_pipe();
+  cudaError_t e = hp.prepare(2 * count + 2);
+  cudaStream_t s_in = hp.in, s_out = hp.out;
+  const std::vector<cudaEvent_t>& ev = hp.ev;
+  cudaEvent_t start = e == cudaSuccess ? ev[0] : nullptr, end = e == cudaSuccess ? ev[1] : nullptr;
   if (e == cudaSuccess) e = cudaEventRecord(start, s);  // nothing starts before the caller's prior work
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s_in, start, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, start, 0);
@@ -610,10 +693,6 @@ int bs_bitserial_conv2d_nhwc_tc_host_group(const bs_tc_host_desc* descs, int cou
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (s_in) cudaStreamSynchronize(s_in);
   if (s_out) cudaStreamSynchronize(s_out);
-  for (auto& x : ev)
-    if (x) cudaEventDestroy(x);
-  if (s_in) cudaStreamDestroy(s_in);
-  if (s_out) cudaStreamDestroy(s_out);
   return cuda_status(e, fn);
 }
 

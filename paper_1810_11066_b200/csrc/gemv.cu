@@ -16,6 +16,7 @@
 //    "tree reduction" of PAPER.md:698/705 — and the 8 results go out as one segment.
 //  * HBM-bound at large N*K (weights are read once: W*N*K/8 bytes), latency-bound
 //    at config 2's 2 MiB.
+#include <atomic>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -181,14 +182,17 @@ cudaError_t launch_aw(const uint32_t* a_packed, const uint8_t* a_codes, const ui
   const int64_t warps = (n + kR - 1) / kR;
   const unsigned grid = unsigned((warps + kGemvThreads / 32 - 1) / (kGemvThreads / 32));
   const bool vec4 = (kwp % 4 == 0) && (reinterpret_cast<uintptr_t>(w_packed) % 16 == 0);
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const uint64_t dev_bit = dev < 64 ? uint64_t(1) << dev : 0;
 #define BS_GEMV(VEC, FUSED)                                                                            \
   {                                                                                                    \
     auto kern = gemv_kernel<A, W, VEC, FUSED>;                                                         \
-    static int configured = 0;                                                                         \
-    if (int(smem) > configured) {                                                                      \
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+    static std::atomic<uint64_t> configured{0}; /* per device: opt-in to kMaxSmem once */           \
+    if (!dev_bit || !(configured.load(std::memory_order_acquire) & dev_bit)) {                         \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxSmem)); \
       if (e != cudaSuccess) return e;                                                                  \
-      configured = int(smem);                                                                          \
+      configured.fetch_or(dev_bit, std::memory_order_release);                                         \
     }                                                                                                  \
     kern<<<grid, kGemvThreads, smem, stream>>>(a_packed, a_codes, w_packed, out, int(m), n, k, int(kwp), bipolar); \
   }

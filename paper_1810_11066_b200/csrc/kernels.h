@@ -35,6 +35,12 @@ struct ConvProblem {
 void note_launch();
 int64_t launch_count();
 
+// Process-wide tuning knobs (bs_set_tuning; atomics, read per launch; 0 = library choice).
+enum TuneKnob : int { kTuneTileN = 0, kTuneEpilogue = 1, kTuneGroupSplit = 2, kTuneBSlots = 3, kTuneCount = 4 };
+int tuning(int knob);
+// SM count of the current device (cached per device).
+int device_sms();
+
 enum class Algo : int { Auto = 0, Popc = 1, PopcLit = 2, Gemv = 3 };
 
 cudaError_t launch_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int64_t kwp, int bits,

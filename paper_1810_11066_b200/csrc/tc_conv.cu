@@ -41,6 +41,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -63,7 +64,7 @@ constexpr int chunk_words(bool f4) { return f4 ? 8 : 4; }
 constexpr int kTeams = BS_TC_TEAMS;                    // producer teams (K chunks in flight)
 constexpr int kProducerWarps = 4 * kTeams;             // a team = 4 warps = one thread per row
 constexpr int kProducerThreads = kProducerWarps * 32;
-constexpr int kBarBytes = 1024;  // mbarriers (2 per A stage, 2 per B slot, 4), the "chunks freed" counter
+constexpr int kBarBytes = 1024;  // mbarriers (2 per A stage, 2 per B slot, 4) and the TMEM address slot
 #ifndef BS_TC_MAX_STAGES
 #define BS_TC_MAX_STAGES 8
 #endif
@@ -115,10 +116,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 // ------------------------------------------------------------------ PTX wrappers
 // Activation gathers allocate in L1: consecutive K chunks (filter taps) of a tile re-read
 // mostly the same pixels (measured 4% faster over the ResNet layers than L1::no_allocate)
-// back-off of a producer team polling the "chunks freed" counter
-#ifndef BS_TC_FREE_NS
-#define BS_TC_FREE_NS 20
-#endif
 #ifndef BS_TC_LDG_HINT
 #define BS_TC_LDG_HINT ""
 #endif
@@ -605,18 +602,18 @@ struct Cfg {
   static constexpr int kFitSmem = (kSmemLimit - kFixed) / kBBytes;   // B chunk slots that fit
   static constexpr int kFitTmem = (512 - 2 * BN - kSFCols) / kACols;  // accumulators: 2 x BN columns
   static constexpr int kFit = kFitSmem < kFitTmem ? kFitSmem : kFitTmem;
-  // A operand ring (tensor memory): kStages stages.  Producers learn that a stage is free
-  // from a monotonic "chunks freed" counter that one warp publishes after waiting on each
-  // stage's empty barrier in chunk order (an mbarrier parity wait by a producer team could
-  // alias two phases when teams visit the same stage), so the stage count is independent
-  // of the team count.
-  static constexpr int kStages = kFitTmem > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFitTmem;
+  // A operand ring (tensor memory): kStages stages, a multiple of the producer teams, so
+  // every stage belongs to ONE team (chunk g -> team g % T, stage g % S): the team waits on
+  // its stage's empty barrier with its own phase count (a hardware-suspended mbarrier wait,
+  // no polling, and no two teams that could alias each other's phases).
+  static constexpr int kFitA = kFitTmem > BS_TC_MAX_STAGES ? BS_TC_MAX_STAGES : kFitTmem;
+  static constexpr int kTeamsUsed = kFitA < kTeams ? kFitA : kTeams;
+  static constexpr int kStages = kFitA / kTeamsUsed * kTeamsUsed;
   // B operand (shared memory): kBSlots chunk slots, decoupled from the A ring.  A tile whose
   // K chunks all fit keeps its weights RESIDENT (chunk kc in slot kc) and the next tile of
   // the same (problem, N block) reuses them without a reload; longer K streams through the
   // slots as a ring (BPlan).
   static constexpr int kBSlots = kFitSmem > 32 ? 32 : kFitSmem;
-  static constexpr int kTeamsUsed = kStages < kTeams ? kStages : kTeams;
   static constexpr int kUsed = kFixed + kBSlots * kBBytes;
   static constexpr int kBytes = kUsed < kMinSmem ? kMinSmem : kUsed;
   static constexpr int kTmemCols = 512;  // 2*BN accumulator columns + the A ring; one CTA per SM
@@ -667,6 +664,7 @@ struct TcArgs {
   int nset0, tiles0;  // grouped launches: problems [0, nset0) (tensor-heavy) own tiles [0, tiles0); the rest
                       // (output-heavy) [tiles0, ntiles); each CTA interleaves its tiles of the two sets
   int b_bytes;        // bytes of the B region (kBSlots chunk slots)
+  int nbs;            // B chunk slots in use (<= kBSlots; BS_TUNE_TC_B_SLOTS caps it)
   int npeer;          // single-problem launches: every output box is also stored through peer[0..npeer)
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                       // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
@@ -780,10 +778,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 4);
   int2* s_tap = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes);  // [NP][kMaxTaps] {offset, ky<<16|kx}
-  int* s_freed = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes - 16);  // chunks whose stage is free
   static_assert(8 * (2 * S + 2 * NB + 4) + 4 <= kBarBytes - 16, "barrier region");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nbs = args.nbs;  // B slots in use (<= NB)
   if (lane == 0 && (warp == 0 || warp == kMmaWarp)) STAMP("start")
   PROF_DECL
 #ifdef BS_TC_PROFILE
@@ -812,7 +810,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(acc_full + a), 1);
       mbar_init(smem_u32(acc_empty + a), kEpiWarps);
     }
-    *s_freed = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -1034,12 +1031,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int enc = nenc;
       const int stage = g % S;
       PROF_BEGIN
-      for (;;) {  // stage of chunk g free (published in chunk order by the TMA warp)
-        int freed;
-        asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(freed) : "r"(smem_u32(s_freed)) : "memory");
-        if (freed > g) break;
-        __nanosleep(BS_TC_FREE_NS);
-      }
+      mbar_wait(smem_u32(empty + stage), ((g / S) & 1) ^ 1);  // this team's stage: its previous chunk consumed
       PROF_END(1)
       tc_fence_after();
       PROF_BEGIN  // slot 2: digit formation + tcgen05.st issue
@@ -1078,12 +1070,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < kProducerWarps) {
     // producer warps of teams this configuration does not use: idle
   } else if (warp == kTmaWarp) {
-    // ================= weight tiles by TMA, and the "chunks freed" counter: waits on each
-    // A stage's empty barrier in chunk order, then publishes that chunk g may be written;
-    // loads the chunk's weights into its B slot unless they are resident (BPlan)
+    // ================= weight tiles by TMA: each K chunk's weights into its B slot unless
+    // they are resident (BPlan); a slot is reloaded once the MMA released its previous use
     if (lane == 0) {
-      int stage = 0, g = 0, pi = 0, tile = 0;
-      uint32_t phase = 0, ldpar = 0;  // ldpar bit b: parity of the loads issued into B slot b
+      int pi = 0, tile = 0;
+      uint32_t ldpar = 0;  // bit b: parity of the loads issued into B slot b
       BPlan plan;
       for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
         const TcProb& P = args.prob[pi];
@@ -1093,15 +1084,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* tw = &maps.w[pi];
         bool res, reload;
         int slot;
-        plan.next(pi, int(nb), nchunks, NB, res, reload, slot);
-        for (int kc = 0; kc < nchunks; ++kc, ++g) {
-          PROF_BEGIN
-          mbar_wait(smem_u32(empty + stage), phase ^ 1u);
-          PROF_END(0)
-          asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_freed)), "r"(g + 1) : "memory");
-          if (reload) {
+        plan.next(pi, int(nb), nchunks, nbs, res, reload, slot);
+        for (int kc = 0; kc < nchunks && reload; ++kc) {
+          {
             const uint32_t bit = 1u << slot;
+            PROF_BEGIN
             mbar_wait(smem_u32(empty_b + slot), (ldpar & bit) ? 0u : 1u);  // the slot's previous use released
+            PROF_END(0)
             ldpar ^= bit;
             const uint32_t fb = smem_u32(full_b + slot);
             mbar_expect_tx(fb, uint32_t(C::kBBytes));
@@ -1109,11 +1098,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < C::kWP; ++j) tma_load_2d(sB + j * BN * C::kBRow, tw, kc * C::kBRow, j * oc + n0, fb);
           }
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1u;
-          }
-          slot = (res || slot + 1 < NB) ? slot + 1 : 0;
+          slot = (res || slot + 1 < nbs) ? slot + 1 : 0;
         }
       }
     }
@@ -1140,7 +1125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_mn(P, tile, mb, nb);
       bool res, reload;
       int slot;
-      plan.next(pi, int(nb), nchunks, NB, res, reload, slot);
+      plan.next(pi, int(nb), nchunks, nbs, res, reload, slot);
       bool keep = false;  // the next tile reuses this tile's resident weights: no release
       if (res && nhave && npi == pi) {
         uint32_t mb2, nb2;
@@ -1183,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           stage = 0;
           phase ^= 1u;
         }
-        slot = (res || slot + 1 < NB) ? slot + 1 : 0;
+        slot = (res || slot + 1 < nbs) ? slot + 1 : 0;
       }
       mma_commit_elect(smem_u32(acc_full + acc));
       if (lane == 0 && first) STAMP("first_tile_issued")
@@ -1231,12 +1216,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           PROF_BEGIN
           tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + cb * 32), r);
           PROF_END(1)
-          if constexpr (F4) {  // FP32 accumulator holding an exact integer |v| < 2^22 -> int32:
-            // v + 1.5*2^23 puts v in the low mantissa bits (one FADD + one IADD instead of
-            // the quarter-rate F2I)
+          if constexpr (F4) {  // FP32 accumulator holding an exact integer (|v| < 2^22) -> int32:
+            // one F2I per value (the conversion pipe; one issue slot per 32 values where the
+            // v + 1.5*2^23 trick takes two — the epilogue's issue slots are the scarce resource)
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              r[c] = uint32_t(__float_as_int(__uint_as_float(r[c]) + 12582912.0f) - 0x4B400000);
+            for (int c = 0; c < 32; ++c) r[c] = uint32_t(__float2int_rz(__uint_as_float(r[c])));
           }
         }
         if (cb + kCbStep >= ncb) {  // this warp's share of the accumulator drained: release it
@@ -1325,16 +1309,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------------ host side
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
-  }
-  return n;
-}
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (the library does not
 // link libcuda, so it still loads on hosts without a driver).
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1375,8 +1349,7 @@ bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvProblem& p
   P.tile0 = tile0;
   // TMA-store epilogue by default (direct 16-byte stores of one row segment per lane
   // measured 1.4-1.8x slower on the output-bound layers); BS_TC_EPI=direct selects them.
-  const char* epi_env = getenv("BS_TC_EPI");
-  const bool want_direct = epi_env && epi_env[0] == 'd';
+  const bool want_direct = tuning(kTuneEpilogue) == 1;
   P.epi = (p.oc % 4) != 0 ? kEpiScalar : (want_direct ? kEpiDirect : kEpiTma);
   const int mma_n = p.oc <= 64 ? 64 : bn;
   P.idesc = f4 ? idesc_mxf4(mma_n) : idesc_i8(mma_n);
@@ -1409,11 +1382,16 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
                       int nset0 = -1, int32_t* const* peers = nullptr, int npeer = 0) {
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
   auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4, NP>;
-  static bool configured = false;
-  if (!configured) {
+  // the dynamic shared-memory opt-in is a per-device function attribute: set once per
+  // device (a bit per device, set after the call succeeded; racing threads set it twice)
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const uint64_t bit = dev < 64 ? uint64_t(1) << dev : 0;
+  if (!bit || !(configured.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_release);
   }
   if (count < 1 || count > NP) return cudaErrorInvalidValue;
   TcArgs<NP> a;
@@ -1443,11 +1421,15 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
   a.npeer = npeer;
   a.tiles0 = a.nset0 < count ? a.prob[a.nset0].tile0 : a.ntiles;
   a.b_bytes = C::kBSlots * C::kBBytes;
-  const char* dbg_env = getenv("BS_TC_DEBUG");
+#if defined(BS_TC_PROFILE) || defined(BS_TC_KNOBS)
+  const char* dbg_env = getenv("BS_TC_DEBUG");  // experiment builds only
   a.debug = dbg_env ? atoi(dbg_env) : 0;
+#endif
+  const int cap = tuning(kTuneBSlots);
+  a.nbs = cap >= 2 && cap < C::kBSlots ? cap : C::kBSlots;
   int smem_bytes = C::kFixed + a.b_bytes;
   if (smem_bytes < kMinSmem) smem_bytes = kMinSmem;
-  const int grid = a.ntiles < num_sms() ? a.ntiles : num_sms();
+  const int grid = a.ntiles < device_sms() ? a.ntiles : device_sms();
   kern<<<grid, kThreads, smem_bytes, stream>>>(a, maps);
   note_launch();
   return cudaPeekAtLastError();
@@ -1456,10 +1438,7 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
 // Tile width: BN = 64 when the filters fit it, else 128 (the widest tile whose double-
 // buffered accumulators leave TMEM room for the A ring).  BS_TC_BN overrides (tests).
 inline int pick_bn(const ConvProblem& p) {
-  if (const char* e = getenv("BS_TC_BN")) {
-    const int v = atoi(e);
-    if (v == 64 || v == 128) return v;
-  }
+  if (const int v = tuning(kTuneTileN)) return v;
   return p.oc <= 64 ? 64 : 128;
 }
 
@@ -1498,8 +1477,7 @@ cudaError_t launch_group_aw(const ConvProblem* ps, const int8_t* const* wexps, i
     // (measured per-SM output rate); set 1: the rest.  Measured neutral on the ResNet-18
     // group (246 us either way), so one set is the default; BS_TC_SPLIT=1 interleaves.
     int nset0 = count;
-    if (const char* e = getenv("BS_TC_SPLIT"))
-      if (e[0] == '1') {
+    if (tuning(kTuneGroupSplit) == 1) {
         nset0 = 0;
         while (nset0 < count && int64_t(tc_kpad(sp[nset0].kp, F4 ? kTcF4 : kTcI8) / 4) * A_BITS * W_BITS * 256 >
                                     int64_t(BN) * BM * 4 / 17)
@@ -1516,12 +1494,7 @@ cudaError_t launch_group_aw(const ConvProblem* ps, const int8_t* const* wexps, i
 }  // namespace tc
 
 int tc_resolve_format(int fmt) {
-  if (fmt == kTcI8 || fmt == kTcF4) return fmt;
-  if (const char* e = getenv("BS_TC_FORMAT")) {  // experiments: i8 / f4
-    if (e[0] == 'i') return kTcI8;
-    if (e[0] == 'f') return kTcF4;
-  }
-  return kTcDefault;
+  return fmt == kTcI8 || fmt == kTcF4 ? fmt : kTcDefault;
 }
 
 int64_t tc_kpad(int64_t kp, int fmt) {

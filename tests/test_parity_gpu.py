@@ -14,6 +14,19 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
+@pytest.fixture
+def tuning():
+    """Set bs_set_tuning knobs for one test; every knob set is reset to 0 afterwards."""
+    used = []
+
+    def set_(knob, value):
+        bs.set_tuning(knob, value)
+        used.append(knob)
+    yield set_
+    for k in used:
+        bs.set_tuning(k, 0)
+
+
 def enc(bipolar):
     return bs.BIPOLAR if bipolar else bs.UNIPOLAR
 
@@ -328,12 +341,12 @@ def _tc_conv_prepared(act, a_bits, wt, w_bits, bipolar, stride, pad, fused, fmt=
 @pytest.mark.parametrize("bn", ["64", "128"])
 @pytest.mark.parametrize("a_bits,w_bits", TC_PRECISIONS)
 @pytest.mark.parametrize("bipolar", [False, True])
-def test_conv_tc_every_tile_width(monkeypatch, fmt, bn, a_bits, w_bits, bipolar):
-    """Each compiled tile width (BS_TC_BN forces it; configurations that do not fit shared
+def test_conv_tc_every_tile_width(tuning, fmt, bn, a_bits, w_bits, bipolar):
+    """Each compiled tile width (BS_TUNE_TC_TILE_N forces it; configurations that do not fit shared
     memory fall back to a narrower one) on a ragged case: M = 2*13*11 = 286 (3 row tiles,
     tail 30), OC = 300 (ragged column tiles, OC % 4 = 0 so the TMA-store epilogue runs),
     K = 9 taps x 4 words (9 K chunks)."""
-    monkeypatch.setenv("BS_TC_BN", bn)
+    tuning(bs.TUNE_TC_TILE_N, int(bn))
     g = inputs.gen(int(bn) + 10 * a_bits + w_bits + (100 if bipolar else 0))
     act = inputs.codes((2, 13, 11, 96), a_bits, g)
     wt = inputs.codes((300, 3, 3, 96), w_bits, g)
@@ -343,16 +356,19 @@ def test_conv_tc_every_tile_width(monkeypatch, fmt, bn, a_bits, w_bits, bipolar)
 
 
 @pytest.mark.parametrize("fmt", TC_FORMATS)
-@pytest.mark.parametrize("resident", ["0", "1"])
-@pytest.mark.parametrize("epi", ["direct", "tma"])
+@pytest.mark.parametrize("slots", [0, 2, 3])
+@pytest.mark.parametrize("epi", [0, 1])
 @pytest.mark.parametrize("a_bits,w_bits,bipolar", [(2, 1, True), (1, 2, False), (4, 2, True)])
-@pytest.mark.parametrize("oc", [64, 100, 128])
-def test_conv_tc_b_modes(monkeypatch, fmt, resident, epi, a_bits, w_bits, bipolar, oc):
-    """Weights resident in shared memory (one N block, whole K loaded once) versus the
-    per-stage TMA ring, and the direct-store versus TMA-store epilogue, on a ragged
-    3x3 s2 case (M = 3*10*10 = 300: 3 row tiles; K = 9 taps x 2 words = 5 chunks)."""
-    monkeypatch.setenv("BS_TC_RESIDENT", resident)
-    monkeypatch.setenv("BS_TC_EPI", epi)
+@pytest.mark.parametrize("oc", [64, 100, 128, 300])
+def test_conv_tc_b_modes(tuning, fmt, slots, epi, a_bits, w_bits, bipolar, oc):
+    """Weights resident in the shared-memory chunk slots (all K chunks fit: loaded once per
+    N block, reused by the CTA's next tiles of that block) versus streamed through a ring of
+    2 or 3 slots (BS_TUNE_TC_B_SLOTS; fewer slots than the 5 / 9 K chunks), with 1..3 N
+    blocks, and the direct-store versus TMA-store epilogue, on a ragged 3x3 s2 case
+    (M = 3*10*10 = 300: 3 row tiles; K = 9 taps x 2 words)."""
+    if slots:
+        tuning(bs.TUNE_TC_B_SLOTS, slots)
+    tuning(bs.TUNE_TC_EPILOGUE, epi)
     g = inputs.gen(oc + 10 * a_bits + w_bits)
     act = inputs.codes((3, 19, 20, 64), a_bits, g)
     wt = inputs.codes((oc, 3, 3, 64), w_bits, g)
@@ -590,14 +606,14 @@ def _group_run(cases, a_bits, w_bits, fmt, encs, seed):
 @pytest.mark.parametrize("bn", ["", "64", "128"])
 @pytest.mark.parametrize("fmt", TC_FORMATS)
 @pytest.mark.parametrize("a_bits,w_bits", TC_PRECISIONS)
-def test_conv_tc_group_mixed(monkeypatch, bn, fmt, a_bits, w_bits):
+def test_conv_tc_group_mixed(tuning, bn, fmt, a_bits, w_bits):
     """bs_bitserial_conv2d_nhwc_tc_group on six problems of different geometry (problems
     reordered by K inside; tiles of all problems interleaved across CTAs): every output
     equals the oracle's.  Default tile widths (OC <= 64 members in a BN = 64 group, the
     rest in a BN = 128 group) and every member forced into one BN = 64 or BN = 128
     launch (N = 64 MMAs for the narrow members).  FP4 mixes the encodings per member."""
     if bn:
-        monkeypatch.setenv("BS_TC_BN", bn)
+        tuning(bs.TUNE_TC_TILE_N, int(bn))
     encs = [(bs.A_UNSIGNED, bs.UNIPOLAR), (bs.A_UNSIGNED, bs.BIPOLAR)]
     if fmt == bs.TC_F4:
         encs += [(bs.A_BIPOLAR, bs.BIPOLAR), (bs.A_SIGNED, bs.SIGNED), (bs.A_UNSIGNED, bs.SIGNED)]
@@ -607,11 +623,11 @@ def test_conv_tc_group_mixed(monkeypatch, bn, fmt, a_bits, w_bits):
 
 
 @pytest.mark.parametrize("split", ["0", "1"])
-def test_conv_tc_group_more_than_one_launch(monkeypatch, split):
+def test_conv_tc_group_more_than_one_launch(tuning, split):
     """More members than one launch holds (16): split into launches of <= 16, all exact;
     a group of one and an empty group.  split=1: each launch interleaves its long-K and
-    short-K members' tiles (BS_TC_SPLIT)."""
-    monkeypatch.setenv("BS_TC_SPLIT", split)
+    short-K members' tiles (BS_TUNE_TC_GROUP_SPLIT)."""
+    tuning(bs.TUNE_TC_GROUP_SPLIT, int(split))
     cases = [(1, 4 + i % 5, 5, 16 + 8 * (i % 3), 8 + 12 * (i % 4), 3, 3, 1 + i % 2, 1, 1, 1) for i in range(19)]
     cases += [(2, 6, 6, 512, 72, 3, 3, 1, 1, 1, 1), (3, 5, 7, 8, 100, 1, 1, 1, 1, 0, 0)]  # long / short K
     outs, refs = _group_run(cases, 2, 1, bs.TC_F4, [(bs.A_UNSIGNED, bs.BIPOLAR)], seed=5)
@@ -771,10 +787,10 @@ def test_tc_group_writes_stay_in_bounds(fmt):
 @pytest.mark.parametrize("fmt", TC_FORMATS)
 @pytest.mark.parametrize("bn", ["64", "128"])
 @pytest.mark.parametrize("a_bits,w_bits", [(2, 1), (4, 3), (1, 4)])
-def test_tc_single_launch_writes_stay_in_bounds(monkeypatch, fmt, bn, a_bits, w_bits):
+def test_tc_single_launch_writes_stay_in_bounds(tuning, fmt, bn, a_bits, w_bits):
     """A single tensor-core launch (ragged M and OC, each tile width) writes exactly its
     output: sentinel guard bands before and after stay intact."""
-    monkeypatch.setenv("BS_TC_BN", bn)
+    tuning(bs.TUNE_TC_TILE_N, int(bn))
     n, h, w, c, oc = 2, 11, 9, 72, 100
     g = inputs.gen(31 * a_bits + w_bits + int(bn))
     act = inputs.codes((n, h, w, c), a_bits, g)

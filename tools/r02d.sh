@@ -1,4 +1,10 @@
-python tools/one_layer.py 2 > gpurun_out/r02d_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:tc_conv_kernel -s 2 -c 1 -o gpurun_out/r02d_l2 python tools/one_layer.py 2 > gpurun_out/r02d_ncu_l2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:tc_conv_kernel -s 2 -c 1 -o gpurun_out/r02d_l9 python tools/one_layer.py 9 > gpurun_out/r02d_ncu_l9.log 2>&1
+python tools/one_layer.py 2 > gpurun_out/r02d_plain.log 2>&1 || exit 1
+for L in 2 9; do
+ncu --set full --clock-control none --import-source on -k regex:tc_conv_kernel -s 2 -c 1 -o /tmp/r02d_l$L python tools/one_layer.py $L > gpurun_out/r02d_ncu_l$L.log 2>&1
+ncu -i /tmp/r02d_l$L.ncu-rep --page raw --csv > gpurun_out/r02d_l${L}_raw.csv 2>&1
+ncu -i /tmp/r02d_l$L.ncu-rep --page details --csv > gpurun_out/r02d_l${L}_details.csv 2>&1
+ncu -i /tmp/r02d_l$L.ncu-rep --page source --csv --print-source sass > gpurun_out/r02d_l${L}_sass.csv 2>&1
+ls -la /tmp/r02d_l$L.ncu-rep >> gpurun_out/r02d_sizes.txt
+done
+du -sh gpurun_out/*
 echo done
