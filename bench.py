@@ -224,6 +224,9 @@ class ConvWorkload:
                                for part in args.group_layers.split("|")]
                 assert sorted(i for grp in self.groups for i in grp) == list(range(len(self.runs)))
             self.group_items = [[self.runs[i].group_item() for i in grp] for grp in self.groups]
+        if args.path == "small":  # every layer in ONE launch of the small-problem path (packing fused)
+            self.small_items = [dict(act=r.act, w_packed=r.wp, out=r.out, w_enc=r.enc, oc=r.L.oc, kh=r.L.k, kw=r.L.k,
+                                     stride=r.L.s, pad=r.L.pad) for r in self.runs]
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
             "layout": "NHWC/OHWI",
@@ -238,6 +241,10 @@ class ConvWorkload:
         }
 
     def describe_step(self, args):
+        if args.path == "small":
+            return ("every layer's conv from raw uint8 codes in ONE bs_bitserial_conv2d_nhwc_i8_group launch (activation "
+                    "packing fused in shared memory, AND+POPC, K slices summed through cluster shared memory; weights "
+                    "packed once, untimed)")
         if args.path != "tc":
             return ("per layer: bitpack(act) + AND/POPC bitserial conv2d via bs_bitserial_conv2d_nhwc_i8 (weights "
                     "prepacked, untimed)")
@@ -253,6 +260,9 @@ class ConvWorkload:
         return f"{packs}; {convs} (weights packed + plane-expanded once, untimed)"
 
     def step(self):
+        if self.args.path == "small":
+            self.runs[0].bs.bitserial_conv2d_nhwc_i8_group(self.small_items, self.args.a_bits, self.args.w_bits)
+            return
         if self.overlap:
             return self.step_overlapped()
         for r in self.runs:
@@ -308,10 +318,21 @@ class ConvWorkload:
             main.wait_stream(s)
         main.wait_stream(side)
 
+    def roofline_small(self, reps):
+        """The small path's one launch per step (packing fused), timed as a whole."""
+        ms = graph_launch_ms(self.step, reps)
+        ops = sum(r.binops() for r in self.runs)
+        nbytes = sum(r.act.numel() + r.wp.numel() * 4 + r.out.numel() * 4 for r in self.runs)
+        return {"kind": "popc", "kernel": f"small_conv_kernel (one launch: {len(self.runs)} layers, fused packing, "
+                                          "AND+POPC, cluster split-K)", "ops": ops, "ms": ms, "launches": 1,
+                "bytes": nbytes, "breakdown": {"step_kernel_us": 1e3 * ms}}
+
     def roofline(self, reps):
         """Per-launch device time of the pack and conv kernels of every layer: each
         kernel captured `reps` times back to back in a CUDA graph, timed with events on
         the stream that replays it (no host launch gaps), per launch = graph time / reps."""
+        if self.args.path == "small":
+            return self.roofline_small(reps)
         for r in self.runs:
             r.pack_only()
             r.conv_only()
@@ -789,13 +810,22 @@ def run_ours(args):
                   "hbm": {"achieved": roof["bytes"] / (roof["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                           "frac": roof["bytes"] / (roof["ms"] / 1e3) / 1e9 / hbm,
                           "algorithmic_bytes": roof["bytes"]},
-                  "time_model": model, "r_popc": r_popc, "x_r_popc": achieved / r_popc}
+                  "time_model": model, "r_popc": r_popc,
+                  # binary ops over the integer-pipe (POPC) roofline, both in binary TOPS
+                  "x_r_popc": roof["ops"] / (roof["ms"] / 1e3) / 1e12 / r_popc}
         if t_hbm >= t_tensor:  # HBM dominates summed over the step's launches
             roofline = dict(common, bound="hbm", achieved=common["hbm"]["achieved"], peak=hbm, unit="GB/s",
                             frac=common["hbm"]["frac"], peak_basis=f"HBM copy bandwidth, {peaks_src}")
         else:
             roofline = dict(common, bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
                             frac=achieved / peak, peak_basis=common["tensor"]["peak_basis"])
+    elif roof["kind"] == "popc":  # one POPC per word pair (bipolar via the identity): the POPC-pipe roofline
+        achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": r_popc, "unit": "binary TOPS",
+                    "frac": achieved / r_popc, "traffic": None, "r_popc": r_popc, "kernel": roof["kernel"],
+                    "peak_basis": f"POPC pipe (measured 16 /clk/SM, profiles/r01_int_pipe_rates.json): 64 binary ops "
+                                  f"per POPC x 16 x {sms} SMs x {f_max:.0f} MHz",
+                    "bytes": roof["bytes"], "hbm_frac": roof["bytes"] / (roof["ms"] / 1e3) / 1e9 / peaks["hbm_gbs"]}
     elif roof["kind"] == "alu":
         achieved = roof["ops"] / (roof["ms"] / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": achieved, "peak": r_int, "unit": "binary TOPS",
@@ -844,7 +874,9 @@ def run_ours(args):
             "dtype": (("u8 codes -> packed u32 bit-planes -> radix-4 e2m1 digits (two planes per nibble, 0.5 x {0..3}) x "
                        "ue8m0 4^d scales on tcgen05 kind::mxf4 (fp32 accum, exact) -> i32" if args.tc_format == "f4" else
                        "u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32")
-                      if args.path == "tc" else "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32"),
+                      if args.path == "tc" else
+                      ("u8 codes -> u32 bit-planes packed in shared memory (AND/POPC) -> i32" if args.path == "small" else
+                       "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32")),
             "scaling": "weak" if getattr(wl, "replicas", 1) > 1 else "strong",
             "data": "synthetic (seeded uniform codes, PAPER.md Table 1 / BASELINE shapes; no dataset)",
             "config": cfg, "roofline": roofline,
@@ -976,14 +1008,17 @@ def main():
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
-    ap.add_argument("--path", choices=["tc", "popc"], default="tc",
-                    help="conv/GEMM kernel: tensor-core bitserial (default) or the AND/POPC integer-pipe kernel")
+    ap.add_argument("--path", choices=["auto", "tc", "popc", "small"], default="auto",
+                    help="conv/GEMM kernel: tensor-core bitserial, the AND/POPC integer-pipe kernel, or the one-launch "
+                         "small-problem path; auto = small for the batch-1 conv workloads, else tc")
     ap.add_argument("--fused-gather", action="store_true",
                     help="gemm, N>1: all-gather fused into the tensor-core epilogue over symmetric memory (SURVEY 8 f2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step's outputs")
     args = ap.parse_args()
+    if args.path == "auto":
+        args.path = "small" if args.workload in ("conv1", "resnet1") else "tc"
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if world == 0 and args.gpus > 1:  # not launched by torchrun: launch N ranks (one per GPU) ourselves
         return relaunch(args.gpus)

@@ -78,19 +78,30 @@ typedef enum { BS_UNIPOLAR = 0, BS_BIPOLAR = 1, BS_SIGNED = 2 } bs_encoding;
  * reduction-axis tail contribute 0 in every encoding. */
 typedef enum { BS_A_UNSIGNED = 0, BS_A_BIPOLAR = 1, BS_A_SIGNED = 2 } bs_a_encoding;
 
-/* Kernel family for the *_ex entry points.  BS_ALGO_AUTO picks per shape.
+/* Kernel family for the *_ex entry points.
+ *   AUTO     : what bs_bitserial_dense / bs_bitserial_conv2d_nhwc run:
+ *                dense with m <= 8 (A in {1,2,4}, W in {1,2})  -> GEMV;
+ *                otherwise, when A <= 4, W <= 4 and K*(2^A-1)*(2^W-1) < 2^22 -> TC;
+ *                otherwise -> POPC.
+ *   TC       : the tensor-core kernel (tcgen05.mma kind::mxf4, radix-4 digits of two bit
+ *              planes, FP32 accumulation exact below the bound above) on the PACKED weight
+ *              planes: its producer warps expand each weight chunk into shared memory
+ *              (no prepared copy, no workspace; weights stay resident per N block when
+ *              their K chunks fit).  BS_ERR_UNSUPPORTED outside A, W <= 4 / the bound.
  *   POPC     : AND + POPC per word pair (Eq. 1 inside Eq. 2) on the integer pipes;
  *              bipolar applied as the exact identity 2*U - (2^W-1)*sum(a).
  *   POPC_LIT : as POPC but bipolar evaluated literally, popc(a&w) - popc(a&~w) per
  *              plane pair (north_star form; twice the POPC work; unipolar = POPC).
  *   GEMV     : warp-per-rows matrix-vector kernel with butterfly multi-row reduction
  *              (PAPER.md:694-705 micro-kernel ideas), for m <= 8 (dense only).
- *   (tensor-core path: see bs_bitserial_conv2d_nhwc_tc below) */
+ * The prepared-weight tensor-core entries below (bs_*_tc_prepared, *_tc_group) skip the
+ * in-kernel weight expansion: the fastest form for weights reused across calls. */
 typedef enum {
   BS_ALGO_AUTO = 0,
   BS_ALGO_POPC = 1,
   BS_ALGO_POPC_LIT = 2,
-  BS_ALGO_GEMV = 3
+  BS_ALGO_GEMV = 3,
+  BS_ALGO_TC = 4
 } bs_algo;
 
 int bs_abi_version(void);
@@ -111,13 +122,16 @@ int64_t bs_kernel_launches(void);
  *   BS_TUNE_TC_B_SLOTS     : cap on the weight chunk slots in shared memory (2..32): fewer slots
  *                            than a tile's K chunks make its weights stream instead of staying
  *                            resident
+ *   BS_TUNE_SMALL_KSPLIT   : K slices (= cluster size) of the one-launch small-problem path
+ *                            (bs_bitserial_conv2d_nhwc_i8_group): 1, 2, 4 or 8
  * bs_set_tuning returns BS_ERR_INVALID_ARG for an unknown knob or value; bs_get_tuning returns
  * the current value (0 for an unknown knob). */
 typedef enum {
   BS_TUNE_TC_TILE_N = 0,
   BS_TUNE_TC_EPILOGUE = 1,
   BS_TUNE_TC_GROUP_SPLIT = 2,
-  BS_TUNE_TC_B_SLOTS = 3
+  BS_TUNE_TC_B_SLOTS = 3,
+  BS_TUNE_SMALL_KSPLIT = 4
 } bs_tune_knob;
 int bs_set_tuning(int knob, int value);
 int bs_get_tuning(int knob);
@@ -214,6 +228,28 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits,
                                 int stride_h, int stride_w, int pad_h, int pad_w,
                                 void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Several convolutions from RAW uint8 codes in ONE launch: the batch-1 latency path
+ * (small layers "can't amortize the bit-packing costs"; packing is timed,
+ * PAPER.md:715).  Each CTA packs the activation codes of its implicit-im2col slab in shared
+ * memory (nothing packed is written to HBM), runs AND + POPC per word pair (Eq. 1 inside
+ * Eq. 2, bipolar through the exact identity), and the K slices of a tile — the CTAs of one
+ * thread-block cluster — are summed through distributed shared memory.  Each descriptor
+ * means what the bs_bitserial_conv2d_nhwc_i8 arguments mean (a dense layer is n = 1,
+ * h = m, w = 1, c = k, kh = kw = 1); no workspace.  a_bits in [1,4], w_bits in [1,2],
+ * unipolar / bipolar weights (BS_ERR_UNSUPPORTED otherwise).  Up to 16 descriptors per
+ * launch (more: consecutive launches).  All descriptors are validated first; count = 0 is
+ * a no-op.  bs_bitserial_conv2d_nhwc_i8 and bs_bitserial_dense_i8 (m > 8) take this path
+ * by themselves for problems of at most 2^24 word-level AND+POPC pairs
+ * (M * OC * K_words * A * W). */
+typedef struct bs_conv_i8_desc {
+  const uint8_t* act;        /* [n][h][w][c] uint8 codes (device) */
+  const uint32_t* w_packed;  /* [w_bits][oc*kh*kw][bs_packed_row_words(c)] (bs_bitpack of OHWI) */
+  int32_t* out;              /* [n][oh][ow][oc] */
+  int w_enc;                 /* BS_UNIPOLAR / BS_BIPOLAR */
+  int n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w;
+} bs_conv_i8_desc;
+int bs_bitserial_conv2d_nhwc_i8_group(const bs_conv_i8_desc* descs, int count, int a_bits, int w_bits, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Tensor-core bitserial (tcgen05.mma on sm_100a, format BS_TC_DEFAULT).  Same operation and
  * operands as bs_bitserial_conv2d_nhwc / bs_bitserial_dense.  The packed activation and
@@ -298,6 +334,18 @@ int bs_bitserial_dense_tc_prepared_gather(const uint32_t* a_packed, int a_bits, 
                                           int w_bits, int w_enc, int tc_format, int32_t* out,
                                           int32_t* const* out_peers, int npeers, int64_t m, int64_t n, int64_t k,
                                           void* stream);
+
+/* The fused all-gather in its NVLS form: as above, but every staged output
+ * row segment is stored ONCE, with multimem.st, to out_mc — the MULTICAST address (NVLink
+ * SHARP / NVLS multicast object, e.g. torch symmetric memory's multicast_ptr) of this rank's
+ * [m][n] row block of the gathered C — and the switch replicates it into every rank's copy
+ * (this rank's included).  Egress per rank is its own block once instead of once per peer.
+ * The caller creates the multicast mapping, checks that the device supports multicast
+ * (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED) and orders the exchange (a barrier on every rank
+ * after the call).  n % 4 == 0. */
+int bs_bitserial_dense_tc_prepared_multicast(const uint32_t* a_packed, int a_bits, int a_enc, const int8_t* w_tc,
+                                             int w_bits, int w_enc, int tc_format, int32_t* out_mc, int64_t m,
+                                             int64_t n, int64_t k, void* stream);
 
 /* Several tensor-core convolutions of one precision in ONE persistent launch (per 16
  * problems): the tiles of all problems form one sequence that the SM-resident CTAs walk,

@@ -18,7 +18,7 @@ import os
 import torch
 
 __all__ = [
-    "UNIPOLAR", "BIPOLAR", "SIGNED", "A_UNSIGNED", "A_BIPOLAR", "A_SIGNED", "ALGO_AUTO", "ALGO_POPC", "ALGO_POPC_LIT", "ALGO_GEMV",
+    "UNIPOLAR", "BIPOLAR", "SIGNED", "A_UNSIGNED", "A_BIPOLAR", "A_SIGNED", "ALGO_AUTO", "ALGO_POPC", "ALGO_POPC_LIT", "ALGO_GEMV", "ALGO_TC",
     "BitserialError", "library_path", "abi_version", "kernel_launches", "packed_row_words", "bitpack",
     "bitserial_dense", "bitserial_dense_i8", "bitserial_conv2d_nhwc", "bitserial_conv2d_nhwc_i8",
     "bitserial_conv2d_nhwc_host", "conv2d_workspace_bytes", "dense_workspace_bytes", "conv_out_extent",
@@ -28,14 +28,15 @@ __all__ = [
     "bitserial_conv2d_nhwc_tc_host", "conv2d_tc_weight_bytes", "dense_tc_weight_bytes", "TC_DEFAULT", "TC_I8",
     "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group",
     "bitserial_dense_tc_gather", "TcHostDesc", "bitserial_conv2d_nhwc_tc_host_group", "set_tuning", "get_tuning",
-    "TUNE_TC_TILE_N", "TUNE_TC_EPILOGUE", "TUNE_TC_GROUP_SPLIT", "TUNE_TC_B_SLOTS",
+    "TUNE_TC_TILE_N", "TUNE_TC_EPILOGUE", "TUNE_TC_GROUP_SPLIT", "TUNE_TC_B_SLOTS", "TUNE_SMALL_KSPLIT", "ConvI8Desc",
+    "bitserial_conv2d_nhwc_i8_group", "bitserial_dense_tc_multicast",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
 A_UNSIGNED, A_BIPOLAR, A_SIGNED = 0, 1, 2    # activation encodings (bs_a_encoding)
 TC_DEFAULT, TC_I8, TC_F4 = 0, 1, 2  # bs_tc_format
-ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV = 0, 1, 2, 3
-TUNE_TC_TILE_N, TUNE_TC_EPILOGUE, TUNE_TC_GROUP_SPLIT, TUNE_TC_B_SLOTS = 0, 1, 2, 3  # bs_tune_knob
+ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV, ALGO_TC = 0, 1, 2, 3, 4
+TUNE_TC_TILE_N, TUNE_TC_EPILOGUE, TUNE_TC_GROUP_SPLIT, TUNE_TC_B_SLOTS, TUNE_SMALL_KSPLIT = 0, 1, 2, 3, 4  # bs_tune_knob
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # BITSERIAL_LIB selects an experiment build of the same library (A/B timing of compile-time
@@ -60,7 +61,8 @@ EXPORTED_SYMBOLS = (
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
     "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitserial_dense_tc_prepared_gather",
-    "bs_bitserial_conv2d_nhwc_tc_host_group", "bs_set_tuning", "bs_get_tuning",
+    "bs_bitserial_conv2d_nhwc_tc_host_group", "bs_set_tuning", "bs_get_tuning", "bs_bitserial_conv2d_nhwc_i8_group",
+    "bs_bitserial_dense_tc_prepared_multicast",
 )
 
 
@@ -116,6 +118,8 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tc_host_group": ([P, I, I, I, I, P], I),
         "bs_bitserial_dense_tc_prepared_gather": ([P, I, I, P, I, I, I, P, P, I, L, L, L, P], I),
         "bs_set_tuning": ([I, I], I),
+        "bs_bitserial_dense_tc_prepared_multicast": ([P, I, I, P, I, I, I, P, L, L, L, P], I),
+        "bs_bitserial_conv2d_nhwc_i8_group": ([P, I, I, I, P], I),
         "bs_get_tuning": ([I], I),
     }
     for name, (args, res) in sig.items():
@@ -282,6 +286,40 @@ def bitserial_conv2d_nhwc_i8(act, a_bits, w_packed, w_bits, w_enc, oc, kh, kw, s
                                                _dev(workspace, "workspace", torch.uint8), workspace.numel(),
                                                _stream(stream)))
     return out
+
+
+class ConvI8Desc(ctypes.Structure):
+    """bs_conv_i8_desc (include/bitserial.h): one convolution of a one-launch small-problem group."""
+    _fields_ = [("act", ctypes.c_void_p), ("w_packed", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("w_enc", ctypes.c_int)] + \
+        [(f, ctypes.c_int) for f in ("n", "h", "w", "c", "oc", "kh", "kw", "stride_h", "stride_w", "pad_h", "pad_w")]
+
+
+def bitserial_conv2d_nhwc_i8_group(convs, a_bits, w_bits, stream=None):
+    """bs_bitserial_conv2d_nhwc_i8_group: several convolutions from raw uint8 NHWC codes in
+    one launch (packing fused; the batch-1 latency path).  `convs`: dicts with act (uint8
+    [n][h][w][c]), w_packed, w_enc, oc, kh, kw and optional stride, pad, out.  Returns the
+    outputs in order."""
+    descs = (ConvI8Desc * max(len(convs), 1))()
+    outs = []
+    for i, cv in enumerate(convs):
+        act = cv["act"]
+        n, h, w, c = act.shape
+        sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, cv["kh"], cv["kw"], cv.get("stride", 1), cv.get("pad", 0))
+        out = cv.get("out")
+        if out is None:
+            out = torch.empty((n, max(oh, 0), max(ow, 0), cv["oc"]), dtype=torch.int32, device=act.device)
+        d = descs[i]
+        d.act = _dev(act, "act", torch.uint8).value
+        d.w_packed = _dev(cv["w_packed"], "w_packed", torch.int32).value
+        d.out = _dev(out, "out", torch.int32).value
+        d.w_enc = int(cv.get("w_enc", UNIPOLAR))
+        d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw = n, h, w, c, cv["oc"], cv["kh"], cv["kw"]
+        d.stride_h, d.stride_w, d.pad_h, d.pad_w = sh, sw, ph, pw
+        outs.append(out)
+    _check(_load().bs_bitserial_conv2d_nhwc_i8_group(ctypes.cast(descs, ctypes.c_void_p), len(convs), a_bits, w_bits,
+                                                     _stream(stream)))
+    return outs
 
 
 def conv2d_tc_workspace_bytes(oc, kh, kw, c, w_bits) -> int:
@@ -464,6 +502,15 @@ def bitserial_dense_tc_gather(a_packed, a_bits, w_tc, w_bits, m, n, k, out, peer
         int(w_enc), int(tc_format), _dev(out, "out", torch.int32), ctypes.cast(ptrs, ctypes.c_void_p), len(peers),
         m, n, k, _stream(stream)))
     return out
+
+
+def bitserial_dense_tc_multicast(a_packed, a_bits, w_tc, w_bits, m, n, k, out_mc, tc_format=TC_DEFAULT, stream=None,
+                                 a_enc=A_UNSIGNED, w_enc=UNIPOLAR):
+    """bs_bitserial_dense_tc_prepared_multicast: this rank's [m][n] row block of C stored once,
+    with multimem.st, to `out_mc` — the multicast (NVLS) device address (int) of that block."""
+    _check(_load().bs_bitserial_dense_tc_prepared_multicast(
+        _dev(a_packed, "a_packed", torch.int32), a_bits, int(a_enc), _dev(w_tc, "w_tc", torch.int8), w_bits,
+        int(w_enc), int(tc_format), ctypes.c_void_p(int(out_mc)), m, n, k, _stream(stream)))
 
 
 def bitserial_conv2d_nhwc_tc_i8(act, a_bits, w_tc, w_bits, oc, kh, kw, stride=1, pad=0, out=None, workspace=None,

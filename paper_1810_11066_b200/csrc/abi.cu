@@ -103,7 +103,7 @@ int check_tc_bound(int64_t k, int a_bits, int w_bits, int tc_format, const char*
 }
 
 int check_algo(int algo, const char* fn) {
-  if (algo < BS_ALGO_AUTO || algo > BS_ALGO_GEMV) return fail(BS_ERR_INVALID_ARG, "%s: bad algo %d", fn, algo);
+  if (algo < BS_ALGO_AUTO || algo > BS_ALGO_TC) return fail(BS_ERR_INVALID_ARG, "%s: bad algo %d", fn, algo);
   return BS_OK;
 }
 
@@ -154,10 +154,34 @@ bs::ConvProblem make_conv(const uint32_t* act, int a_bits, const uint32_t* wt, i
   return p;
 }
 
+// The tensor-core path for the packed-weight entries (three-call boundary): FP4 digits with
+// the weight planes expanded inside the kernel; needs A, W <= 4, unipolar / bipolar weights
+// and the FP4 format's exactness bound K * (2^A - 1) * (2^W - 1) < 2^22.
+bool tc_auto_ok(const bs::ConvProblem& p) {
+  const int64_t k = int64_t(p.kh) * p.kwid * p.c_tap;
+  return bs::tc_supported(p.a_bits, p.w_bits) && p.bipolar <= 1 &&
+         double(k) * double((1 << p.a_bits) - 1) * double((1 << p.w_bits) - 1) < 4194304.0;
+}
+
 int launch_conv(const bs::ConvProblem& p, int algo, cudaStream_t s, const char* fn) {
   if (algo == BS_ALGO_GEMV) return fail(BS_ERR_UNSUPPORTED, "%s: GEMV algo applies to dense only", fn);
+  if (algo == BS_ALGO_TC || (algo == BS_ALGO_AUTO && tc_auto_ok(p))) {
+    if (!tc_auto_ok(p))
+      return fail(BS_ERR_UNSUPPORTED, "%s: tensor-core path needs A, W <= 4, unipolar/bipolar weights and "
+                  "K*(2^A-1)*(2^W-1) < 2^22", fn);
+    return cuda_status(bs::launch_tc_conv_raw(p, s), fn);
+  }
   const bs::Algo a = algo == BS_ALGO_POPC_LIT ? bs::Algo::PopcLit : bs::Algo::Popc;
   return cuda_status(bs::launch_popc_conv(p, a, s), fn);
+}
+
+// Small problems (batch-1 layers) run as ONE launch with the activation packing fused
+// (small_conv.cu): below ~16 M word-level AND+POPC pairs a persistent tensor-core launch
+// plus a separate pack launch costs more than the whole problem on the integer pipes.
+constexpr int64_t kSmallWordOps = int64_t(16) << 20;
+bool use_small(const bs::ConvProblem& p) {
+  return bs::small_supported(p.a_bits, p.w_bits) && p.bipolar != 2 && p.kh * p.kwid <= 64 &&
+         p.M * p.oc * p.kp * p.a_bits * p.w_bits <= kSmallWordOps;
 }
 
 int dense_core(const uint32_t* a_packed, const uint8_t* a_codes, int a_bits, const uint32_t* w_packed, int w_bits,
@@ -263,6 +287,10 @@ int bs_set_tuning(int knob, int value) {
     case BS_TUNE_TC_B_SLOTS:
       if (value != 0 && (value < 2 || value > 32)) return fail(BS_ERR_INVALID_ARG, "%s: B slots %d", fn, value);
       break;
+    case BS_TUNE_SMALL_KSPLIT:
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+        return fail(BS_ERR_INVALID_ARG, "%s: K split %d not in {1,2,4,8}", fn, value);
+      break;
     default:
       return fail(BS_ERR_INVALID_ARG, "%s: unknown knob %d", fn, knob);
   }
@@ -331,6 +359,11 @@ int bs_bitserial_dense_i8(const uint8_t* a, int a_bits, const uint32_t* w_packed
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (bs::gemv_supported(m, k, a_bits, w_bits))  // one fused launch: pack in-kernel + GEMV
     return dense_core(nullptr, a, a_bits, w_packed, w_bits, w_enc, out, m, n, k, BS_ALGO_GEMV, s, fn);
+  if (m <= kMaxRows && n <= (int64_t(1) << 31) - 1 && k <= (int64_t(1) << 31) - 1) {
+    const ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};  // dense = 1x1 conv over m "pixels"
+    bs::SmallConv sc{make_conv(nullptr, a_bits, w_packed, w_bits, w_enc, out, g), a};
+    if (use_small(sc.p)) return cuda_status(bs::launch_small_conv(&sc, 1, a_bits, w_bits, s), fn);
+  }
   const int64_t need = bs_dense_workspace_bytes(m, k, a_bits);
   if (!workspace || workspace_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: workspace needs %lld bytes", fn, (long long)need);
   if (!aligned16(workspace)) return fail(BS_ERR_ALIGN, "%s: workspace must be 16-byte aligned", fn);
@@ -379,9 +412,41 @@ int bs_bitserial_conv2d_nhwc_i8(const uint8_t* act, int a_bits, const uint32_t* 
     return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint32_t* ap = static_cast<uint32_t*>(workspace);
-  if (int st = cuda_status(bs::launch_bitpack(act, ap, int64_t(n) * h * w, c, row_words(c), a_bits, s), fn)) return st;
   bs::ConvProblem p = make_conv(ap, a_bits, w_packed, w_bits, w_enc, out, g);
+  if (use_small(p)) {  // one launch, packing fused (the workspace is not touched)
+    const bs::SmallConv sc{p, act};
+    return cuda_status(bs::launch_small_conv(&sc, 1, a_bits, w_bits, s), fn);
+  }
+  if (int st = cuda_status(bs::launch_bitpack(act, ap, int64_t(n) * h * w, c, row_words(c), a_bits, s), fn)) return st;
   return launch_conv(p, BS_ALGO_AUTO, s, fn);
+}
+
+int bs_bitserial_conv2d_nhwc_i8_group(const bs_conv_i8_desc* descs, int count, int a_bits, int w_bits, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_i8_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  if (!bs::small_supported(a_bits, w_bits))
+    return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,2]", fn);
+  std::vector<bs::SmallConv> ps(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_conv_i8_desc& d = descs[q];
+    const ConvArgs g{d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw, d.stride_h, d.stride_w, d.pad_h, d.pad_w};
+    if (int st = check_conv(g, a_bits, w_bits, d.w_enc, fn)) return st;
+    if (d.w_enc == BS_SIGNED) return fail(BS_ERR_UNSUPPORTED, "%s: descriptor %d: signed weights", fn, q);
+    if (int64_t(d.kh) * d.kw > 64) return fail(BS_ERR_UNSUPPORTED, "%s: descriptor %d: more than 64 filter taps", fn, q);
+    if (!d.act || !d.w_packed || !d.out) return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    if (!aligned16(d.act) || !aligned16(d.w_packed) || !aligned16(d.out))
+      return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
+    if (int64_t(d.n) * d.h * d.w * d.c > (int64_t(1) << 40)) return fail(BS_ERR_SHAPE, "%s: descriptor %d too large", fn, q);
+    ps[q] = bs::SmallConv{make_conv(nullptr, a_bits, d.w_packed, w_bits, d.w_enc, d.out, g), d.act};
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int q0 = 0; q0 < count; q0 += bs::kSmallMax) {
+    const int cnt = count - q0 < bs::kSmallMax ? count - q0 : bs::kSmallMax;
+    if (int st = cuda_status(bs::launch_small_conv(ps.data() + q0, cnt, a_bits, w_bits, s), fn)) return st;
+  }
+  return BS_OK;
 }
 
 int64_t bs_conv2d_tc_workspace_bytes(int oc, int kh, int kw, int c, int w_bits) {
@@ -593,6 +658,26 @@ int bs_bitserial_dense_tc_prepared_gather(const uint32_t* a_packed, int a_bits, 
   p.a_enc = a_enc;
   return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream), out_peers,
                                                  npeers), fn);
+}
+
+int bs_bitserial_dense_tc_prepared_multicast(const uint32_t* a_packed, int a_bits, int a_enc, const int8_t* w_tc,
+                                             int w_bits, int w_enc, int tc_format, int32_t* out_mc, int64_t m,
+                                             int64_t n, int64_t k, void* stream) {
+  const char* fn = "bs_bitserial_dense_tc_prepared_multicast";
+  if (int st = check_format(tc_format, fn)) return st;
+  if (int st = check_tc_enc(a_enc, w_enc, tc_format, fn)) return st;
+  if (int st = check_dense(a_packed, reinterpret_cast<const uint32_t*>(w_tc), out_mc, a_bits, w_bits, BS_UNIPOLAR, m,
+                           n, k, fn))
+    return st;
+  if (int st = check_tc_bound(k, a_bits, w_bits, tc_format, fn, a_enc, w_enc)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1) return fail(BS_ERR_SHAPE, "%s: m or n too large", fn);
+  if (n % 4 != 0) return fail(BS_ERR_UNSUPPORTED, "%s: the multicast epilogue needs n %% 4 == 0", fn);
+  ConvArgs g{1, int(m), 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
+  bs::ConvProblem p = make_conv(a_packed, a_bits, nullptr, w_bits, BS_UNIPOLAR, out_mc, g);
+  p.a_enc = a_enc;
+  return cuda_status(bs::launch_tc_conv_prepared(p, w_tc, tc_format, static_cast<cudaStream_t>(stream), nullptr, 0,
+                                                 out_mc), fn);
 }
 
 int bs_bitserial_dense_tc_i8(const uint8_t* a, int a_bits, int a_enc, const int8_t* w_tc, int w_bits, int w_enc,

@@ -24,7 +24,7 @@ namespace bs {
 
 namespace {
 
-constexpr int kGemvThreads = 128;  // 4 warps per CTA
+constexpr int kGemvThreads = 64;   // 2 warps per CTA: 16 weight rows, 256 CTAs for n = 4096 (> 148 SMs)
 constexpr int kR = 8;              // weight rows per warp
 constexpr int kMaxM = 8;
 constexpr size_t kMaxSmem = 96 * 1024;
@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
                                                              const uint32_t* __restrict__ w_packed,
                                                              int32_t* __restrict__ out, int m, int64_t n,
                                                              int64_t k, int kwp, int bipolar) {
-  extern __shared__ __align__(16) uint32_t s_act[];  // [A][m][kwp], then rowsum[m]
-  int* s_rowsum = reinterpret_cast<int*>(s_act + A * m * kwp);
+  extern __shared__ __align__(16) uint32_t s_act[];  // [A][m][kwp], then per-warp row sums [warps][m]
+  int* s_part = reinterpret_cast<int*>(s_act + A * m * kwp);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n0 = (int64_t(blockIdx.x) * (kGemvThreads / 32) + warp) * kR;
   const int64_t w_plane = n * kwp;
@@ -63,7 +63,12 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
   const bool prefetched = n0 < n && lane < nchunks;
   if (prefetched) load_w(lane, wv0);
 
-  // ---- stage the activation operand (packed) in shared memory
+  // ---- stage the activation operand (packed) in shared memory; bipolar: the row sums
+  // sum_k a[r][k] = sum_b 2^b popc(plane b) are gathered on the way (per warp, no second
+  // pass and no second barrier)
+  int rs[kMaxM];
+#pragma unroll
+  for (int r = 0; r < kMaxM; ++r) rs[r] = 0;
   if (FUSED) {
     const bool al16 = (reinterpret_cast<uintptr_t>(a_codes) % 16 == 0) && (k % 16 == 0);
     for (int t = tid; t < m * kwp; t += kGemvThreads) {
@@ -84,23 +89,39 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
           v[q] = x;
         }
       }
+      int s = 0;
 #pragma unroll
-      for (int b = 0; b < A; ++b) s_act[(b * m + r) * kwp + j] = plane_word(v, b);
+      for (int b = 0; b < A; ++b) {
+        const uint32_t wd = plane_word(v, b);
+        s_act[(b * m + r) * kwp + j] = wd;
+        s += __popc(wd) << b;
+      }
+#pragma unroll
+      for (int rr = 0; rr < kMaxM; ++rr) rs[rr] += rr == r ? s : 0;
     }
   } else {
-    for (int t = tid; t < A * m * kwp; t += kGemvThreads) s_act[t] = __ldg(a_packed + t);
+    for (int t = tid; t < A * m * kwp; t += kGemvThreads) {
+      const uint32_t wd = __ldg(a_packed + t);
+      s_act[t] = wd;
+      const int b = t / (m * kwp), r = (t / kwp) % m;
+#pragma unroll
+      for (int rr = 0; rr < kMaxM; ++rr) rs[rr] += rr == r ? (__popc(wd) << b) : 0;
+    }
+  }
+  if (bipolar) {
+    for (int r = 0; r < m; ++r) {
+      const int s = __reduce_add_sync(0xffffffffu, rs[r]);
+      if (lane == 0) s_part[warp * kMaxM + r] = s;
+    }
   }
   __syncthreads();
-  if (bipolar) {  // rowsum[r] = sum_k a[r][k] = sum_b 2^b popc(plane b)
-    for (int r = warp; r < m; r += kGemvThreads / 32) {
-      int s = 0;
-      for (int j = lane; j < kwp; j += 32)
+  int rowsum[kMaxM];
 #pragma unroll
-        for (int b = 0; b < A; ++b) s += __popc(s_act[(b * m + r) * kwp + j]) << b;
-      s = __reduce_add_sync(0xffffffffu, s);
-      if (lane == 0) s_rowsum[r] = s;
-    }
-    __syncthreads();
+  for (int r = 0; r < kMaxM; ++r) {
+    rowsum[r] = 0;
+    if (bipolar && r < m)
+#pragma unroll
+      for (int w2 = 0; w2 < kGemvThreads / 32; ++w2) rowsum[r] += s_part[w2 * kMaxM + r];
   }
 
   if (n0 >= n) return;
@@ -169,7 +190,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
       const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
       if (n0 + r < n) {
         const int u = part[0];
-        out[int64_t(mi) * n + n0 + r] = bipolar ? 2 * u - ((1 << W) - 1) * s_rowsum[mi] : u;
+        int rsum = 0;
+#pragma unroll
+        for (int rr = 0; rr < kMaxM; ++rr) rsum = rr == mi ? rowsum[rr] : rsum;
+        out[int64_t(mi) * n + n0 + r] = bipolar ? 2 * u - ((1 << W) - 1) * rsum : u;
       }
     }
   }
@@ -178,7 +202,7 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
 template <int A, int W>
 cudaError_t launch_aw(const uint32_t* a_packed, const uint8_t* a_codes, const uint32_t* w_packed, int bipolar,
                       int32_t* out, int64_t m, int64_t n, int64_t k, int64_t kwp, cudaStream_t stream) {
-  const size_t smem = size_t(A) * m * kwp * 4 + kMaxM * 4;
+  const size_t smem = size_t(A) * m * kwp * 4 + (kGemvThreads / 32) * kMaxM * 4;
   const int64_t warps = (n + kR - 1) / kR;
   const unsigned grid = unsigned((warps + kGemvThreads / 32 - 1) / (kGemvThreads / 32));
   const bool vec4 = (kwp % 4 == 0) && (reinterpret_cast<uintptr_t>(w_packed) % 16 == 0);
@@ -211,7 +235,7 @@ cudaError_t launch_aw(const uint32_t* a_packed, const uint8_t* a_codes, const ui
 bool gemv_supported(int64_t m, int64_t k, int a_bits, int w_bits) {
   const bool bits_ok = (a_bits == 1 || a_bits == 2 || a_bits == 4) && (w_bits == 1 || w_bits == 2);
   const int64_t kwp = ((k + 31) / 32 + 1) / 2 * 2;
-  return bits_ok && m >= 1 && m <= kMaxM && size_t(a_bits) * m * kwp * 4 + kMaxM * 4 <= kMaxSmem;
+  return bits_ok && m >= 1 && m <= kMaxM && size_t(a_bits) * m * kwp * 4 + (kGemvThreads / 32) * kMaxM * 4 <= kMaxSmem;
 }
 
 cudaError_t launch_gemv(const uint32_t* a_packed, const uint8_t* a_codes, int a_bits, const uint32_t* w_packed,

@@ -36,7 +36,7 @@ void note_launch();
 int64_t launch_count();
 
 // Process-wide tuning knobs (bs_set_tuning; atomics, read per launch; 0 = library choice).
-enum TuneKnob : int { kTuneTileN = 0, kTuneEpilogue = 1, kTuneGroupSplit = 2, kTuneBSlots = 3, kTuneCount = 4 };
+enum TuneKnob : int { kTuneTileN = 0, kTuneEpilogue = 1, kTuneGroupSplit = 2, kTuneBSlots = 3, kTuneSmallKs = 4, kTuneCount = 5 };
 int tuning(int knob);
 // SM count of the current device (cached per device).
 int device_sms();
@@ -83,12 +83,29 @@ cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w
                                      int c_tap, int kw_tap, int8_t* wexp, int fmt, cudaStream_t stream);
 // peers (npeer <= 8): the output is also stored, box by box from the same staged tile, to
 // these [M][oc] blocks (other ranks' gathered buffers mapped over NVLink): a fused all-gather.
+// mcast: the multicast (NVLS) address of the output instead: one multimem store per staged
+// row segment reaches every device bound to the multicast object (fused all-gather, §8 f2).
 cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream,
-                                    int32_t* const* peers = nullptr, int npeer = 0);
+                                    int32_t* const* peers = nullptr, int npeer = 0, int32_t* mcast = nullptr);
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream);
+// FP4 tensor-core conv / dense on the PACKED weight planes (no prepared copy): the producer
+// warps expand each weight chunk in shared memory (unipolar / bipolar weights, unsigned
+// activations; FP4 exactness bound applies).  The three-call boundary's tensor-core path.
+cudaError_t launch_tc_conv_raw(const ConvProblem& p, cudaStream_t stream);
 // Several problems of one (a_bits, w_bits) in one persistent launch per 16 problems.
 cudaError_t launch_tc_conv_group(const ConvProblem* ps, const int8_t* const* wexps, int count, int fmt,
                                  cudaStream_t stream);
+
+// Small problems in ONE launch (small_conv.cu): activation packing fused, AND+POPC, K split
+// across a thread-block cluster and reduced through distributed shared memory.
+// a_bits in [1,4], w_bits in [1,2], unipolar / bipolar weights; up to kSmallMax problems.
+constexpr int kSmallMax = 16;
+struct SmallConv {
+  ConvProblem p;        // geometry, packed weights (p.wt), output (p.out); p.act unused
+  const uint8_t* act;   // uint8 NHWC activation codes
+};
+bool small_supported(int a_bits, int w_bits);
+cudaError_t launch_small_conv(const SmallConv* ps, int count, int a_bits, int w_bits, cudaStream_t stream);
 
 // Matrix-vector kernel for m <= 8 dense products.
 //   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)

@@ -317,12 +317,9 @@ template <int A_T, int W_T, int BM, int BN, bool LIT, int G>
 cudaError_t launch_cfg(const ConvProblem& p, int BK, cudaStream_t stream) {
   const size_t smem = SmemLayout<BM, BN>::bytes(p.a_bits, p.w_bits);
   auto kern = popc_conv_kernel<A_T, W_T, BM, BN, LIT, G>;
-  static int configured_bytes = 0;  // per instantiation; attribute only grows
-  if (int(smem) > configured_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    configured_bytes = int(smem);
-  }
+  // the dynamic shared-memory opt-in is per device and per size: set it on every launch
+  // (a host-side attribute write; this is not the hot path)
+  if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) return e;
   // Split K across CTAs when the M x N tiles cannot fill the 148 SMs twice (batch-1
   // layers): keep >= 2 k-tiles per slice; partials are summed with int32 atomics into
   // a zeroed output (exact: integer addition is associative).

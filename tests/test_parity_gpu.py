@@ -806,3 +806,207 @@ def test_tc_single_launch_writes_stay_in_bounds(tuning, fmt, bn, a_bits, w_bits)
     host = flat.cpu().numpy()
     np.testing.assert_array_equal(host[guard:guard + cnt].reshape(ref.shape), ref)
     assert (host[:guard] == 0x3C3C3C3C).all() and (host[guard + cnt:] == 0x3C3C3C3C).all()
+
+
+# ------------------------------------------------- one-launch small-problem path (N6)
+SMALL_CASES = CONV_CASES + [(1, 1, 300, 100, 70, 1, 1, 1, 1, 0, 0),   # dense 300 x 70, k = 100
+                            (1, 1, 17, 4096, 130, 1, 1, 1, 1, 0, 0)]  # dense 17 x 130, k = 4096
+
+
+def _small_run(cases, a_bits, w_bits, encs, seed):
+    items, refs = [], []
+    for i, (n, h, w, c, oc, kh, kw, sh, sw, ph, pw) in enumerate(cases):
+        g = inputs.gen(seed * 1000 + i)
+        act = inputs.codes((n, h, w, c), a_bits, g)
+        wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+        we = encs[i % len(encs)]
+        refs.append(oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, we == bs.BIPOLAR, stride=(sh, sw),
+                                       pad=(ph, pw)))
+        items.append(dict(act=act.to(DEV), w_packed=gpu_pack(wt.view(oc * kh * kw, c), w_bits), w_enc=we, oc=oc,
+                          kh=kh, kw=kw, stride=(sh, sw), pad=(ph, pw)))
+    return bs.bitserial_conv2d_nhwc_i8_group(items, a_bits, w_bits), refs
+
+
+@pytest.mark.parametrize("ks", [0, 1, 2, 4, 8])
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (3, 1), (4, 2), (1, 2)])
+def test_small_group_ragged(tuning, ks, a_bits, w_bits):
+    """bs_bitserial_conv2d_nhwc_i8_group (fused packing, AND+POPC, K slices of a tile summed
+    through distributed shared memory) on the ragged conv cases and two dense layers, every
+    K split (0 = automatic), unipolar and bipolar members in one launch: exact."""
+    if ks:
+        tuning(bs.TUNE_SMALL_KSPLIT, ks)
+    outs, refs = _small_run(SMALL_CASES, a_bits, w_bits, [bs.UNIPOLAR, bs.BIPOLAR], seed=10 * a_bits + w_bits + ks)
+    for i, (o, r) in enumerate(zip(outs, refs)):
+        np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"member {i} {SMALL_CASES[i]}")
+
+
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2)])
+@pytest.mark.parametrize("bipolar", [False, True])
+def test_small_group_resnet_batch1(a_bits, w_bits, bipolar):
+    """BASELINE configs[2]: the ten ResNet-18 layers at batch 1 in ONE launch of the small
+    path (the bench's resnet1 step), every output vs the oracle."""
+    cases = [(1, L.h, L.w, L.ic, L.oc, L.k, L.k, L.s, L.s, L.pad, L.pad)
+             for L in (inputs.TABLE1[li] for li in inputs.BASELINE_LAYERS)]
+    enc_ = bs.BIPOLAR if bipolar else bs.UNIPOLAR
+    outs, refs = _small_run(cases, a_bits, w_bits, [enc_], seed=77 + a_bits * 10 + w_bits)
+    for li, o, r in zip(inputs.BASELINE_LAYERS, outs, refs):
+        np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"layer {li}")
+
+
+def test_small_group_validation():
+    """Unsupported precisions / signed weights are refused before launch; more than 16
+    members run as consecutive launches; an empty group is a no-op."""
+    g = inputs.gen(3)
+    act = inputs.codes((1, 5, 5, 8), 2, g).to(DEV)
+    wt = gpu_pack(inputs.codes((4, 8), 3, g), 3)
+    with pytest.raises(bs.BitserialError, match="UNSUPPORTED"):
+        bs.bitserial_conv2d_nhwc_i8_group([dict(act=act, w_packed=wt, oc=4, kh=1, kw=1)], 2, 3)
+    wt1 = gpu_pack(inputs.codes((4, 8), 1, g), 1)
+    with pytest.raises(bs.BitserialError, match="UNSUPPORTED|INVALID_ARG"):
+        bs.bitserial_conv2d_nhwc_i8_group([dict(act=act, w_packed=wt1, w_enc=bs.SIGNED, oc=4, kh=1, kw=1)], 2, 1)
+    assert bs.bitserial_conv2d_nhwc_i8_group([], 2, 1) == []
+    cases = [(1, 3 + i % 4, 4 + i % 3, 8 + 8 * (i % 5), 5 + 3 * i, 3, 3, 1 + i % 2, 1, 1, 1) for i in range(19)]
+    outs, refs = _small_run(cases, 2, 1, [bs.BIPOLAR, bs.UNIPOLAR], seed=4)
+    for i, (o, r) in enumerate(zip(outs, refs)):
+        np.testing.assert_array_equal(o.cpu().numpy(), r, err_msg=f"member {i}")
+
+
+# ------------------------------- the three-call boundary on the tensor cores (packed weights)
+THREE_CALL_CONV = [(2, 13, 11, 96, 40, 3, 3, 1, 1, 1, 1), (3, 10, 10, 64, 300, 3, 3, 2, 2, 1, 1),
+                   (1, 9, 7, 5, 3, 3, 3, 1, 1, 1, 1), (2, 5, 9, 17, 6, 2, 3, 3, 1, 2, 0),
+                   (2, 7, 7, 512, 64, 3, 3, 1, 1, 1, 1), (4, 14, 14, 256, 130, 3, 3, 1, 1, 1, 1),
+                   (2, 8, 8, 64, 128, 1, 1, 2, 2, 0, 0)]
+
+
+@pytest.mark.parametrize("case", THREE_CALL_CONV)
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (4, 2), (3, 3), (4, 4)])
+@pytest.mark.parametrize("bipolar", [False, True])
+def test_three_call_conv_tc(case, a_bits, w_bits, bipolar):
+    """bs_bitpack + bs_bitserial_conv2d_nhwc (BS_ALGO_AUTO -> the tensor-core kernel on the
+    PACKED weight planes, expanded in shared memory by the producer warps) and BS_ALGO_TC
+    explicitly: exact on ragged geometries, every precision A, W <= 4, both encodings."""
+    n, h, w, c, oc, kh, kw, sh, sw, ph, pw = case
+    g = inputs.gen(sum(case) * 13 + a_bits * 7 + w_bits + (1000 if bipolar else 0))
+    act = inputs.codes((n, h, w, c), a_bits, g)
+    wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+    ref = oracle.conv2d_nhwc(act.numpy(), a_bits, wt.numpy(), w_bits, bipolar, stride=(sh, sw), pad=(ph, pw))
+    ap = gpu_pack(act.view(-1, c), a_bits)
+    wp = gpu_pack(wt.view(oc * kh * kw, c), w_bits)
+    for algo in (bs.ALGO_AUTO, bs.ALGO_TC):
+        got = bs.bitserial_conv2d_nhwc(ap, a_bits, wp, w_bits, enc(bipolar), n, h, w, c, oc, kh, kw, (sh, sw),
+                                       (ph, pw), algo=algo)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"algo {algo}")
+
+
+@pytest.mark.parametrize("slots", [0, 2, 3])
+@pytest.mark.parametrize("bn", [0, 64, 128])
+def test_three_call_conv_tc_weight_slots(tuning, slots, bn):
+    """Packed-weight tensor-core launches with the weight chunks resident (loaded once per N
+    block and CTA) and streamed through 2 or 3 slots (every chunk re-expanded by the producer
+    team that handles it), both tile widths, 3 N blocks, 18 K chunks."""
+    if slots:
+        tuning(bs.TUNE_TC_B_SLOTS, slots)
+    if bn:
+        tuning(bs.TUNE_TC_TILE_N, bn)
+    n, h, w, c, oc = 2, 9, 9, 512, 300
+    for bipolar in (False, True):
+        g = inputs.gen(slots * 10 + bn + bipolar)
+        act = inputs.codes((n, h, w, c), 2, g)
+        wt = inputs.codes((oc, 3, 3, c), 2, g)
+        ref = oracle.conv2d_nhwc(act.numpy(), 2, wt.numpy(), 2, bipolar, stride=(1, 1), pad=(1, 1))
+        got = bs.bitserial_conv2d_nhwc(gpu_pack(act.view(-1, c), 2), 2, gpu_pack(wt.view(oc * 9, c), 2), 2,
+                                       enc(bipolar), n, h, w, c, oc, 3, 3, 1, 1, algo=bs.ALGO_TC)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("m,n,k", [(9, 7, 33), (129, 65, 250), (300, 200, 576), (257, 130, 1000), (64, 256, 4096)])
+@pytest.mark.parametrize("a_bits,w_bits", [(1, 1), (2, 1), (2, 2), (4, 1)])
+def test_three_call_dense_tc(m, n, k, a_bits, w_bits):
+    """bs_bitserial_dense (AUTO: the tensor-core kernel on packed weights for m > 8)."""
+    for bipolar in (False, True):
+        a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=m + n + k + 10 * a_bits + w_bits + bipolar)
+        ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+        for algo in (bs.ALGO_AUTO, bs.ALGO_TC):
+            got = bs.bitserial_dense(gpu_pack(a, a_bits), a_bits, gpu_pack(w, w_bits), w_bits, enc(bipolar), m, n, k,
+                                     algo=algo)
+            np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+def test_three_call_tc_refusals():
+    """BS_ALGO_TC outside its domain is refused before launch: W = 6, and the FP4 bound."""
+    a = gpu_pack(torch.ones((4, 64), dtype=torch.uint8), 2)
+    w6 = gpu_pack(torch.ones((4, 64), dtype=torch.uint8), 6)
+    with pytest.raises(bs.BitserialError, match="UNSUPPORTED"):
+        bs.bitserial_dense(a, 2, w6, 6, bs.UNIPOLAR, 4, 4, 64, algo=bs.ALGO_TC)
+    k = 18_642
+    a4 = gpu_pack(torch.full((2, k), 15, dtype=torch.uint8), 4)
+    w4 = gpu_pack(torch.full((3, k), 15, dtype=torch.uint8), 4)
+    with pytest.raises(bs.BitserialError, match="UNSUPPORTED"):
+        bs.bitserial_dense(a4, 4, w4, 4, bs.UNIPOLAR, 2, 3, k, algo=bs.ALGO_TC)
+    # AUTO past the bound falls back to the integer pipes, still exact
+    got = bs.bitserial_dense(a4, 4, w4, 4, bs.UNIPOLAR, 2, 3, k)
+    assert int(got[0, 0]) == k * 225
+
+
+def test_three_call_headline_config():
+    """BASELINE configs[3] (ten ResNet-18 layers, batch 256, A2W1 bipolar) through the
+    north_star's three calls only — bs_bitpack of the activations and bs_bitserial_conv2d_nhwc
+    on packed weights (AUTO: tensor cores) — every layer checked against the oracle on
+    sampled images; the step time is compared with the grouped prepared-weight step."""
+    import time
+    runs = []
+    for li in inputs.BASELINE_LAYERS:
+        L = inputs.TABLE1[li]
+        act, wt = inputs.conv_operands(L, 256, 2, 1, inputs.seed_for(4, 2, 1, "bipolar", li))
+        wp = gpu_pack(wt.view(L.oc * L.k * L.k, L.ic), 1)
+        runs.append((L, act, wt, act.to(DEV), wp))
+
+    def step(outs=None):
+        res = []
+        for L, _, _, act_d, wp in runs:
+            ap = bs.bitpack(act_d.view(-1, L.ic), 2)
+            res.append(bs.bitserial_conv2d_nhwc(ap, 2, wp, 1, bs.BIPOLAR, 256, L.h, L.w, L.ic, L.oc, L.k, L.k, L.s,
+                                                L.pad))
+        return res
+    outs = step()
+    torch.cuda.synchronize()
+    for (L, act, wt, _, _), o in zip(runs, outs):
+        for img in (0, 131, 255):
+            ref = oracle.conv2d_nhwc(act[img:img + 1].numpy(), 2, wt.numpy(), 1, True, stride=(L.s, L.s),
+                                     pad=(L.pad, L.pad))
+            np.testing.assert_array_equal(o[img:img + 1].cpu().numpy(), ref, err_msg=f"layer {L}")
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"three-call step: {e0.elapsed_time(e1) / 5:.3f} ms")
+
+
+def test_dense_tc_multicast_epilogue_single_device():
+    """The NVLS form of the fused all-gather (bs_bitserial_dense_tc_prepared_multicast): the
+    epilogue stores every row segment with multimem.st to a multicast address.  On one GPU a
+    multicast object bound to that device alone stands in for the NVSwitch group: the C
+    read back through the unicast mapping equals the oracle (multi-GPU replication is
+    unverified here)."""
+    from paper_1810_11066_b200.dist import SingleDeviceMulticast
+    m, n, k = 300, 200, 576
+    try:
+        mc = SingleDeviceMulticast(m * n * 4)
+    except Exception as e:  # noqa: BLE001
+        pytest.skip(f"multicast not available on this device/driver: {e}")
+    try:
+        for a_bits, w_bits, bipolar in ((2, 1, True), (4, 2, False)):
+            a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=a_bits * 10 + w_bits)
+            ref = oracle.dense(a.numpy(), a_bits, w.numpy(), w_bits, bipolar)
+            w_tc = bs.dense_tc_prepare_weights(gpu_pack(w, w_bits), w_bits, enc(bipolar), n, k)
+            bs.bitserial_dense_tc_multicast(gpu_pack(a, a_bits), a_bits, w_tc, w_bits, m, n, k, mc.multicast_ptr(),
+                                            w_enc=enc(bipolar))
+            got = mc.read(m * n * 4).view(torch.int32).view(m, n).numpy()
+            np.testing.assert_array_equal(got, ref)
+    finally:
+        mc.close()

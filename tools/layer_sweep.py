@@ -25,6 +25,9 @@ ap.add_argument("--layers", default=",".join(map(str, inputs.BASELINE_LAYERS)))
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--tc", action="store_true", help="tensor-core path on prepared weights")
 ap.add_argument("--fused", action="store_true", help="include activation packing (the *_i8 entry)")
+ap.add_argument("--raw", action="store_true",
+                help="tensor cores on the PACKED weights (bs_bitserial_conv2d_nhwc, BS_ALGO_TC: weights expanded "
+                     "in the kernel)")
 ap.add_argument("--group", action="store_true",
                 help="tensor-core path through bs_bitserial_conv2d_nhwc_tc_group: each layer as a group of one, "
                      "then all layers in one group")
@@ -74,7 +77,10 @@ for li in map(int, args.layers.split(",")):
     ws = torch.empty(max(16, bs.conv2d_workspace_bytes(args.batch, L.h, L.w, L.ic, args.a)), dtype=torch.uint8,
                      device=dev)
     w_tc = bs.conv2d_tc_prepare_weights(wp, args.w, enc, L.oc, L.k, L.k, L.ic) if args.tc else None
-    if args.group:
+    if args.raw:
+        run = lambda s: bs.bitserial_conv2d_nhwc(ap_, args.a, wp, args.w, enc, args.batch, L.h, L.w, L.ic, L.oc,  # noqa
+                                                 L.k, L.k, L.s, L.pad, out=out, algo=bs.ALGO_TC, stream=s)
+    elif args.group:
         item = dict(act_packed=ap_, w_tc=w_tc, out=out, n=args.batch, h=L.h, w=L.w, c=L.ic, oc=L.oc, kh=L.k, kw=L.k,
                     stride=L.s, pad=L.pad, w_enc=enc)
         items.append(item)
