@@ -1010,15 +1010,15 @@ def main():
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
     ap.add_argument("--path", choices=["auto", "tc", "popc", "small"], default="auto",
                     help="conv/GEMM kernel: tensor-core bitserial, the AND/POPC integer-pipe kernel, or the one-launch "
-                         "small-problem path; auto = small for the batch-1 conv workloads, else tc")
+                         "small-problem path; auto = small for conv1, else tc")
     ap.add_argument("--fused-gather", action="store_true",
                     help="gemm, N>1: all-gather fused into the tensor-core epilogue over symmetric memory (SURVEY 8 f2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step's outputs")
     args = ap.parse_args()
-    if args.path == "auto":
-        args.path = "small" if args.workload in ("conv1", "resnet1") else "tc"
+    if args.path == "auto":  # measured: small wins the single batch-1 layer, tc the ten-layer batch-1 step
+        args.path = "small" if args.workload == "conv1" else "tc"
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if world == 0 and args.gpus > 1:  # not launched by torchrun: launch N ranks (one per GPU) ourselves
         return relaunch(args.gpus)

@@ -88,6 +88,8 @@ cudaError_t launch_tc_expand_weights(const uint32_t* w_packed, int w_bits, int w
 cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, int fmt, cudaStream_t stream,
                                     int32_t* const* peers = nullptr, int npeer = 0, int32_t* mcast = nullptr);
 cudaError_t launch_tc_conv(const ConvProblem& p, int8_t* wexp_ws, int fmt, cudaStream_t stream);
+// FP4 prepared-weight launch whose epilogue stores through the multicast address `mcast`.
+cudaError_t launch_tc_conv_mcast(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream, int32_t* mcast);
 // FP4 tensor-core conv / dense on the PACKED weight planes (no prepared copy): the producer
 // warps expand each weight chunk in shared memory (unipolar / bipolar weights, unsigned
 // activations; FP4 exactness bound applies).  The three-call boundary's tensor-core path.

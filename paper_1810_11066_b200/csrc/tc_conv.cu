@@ -113,10 +113,11 @@ cudaError_t launch_tc_conv_prepared(const ConvProblem& p, const int8_t* wexp, in
                                     int32_t* const* peers, int npeer, int32_t* mcast) {
   if (!tc_supported(p.a_bits, p.w_bits)) return cudaErrorNotSupported;
   const bool f4 = tc_resolve_format(fmt) == kTcF4;
+  if (mcast) return f4 ? launch_tc_conv_mcast(p, wexp, stream, mcast) : cudaErrorNotSupported;
 #define BS_TC(A, W, CALL)                                                                 \
   if (p.a_bits == A && p.w_bits == W)                                                     \
-    return f4 ? tc::launch_aw<A, W, true>(p, wexp, stream, peers, npeer, mcast)           \
-              : tc::launch_aw<A, W, false>(p, wexp, stream, peers, npeer, mcast);
+    return f4 ? tc::launch_aw<A, W, true>(p, wexp, stream, peers, npeer)                  \
+              : tc::launch_aw<A, W, false>(p, wexp, stream, peers, npeer);
   BS_TC_DISPATCH(0)
 #undef BS_TC
   return cudaErrorNotSupported;

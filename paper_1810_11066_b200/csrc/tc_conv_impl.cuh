@@ -593,6 +593,7 @@ struct Cfg {
 // the switch replicates it to every rank's copy, this rank's included).
 enum EpiMode : int { kEpiDirect = 0, kEpiTma = 1, kEpiScalar = 2, kEpiMcast = 3 };
 
+
 // 16 bytes to a multicast (NVLS) address: every device bound to the multicast object gets them.
 __device__ __forceinline__ void multimem_st_v4(int32_t* p, uint4 v) {
   asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
@@ -644,6 +645,10 @@ struct TcArgs {
   int nbs;            // B chunk slots in use (<= kBSlots; BS_TUNE_TC_B_SLOTS caps it)
   int npeer;          // single-problem launches: every output box is also stored through peer[0..npeer)
   int32_t* mcast;     // single-problem kEpiMcast launches: multicast address of out[0][0]
+  int blocked;        // raw-weight launches with several N blocks: each CTA walks a contiguous range of the
+                      // N-major tiles, so the weights it expanded for an N block serve its next tiles
+                      // (otherwise a grid stride: neighbouring CTAs on neighbouring tiles, which the
+                      // output writes and the activation halos favour)
   int debug;          // BS_TC_PROFILE / BS_TC_KNOBS builds only: bit 0 skip output stores, 1 skip A tcgen05.st,
                       // 2 skip accumulator tcgen05.ld, 3 skip the producers' global loads,
                       // 4 MMA warp ignores full_a, 5 producers idle, 6 producers keep their first tile's
@@ -713,16 +718,29 @@ struct RawTrack {
 // K: producer / MMA work) alternate with output-heavy ones (1x1 layers: epilogue and HBM
 // work) and the roles of one SM overlap the two kinds; the problem index is tracked per
 // set (it only grows within a set).  Every role walks an identical copy.
-template <int NP>
+template <int NP, bool BLOCKED = false>
 struct TileSeq {
   int c, g, a, b, j0, j1, pi0, pi1;
   __device__ __forceinline__ explicit TileSeq(const TcArgs<NP>& args) {
     c = int(blockIdx.x);
     g = int(gridDim.x);
     const int t0 = NP > 1 ? args.tiles0 : args.ntiles, t1 = args.ntiles - t0;
-    a = t0 > c ? (t0 - 1 - c) / g + 1 : 0;
-    b = t1 > c ? (t1 - 1 - c) / g + 1 : 0;
-    j0 = j1 = 0;
+    if (NP == 1 && BLOCKED && args.blocked) {  // a contiguous range of the N-major tiles: consecutive tiles share
+      // an N block (its weights stay resident) even when the M blocks are fewer than the CTAs
+      j0 = int(int64_t(c) * t0 / g);
+      a = int(int64_t(c + 1) * t0 / g);
+      b = 0;
+      g = 1;
+    } else if (NP == 1) {
+      j0 = 0;
+      a = t0 > c ? (t0 - 1 - c) / g + 1 : 0;
+      b = 0;
+    } else {  // grid stride: every CTA gets a share of each member (members are sorted by K)
+      a = t0 > c ? (t0 - 1 - c) / g + 1 : 0;
+      b = t1 > c ? (t1 - 1 - c) / g + 1 : 0;
+      j0 = 0;
+    }
+    j1 = 0;
     pi0 = 0;
     pi1 = NP > 1 ? args.nset0 : 0;
   }
@@ -730,7 +748,8 @@ struct TileSeq {
   __device__ __forceinline__ bool next(const TcArgs<NP>& args, int& tile, int& pi) {
     if constexpr (NP == 1) {
       if (j0 >= a) return false;
-      tile = c + j0++ * g;
+      tile = (BLOCKED && args.blocked) ? j0 : c + j0 * g;  // blocked ranges start j0 at the range
+      ++j0;
       pi = 0;
       return true;
     } else {
@@ -751,9 +770,15 @@ struct TileSeq {
   }
 };
 
-template <int A_BITS, int W_BITS, int BN, bool F4, int NP, bool RAW = false>
+// Kernel variants (compile-time, so each path costs the others nothing): prepared weights
+// loaded by TMA; RAW packed weight planes expanded by the producers; MCAST prepared weights with
+// the NVLS multicast epilogue.
+enum TcVariant : int { kVarPrep = 0, kVarRaw = 1, kVarMcast = 2 };
+
+template <int A_BITS, int W_BITS, int BN, bool F4, int NP, int VAR = kVarPrep>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_conv_kernel(const __grid_constant__ TcArgs<NP> args, const __grid_constant__ TcMaps<NP> maps) {
+  constexpr bool RAW = VAR == kVarRaw, MCAST = VAR == kVarMcast;
   static_assert(!RAW || (F4 && NP == 1), "raw-weight launches: FP4 format, single problem");
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
   constexpr int S = C::kStages;   // A ring stages (tensor memory)
@@ -986,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     // iterator of the next chunk to load: tile t (of problem pi), chunk kc
-    TileSeq<NP> seq(args);
+    TileSeq<NP, RAW> seq(args);
     int t = -1, kc = team, cur_tile = -1;
     RawTrack rt;  // RAW: weight-slot loads of every tile (all teams')
     auto next_tile = [&]() -> bool {
@@ -1017,8 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int nenc = 0;
     // RAW: the chunk's weight row (this thread's filter) prefetched with its activations
     constexpr int kRW = RAW ? W_BITS : 1;
-    uint2 wnx[kRW][4];
-    uint32_t wvalid = 0;                   // valid-element mask of each of the 8 words, nibble-spread later
+    int wn = 0;  // the thread's filter row of the chunk's N block
     int wslot = 0, wreload = 0, wg = 0;  // the chunk's B slot, reload flag, its index in the CTA's chunk sequence
     int wkk0 = 0, lg = team;             // lg: sequence index of the chunk advance_load loads
     auto advance_load = [&]() -> bool {
@@ -1033,21 +1057,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         wslot = rt.res ? kc : (rt.slot0 + kc) % nbs;
         wreload = rt.reload;
         wg = lg;
-        if (wreload) {
-          const TcProb& P = args.prob[pi];
+        if (wreload) {  // (the weight words are loaded when the chunk is expanded: reloads are rare
+          // when weights stay resident, and holding them from here would spill registers)
           uint32_t mb_, nb_;
-          tile_mn(P, t, mb_, nb_);
-          const int n = int(nb_) * BN + arow;
-          const int kp = int(P.p.kp);
+          tile_mn(args.prob[pi], t, mb_, nb_);
+          wn = int(nb_) * BN + arow;
           wkk0 = kc * C::kCW;
-          const bool rowok = arow < BN && n < P.p.oc;
-          const uint32_t* wrow = P.p.wt + (int64_t(n) * kp + wkk0);
-#pragma unroll
-          for (int j = 0; j < kRW; ++j)
-#pragma unroll
-            for (int q = 0; q < 4; ++q)  // packed rows have an even word count: 2-word pieces are all-in or all-out
-              wnx[j][q] = (rowok && wkk0 + 2 * q < kp) ? ldg_nc_v2(wrow + int64_t(j) * P.p.oc * kp + 2 * q)
-                                                       : make_uint2(0u, 0u);
         }
       }
       kc += kTeams;
@@ -1097,6 +1112,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (RAW) {
         if (wreload) {  // this chunk's weights: packed planes -> E2M1 digit rows of the B slot
           const TcProb& P = args.prob[0];
+          uint2 wnx[kRW][4];
+          {
+            const int kp = int(P.p.kp);
+            const bool rowok = arow < BN && wn < P.p.oc;
+            const uint32_t* wrow = P.p.wt + (int64_t(wn) * kp + wkk0);
+#pragma unroll
+            for (int j = 0; j < kRW; ++j)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)  // packed rows have an even word count: 2-word pieces are all-in or all-out
+                wnx[j][q] = (rowok && wkk0 + 2 * q < kp) ? ldg_nc_v2(wrow + int64_t(j) * P.p.oc * kp + 2 * q)
+                                                         : make_uint2(0u, 0u);
+          }
           for (;;) {  // the TMA warp released the slot to this chunk (its previous use consumed)
             int r;
             asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(r) : "r"(smem_u32(s_ready + wslot)) : "memory");
@@ -1171,7 +1198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pi = 0, tile = 0, g = 0;
       uint32_t ldpar = 0;  // bit b: parity of the writes released into B slot b
       BPlan plan;
-      TileSeq<NP> seq(args);
+      TileSeq<NP, RAW> seq(args);
       bool have = seq.next(args, tile, pi);
       while (have) {
         const TcProb& P = args.prob[pi];
@@ -1196,7 +1223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pi = 0, tile = 0;
       uint32_t ldpar = 0;  // bit b: parity of the loads issued into B slot b
       BPlan plan;
-      for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
+      for (TileSeq<NP, RAW> seq(args); seq.next(args, tile, pi);) {
         const TcProb& P = args.prob[pi];
         uint32_t mb, nb;
         tile_mn(P, tile, mb, nb);
@@ -1230,7 +1257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool first = true;
     const uint64_t bdesc0 = smem_desc_sw128(smem_u32(s_stage));
     BPlan plan;
-    TileSeq<NP> seq(args);
+    TileSeq<NP, RAW> seq(args);
     bool have = seq.next(args, tile, pi);
     while (have) {
       int ntile = 0, npi = 0;
@@ -1310,7 +1337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0, buf = 0, pi = 0, tile = 0;
     uint32_t acc_phase = 0;
     bool first = true;
-    for (TileSeq<NP> seq(args); seq.next(args, tile, pi);) {
+    for (TileSeq<NP, RAW> seq(args); seq.next(args, tile, pi);) {
       const TcProb& P = args.prob[pi];
       uint32_t mb, nb;
       tile_mn(P, tile, mb, nb);
@@ -1388,7 +1415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           PROF_END(3)
           buf = buf + 1 == kEpiBufs ? 0 : buf + 1;
-        } else if (NP == 1 && epi == kEpiMcast) {  // swizzled staging, then row-contiguous multimem stores
+        } else if (MCAST) {  // swizzled staging, then row-contiguous multimem stores
           uint8_t* b0 = ebuf + buf * kEpiBufBytes;
           const uint32_t swz = uint32_t(lane & 7);
 #pragma unroll
@@ -1514,11 +1541,12 @@ inline bool make_prob(TcProb& P, CUtensorMap& tw, CUtensorMap& to, const ConvPro
   return true;
 }
 
-template <int A_BITS, int W_BITS, int BN, bool F4, int NP, bool RAW = false>
+template <int A_BITS, int W_BITS, int BN, bool F4, int NP, int VAR = kVarPrep>
 cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int count, cudaStream_t stream,
                       int nset0 = -1, int32_t* const* peers = nullptr, int npeer = 0, int32_t* mcast = nullptr) {
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
-  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4, NP, RAW>;
+  constexpr bool RAW = VAR == kVarRaw;
+  auto kern = tc_conv_kernel<A_BITS, W_BITS, BN, F4, NP, VAR>;
   // the dynamic shared-memory opt-in is a per-device function attribute: set once per
   // device (a bit per device, set after the call succeeded; racing threads set it twice)
   static std::atomic<uint64_t> configured{0};
@@ -1547,6 +1575,7 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
   if (total == 0) return cudaSuccess;
   a.ntiles = int(total);
   a.nset0 = nset0 < 0 || nset0 > count ? count : nset0;
+  a.blocked = RAW && a.prob[0].ntn > 1;
   if (npeer > 0) {  // fused all-gather (single problem, TMA-store epilogue)
     if (NP != 1 || npeer > kMaxPeers || a.prob[0].epi != kEpiTma) return cudaErrorNotSupported;
     const ConvProblem& p = ps[0];
@@ -1556,6 +1585,7 @@ cudaError_t launch_bn(const ConvProblem* ps, const int8_t* const* wexps, int cou
         return cudaErrorInvalidValue;
   }
   a.npeer = npeer;
+  if ((mcast != nullptr) != (VAR == kVarMcast)) return cudaErrorInvalidValue;
   if (mcast) {  // NVLS fused all-gather (single problem, oc % 4 == 0)
     if (NP != 1 || a.prob[0].epi != kEpiTma || npeer > 0) return cudaErrorNotSupported;
     a.prob[0].epi = kEpiMcast;
@@ -1586,15 +1616,25 @@ inline int pick_bn(const ConvProblem& p) {
 
 template <int A_BITS, int W_BITS, bool F4>
 cudaError_t launch_aw(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream, int32_t* const* peers = nullptr,
-                      int npeer = 0, int32_t* mcast = nullptr) {
+                      int npeer = 0) {
   switch (pick_bn(p)) {
     case 128:
       if constexpr (Cfg<A_BITS, W_BITS, 128, F4>::kFit >= 2)
-        return launch_bn<A_BITS, W_BITS, 128, F4, 1>(&p, &wexp, 1, stream, -1, peers, npeer, mcast);
+        return launch_bn<A_BITS, W_BITS, 128, F4, 1>(&p, &wexp, 1, stream, -1, peers, npeer);
       [[fallthrough]];
     default:
-      return launch_bn<A_BITS, W_BITS, 64, F4, 1>(&p, &wexp, 1, stream, -1, peers, npeer, mcast);
+      return launch_bn<A_BITS, W_BITS, 64, F4, 1>(&p, &wexp, 1, stream, -1, peers, npeer);
   }
+}
+
+// The NVLS multicast epilogue variant (FP4, single problem; tc_conv_mcast.cu instantiates it).
+template <int A_BITS, int W_BITS>
+cudaError_t launch_mcast_aw(const ConvProblem& p, const int8_t* wexp, cudaStream_t stream, int32_t* mcast) {
+  if (pick_bn(p) == 128) {
+    if constexpr (Cfg<A_BITS, W_BITS, 128, true>::kFit >= 2)
+      return launch_bn<A_BITS, W_BITS, 128, true, 1, kVarMcast>(&p, &wexp, 1, stream, -1, nullptr, 0, mcast);
+  }
+  return launch_bn<A_BITS, W_BITS, 64, true, 1, kVarMcast>(&p, &wexp, 1, stream, -1, nullptr, 0, mcast);
 }
 
 // Raw-weight launch (the three-call boundary: packed weight planes, no prepared copy): the
@@ -1609,9 +1649,9 @@ cudaError_t launch_raw_aw(const ConvProblem& p, cudaStream_t stream) {
   int bn = pick_bn(p);
   if (bn == 128 && !tuning(kTuneTileN) && nchunks > C128::kBSlots && nchunks <= C64::kBSlots) bn = 64;
   if constexpr (C128::kFit >= 2) {
-    if (bn == 128) return launch_bn<A_BITS, W_BITS, 128, true, 1, true>(&p, nullptr, 1, stream);
+    if (bn == 128) return launch_bn<A_BITS, W_BITS, 128, true, 1, kVarRaw>(&p, nullptr, 1, stream);
   }
-  return launch_bn<A_BITS, W_BITS, 64, true, 1, true>(&p, nullptr, 1, stream);
+  return launch_bn<A_BITS, W_BITS, 64, true, 1, kVarRaw>(&p, nullptr, 1, stream);
 }
 
 // Group launch: up to kGroupMax problems of one (A, W) precision in one persistent

@@ -31,8 +31,11 @@ ap.add_argument("--raw", action="store_true",
 ap.add_argument("--group", action="store_true",
                 help="tensor-core path through bs_bitserial_conv2d_nhwc_tc_group: each layer as a group of one, "
                      "then all layers in one group")
+ap.add_argument("--tile-n", type=int, default=0, help="BS_TUNE_TC_TILE_N (0 = library choice)")
 args = ap.parse_args()
 dev = torch.device("cuda")
+if args.tile_n:
+    bs.set_tuning(bs.TUNE_TC_TILE_N, args.tile_n)
 enc = bs.UNIPOLAR if args.unipolar else bs.BIPOLAR
 res = {}
 tot_ops, tot_ms = 0, 0.0
