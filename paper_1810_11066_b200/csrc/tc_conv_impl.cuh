@@ -274,13 +274,15 @@ __device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint
         "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
         "elect.sync x|e, 0xffffffff;\n"
         "setp.ne.b32 p, %3, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n"
+        "@!e bra SKIP%=;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n"
         "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
         "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
         "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+        "SKIP%=:\n"
         "}" ::"r"(d),
         "r"(a), "l"(b), "r"(accumulate), "n"(IDESC));
     return;
@@ -289,13 +291,15 @@ __device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
       "elect.sync x|e, 0xffffffff;\n"
       "setp.ne.b32 p, %3, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n"
+      "@!e bra SKIP%=;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, p;\n"
       "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
       "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
       "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n"
+      "SKIP%=:\n"
       "}" ::"r"(d),
       "r"(a), "l"(b), "r"(accumulate), "r"(idesc));
 }
@@ -304,7 +308,9 @@ __device__ __forceinline__ void mma4_ts(uint32_t d, uint32_t a, uint64_t b, uint
 __device__ __forceinline__ void mma_commit_elect(uint32_t mbar) {
   asm volatile(
       "{.reg .pred e; .reg .b32 x; elect.sync x|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];}" ::"r"(mbar)
+      "@!e bra SKIP%=;\n"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "SKIP%=:\n}" ::"r"(mbar)
       : "memory");
 }
 
@@ -493,13 +499,15 @@ __device__ __forceinline__ void mma4_f4(uint32_t d, uint32_t a, uint64_t b, uint
         "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
         "elect.sync x|e, 0xffffffff;\n"
         "setp.ne.b32 p, %3, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
+        "@!e bra SKIP%=;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
         "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
         "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
         "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+        "SKIP%=:\n"
         "}" ::"r"(d),
         "r"(a), "l"(b), "r"(accumulate), "n"(IDESC), "r"(sfa), "r"(sfb));
     return;
@@ -508,13 +516,15 @@ __device__ __forceinline__ void mma4_f4(uint32_t d, uint32_t a, uint64_t b, uint
       "{.reg .pred p, e; .reg .b32 x, a1; .reg .b64 b1;\n"
       "elect.sync x|e, 0xffffffff;\n"
       "setp.ne.b32 p, %3, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
+      "@!e bra SKIP%=;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %4, [%5], [%6], p;\n"
       "add.u32 a1, %1, 8; add.u64 b1, %2, 2;\n"
-      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
       "add.u32 a1, %1, 16; add.u64 b1, %2, 4;\n"
-      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
       "add.u32 a1, %1, 24; add.u64 b1, %2, 6;\n"
-      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [a1], b1, %4, [%5], [%6], 1;\n"
+      "SKIP%=:\n"
       "}" ::"r"(d),
       "r"(a), "l"(b), "r"(accumulate), "r"(idesc), "r"(sfa), "r"(sfb));
 }
