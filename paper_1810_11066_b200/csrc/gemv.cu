@@ -71,33 +71,52 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(const uint32_t* __re
   for (int r = 0; r < kMaxM; ++r) rs[r] = 0;
   if (FUSED) {
     const bool al16 = (reinterpret_cast<uintptr_t>(a_codes) % 16 == 0) && (k % 16 == 0);
-    for (int t = tid; t < m * kwp; t += kGemvThreads) {
-      const int r = t / kwp, j = t - r * kwp;
-      const int64_t e0 = 32 * int64_t(j);
-      const uint8_t* src = a_codes + r * k + e0;
-      uint32_t v[8];
-      if (al16 && e0 + 32 <= k) {
-        const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src)), hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-        v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w; v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
-      } else {
+    // two words per thread per pass, both words' codes loaded before either is packed (the
+    // loads are the latency of this phase)
+    for (int t0 = tid; t0 < m * kwp; t0 += 2 * kGemvThreads) {
+      uint32_t v[2][8];
+      int rr_[2], jj[2];
+      bool ok[2];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint32_t x = 0;
+      for (int u = 0; u < 2; ++u) {
+        const int t = t0 + u * kGemvThreads;
+        ok[u] = t < m * kwp;
+        const int r = ok[u] ? t / kwp : 0, j = ok[u] ? t - r * kwp : 0;
+        rr_[u] = r;
+        jj[u] = j;
+        const int64_t e0 = 32 * int64_t(j);
+        const uint8_t* src = a_codes + r * k + e0;
+        if (!ok[u]) {
 #pragma unroll
-          for (int rr = 0; rr < 4; ++rr)
-            if (e0 + 4 * q + rr < k) x |= uint32_t(__ldg(src + 4 * q + rr)) << (8 * rr);
-          v[q] = x;
+          for (int q = 0; q < 8; ++q) v[u][q] = 0;
+        } else if (al16 && e0 + 32 <= k) {
+          const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src)), hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+          v[u][0] = lo.x; v[u][1] = lo.y; v[u][2] = lo.z; v[u][3] = lo.w;
+          v[u][4] = hi.x; v[u][5] = hi.y; v[u][6] = hi.z; v[u][7] = hi.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr)
+              if (e0 + 4 * q + rr < k) x |= uint32_t(__ldg(src + 4 * q + rr)) << (8 * rr);
+            v[u][q] = x;
+          }
         }
       }
-      int s = 0;
 #pragma unroll
-      for (int b = 0; b < A; ++b) {
-        const uint32_t wd = plane_word(v, b);
-        s_act[(b * m + r) * kwp + j] = wd;
-        s += __popc(wd) << b;
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
+        int s = 0;
+#pragma unroll
+        for (int b = 0; b < A; ++b) {
+          const uint32_t wd = plane_word(v[u], b);
+          s_act[(b * m + rr_[u]) * kwp + jj[u]] = wd;
+          s += __popc(wd) << b;
+        }
+#pragma unroll
+        for (int rr = 0; rr < kMaxM; ++rr) rs[rr] += rr == rr_[u] ? s : 0;
       }
-#pragma unroll
-      for (int rr = 0; rr < kMaxM; ++rr) rs[rr] += rr == r ? s : 0;
     }
   } else {
     for (int t = tid; t < A * m * kwp; t += kGemvThreads) {
