@@ -61,6 +61,12 @@ def _load():
         lib.oracle_dense_enc.restype = I
         lib.oracle_conv2d_nhwc_enc.argtypes = [P, I, I, P, I, I, P] + [I] * 11
         lib.oracle_conv2d_nhwc_enc.restype = I
+        lib.oracle_e2m1_twice.argtypes = [I]
+        lib.oracle_e2m1_twice.restype = I
+        lib.oracle_digit_value.argtypes = [I, I, I, I]
+        lib.oracle_digit_value.restype = I
+        lib.oracle_digitpack.argtypes = [P, P, L, L, I, I]
+        lib.oracle_digitpack.restype = I
         _lib = lib
     return _lib
 
@@ -192,4 +198,33 @@ def bitpack(x, bits: int) -> np.ndarray:
     out = np.empty((bits, rows, packed_row_words(k)), dtype=np.uint32)
     if _load().oracle_bitpack(_ptr(x), _ptr(out), rows, k, bits) != 0:
         raise ValueError("oracle_bitpack rejected its arguments")
+    return out
+
+
+def e2m1_twice(nib: int) -> int:
+    """2 x the value of a 4-bit E2M1 field (sign bit 3, exponent bits 2..1, mantissa bit 0)."""
+    return int(_load().oracle_e2m1_twice(int(nib)))
+
+
+def digit_value(code: int, bits: int, enc: int, d: int) -> int:
+    """Radix-4 digit d of a code (planes 2d, 2d+1; R21/R24) in its encoding."""
+    return int(_load().oracle_digit_value(int(code), int(bits), int(enc), int(d)))
+
+
+def digit_row_bytes(k: int) -> int:
+    """Bytes per digit-packed row: 16 x packed_row_words(k) (4 bits per element)."""
+    return 16 * packed_row_words(k)
+
+
+def digitpack(x, bits: int, enc: int = UNSIGNED) -> np.ndarray:
+    """Digit packing (the C ABI's digit-packed layout, R24): uint8
+    [ceil(bits/2)][rows][digit_row_bytes(k)], element t of a row in nibble t % 2 of byte
+    t // 2, holding the E2M1 code of 0.5 x its digit value; zero past k."""
+    x = _u8(x)
+    if x.ndim != 2:
+        raise ValueError("digitpack: x [rows][K]")
+    rows, k = x.shape
+    out = np.empty(((bits + 1) // 2, rows, digit_row_bytes(k)), dtype=np.uint8)
+    if _load().oracle_digitpack(_ptr(x), _ptr(out), rows, k, bits, enc) != 0:
+        raise ValueError("oracle_digitpack rejected its arguments")
     return out

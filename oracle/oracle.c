@@ -19,6 +19,9 @@
  *                        (both-bipolar XNOR form; signed
  *                        two's-complement data)
  *   oracle_bitpack       the packed bit-plane layout of the C ABI (defines it)
+ *   oracle_digitpack     the digit-packed layout of the C ABI (defines it): bit planes
+ *                        (2d, 2d+1) of each element as one radix-4 digit (Eq. 2 regrouped,
+ *                        PAPER.md:512; R21/R24) stored as a 4-bit E2M1 field
  *
  * No bit-planes, no popcount, no blocking or reordering: straight loops over the
  * decoded integer values in the order of the definitions.  The only parallelism is
@@ -253,6 +256,53 @@ int oracle_bitpack(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, in
           if (ki < k && ((in[r * k + ki] >> b) & 1)) word |= (uint32_t)1 << t;
         }
         out[(b * rows + r) * kwp + j] = word;
+      }
+  return 0;
+}
+
+/* E2M1 (4-bit float: sign bit 3, exponent bits 2..1 with bias 1, mantissa bit 0) value of
+ * a 4-bit field, times 2 (an integer): e == 0 -> 0.5 * m (subnormal), else 2^(e-1) (1 + m/2). */
+int oracle_e2m1_twice(int nib) {
+  const int s = (nib >> 3) & 1, e = (nib >> 1) & 3, m = nib & 1;
+  const int twice = e == 0 ? m : (1 << (e - 1)) * (2 + m);
+  return s ? -twice : twice;
+}
+
+/* Digit value of digit d of a code (R21/R24): planes lo = 2d and hi = 2d+1 (hi
+ * only when 2d+1 < bits).  Unsigned: b_lo + 2 b_hi.  Bipolar: each plane a +/-1 digit
+ * (reading R2/R20): (2 b_lo - 1) + 2 (2 b_hi - 1).  Signed (PAPER.md:517,
+ * reading R19): the digit holding plane bits-1 weighs that plane -2^(bits-1), i.e.
+ * b_lo - 2 b_hi (or -b_lo when the top plane is the digit's lo plane); lower digits as
+ * unsigned.  sum_d 4^d value = oracle_code_value (pinned). */
+int oracle_digit_value(int code, int bits, int enc, int d) {
+  const int lo = (code >> (2 * d)) & 1;
+  const int has_hi = 2 * d + 1 < bits;
+  const int hi = has_hi ? (code >> (2 * d + 1)) & 1 : 0;
+  const int top = 2 * d + 2 >= bits;
+  if (enc == 1) return has_hi ? (2 * lo - 1) + 2 * (2 * hi - 1) : 2 * lo - 1;
+  if (enc == 2 && top) return has_hi ? lo - 2 * hi : -lo;
+  return lo + 2 * hi;
+}
+
+/* Digit packing: out [D][rows][16 * packed_row_words(k)] bytes, D = ceil(bits/2); element t
+ * of row r is the 4-bit field t % 2 (low nibble first) of byte t / 2; the field holds the
+ * E2M1 code whose value is 0.5 * digit value (found by decoding every code, so this follows
+ * the format definition directly); elements >= k are 0. */
+int oracle_digitpack(const uint8_t* in, uint8_t* out, int64_t rows, int64_t k, int bits, int enc) {
+  if (rows <= 0 || k <= 0 || bits < 1 || bits > 4 || !enc_ok(enc)) return -1;
+  if (!codes_in_range(in, rows * k, bits)) return -1;
+  const int64_t rb = 16 * oracle_packed_row_words(k);
+  const int D = (bits + 1) / 2;
+  memset(out, 0, (size_t)(D * rows * rb));
+  for (int d = 0; d < D; ++d)
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t t = 0; t < k; ++t) {
+        const int v = oracle_digit_value(in[r * k + t], bits, enc, d);
+        int nib = -1;
+        for (int x = 0; x < 16 && nib < 0; ++x)
+          if (oracle_e2m1_twice(x) == v && !(v == 0 && x != 0)) nib = x;  /* +0 for zero */
+        if (nib < 0) return -1;
+        out[(d * rows + r) * rb + t / 2] |= (uint8_t)(nib << (4 * (t % 2)));
       }
   return 0;
 }

@@ -414,3 +414,90 @@ def test_encoded_closed_forms():
     assert (oracle.dense_enc(np.full((1, k), 2, np.uint8), 2, 2, np.full((1, k), 1, np.uint8), 2, 2) == -2 * k).all()
     with pytest.raises(ValueError):
         oracle.dense_enc(a, 2, 3, w, 1, 0)
+
+
+# ------------------------------------------------------------- digit packing (R21/R24)
+def test_e2m1_decode_table():
+    """The 4-bit E2M1 format's magnitudes are {0, 0.5, 1, 1.5, 2, 3, 4, 6} (codes 0-7), the
+    sign bit negates (codes 8-15): the format definition the digit fields are written in."""
+    twice = [oracle.e2m1_twice(x) for x in range(16)]
+    assert twice[:8] == [0, 1, 2, 3, 4, 6, 8, 12]
+    assert twice[8:] == [-v for v in twice[:8]]
+
+
+def test_digitpack_golden():
+    with open(os.path.join(GOLD, "digit_examples.json")) as f:
+        gold = json.load(f)
+    for case in gold["cases"]:
+        x = np.array(case["codes"], dtype=np.uint8)
+        got = oracle.digitpack(x, case["bits"], case["enc"])
+        assert got.shape == (len(case["digits"]), x.shape[0], case["row_bytes"])
+        for d, want in enumerate(case["digits"]):
+            np.testing.assert_array_equal(got[d, 0, :len(want)], want, err_msg=case["note"])
+            assert not got[d, 0, len(want):].any(), case["note"]
+
+
+@pytest.mark.parametrize("bits", [1, 2, 3, 4])
+@pytest.mark.parametrize("enc", [0, 1, 2])
+def test_digitpack_digits_sum_to_code_value(bits, enc):
+    """Exhaustively over every code: sum_d 4^d * value(field_d) is the code's value in its
+    encoding (Eq. 2's plane weights 2^i regrouped as 4^d (2^0, 2^1) per digit) — read back
+    from the packed bytes with Python bit operations, independent of the C digit rules."""
+    codes = np.arange(1 << bits, dtype=np.uint8).reshape(1, -1)
+    got = oracle.digitpack(codes, bits, enc)
+    for t, code in enumerate(codes[0]):
+        total = 0
+        for d in range(got.shape[0]):
+            nib = (int(got[d, 0, t // 2]) >> (4 * (t % 2))) & 0xF
+            total += 4 ** d * oracle.e2m1_twice(nib)
+        if enc == 1:
+            want = sum((1 << j) * (2 * ((int(code) >> j) & 1) - 1) for j in range(bits))
+        elif enc == 2:
+            want = int(code) - (1 << bits) if code >= 1 << (bits - 1) else int(code)
+        else:
+            want = int(code)
+        assert total == want, (bits, enc, int(code))
+
+
+def test_digitpack_unsigned_fields_are_bit_planes():
+    """Unsigned digit fields hold exactly the two bit planes of the packed layout: field bit
+    0 = plane 2d, bit 1 = plane 2d+1 (the same element order as oracle.bitpack), bits 2-3
+    zero; the zero tail past k matches the packed rows' zero pad bits."""
+    g = np.random.default_rng(7)
+    for bits, rows, k in ((2, 5, 70), (4, 3, 33), (3, 4, 128), (1, 2, 5)):
+        x = g.integers(0, 1 << bits, size=(rows, k), dtype=np.uint8)
+        dig = oracle.digitpack(x, bits, 0)
+        planes = oracle.bitpack(x, bits)
+        kwp = planes.shape[2]
+        assert dig.shape[2] == 16 * kwp
+        for d in range(dig.shape[0]):
+            for r in range(rows):
+                for t in range(32 * kwp):
+                    nib = (int(dig[d, r, t // 2]) >> (4 * (t % 2))) & 0xF
+                    lo = (int(planes[2 * d, r, t // 32]) >> (t % 32)) & 1
+                    hi = (int(planes[2 * d + 1, r, t // 32]) >> (t % 32)) & 1 if 2 * d + 1 < bits else 0
+                    assert nib == lo | (hi << 1), (bits, d, r, t)
+
+
+def test_digitpack_dot_product_matches_dense_enc():
+    """Eq. 2 from the digit fields: sum_{d,e} 4^(d+e) sum_k v_a[k,d] v_w[k,e] equals the
+    oracle's plain dense product, for every encoding pair (a dropped digit, a wrong digit
+    weight or a wrong sign rule fails here)."""
+    g = np.random.default_rng(11)
+    for a_bits, w_bits in ((2, 1), (3, 2), (4, 4), (1, 3)):
+        for a_enc in (0, 1, 2):
+            for w_enc in (0, 1, 2):
+                a = g.integers(0, 1 << a_bits, size=(3, 45), dtype=np.uint8)
+                w = g.integers(0, 1 << w_bits, size=(4, 45), dtype=np.uint8)
+                da, dw = oracle.digitpack(a, a_bits, a_enc), oracle.digitpack(w, w_bits, w_enc)
+
+                def vals(p):  # [D][rows][elements] digit values decoded from the fields
+                    lo = np.vectorize(oracle.e2m1_twice)(p & 0xF)
+                    hi = np.vectorize(oracle.e2m1_twice)(p >> 4)
+                    return np.stack([lo, hi], axis=-1).reshape(p.shape[0], p.shape[1], -1).astype(np.int64)
+                va, vw = vals(da), vals(dw)
+                out = np.zeros((3, 4), dtype=np.int64)
+                for d in range(va.shape[0]):
+                    for e in range(vw.shape[0]):
+                        out += 4 ** (d + e) * (va[d] @ vw[e].T)
+                np.testing.assert_array_equal(out, oracle.dense_enc(a, a_bits, a_enc, w, w_bits, w_enc))
