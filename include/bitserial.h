@@ -420,6 +420,75 @@ int bs_bitserial_conv2d_nhwc_tc_host(const uint8_t* act_host, int a_bits, int a_
                                      uint8_t* act_dev, int32_t* out_dev,
                                      void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Digit-packed operands and the TMA-fed tensor-core kernel (the product path of the
+ * timed step).  Eq. 2 is a sum over plane pairs; grouping planes
+ * (2d, 2d+1) into radix-4 digits (R21) and storing each element's digit as one
+ * 4-bit E2M1 field (value 0.5 * digit) makes the packed tensor a tensor-core operand that
+ * TMA moves into shared memory unchanged (R24) — no expansion inside the conv.
+ *
+ * Digit-packed layout ("digits"): uint8 [D][rows][bs_digit_row_bytes(k)], D = ceil(bits/2),
+ * row bytes = 16 * bs_packed_row_words(k) (the bit-plane row length, 4 bits per element
+ * per digit); byte b of a row holds elements 2b (low nibble) and 2b+1 (high nibble);
+ * elements >= k are 0.  Nibble of digit value v in {-3..3}: (v < 0 ? 8 : 0) | |v|.  Digit
+ * d holds planes lo = 2d and hi = 2d+1 (when 2d+1 < bits):
+ *     BS_A_UNSIGNED / BS_UNIPOLAR : v = b_lo + 2 b_hi
+ *     BS_A_BIPOLAR  / BS_BIPOLAR  : v = (2 b_lo - 1) + 2 (2 b_hi - 1)      (alone: 2 b_lo - 1)
+ *     BS_A_SIGNED   / BS_SIGNED   : the digit holding plane bits-1: b_lo - 2 b_hi (alone: -b_lo);
+ *                                   lower digits as unsigned
+ * so that sum_d 4^d v_d is the code's value.  Activations: bs_digitpack of the [rows][k]
+ * codes (conv: rows = n*h*w pixels, k = c).  Weights: bs_*_tcd_prepare_weights of the
+ * packed weight planes (untimed, like the weight packing).
+ * Supported: bits in [1,4] for both operands; the FP4 exactness bound
+ * K * max|a| * max|w| < 2^22 (BS_ERR_OVERFLOW); conv geometry that the TMA im2col mode
+ * encodes: pad <= 128, stride <= 8, (out-1)*stride - pad - (in-1) in [-128, 127]
+ * (BS_ERR_UNSUPPORTED otherwise).  All pointers device, 16-byte aligned.
+ */
+int64_t bs_digit_row_bytes(int64_t k);
+/* in [rows][k] uint8 codes -> out [ceil(bits/2)][rows][bs_digit_row_bytes(k)]; enc is a
+ * bs_a_encoding (or the same value of a bs_encoding for weight codes).  HBM-bound: 1 byte
+ * read + ceil(bits/2)/2 bytes written per element. */
+int bs_digitpack(const uint8_t* in, uint8_t* out, int64_t rows, int64_t k, int bits, int enc, void* stream);
+typedef struct bs_digit_pack_desc {
+  const uint8_t* in; /* [rows][k] codes */
+  uint8_t* out;      /* [ceil(bits/2)][rows][bs_digit_row_bytes(k)] */
+  int64_t rows, k;
+} bs_digit_pack_desc;
+/* Several tensors of one bit width and encoding in ONE launch (the bench step's packing). */
+int bs_digitpack_group(const bs_digit_pack_desc* descs, int count, int bits, int enc, void* stream);
+
+/* Weight digits from PACKED weight planes (bs_bitpack of OHWI codes, or of [n][k] for dense):
+ * [ceil(w_bits/2)][oc][kh*kw*bs_digit_row_bytes(c)] (dense: [..][n][bs_digit_row_bytes(k)])
+ * bytes; channel padding inside each tap is 0. */
+int64_t bs_conv2d_tcd_weight_bytes(int oc, int kh, int kw, int c, int w_bits);
+int64_t bs_dense_tcd_weight_bytes(int64_t n, int64_t k, int w_bits);
+int bs_conv2d_tcd_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                                  uint8_t* w_dig, int64_t w_dig_bytes, void* stream);
+int bs_dense_tcd_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t k,
+                                 uint8_t* w_dig, int64_t w_dig_bytes, void* stream);
+
+/* Conv2d NHWC / dense on digit-packed activations and prepared weight digits: one
+ * persistent warp-specialized launch; TMA im2col (conv) or tiled (dense) loads of the
+ * activation digits, TMA loads of the weight digits, tcgen05.mma kind::mxf4 with the digit
+ * weights 4^d as UE8M0 block scales, FP32 accumulation in TMEM (exact below 2^22), F2I,
+ * TMA-store epilogue.  a_enc / w_enc are the encodings the operands were packed with (they
+ * set the exactness bound).  out: int32 [n][oh][ow][oc] / [m][n]. */
+int bs_bitserial_conv2d_nhwc_tcd(const uint8_t* act_dig, int a_bits, int a_enc, const uint8_t* w_dig, int w_bits,
+                                 int w_enc, int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                 int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
+int bs_bitserial_dense_tcd(const uint8_t* a_dig, int a_bits, int a_enc, const uint8_t* w_dig, int w_bits, int w_enc,
+                           int32_t* out, int64_t m, int64_t n, int64_t k, void* stream);
+typedef struct bs_tcd_conv_desc {
+  const uint8_t* act_dig; /* [ceil(a_bits/2)][n*h*w][bs_digit_row_bytes(c)] */
+  const uint8_t* w_dig;   /* bs_conv2d_tcd_prepare_weights */
+  int32_t* out;           /* [n][oh][ow][oc] */
+  int a_enc, w_enc;
+  int n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w;
+} bs_tcd_conv_desc;
+/* Several convolutions of one (a_bits, w_bits) in one launch per 16 (tiles concatenated). */
+int bs_bitserial_conv2d_nhwc_tcd_group(const bs_tcd_conv_desc* descs, int count, int a_bits, int w_bits,
+                                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

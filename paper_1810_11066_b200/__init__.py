@@ -30,6 +30,9 @@ __all__ = [
     "bitserial_dense_tc_gather", "TcHostDesc", "bitserial_conv2d_nhwc_tc_host_group", "set_tuning", "get_tuning",
     "TUNE_TC_TILE_N", "TUNE_TC_EPILOGUE", "TUNE_TC_GROUP_SPLIT", "TUNE_TC_B_SLOTS", "TUNE_SMALL_KSPLIT", "ConvI8Desc",
     "bitserial_conv2d_nhwc_i8_group", "bitserial_dense_tc_multicast",
+    "digit_row_bytes", "digitpack", "DigitPackDesc", "digitpack_group", "conv2d_tcd_weight_bytes",
+    "dense_tcd_weight_bytes", "conv2d_tcd_prepare_weights", "dense_tcd_prepare_weights", "bitserial_conv2d_nhwc_tcd",
+    "bitserial_dense_tcd", "TcdConvDesc", "bitserial_conv2d_nhwc_tcd_group",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
@@ -62,7 +65,10 @@ EXPORTED_SYMBOLS = (
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
     "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitserial_dense_tc_prepared_gather",
     "bs_bitserial_conv2d_nhwc_tc_host_group", "bs_set_tuning", "bs_get_tuning", "bs_bitserial_conv2d_nhwc_i8_group",
-    "bs_bitserial_dense_tc_prepared_multicast",
+    "bs_bitserial_dense_tc_prepared_multicast", "bs_digit_row_bytes", "bs_digitpack", "bs_digitpack_group",
+    "bs_conv2d_tcd_weight_bytes", "bs_dense_tcd_weight_bytes", "bs_conv2d_tcd_prepare_weights",
+    "bs_dense_tcd_prepare_weights", "bs_bitserial_conv2d_nhwc_tcd", "bs_bitserial_dense_tcd",
+    "bs_bitserial_conv2d_nhwc_tcd_group",
 )
 
 
@@ -121,6 +127,16 @@ def _load():
         "bs_bitserial_dense_tc_prepared_multicast": ([P, I, I, P, I, I, I, P, L, L, L, P], I),
         "bs_bitserial_conv2d_nhwc_i8_group": ([P, I, I, I, P], I),
         "bs_get_tuning": ([I], I),
+        "bs_digit_row_bytes": ([L], L),
+        "bs_digitpack": ([P, P, L, L, I, I, P], I),
+        "bs_digitpack_group": ([P, I, I, I, P], I),
+        "bs_conv2d_tcd_weight_bytes": ([I, I, I, I, I], L),
+        "bs_dense_tcd_weight_bytes": ([L, L, I], L),
+        "bs_conv2d_tcd_prepare_weights": ([P, I, I, I, I, I, I, P, L, P], I),
+        "bs_dense_tcd_prepare_weights": ([P, I, I, L, L, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tcd": ([P, I, I, P, I, I, P] + [I] * 11 + [P], I),
+        "bs_bitserial_dense_tcd": ([P, I, I, P, I, I, P, L, L, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tcd_group": ([P, I, I, I, P], I),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("BITSERIAL_LIB") and not hasattr(lib, name):
@@ -583,3 +599,127 @@ def bitserial_conv2d_nhwc_host(act_host, a_bits, w_packed, w_bits, w_enc, oc, kh
         _dev(act_dev, "act_dev", torch.uint8), _dev(out_dev, "out_dev", torch.int32),
         _dev(workspace, "workspace", torch.uint8), workspace.numel(), _stream(stream)))
     return out_host
+
+
+# ---------------------------------------------------------------- digit-packed path
+def digit_row_bytes(k: int) -> int:
+    """bs_digit_row_bytes: bytes per digit-packed row (16 * packed_row_words(k))."""
+    return int(_load().bs_digit_row_bytes(int(k)))
+
+
+def digitpack(x: torch.Tensor, bits: int, enc: int = A_UNSIGNED, out: torch.Tensor | None = None,
+              stream=None) -> torch.Tensor:
+    """bs_digitpack: uint8 codes [rows][k] (reduction axis last) -> uint8 E2M1 digit fields
+    [ceil(bits/2)][rows][digit_row_bytes(k)] (two bit planes per 4-bit field, R24)."""
+    k = x.shape[-1]
+    rows = x.numel() // k
+    if out is None:
+        out = torch.empty(((bits + 1) // 2, rows, digit_row_bytes(k)), dtype=torch.uint8, device=x.device)
+    _check(_load().bs_digitpack(_dev(x, "x", torch.uint8), _dev(out, "out", torch.uint8), rows, k, bits, int(enc),
+                                _stream(stream)))
+    return out
+
+
+class DigitPackDesc(ctypes.Structure):
+    """bs_digit_pack_desc (include/bitserial.h): one member of a grouped digit pack."""
+    _fields_ = [("in_", ctypes.c_void_p), ("out", ctypes.c_void_p), ("rows", ctypes.c_int64), ("k", ctypes.c_int64)]
+
+
+def digitpack_group(xs, bits, enc=A_UNSIGNED, outs=None, stream=None):
+    """bs_digitpack_group: digit-pack every tensor of `xs` in one launch."""
+    descs = (DigitPackDesc * max(len(xs), 1))()
+    res = []
+    for i, x in enumerate(xs):
+        k = x.shape[-1]
+        rows = x.numel() // k
+        out = outs[i] if outs is not None else torch.empty(((bits + 1) // 2, rows, digit_row_bytes(k)),
+                                                            dtype=torch.uint8, device=x.device)
+        d = descs[i]
+        d.in_ = _dev(x, "x", torch.uint8).value
+        d.out = _dev(out, "out", torch.uint8).value
+        d.rows, d.k = rows, k
+        res.append(out)
+    _check(_load().bs_digitpack_group(ctypes.cast(descs, ctypes.c_void_p), len(xs), bits, int(enc), _stream(stream)))
+    return res
+
+
+def conv2d_tcd_weight_bytes(oc, kh, kw, c, w_bits) -> int:
+    return int(_load().bs_conv2d_tcd_weight_bytes(oc, kh, kw, c, w_bits))
+
+
+def dense_tcd_weight_bytes(n, k, w_bits) -> int:
+    return int(_load().bs_dense_tcd_weight_bytes(n, k, w_bits))
+
+
+def conv2d_tcd_prepare_weights(w_packed, w_bits, w_enc, oc, kh, kw, c, out=None, stream=None):
+    """bs_conv2d_tcd_prepare_weights: packed OHWI weight planes -> weight digits (offline)."""
+    if out is None:
+        out = torch.empty(max(16, conv2d_tcd_weight_bytes(oc, kh, kw, c, w_bits)), dtype=torch.uint8,
+                          device=w_packed.device)
+    _check(_load().bs_conv2d_tcd_prepare_weights(_dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc), oc, kh,
+                                                 kw, c, _dev(out, "w_dig", torch.uint8), out.numel(), _stream(stream)))
+    return out
+
+
+def dense_tcd_prepare_weights(w_packed, w_bits, w_enc, n, k, out=None, stream=None):
+    """bs_dense_tcd_prepare_weights: packed [n][k] weight planes -> weight digits (offline)."""
+    if out is None:
+        out = torch.empty(max(16, dense_tcd_weight_bytes(n, k, w_bits)), dtype=torch.uint8, device=w_packed.device)
+    _check(_load().bs_dense_tcd_prepare_weights(_dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc), n, k,
+                                                _dev(out, "w_dig", torch.uint8), out.numel(), _stream(stream)))
+    return out
+
+
+def bitserial_conv2d_nhwc_tcd(act_dig, a_bits, w_dig, w_bits, n, h, w, c, oc, kh, kw, stride=1, pad=0, out=None,
+                              a_enc=A_UNSIGNED, w_enc=UNIPOLAR, stream=None):
+    """bs_bitserial_conv2d_nhwc_tcd: digit-packed activations x weight digits -> int32 NHWC."""
+    sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
+    if out is None:
+        out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act_dig.device)
+    _check(_load().bs_bitserial_conv2d_nhwc_tcd(
+        _dev(act_dig, "act_dig", torch.uint8), a_bits, int(a_enc), _dev(w_dig, "w_dig", torch.uint8), w_bits,
+        int(w_enc), _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _stream(stream)))
+    return out
+
+
+def bitserial_dense_tcd(a_dig, a_bits, w_dig, w_bits, m, n, k, out=None, a_enc=A_UNSIGNED, w_enc=UNIPOLAR,
+                        stream=None):
+    """bs_bitserial_dense_tcd: digit-packed activations [D][m][..] x weight digits -> int32 [m][n]."""
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int32, device=a_dig.device)
+    _check(_load().bs_bitserial_dense_tcd(_dev(a_dig, "a_dig", torch.uint8), a_bits, int(a_enc),
+                                          _dev(w_dig, "w_dig", torch.uint8), w_bits, int(w_enc),
+                                          _dev(out, "out", torch.int32), m, n, k, _stream(stream)))
+    return out
+
+
+class TcdConvDesc(ctypes.Structure):
+    """bs_tcd_conv_desc (include/bitserial.h): one member of a grouped digit-path launch."""
+    _fields_ = [("act_dig", ctypes.c_void_p), ("w_dig", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("a_enc", ctypes.c_int), ("w_enc", ctypes.c_int)] + \
+        [(f, ctypes.c_int) for f in ("n", "h", "w", "c", "oc", "kh", "kw", "stride_h", "stride_w", "pad_h", "pad_w")]
+
+
+def bitserial_conv2d_nhwc_tcd_group(convs, a_bits, w_bits, stream=None):
+    """bs_bitserial_conv2d_nhwc_tcd_group: several digit-path convolutions of one precision in
+    one launch.  `convs`: dicts with act_dig, w_dig, n, h, w, c, oc, kh, kw and optional
+    stride, pad, out, a_enc, w_enc.  Returns the outputs in order."""
+    descs = (TcdConvDesc * max(len(convs), 1))()
+    outs = []
+    for i, cv in enumerate(convs):
+        n, h, w, c, oc, kh, kw = (cv[k] for k in ("n", "h", "w", "c", "oc", "kh", "kw"))
+        sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, cv.get("stride", 1), cv.get("pad", 0))
+        out = cv.get("out")
+        if out is None:
+            out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=cv["act_dig"].device)
+        d = descs[i]
+        d.act_dig = _dev(cv["act_dig"], "act_dig", torch.uint8).value
+        d.w_dig = _dev(cv["w_dig"], "w_dig", torch.uint8).value
+        d.out = _dev(out, "out", torch.int32).value
+        d.a_enc, d.w_enc = int(cv.get("a_enc", A_UNSIGNED)), int(cv.get("w_enc", UNIPOLAR))
+        d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw = n, h, w, c, oc, kh, kw
+        d.stride_h, d.stride_w, d.pad_h, d.pad_w = sh, sw, ph, pw
+        outs.append(out)
+    _check(_load().bs_bitserial_conv2d_nhwc_tcd_group(ctypes.cast(descs, ctypes.c_void_p), len(convs), a_bits, w_bits,
+                                                      _stream(stream)))
+    return outs

@@ -247,6 +247,34 @@ HostPipe& host_pipe() {
   return p;
 }
 
+
+// ---- digit path (digit.cu, tcd_conv.cu)
+// TMA im2col limits: padding corners in [-128, 127], traversal stride <= 8.
+int check_tcd_conv(const ConvArgs& g, int a_bits, int w_bits, int a_enc, int w_enc, const char* fn) {
+  if (int st = check_tc_enc(a_enc, w_enc, BS_TC_F4, fn)) return st;
+  if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+  if (int st = check_tc_bound(int64_t(g.kh) * g.kw * g.c, a_bits, w_bits, BS_TC_F4, fn, a_enc, w_enc)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  const int oh = conv_out(g.h, g.kh, g.sh, g.ph), ow = conv_out(g.w, g.kw, g.sw, g.pw);
+  const int up_w = (ow - 1) * g.sw - g.pw - (g.w - 1), up_h = (oh - 1) * g.sh - g.ph - (g.h - 1);
+  if (g.ph > 128 || g.pw > 128 || up_w < -128 || up_w > 127 || up_h < -128 || up_h > 127 || g.sh > 8 || g.sw > 8)
+    return fail(BS_ERR_UNSUPPORTED, "%s: TMA im2col needs padding <= 128, stride <= 8 and kernel extent <= pad + 129",
+                fn);
+  return BS_OK;
+}
+
+bs::TcdProblem make_tcd(const uint8_t* act, const uint8_t* wdig, int32_t* out, int a_bits, int w_bits,
+                        const ConvArgs& g) {
+  bs::TcdProblem p{};
+  p.act = act; p.wdig = wdig; p.out = out;
+  p.n = g.n; p.h = g.h; p.w = g.w; p.c = g.c; p.oc = g.oc; p.kh = g.kh; p.kw = g.kw;
+  p.sh = g.sh; p.sw = g.sw; p.ph = g.ph; p.pw = g.pw;
+  p.oh = conv_out(g.h, g.kh, g.sh, g.ph); p.ow = conv_out(g.w, g.kw, g.sw, g.pw);
+  p.a_digits = (a_bits + 1) / 2; p.w_digits = (w_bits + 1) / 2;
+  p.dense = 0;
+  return p;
+}
+
 }  // namespace
 
 extern "C" {
@@ -798,6 +826,132 @@ int bs_bitserial_conv2d_nhwc_host(const uint8_t* act_host, int a_bits, const uin
     return st;
   if (int st = cuda_status(cudaMemcpyAsync(out_host, out_dev, out_bytes, cudaMemcpyDeviceToHost, s), fn)) return st;
   return cuda_status(cudaStreamSynchronize(s), fn);
+}
+
+// ------------------------------------------------------------------ digit path
+int64_t bs_digit_row_bytes(int64_t k) { return bs::digit_row_bytes(k); }
+
+int bs_digitpack_group(const bs_digit_pack_desc* descs, int count, int bits, int enc, void* stream) {
+  const char* fn = "bs_digitpack_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  if (bits < 1 || bits > 4) return fail(BS_ERR_INVALID_ARG, "%s: bits=%d not in [1,4]", fn, bits);
+  if (enc < BS_A_UNSIGNED || enc > BS_A_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad encoding %d", fn, enc);
+  std::vector<bs::DigitSeg> segs(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_digit_pack_desc& d = descs[q];
+    if (!d.in || !d.out) return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    if (d.rows <= 0 || d.k <= 0) return fail(BS_ERR_SHAPE, "%s: descriptor %d: rows and k must be >= 1", fn, q);
+    if (!aligned16(d.out)) return fail(BS_ERR_ALIGN, "%s: descriptor %d: out must be 16-byte aligned", fn, q);
+    bs::DigitSeg g{};
+    g.in = d.in;
+    g.out = d.out;
+    g.rows = d.rows;
+    g.k = d.k;
+    segs[q] = g;
+  }
+  return cuda_status(bs::launch_digitpack_group(segs.data(), count, bits, enc, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_digitpack(const uint8_t* in, uint8_t* out, int64_t rows, int64_t k, int bits, int enc, void* stream) {
+  const bs_digit_pack_desc d{in, out, rows, k};
+  const int st = bs_digitpack_group(&d, 1, bits, enc, stream);
+  if (st != BS_OK) {  // name the single-tensor entry in the message
+    char tmp[512];
+    snprintf(tmp, sizeof(tmp), "%s", g_last_error);
+    const char* rest = strncmp(tmp, "bs_digitpack_group", 18) == 0 ? tmp + 18 : tmp;
+    fail(st, "bs_digitpack%s", rest);
+  }
+  return st;
+}
+
+int64_t bs_conv2d_tcd_weight_bytes(int oc, int kh, int kw, int c, int w_bits) {
+  if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0 || w_bits < 1 || w_bits > 4) return 0;
+  return bs::tcd_weight_bytes(oc, int64_t(kh) * kw * row_words(c), w_bits);
+}
+
+int64_t bs_dense_tcd_weight_bytes(int64_t n, int64_t k, int w_bits) {
+  if (n <= 0 || k <= 0 || w_bits < 1 || w_bits > 4) return 0;
+  return bs::tcd_weight_bytes(n, row_words(k), w_bits);
+}
+
+int bs_conv2d_tcd_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                                  uint8_t* w_dig, int64_t w_dig_bytes, void* stream) {
+  const char* fn = "bs_conv2d_tcd_prepare_weights";
+  if (!w_packed || !w_dig) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (w_bits < 1 || w_bits > 4) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits=%d not in [1,4]", fn, w_bits);
+  if (w_enc < BS_UNIPOLAR || w_enc > BS_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad w_enc %d", fn, w_enc);
+  if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0) return fail(BS_ERR_SHAPE, "%s: non-positive extent", fn);
+  const int64_t need = bs_conv2d_tcd_weight_bytes(oc, kh, kw, c, w_bits);
+  if (w_dig_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_dig needs %lld bytes", fn, (long long)need);
+  if (!aligned16(w_packed) || !aligned16(w_dig)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return cuda_status(bs::launch_weight_digits(w_packed, w_bits, w_enc, oc, int64_t(kh) * kw * row_words(c), c,
+                                              int(row_words(c)), w_dig, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_dense_tcd_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t k, uint8_t* w_dig,
+                                 int64_t w_dig_bytes, void* stream) {
+  const char* fn = "bs_dense_tcd_prepare_weights";
+  if (!w_packed || !w_dig) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (w_bits < 1 || w_bits > 4) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits=%d not in [1,4]", fn, w_bits);
+  if (w_enc < BS_UNIPOLAR || w_enc > BS_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad w_enc %d", fn, w_enc);
+  if (n <= 0 || k <= 0 || n > (int64_t(1) << 31) - 1 || k > (int64_t(1) << 31) - 1)
+    return fail(BS_ERR_SHAPE, "%s: bad n or k", fn);
+  const int64_t need = bs_dense_tcd_weight_bytes(n, k, w_bits);
+  if (w_dig_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_dig needs %lld bytes", fn, (long long)need);
+  if (!aligned16(w_packed) || !aligned16(w_dig)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return cuda_status(bs::launch_weight_digits(w_packed, w_bits, w_enc, n, row_words(k), int(k), int(row_words(k)),
+                                              w_dig, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tcd_group(const bs_tcd_conv_desc* descs, int count, int a_bits, int w_bits,
+                                       void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tcd_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  std::vector<bs::TcdProblem> ps(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_tcd_conv_desc& d = descs[q];
+    const ConvArgs g{d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw, d.stride_h, d.stride_w, d.pad_h, d.pad_w};
+    if (int st = check_tcd_conv(g, a_bits, w_bits, d.a_enc, d.w_enc, fn)) return st;
+    if (!d.act_dig || !d.w_dig || !d.out) return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    if (!aligned16(d.act_dig) || !aligned16(d.w_dig) || !aligned16(d.out))
+      return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
+    ps[q] = make_tcd(d.act_dig, d.w_dig, d.out, a_bits, w_bits, g);
+  }
+  return cuda_status(bs::launch_tcd_group(ps.data(), count, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tcd(const uint8_t* act_dig, int a_bits, int a_enc, const uint8_t* w_dig, int w_bits,
+                                 int w_enc, int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                 int stride_h, int stride_w, int pad_h, int pad_w, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tcd";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_tcd_conv(g, a_bits, w_bits, a_enc, w_enc, fn)) return st;
+  if (!act_dig || !w_dig || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (!aligned16(act_dig) || !aligned16(w_dig) || !aligned16(out))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  const bs::TcdProblem p = make_tcd(act_dig, w_dig, out, a_bits, w_bits, g);
+  return cuda_status(bs::launch_tcd_group(&p, 1, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_dense_tcd(const uint8_t* a_dig, int a_bits, int a_enc, const uint8_t* w_dig, int w_bits, int w_enc,
+                           int32_t* out, int64_t m, int64_t n, int64_t k, void* stream) {
+  const char* fn = "bs_bitserial_dense_tcd";
+  if (int st = check_tc_enc(a_enc, w_enc, BS_TC_F4, fn)) return st;
+  if (int st = check_dense(a_dig, reinterpret_cast<const uint32_t*>(w_dig), out, a_bits, w_bits, BS_UNIPOLAR, m, n,
+                           k, fn))
+    return st;
+  if (int st = check_tc_bound(k, a_bits, w_bits, BS_TC_F4, fn, a_enc, w_enc)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  if (m > kMaxRows || n > (int64_t(1) << 31) - 1 || k > (int64_t(1) << 31) - 1)
+    return fail(BS_ERR_SHAPE, "%s: m, n or k too large", fn);
+  const ConvArgs g{int(m), 1, 1, int(k), int(n), 1, 1, 1, 1, 0, 0};
+  bs::TcdProblem p = make_tcd(a_dig, w_dig, out, a_bits, w_bits, g);
+  p.dense = 1;
+  return cuda_status(bs::launch_tcd_group(&p, 1, static_cast<cudaStream_t>(stream)), fn);
 }
 
 }  // extern "C"

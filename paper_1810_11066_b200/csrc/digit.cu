@@ -1,0 +1,256 @@
+// digit.cu — digit packing: the bit-packing step emitting the
+// operand format of the TMA-fed tensor-core kernel (tcd_conv.cu).
+//
+// PAPER.md:519-523 (Sec. 2.2) splits the codes into bit planes and packs them along the
+// reduction axis; PAPER.md:555-567 (Sec. 3.1) adds a bit axis to the packed tensor.  Eq. 2
+// is a sum over plane pairs, so planes (2d, 2d+1) may be grouped into one
+// radix-4 digit d of weight 4^d (reading R21).  The digit-packed tensor keeps
+// the bit-plane layout with its bit axis split into (digit, bit-in-digit) and the
+// bit-in-digit axis innermost: element t of a row stores its two plane bits of digit d in
+// one 4-bit field, as the E2M1 value 0.5 * digit (reading R24):
+//
+//   out [D][rows][row_bytes]  uint8, D = ceil(bits / 2), row_bytes = 16 * bs_packed_row_words(k)
+//   byte b of a row holds elements 2b (low nibble) and 2b+1 (high nibble); elements >= k are 0
+//   nibble of a digit value v in {-3..3}: (v < 0 ? 8 : 0) | |v|   (E2M1: 0.5 * |v|, sign bit 3)
+//
+// digit value of digit d (planes lo = 2d, hi = 2d+1 when 2d+1 < bits):
+//   unsigned  b_lo + 2 b_hi                       (the code's radix-4 digit)
+//   bipolar   (2 b_lo - 1) + 2 (2 b_hi - 1)       (each plane a +/-1 digit, reading R2/R20)
+//   signed    the digit holding plane bits-1: b_lo - 2 b_hi (or -b_lo alone), others unsigned
+//             (two's complement, reading R19)
+// so sum_d 4^d * value_d is the code's value in its encoding (pinned by tests).
+//
+// The packer is HBM-bound: 1 byte read + D/2 bytes written per element.
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bs {
+
+// byte c of the result = nibble of the digit whose plane bits are c (bit 0 lo, bit 1 hi)
+uint32_t digit_lut(int bits, int enc, int d) {
+  const bool has_hi = 2 * d + 1 < bits, top = 2 * d + 2 >= bits;
+  uint32_t lut = 0;
+  for (int c = 0; c < (has_hi ? 4 : 2); ++c) {
+    const int lo = c & 1, hi = (c >> 1) & 1;
+    int v;
+    if (enc == 1)
+      v = has_hi ? (2 * lo - 1) + 2 * (2 * hi - 1) : 2 * lo - 1;
+    else if (enc == 2 && top)
+      v = has_hi ? lo - 2 * hi : -lo;
+    else
+      v = lo + 2 * hi;
+    const uint32_t nib = uint32_t((v < 0 ? 8 : 0) | (v < 0 ? -v : v));
+    lut |= nib << (8 * c);
+  }
+  return lut;
+}
+
+namespace {
+
+// 4 bytes holding values < 16 -> one 16-bit field of 4 nibbles (byte r -> nibble r)
+__device__ __forceinline__ uint32_t nib4(uint32_t x) {
+  const uint32_t y = x | (x >> 4);
+  return (y & 0xFFu) | ((y >> 8) & 0xFF00u);
+}
+
+// 32 codes (element 4q+r in byte r of v[q]) -> the 16 digit bytes of digit D
+template <int D, int BITS>
+__device__ __forceinline__ uint4 digit_row16(const uint32_t (&v)[8], uint32_t lut, bool ident) {
+  constexpr bool kHi = 2 * D + 1 < BITS;
+  constexpr uint32_t kMask = kHi ? 0x03030303u : 0x01010101u;
+  uint32_t h[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t x = (v[q] >> (2 * D)) & kMask;  // byte r = plane bits of element 4q+r
+    const uint32_t sel = nib4(x);                 // byte selectors
+    h[q] = nib4(ident ? x : __byte_perm(lut, 0u, sel));
+  }
+  return make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+}
+
+// nvalid < 32: elements past the row end are value 0 whatever the encoding (a bipolar code 0
+// would otherwise become -1.5)
+__device__ __forceinline__ uint4 keep_nibbles(uint4 x, int nvalid) {
+  uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int nv = nvalid - 8 * i;
+    w[i] = nv >= 8 ? w[i] : (nv <= 0 ? 0u : w[i] & ((1u << (4 * nv)) - 1u));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int D, int BITS>
+__device__ __forceinline__ void store_digits(uint8_t* dst, int64_t plane_stride, const uint32_t (&v)[8],
+                                             const uint32_t (&lut)[2], bool ident, int nvalid = 32) {
+  if constexpr (2 * D < BITS) {
+    uint4 o = digit_row16<D, BITS>(v, lut[D], ident);
+    if (nvalid < 32) o = keep_nibbles(o, nvalid);
+    *reinterpret_cast<uint4*>(dst + D * plane_stride) = o;
+    store_digits<D + 1, BITS>(dst, plane_stride, v, lut, ident, nvalid);
+  }
+}
+
+// the 32 codes of task (row r, word j); zeros past k
+__device__ __forceinline__ void load32(const uint8_t* __restrict__ in, int64_t r, int64_t j, int64_t k, bool aligned16,
+                                       uint32_t (&v)[8]) {
+  const int64_t e0 = 32 * j;
+  const uint8_t* src = in + r * k + e0;
+  if (aligned16 && e0 + 32 <= k) {
+    const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
+    const uint4 hi = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+    v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+    v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+  } else if (aligned16 && e0 + 16 == k) {
+    const uint4 lo = __ldg(reinterpret_cast<const uint4*>(src));
+    v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+    v[4] = v[5] = v[6] = v[7] = 0u;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int64_t e = e0 + 4 * q + rr;
+        if (e < k) x |= uint32_t(__ldg(src + 4 * q + rr)) << (8 * rr);
+      }
+      v[q] = x;
+    }
+  }
+}
+
+// Grouped digit packing: the (row, word) tasks of all segments form one sequence walked
+// with a grid stride (as bitpack_group_kernel); one task = 32 codes -> 16 bytes per digit.
+// FAST segments (k % 32 == 0, 16-byte rows, no pad words) keep 4 tasks' loads in flight.
+template <int BITS>
+__global__ void __launch_bounds__(256) digitpack_group_kernel(const __grid_constant__ DigitPackArgs a) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int s = 0;
+  int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  constexpr int kBatch = 4;
+  for (; t < a.tasks; t += stride) {
+    while (s + 1 < a.nseg && t >= a.seg[s + 1].task0) ++s;
+    const DigitSeg& g = a.seg[s];
+    const int64_t end = s + 1 < a.nseg ? a.seg[s + 1].task0 : a.tasks;
+    if (g.fast && t + (kBatch - 1) * stride < end) {  // kBatch tasks of this segment, loads first
+      uint4 lo[kBatch], hi[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int64_t lt = t + u * stride - g.task0;
+        const int64_t r = lt >> g.shift, j = lt - (r << g.shift);
+        const uint4* src = reinterpret_cast<const uint4*>(g.in + r * g.k + 32 * j);
+        lo[u] = __ldg(src);
+        hi[u] = __ldg(src + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int64_t lt = t + u * stride - g.task0;
+        const uint32_t v[8] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
+        store_digits<0, BITS>(g.out + lt * 16, g.plane_bytes, v, g.lut, g.ident);
+      }
+      t += (kBatch - 1) * stride;
+      continue;
+    }
+    const int64_t lt = t - g.task0;
+    const int64_t r = g.shift >= 0 ? (lt >> g.shift) : lt / g.kwp;
+    const int64_t j = lt - r * g.kwp;
+    uint32_t v[8];
+    load32(g.in, r, j, g.k, g.aligned16, v);
+    const int64_t left = g.k - 32 * j;
+    store_digits<0, BITS>(g.out + lt * 16, g.plane_bytes, v, g.lut, g.ident, left >= 32 ? 32 : int(left < 0 ? 0 : left));
+  }
+}
+
+}  // namespace
+
+int64_t digit_row_bytes(int64_t k) {
+  const int64_t w = (k + 31) / 32;
+  return k <= 0 ? 0 : 16 * (w + (w & 1));
+}
+
+cudaError_t launch_digitpack_group(const DigitSeg* segs, int count, int bits, int enc, cudaStream_t stream) {
+  for (int q0 = 0; q0 < count; q0 += kPackGroupMax) {
+    DigitPackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.nseg = count - q0 < kPackGroupMax ? count - q0 : kPackGroupMax;
+    int64_t tasks = 0;
+    for (int q = 0; q < a.nseg; ++q) {
+      DigitSeg g = segs[q0 + q];
+      g.kwp = digit_row_bytes(g.k) / 16;
+      g.task0 = tasks;
+      g.plane_bytes = g.rows * g.kwp * 16;
+      g.shift = -1;
+      for (int sh = 0; sh < 62; ++sh)
+        if ((int64_t(1) << sh) == g.kwp) g.shift = sh;
+      g.aligned16 = (reinterpret_cast<uintptr_t>(g.in) % 16 == 0) && (g.k % 16 == 0);
+      g.fast = g.aligned16 && g.k % 32 == 0 && g.kwp * 32 == g.k && g.shift >= 0;
+      g.lut[0] = digit_lut(bits, enc, 0);
+      g.lut[1] = digit_lut(bits, enc, 1);
+      g.ident = enc == 0;
+      tasks += g.rows * g.kwp;
+      a.seg[q] = g;
+    }
+    a.tasks = tasks;
+    int64_t blocks = (tasks + 255) / 256;
+    const int64_t max_blocks = int64_t(device_sms()) * 8 * 2;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) continue;
+    switch (bits) {
+      case 1: digitpack_group_kernel<1><<<blocks, 256, 0, stream>>>(a); break;
+      case 2: digitpack_group_kernel<2><<<blocks, 256, 0, stream>>>(a); break;
+      case 3: digitpack_group_kernel<3><<<blocks, 256, 0, stream>>>(a); break;
+      default: digitpack_group_kernel<4><<<blocks, 256, 0, stream>>>(a); break;
+    }
+    note_launch();
+    if (cudaError_t e = cudaPeekAtLastError()) return e;
+  }
+  return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ weight digits
+// Packed weight planes [W][n][kp] words (filter rows of `taps` taps of kw_tap words, c_tap
+// elements per tap) -> digit rows [P][n][16 kp] bytes, P = ceil(W/2), in the same element
+// order as the activation digits; positions past c_tap inside a tap (padding) are 0.
+namespace {
+__global__ void weight_digits_kernel(const uint32_t* __restrict__ wp, int w_bits, int64_t n, int64_t kp, int c_tap,
+                                     int kw_tap, uint32_t lut0, uint32_t lut1, uint8_t* __restrict__ out) {
+  const int P = (w_bits + 1) / 2;
+  const int64_t total = int64_t(P) * n * kp;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int e = int(t / (n * kp));
+    const int64_t rk = t - e * n * kp;  // row * kp + kk
+    const int64_t kk = rk % kp;
+    const bool has_hi = 2 * e + 1 < w_bits;
+    const uint32_t lo = wp[int64_t(2 * e) * n * kp + rk];
+    const uint32_t hi = has_hi ? wp[int64_t(2 * e + 1) * n * kp + rk] : 0u;
+    const int wt = int(kk % kw_tap), base = wt * 32;
+    const uint32_t lut = e == 0 ? lut0 : lut1;
+    uint32_t o[4] = {0u, 0u, 0u, 0u};
+    for (int b = 0; b < 32; ++b) {
+      if (base + b >= c_tap) break;  // tap padding: value 0
+      const uint32_t c = ((lo >> b) & 1u) | (((hi >> b) & 1u) << 1);
+      const uint32_t nib = (lut >> (8 * c)) & 0xFu;
+      o[b >> 3] |= nib << (4 * (b & 7));
+    }
+    *reinterpret_cast<uint4*>(out + t * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+}  // namespace
+
+int64_t tcd_weight_bytes(int64_t n, int64_t kp, int w_bits) { return int64_t((w_bits + 1) / 2) * n * kp * 16; }
+
+cudaError_t launch_weight_digits(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp, int c_tap,
+                                 int kw_tap, uint8_t* out, cudaStream_t stream) {
+  const int64_t total = int64_t((w_bits + 1) / 2) * n * kp;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  weight_digits_kernel<<<blocks, 256, 0, stream>>>(w_packed, w_bits, n, kp, c_tap, kw_tap, digit_lut(w_bits, w_enc, 0),
+                                                   digit_lut(w_bits, w_enc, 1), out);
+  note_launch();
+  return cudaPeekAtLastError();
+}
+
+}  // namespace bs

@@ -109,6 +109,42 @@ struct SmallConv {
 bool small_supported(int a_bits, int w_bits);
 cudaError_t launch_small_conv(const SmallConv* ps, int count, int a_bits, int w_bits, cudaStream_t stream);
 
+// ---- digit-packed operands and the TMA-fed tensor-core kernel (digit.cu, tcd_conv.cu)
+// Digit packing: [rows][k] codes -> [ceil(bits/2)][rows][digit_row_bytes(k)] E2M1 digit
+// nibbles (two bit planes per 4-bit field; R24).  One segment per tensor.
+struct DigitSeg {
+  const uint8_t* in;  // [rows][k] codes
+  uint8_t* out;       // [D][rows][digit_row_bytes(k)]
+  int64_t rows, k;    // set by the caller; the rest by the launcher
+  int64_t kwp, task0, plane_bytes;
+  int shift, aligned16, fast, ident;
+  uint32_t lut[2];
+};
+struct DigitPackArgs {
+  int nseg;
+  int64_t tasks;
+  DigitSeg seg[kPackGroupMax];
+};
+int64_t digit_row_bytes(int64_t k);  // 16 * packed row words
+uint32_t digit_lut(int bits, int enc, int d);
+cudaError_t launch_digitpack_group(const DigitSeg* segs, int count, int bits, int enc, cudaStream_t stream);
+// prepared weight digits [ceil(w_bits/2)][n][16 kp] bytes from packed planes [w_bits][n][kp]
+int64_t tcd_weight_bytes(int64_t n, int64_t kp, int w_bits);
+cudaError_t launch_weight_digits(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp, int c_tap,
+                                 int kw_tap, uint8_t* out, cudaStream_t stream);
+// One problem of the TMA-fed kernel: activation digits (conv: [DA][n][h][w][row_bytes(c)];
+// dense, kh = kw = h = w = 1 and c = k with `dense` set: [DA][n][row_bytes(k)]), weight digits
+// [DW][oc][kh*kw*row_bytes(c)], int32 output [n*oh*ow][oc].
+struct TcdProblem {
+  const uint8_t* act;
+  const uint8_t* wdig;
+  int32_t* out;
+  int n, h, w, c, oc, kh, kw, sh, sw, ph, pw, oh, ow;
+  int a_digits, w_digits;
+  int dense;  // 1: tiled 2-D operand map over [DA*n][row_bytes] (no im2col)
+};
+cudaError_t launch_tcd_group(const TcdProblem* ps, int count, cudaStream_t stream);
+
 // Matrix-vector kernel for m <= 8 dense products.
 //   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)
 //   a_codes  : uint8 [m][k] raw codes to pack in-kernel (fused; nullptr otherwise)
