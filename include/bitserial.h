@@ -116,7 +116,9 @@ int64_t bs_kernel_launches(void);
 /* Tuning knobs of the tensor-core path, process-wide (atomic; every later launch on any
  * thread sees the new value).  They never change results, only the launch configuration;
  * 0 is the library's choice.  For tests and experiments:
- *   BS_TUNE_TC_TILE_N      : output tile width 64 or 128 (default: 64 when oc <= 64, else 128)
+ *   BS_TUNE_TC_TILE_N      : output tile width 64 or 128 (default: 64 when oc <= 64, else 128);
+ *                            224: the digit path's single-problem launches (default for dense
+ *                            products with n >= 1024)
  *   BS_TUNE_TC_EPILOGUE    : 1 = direct 16-byte global stores instead of TMA stores
  *   BS_TUNE_TC_GROUP_SPLIT : 1 = grouped launches interleave long-K and short-K members' tiles
  *   BS_TUNE_TC_B_SLOTS     : cap on the weight chunk slots in shared memory (2..32): fewer slots
@@ -124,6 +126,10 @@ int64_t bs_kernel_launches(void);
  *                            resident
  *   BS_TUNE_SMALL_KSPLIT   : K slices (= cluster size) of the one-launch small-problem path
  *                            (bs_bitserial_conv2d_nhwc_i8_group): 1, 2, 4 or 8
+ *   BS_TUNE_TCD_A_SRC      : digit-path conv activations: 1 = TMA im2col loads, 2 = cp.async
+ *                            gathers by producer warps (the default)
+ *   BS_TUNE_TCD_B_STREAM   : 1 = digit-path weights always streamed per stage (default: a weight
+ *                            block of up to 96 KB stays resident per N block)
  * bs_set_tuning returns BS_ERR_INVALID_ARG for an unknown knob or value; bs_get_tuning returns
  * the current value (0 for an unknown knob). */
 typedef enum {
@@ -131,7 +137,9 @@ typedef enum {
   BS_TUNE_TC_EPILOGUE = 1,
   BS_TUNE_TC_GROUP_SPLIT = 2,
   BS_TUNE_TC_B_SLOTS = 3,
-  BS_TUNE_SMALL_KSPLIT = 4
+  BS_TUNE_SMALL_KSPLIT = 4,
+  BS_TUNE_TCD_A_SRC = 5,
+  BS_TUNE_TCD_B_STREAM = 6
 } bs_tune_knob;
 int bs_set_tuning(int knob, int value);
 int bs_get_tuning(int knob);
@@ -458,8 +466,9 @@ typedef struct bs_digit_pack_desc {
 int bs_digitpack_group(const bs_digit_pack_desc* descs, int count, int bits, int enc, void* stream);
 
 /* Weight digits from PACKED weight planes (bs_bitpack of OHWI codes, or of [n][k] for dense):
- * [ceil(w_bits/2)][oc][kh*kw*bs_digit_row_bytes(c)] (dense: [..][n][bs_digit_row_bytes(k)])
- * bytes; channel padding inside each tap is 0. */
+ * [ceil(w_bits/2)][oc][R] bytes, each row R = kh*kw*bs_digit_row_bytes(c) bytes of digits
+ * (dense: bs_digit_row_bytes(k)) zero-padded to the next multiple of 128 bytes; channel padding
+ * inside each tap is 0. */
 int64_t bs_conv2d_tcd_weight_bytes(int oc, int kh, int kw, int c, int w_bits);
 int64_t bs_dense_tcd_weight_bytes(int64_t n, int64_t k, int w_bits);
 int bs_conv2d_tcd_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,

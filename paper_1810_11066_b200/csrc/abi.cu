@@ -306,7 +306,8 @@ int bs_set_tuning(int knob, int value) {
   const char* fn = "bs_set_tuning";
   switch (knob) {
     case BS_TUNE_TC_TILE_N:
-      if (value != 0 && value != 64 && value != 128) return fail(BS_ERR_INVALID_ARG, "%s: tile width %d", fn, value);
+      if (value != 0 && value != 64 && value != 128 && value != 224)
+        return fail(BS_ERR_INVALID_ARG, "%s: tile width %d", fn, value);
       break;
     case BS_TUNE_TC_EPILOGUE:
     case BS_TUNE_TC_GROUP_SPLIT:
@@ -314,6 +315,12 @@ int bs_set_tuning(int knob, int value) {
       break;
     case BS_TUNE_TC_B_SLOTS:
       if (value != 0 && (value < 2 || value > 32)) return fail(BS_ERR_INVALID_ARG, "%s: B slots %d", fn, value);
+      break;
+    case BS_TUNE_TCD_A_SRC:
+      if (value < 0 || value > 2) return fail(BS_ERR_INVALID_ARG, "%s: value %d not in {0,1,2}", fn, value);
+      break;
+    case BS_TUNE_TCD_B_STREAM:
+      if (value != 0 && value != 1) return fail(BS_ERR_INVALID_ARG, "%s: value %d not 0 or 1", fn, value);
       break;
     case BS_TUNE_SMALL_KSPLIT:
       if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)

@@ -211,11 +211,14 @@ cudaError_t launch_digitpack_group(const DigitSeg* segs, int count, int bits, in
 
 // ------------------------------------------------------------------ weight digits
 // Packed weight planes [W][n][kp] words (filter rows of `taps` taps of kw_tap words, c_tap
-// elements per tap) -> digit rows [P][n][16 kp] bytes, P = ceil(W/2), in the same element
-// order as the activation digits; positions past c_tap inside a tap (padding) are 0.
+// elements per tap) -> digit rows [P][n][tcd_wrow_bytes(kp)] bytes, P = ceil(W/2), in the same
+// element order as the activation digits; positions past c_tap inside a tap (padding) and the
+// row tail up to the next 128-byte multiple are 0 (the kernel's weight boxes are 128 bytes
+// wide and never leave the tensor: TMA boxes reaching past a row end measured several times
+// slower).
 namespace {
 __global__ void weight_digits_kernel(const uint32_t* __restrict__ wp, int w_bits, int64_t n, int64_t kp, int c_tap,
-                                     int kw_tap, uint32_t lut0, uint32_t lut1, uint8_t* __restrict__ out) {
+                                     int kw_tap, uint32_t lut0, uint32_t lut1, int64_t wrow, uint8_t* __restrict__ out) {
   const int P = (w_bits + 1) / 2;
   const int64_t total = int64_t(P) * n * kp;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
@@ -234,21 +237,23 @@ __global__ void weight_digits_kernel(const uint32_t* __restrict__ wp, int w_bits
       const uint32_t nib = (lut >> (8 * c)) & 0xFu;
       o[b >> 3] |= nib << (4 * (b & 7));
     }
-    *reinterpret_cast<uint4*>(out + t * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(out + (int64_t(e) * n + rk / kp) * wrow + kk * 16) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 }  // namespace
 
-int64_t tcd_weight_bytes(int64_t n, int64_t kp, int w_bits) { return int64_t((w_bits + 1) / 2) * n * kp * 16; }
+int64_t tcd_wrow_bytes(int64_t kp) { return (kp * 16 + 127) / 128 * 128; }
+int64_t tcd_weight_bytes(int64_t n, int64_t kp, int w_bits) { return int64_t((w_bits + 1) / 2) * n * tcd_wrow_bytes(kp); }
 
 cudaError_t launch_weight_digits(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp, int c_tap,
                                  int kw_tap, uint8_t* out, cudaStream_t stream) {
   const int64_t total = int64_t((w_bits + 1) / 2) * n * kp;
   if (total == 0) return cudaSuccess;
+  if (cudaError_t e = cudaMemsetAsync(out, 0, size_t(tcd_weight_bytes(n, kp, w_bits)), stream)) return e;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   weight_digits_kernel<<<blocks, 256, 0, stream>>>(w_packed, w_bits, n, kp, c_tap, kw_tap, digit_lut(w_bits, w_enc, 0),
-                                                   digit_lut(w_bits, w_enc, 1), out);
+                                                   digit_lut(w_bits, w_enc, 1), tcd_wrow_bytes(kp), out);
   note_launch();
   return cudaPeekAtLastError();
 }

@@ -36,7 +36,10 @@ void note_launch();
 int64_t launch_count();
 
 // Process-wide tuning knobs (bs_set_tuning; atomics, read per launch; 0 = library choice).
-enum TuneKnob : int { kTuneTileN = 0, kTuneEpilogue = 1, kTuneGroupSplit = 2, kTuneBSlots = 3, kTuneSmallKs = 4, kTuneCount = 5 };
+enum TuneKnob : int {
+  kTuneTileN = 0, kTuneEpilogue = 1, kTuneGroupSplit = 2, kTuneBSlots = 3, kTuneSmallKs = 4, kTuneTcdASrc = 5,
+  kTuneTcdBStream = 6, kTuneCount = 7
+};
 int tuning(int knob);
 // SM count of the current device (cached per device).
 int device_sms();
@@ -128,7 +131,9 @@ struct DigitPackArgs {
 int64_t digit_row_bytes(int64_t k);  // 16 * packed row words
 uint32_t digit_lut(int bits, int enc, int d);
 cudaError_t launch_digitpack_group(const DigitSeg* segs, int count, int bits, int enc, cudaStream_t stream);
-// prepared weight digits [ceil(w_bits/2)][n][16 kp] bytes from packed planes [w_bits][n][kp]
+// prepared weight digits [ceil(w_bits/2)][n][tcd_wrow_bytes(kp)] bytes from packed planes
+// [w_bits][n][kp]: each row 16 kp bytes of digits, zero-padded to a multiple of 128 bytes
+int64_t tcd_wrow_bytes(int64_t kp);
 int64_t tcd_weight_bytes(int64_t n, int64_t kp, int w_bits);
 cudaError_t launch_weight_digits(const uint32_t* w_packed, int w_bits, int w_enc, int64_t n, int64_t kp, int c_tap,
                                  int kw_tap, uint8_t* out, cudaStream_t stream);

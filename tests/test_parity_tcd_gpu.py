@@ -54,9 +54,12 @@ def test_weight_digits_match_digitpack(w_bits, w_enc):
     for oc, kh, kw, c in ((5, 3, 3, 33), (64, 3, 3, 64), (7, 1, 1, 100), (3, 2, 3, 192)):
         g = inputs.gen(oc * 13 + c + w_bits)
         wt = inputs.codes((oc, kh, kw, c), w_bits, g)
-        got = wdig_conv(wt, w_bits, w_enc).cpu().numpy()
         ref = oracle.digitpack(wt.reshape(oc * kh * kw, c).numpy(), w_bits, w_enc)  # [P][oc*taps][rb]
-        np.testing.assert_array_equal(got[:ref.size].reshape(ref.shape), ref)
+        row = kh * kw * ref.shape[2]
+        rpad = (row + 127) // 128 * 128  # rows zero-padded to 128-byte multiples
+        got = wdig_conv(wt, w_bits, w_enc).cpu().numpy().reshape(ref.shape[0], oc, rpad)
+        np.testing.assert_array_equal(got[:, :, :row], ref.reshape(ref.shape[0], oc, row))
+        assert not got[:, :, row:].any()
 
 
 # ------------------------------------------------------------------ conv
@@ -183,7 +186,8 @@ def test_conv_tcd_rejects():
 
 # ------------------------------------------------------------------ dense
 DENSE_SHAPES = [(1, 1, 1), (1, 7, 33), (3, 5, 100), (129, 65, 250), (300, 200, 576), (64, 256, 4096),
-                (257, 130, 1000), (5, 1000, 129), (1000, 512, 96), (128, 128, 256)]
+                (257, 130, 1000), (5, 1000, 129), (1000, 512, 96), (128, 128, 256), (300, 1500, 1000),
+                (129, 1024, 520)]
 
 
 @pytest.mark.parametrize("m,n,k", DENSE_SHAPES)
@@ -257,3 +261,33 @@ def test_dense_tcd_gemm_sweep_sampled(size, a_bits, w_bits):
     rows = sorted(set([0, m - 1] + list(range(7, m, m // 64))))
     ref = oracle.dense_enc(a[rows].numpy(), a_bits, 0, w.numpy(), w_bits, bs.BIPOLAR)
     np.testing.assert_array_equal(got[rows].cpu().numpy(), ref)
+
+
+@pytest.fixture
+def tuning():
+    used = []
+
+    def set_(knob, value):
+        bs.set_tuning(knob, value)
+        used.append(knob)
+    yield set_
+    for k in used:
+        bs.set_tuning(k, 0)
+
+
+@pytest.mark.parametrize("a_src", [1, 2])
+@pytest.mark.parametrize("b_stream", [0, 1])
+@pytest.mark.parametrize("a_bits,w_bits", [(2, 1), (4, 2), (1, 3)])
+def test_conv_tcd_operand_sources(tuning, a_src, b_stream, a_bits, w_bits):
+    """Every conv case with the activations gathered by TMA im2col (1) or by the cp.async
+    producer warps (2), and the weights resident per N block or streamed per stage."""
+    tuning(bs.TUNE_TCD_A_SRC, a_src)
+    tuning(bs.TUNE_TCD_B_STREAM, b_stream)
+    for case in CONV_CASES:
+        n, h, w, c, oc, kh, kw, s, p = case
+        g = inputs.gen(n * 1000 + h * 37 + c * 7 + oc + 11 * a_bits + w_bits + 5 * a_src + b_stream)
+        act = inputs.codes((n, h, w, c), a_bits, g)
+        wt = inputs.codes((oc, kh, kw, c), w_bits, g)
+        ref = oracle.conv2d_nhwc_enc(act.numpy(), a_bits, 0, wt.numpy(), w_bits, 1, stride=(s, s), pad=(p, p))
+        got = run_conv(act, a_bits, 0, wt, w_bits, 1, s, p)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"{case} a_src={a_src} b_stream={b_stream}")
