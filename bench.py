@@ -481,10 +481,17 @@ class DenseWorkload:
         del w
         self.tc = args.path == "tc" and (hi - lo) > 8  # GEMV (m <= 8) stays on the HBM-bound matvec kernel
         self.fmt = tc_fmt(args)
+        # the digit path (digit-packed operands, TMA-fed tcgen05 kernel) unless the I8 format or
+        # the fused all-gather epilogue (a variant of the expansion kernel) is asked for
+        self.digit = self.tc and args.tc_format == "f4" and not args.fused_gather
         self.w_tc = (bs.dense_tc_prepare_weights(self.wp, args.w_bits, self.enc, n, k, tc_format=self.fmt)
-                     if self.tc else None)
+                     if self.tc and not self.digit else None)
+        self.w_dig = bs.dense_tcd_prepare_weights(self.wp, args.w_bits, self.enc, n, k) if self.digit else None
+        self.a_dig = (torch.empty(((args.a_bits + 1) // 2, hi - lo, bs.digit_row_bytes(k)), dtype=torch.uint8,
+                                  device=dev) if self.digit else None)
         self.out = torch.empty((hi - lo, n), dtype=torch.int32, device=dev)
-        self.full = torch.empty((m, n), dtype=torch.int32, device=dev) if gather else None
+        # one rank: its row block IS the whole C (no exchange step, no copy)
+        self.full = (torch.empty((m, n), dtype=torch.int32, device=dev) if world > 1 else self.out) if gather else None
         self.ws = torch.empty(max(16, bs.dense_workspace_bytes(hi - lo, k, args.a_bits)), dtype=torch.uint8, device=dev)
         kwp = bs.packed_row_words(k)
         self.packed = self.ws[:args.a_bits * (hi - lo) * kwp * 4].view(torch.int32).view(args.a_bits, hi - lo, kwp)
@@ -501,11 +508,13 @@ class DenseWorkload:
             "workload": f"{name}_m{m}_n{n}_k{k}_a{args.a_bits}w{args.w_bits}_{enc}", "m": m, "n": n, "k": k,
             "parallelism": (f"row-sharded tp{world} + all_gather_into_tensor(int32 C) over NCCL" if gather else
                             "single GPU (replicas only)"),
-            "step": ("bs_bitserial_dense_tc_i8 (activation pack + tensor-core dense)" if self.tc else
+            "step": ("bs_digitpack (activation digit packing) + bs_bitserial_dense_tcd (TMA-fed tensor-core dense)"
+                     if self.digit else
+                     "bs_bitserial_dense_tc_i8 (activation pack + tensor-core dense)" if self.tc else
                      "bs_bitserial_dense_i8 (activation pack + dense" + (", fused single launch" if (hi - lo) <= 8
                                                                          else "") + ")")
                     + (" + NCCL all-gather of C" if gather else ""),
-            "path": "tc" if self.tc else ("gemv" if (hi - lo) <= 8 else "popc"),
+            "path": ("tc-digit" if self.digit else "tc") if self.tc else ("gemv" if (hi - lo) <= 8 else "popc"),
         }
         if self.fused is not None:
             self.config["parallelism"] = (f"row-sharded tp{world}; all-gather fused into the tensor-core epilogue "
@@ -522,13 +531,18 @@ class DenseWorkload:
                                               w_enc=self.enc)
             self.fused.barrier()
             return
-        if self.tc:
+        if self.digit:
+            rows = self.rows[1] - self.rows[0]
+            self.bs.digitpack(self.a, self.a_bits, out=self.a_dig)
+            self.bs.bitserial_dense_tcd(self.a_dig, self.a_bits, self.w_dig, self.w_bits, rows, self.n, self.k,
+                                        out=self.out, w_enc=self.enc)
+        elif self.tc:
             self.bs.bitserial_dense_tc_i8(self.a, self.a_bits, self.w_tc, self.w_bits, self.n, out=self.out,
                                           workspace=self.ws, tc_format=self.fmt)
         else:
             self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
                                        workspace=self.ws)
-        if self.gather:
+        if self.gather and self.world > 1:
             bsdist.gather_rows(self.full, self.out)
 
     def roofline(self, reps):
@@ -540,13 +554,18 @@ class DenseWorkload:
             if gemv:
                 self.bs.bitserial_dense_i8(self.a, self.a_bits, self.wp, self.w_bits, self.enc, self.n, out=self.out,
                                            workspace=self.ws)
+            elif self.digit:
+                self.bs.bitserial_dense_tcd(self.a_dig, self.a_bits, self.w_dig, self.w_bits, rows, self.n, self.k,
+                                            out=self.out, w_enc=self.enc)
             elif self.tc:
                 self.bs.bitserial_dense_tc_prepared(self.packed, self.a_bits, self.w_tc, self.w_bits, rows, self.n,
                                                     self.k, out=self.out, tc_format=self.fmt)
             else:
                 self.bs.bitserial_dense(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, rows, self.n,
                                         self.k, out=self.out)
-        if not gemv:
+        if self.digit:
+            self.bs.digitpack(self.a, self.a_bits, out=self.a_dig)
+        elif not gemv:
             self.bs.bitpack(self.a, self.a_bits, out=self.packed)
         kernel()
         torch.cuda.synchronize()
@@ -575,6 +594,12 @@ class DenseWorkload:
             nbytes = self.wp.numel() * 4 + self.a.numel() + self.out.numel() * 4
             return {"kind": "hbm", "kernel": "gemv_kernel (fused pack + GEMV, one launch, cold L2)", "bytes": nbytes,
                     "ops": ops, "ms": ms, "breakdown": {"gemv_ms": ms}}
+        if self.digit:
+            return {"kind": "tensor", "ops": ops, "ms": ms, "launches": 1,
+                    "kernel": "tcd_conv_kernel (TMA-fed tcgen05 kind::mxf4 on digit-packed operands, 128x224 tiles; "
+                              "rank 0 shard)",
+                    "bytes": self.a_dig.numel() + self.w_dig.numel() + self.out.numel() * 4,
+                    "breakdown": {"dense_ms": ms, "allgather_ms": comm_ms}}
         return {"kind": "tensor" if self.tc else "alu",
                 "kernel": (f"tc_conv_kernel (tcgen05 kind::{'mxf4' if self.args.tc_format == 'f4' else 'i8'}; dense = "
                            "1x1 implicit GEMM, rank 0 shard)" if self.tc else
@@ -871,12 +896,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "binary TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "vs_baseline": None,
-            "dtype": (("u8 codes -> packed u32 bit-planes -> radix-4 e2m1 digits (two planes per nibble, 0.5 x {0..3}) x "
-                       "ue8m0 4^d scales on tcgen05 kind::mxf4 (fp32 accum, exact) -> i32" if args.tc_format == "f4" else
-                       "u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32")
-                      if args.path == "tc" else
-                      ("u8 codes -> u32 bit-planes packed in shared memory (AND/POPC) -> i32" if args.path == "small" else
-                       "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32")),
+            "dtype": dtype_of(args, wl),
             "scaling": "weak" if getattr(wl, "replicas", 1) > 1 else "strong",
             "data": "synthetic (seeded uniform codes, PAPER.md Table 1 / BASELINE shapes; no dataset)",
             "config": cfg, "roofline": roofline,
@@ -889,6 +909,20 @@ def run_ours(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def dtype_of(args, wl):
+    """The arithmetic the timed path computes in (not a precision claim)."""
+    if getattr(wl, "digit", False):
+        return ("u8 codes -> digit-packed e2m1 fields (two bit-planes per nibble, 0.5 x {0..3}) x ue8m0 4^d scales on "
+                "tcgen05 kind::mxf4 (fp32 accum, exact) -> i32")
+    if args.path == "tc":
+        return ("u8 codes -> packed u32 bit-planes -> radix-4 e2m1 digits (two planes per nibble, 0.5 x {0..3}) x "
+                "ue8m0 4^d scales on tcgen05 kind::mxf4 (fp32 accum, exact) -> i32" if args.tc_format == "f4" else
+                "u8 codes -> packed u32 bit-planes -> i8 0/1 planes on tcgen05 kind::i8 -> i32")
+    if args.path == "small":
+        return "u8 codes -> u32 bit-planes packed in shared memory (AND/POPC) -> i32"
+    return "u8 codes -> packed u32 bit-planes (AND/POPC) -> i32"
 
 
 def cpu_model():
