@@ -211,6 +211,7 @@ class ConvWorkload:
             self.side_stream = torch.cuda.Stream(device=dev)
             self.pack_events = [torch.cuda.Event() for _ in self.runs]
             self.pack_ctas = args.pack_ctas_per_sm * torch.cuda.get_device_properties(dev).multi_processor_count
+            self.split_ctas = max(1, args.split_pack_ctas_per_sm) * torch.cuda.get_device_properties(dev).multi_processor_count
             self.conv_streams = args.conv_streams
             self.extra_conv_streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
             self.packs_first = args.packs_first
@@ -238,6 +239,7 @@ class ConvWorkload:
             "tc_format": args.tc_format if args.path == "tc" else None,
             "conv_groups": (args.conv_groups if self.overlap else 0),
             "pack_group": bool(self.overlap and args.pack_group),
+            "pack_split": bool(self.overlap and args.pack_group and args.pack_split and self.groups),
         }
 
     def describe_step(self, args):
@@ -251,7 +253,9 @@ class ConvWorkload:
         if args.no_overlap:
             return ("per layer: bitpack(act) + tensor-core bitserial conv2d via bs_bitserial_conv2d_nhwc_tc_i8 "
                     "(weights packed + plane-expanded once, untimed)")
-        packs = ("every layer's activations packed by ONE bs_bitpack_group launch [side stream]" if args.pack_group
+        packs = ("the activations packed by one bs_bitpack_group launch per conv group, in group order [side stream]"
+                 if args.pack_group and args.pack_split and self.groups else
+                 "every layer's activations packed by ONE bs_bitpack_group launch [side stream]" if args.pack_group
                  else "per layer bs_bitpack [side stream]")
         convs = (f"the layers' tensor-core convs in {len(self.groups)} bs_bitserial_conv2d_nhwc_tc_group calls "
                  f"{[[self.layers[i] for i in g] for g in self.groups]} on alternating streams (each waits for its "
@@ -278,7 +282,18 @@ class ConvWorkload:
         side = self.side_stream
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            if self.args.pack_group:  # every layer's activations packed by one launch
+            if self.args.pack_group and self.args.pack_split and self.groups:
+                # one grouped pack per conv group, in group order: a group's convs start as soon as
+                # its own layers are packed while the later groups' packs run beside them
+                for gi, grp in enumerate(self.groups):
+                    # later groups' packs run beside the earlier groups' persistent convs: a capped
+                    # grid of 128-thread CTAs fits next to a conv CTA on each SM
+                    self.runs[0].bs.bitpack_group([self.runs[i].act for i in grp], self.args.a_bits,
+                                                  outs=[self.runs[i].packed for i in grp],
+                                                  max_ctas=0 if gi == 0 else self.split_ctas)
+                    for i in grp:
+                        self.pack_events[i].record(side)
+            elif self.args.pack_group:  # every layer's activations packed by one launch
                 self.runs[0].bs.bitpack_group([r.act for r in self.runs], self.args.a_bits,
                                               outs=[r.packed for r in self.runs])
                 for e in self.pack_events:
@@ -1034,6 +1049,11 @@ def main():
                     help="overlapped step: convs of consecutive (independent) layers on 1 or 2 streams")
     ap.add_argument("--no-pack-group", dest="pack_group", action="store_false",
                     help="tensor-core path: one bs_bitpack launch per layer instead of one bs_bitpack_group launch")
+    ap.add_argument("--pack-split", action="store_true",
+                    help="one pack launch per conv group (later ones capped to fit beside the running convs) instead "
+                         "of one for every layer (measured slower: profiles/r02e_step_sweep.jsonl)")
+    ap.add_argument("--split-pack-ctas-per-sm", type=int, default=1,
+                    help="split packs after the first: grid cap in 128-thread CTAs per SM")
     ap.add_argument("--group-layers", default="",
                     help="explicit conv groups as layer lists, e.g. '2|4,5,6,7,8,9,10,11,12' (overrides --conv-groups)")
     ap.add_argument("--conv-groups", type=int, default=2,

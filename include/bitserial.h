@@ -176,6 +176,10 @@ typedef struct bs_pack_desc {
   int64_t rows, k;
 } bs_pack_desc;
 int bs_bitpack_group(const bs_pack_desc* descs, int count, int bits, void* stream);
+/* As bs_bitpack_group with the grid capped at max_ctas 128-thread CTAs (0 = library choice): a
+ * capped pack fits beside a running persistent tensor-core conv (one CTA per SM), so later
+ * layers can be packed while an earlier layer's conv runs. */
+int bs_bitpack_group_ex(const bs_pack_desc* descs, int count, int bits, int max_ctas, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Bitserial dense / matrix multiply (Sec. 3.2 and 6.2.1).

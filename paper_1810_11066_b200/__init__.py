@@ -65,7 +65,7 @@ EXPORTED_SYMBOLS = (
     "bs_conv2d_tc_prepare_weights", "bs_dense_tc_prepare_weights", "bs_bitserial_conv2d_nhwc_tc_prepared",
     "bs_bitserial_dense_tc_prepared", "bs_bitserial_conv2d_nhwc_tc_i8", "bs_bitserial_dense_tc_i8",
     "bs_bitserial_conv2d_nhwc_tc_host", "bs_conv2d_tc_weight_bytes", "bs_dense_tc_weight_bytes",
-    "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitserial_dense_tc_prepared_gather",
+    "bs_bitserial_conv2d_nhwc_tc_group", "bs_bitpack_group", "bs_bitpack_group_ex", "bs_bitserial_dense_tc_prepared_gather",
     "bs_bitserial_conv2d_nhwc_tc_host_group", "bs_set_tuning", "bs_get_tuning", "bs_bitserial_conv2d_nhwc_i8_group",
     "bs_bitserial_dense_tc_prepared_multicast", "bs_digit_row_bytes", "bs_digitpack", "bs_digitpack_group",
     "bs_conv2d_tcd_weight_bytes", "bs_dense_tcd_weight_bytes", "bs_conv2d_tcd_prepare_weights",
@@ -123,6 +123,7 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tc_host": ([P, I, I, P, I, I, I, P] + [I] * 11 + [P, P, P, L, P], I),
         "bs_bitserial_conv2d_nhwc_tc_group": ([P, I, I, I, I, P], I),
         "bs_bitpack_group": ([P, I, I, P], I),
+        "bs_bitpack_group_ex": ([P, I, I, I, P], I),
         "bs_bitserial_conv2d_nhwc_tc_host_group": ([P, I, I, I, I, P], I),
         "bs_bitserial_dense_tc_prepared_gather": ([P, I, I, P, I, I, I, P, P, I, L, L, L, P], I),
         "bs_set_tuning": ([I, I], I),
@@ -223,7 +224,7 @@ class PackDesc(ctypes.Structure):
     _fields_ = [("in_", ctypes.c_void_p), ("out", ctypes.c_void_p), ("rows", ctypes.c_int64), ("k", ctypes.c_int64)]
 
 
-def bitpack_group(xs, bits, outs=None, stream=None):
+def bitpack_group(xs, bits, outs=None, stream=None, max_ctas=0):
     """bs_bitpack_group: bitpack every tensor of `xs` (uint8 codes, reduction axis last)
     at `bits` in one launch; returns the packed tensors (or fills `outs`)."""
     descs = (PackDesc * max(len(xs), 1))()
@@ -238,7 +239,8 @@ def bitpack_group(xs, bits, outs=None, stream=None):
         d.out = _dev(out, "out", torch.int32).value
         d.rows, d.k = rows, k
         res.append(out)
-    _check(_load().bs_bitpack_group(ctypes.cast(descs, ctypes.c_void_p), len(xs), bits, _stream(stream)))
+    _check(_load().bs_bitpack_group_ex(ctypes.cast(descs, ctypes.c_void_p), len(xs), bits, int(max_ctas),
+                                       _stream(stream)))
     return res
 
 

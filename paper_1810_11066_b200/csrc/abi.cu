@@ -351,7 +351,12 @@ int bs_bitpack_ex(const uint8_t* in, uint32_t* out, int64_t rows, int64_t k, int
 }
 
 int bs_bitpack_group(const bs_pack_desc* descs, int count, int bits, void* stream) {
+  return bs_bitpack_group_ex(descs, count, bits, 0, stream);
+}
+
+int bs_bitpack_group_ex(const bs_pack_desc* descs, int count, int bits, int max_ctas, void* stream) {
   const char* fn = "bs_bitpack_group";
+  if (max_ctas < 0) return fail(BS_ERR_INVALID_ARG, "%s: max_ctas < 0", fn);
   if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
   if (count == 0) return BS_OK;
   if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
@@ -365,7 +370,8 @@ int bs_bitpack_group(const bs_pack_desc* descs, int count, int bits, void* strea
       return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
     segs[q] = bs::PackSeg{d.in, d.out, d.rows, d.k, row_words(d.k), 0, -1, 0};
   }
-  return cuda_status(bs::launch_bitpack_group(segs.data(), count, bits, static_cast<cudaStream_t>(stream)), fn);
+  return cuda_status(bs::launch_bitpack_group(segs.data(), count, bits, static_cast<cudaStream_t>(stream), max_ctas),
+                     fn);
 }
 
 int bs_bitserial_dense_ex(const uint32_t* a_packed, int a_bits, const uint32_t* w_packed, int w_bits, int w_enc,

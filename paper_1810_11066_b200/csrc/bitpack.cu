@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) bitpack_group_kernel(const __grid_constan
   }
 }
 
-cudaError_t launch_bitpack_group(const PackSeg* segs, int count, int bits, cudaStream_t stream) {
+cudaError_t launch_bitpack_group(const PackSeg* segs, int count, int bits, cudaStream_t stream, int max_ctas) {
   for (int q0 = 0; q0 < count; q0 += kPackGroupMax) {
     PackGroupArgs a;
     memset(&a, 0, sizeof(a));
@@ -174,19 +174,24 @@ cudaError_t launch_bitpack_group(const PackSeg* segs, int count, int bits, cudaS
       a.seg[q] = g;
     }
     a.tasks = tasks;
-    int64_t blocks = (tasks + 255) / 256;
-    const int64_t max_blocks = int64_t(kNumSMs) * 8 * 4;
+    // 128-thread CTAs (4 K registers each): one fits beside a persistent tensor-core conv CTA
+    // (832 threads x 72 registers leave 5.6 K of the SM's 64 K), so packing the later layers
+    // can run on the SMs while an earlier layer's conv occupies them
+    constexpr int kThr = 128;
+    int64_t blocks = (tasks + kThr - 1) / kThr;
+    const int64_t max_blocks = int64_t(kNumSMs) * 16 * 4;
     if (blocks > max_blocks) blocks = max_blocks;
+    if (max_ctas > 0 && blocks > max_ctas) blocks = max_ctas;
     if (blocks < 1) continue;
     switch (bits) {
-      case 1: bitpack_group_kernel<1><<<blocks, 256, 0, stream>>>(a); break;
-      case 2: bitpack_group_kernel<2><<<blocks, 256, 0, stream>>>(a); break;
-      case 3: bitpack_group_kernel<3><<<blocks, 256, 0, stream>>>(a); break;
-      case 4: bitpack_group_kernel<4><<<blocks, 256, 0, stream>>>(a); break;
-      case 5: bitpack_group_kernel<5><<<blocks, 256, 0, stream>>>(a); break;
-      case 6: bitpack_group_kernel<6><<<blocks, 256, 0, stream>>>(a); break;
-      case 7: bitpack_group_kernel<7><<<blocks, 256, 0, stream>>>(a); break;
-      default: bitpack_group_kernel<8><<<blocks, 256, 0, stream>>>(a); break;
+      case 1: bitpack_group_kernel<1><<<blocks, kThr, 0, stream>>>(a); break;
+      case 2: bitpack_group_kernel<2><<<blocks, kThr, 0, stream>>>(a); break;
+      case 3: bitpack_group_kernel<3><<<blocks, kThr, 0, stream>>>(a); break;
+      case 4: bitpack_group_kernel<4><<<blocks, kThr, 0, stream>>>(a); break;
+      case 5: bitpack_group_kernel<5><<<blocks, kThr, 0, stream>>>(a); break;
+      case 6: bitpack_group_kernel<6><<<blocks, kThr, 0, stream>>>(a); break;
+      case 7: bitpack_group_kernel<7><<<blocks, kThr, 0, stream>>>(a); break;
+      default: bitpack_group_kernel<8><<<blocks, kThr, 0, stream>>>(a); break;
     }
     note_launch();
     if (cudaError_t e = cudaPeekAtLastError()) return e;

@@ -63,7 +63,7 @@ struct PackGroupArgs {
   int64_t tasks;
   PackSeg seg[kPackGroupMax];
 };
-cudaError_t launch_bitpack_group(const PackSeg* segs, int count, int bits, cudaStream_t stream);
+cudaError_t launch_bitpack_group(const PackSeg* segs, int count, int bits, cudaStream_t stream, int max_ctas = 0);
 
 // Tiled AND+POPC implicit-GEMM kernel (conv and dense); returns cudaErrorNotSupported
 // when no instantiation covers (a_bits, w_bits, algo).
