@@ -20,7 +20,9 @@ ap.add_argument("--group", action="store_true", help="all listed layers in one g
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--gemm", type=int, default=0, help="M=N=K of a dense A2W1 product instead of conv layers")
 ap.add_argument("--tile-n", type=int, default=0)
+ap.add_argument("--asrc", type=int, default=0)
 a = ap.parse_args()
+bs.set_tuning(bs.TUNE_TCD_A_SRC, a.asrc)
 if a.tile_n:
     bs.set_tuning(bs.TUNE_TC_TILE_N, a.tile_n)
 if a.gemm:
