@@ -137,6 +137,11 @@ class ConvLayerRun:
         self.fmt = fmt
         self.w_tc = (bs.conv2d_tc_prepare_weights(self.wp, w_bits, self.enc, L.oc, L.k, L.k, L.ic, tc_format=fmt)
                      if path == "tc" else None)
+        # digit path: weight digits (offline) and the digit-packed activation buffer
+        self.w_dig = (bs.conv2d_tcd_prepare_weights(self.wp, w_bits, self.enc, L.oc, L.k, L.k, L.ic)
+                      if path == "tcd" else None)
+        self.dig = (torch.empty(((a_bits + 1) // 2, self.n * L.h * L.w, bs.digit_row_bytes(L.ic)), dtype=torch.uint8,
+                                device=dev) if path == "tcd" else None)
 
     def binops(self):
         return binops_conv(self.L, self.n, self.a_bits, self.w_bits)
@@ -162,6 +167,11 @@ class ConvLayerRun:
         else:
             self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h,
                                           L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
+
+    def tcd_item(self):
+        L = self.L
+        return dict(act_dig=self.dig, w_dig=self.w_dig, out=self.out, n=self.n, h=L.h, w=L.w, c=L.ic, oc=L.oc,
+                    kh=L.k, kw=L.k, stride=L.s, pad=L.pad, w_enc=self.enc)
 
     def group_item(self):
         L = self.L
@@ -225,6 +235,22 @@ class ConvWorkload:
                                for part in args.group_layers.split("|")]
                 assert sorted(i for grp in self.groups for i in grp) == list(range(len(self.runs)))
             self.group_items = [[self.runs[i].group_item() for i in grp] for grp in self.groups]
+        if args.path == "tcd":  # digit path: one digit-pack launch + one TMA-fed conv launch for every layer
+            # every layer's activations and outputs live in one flat device buffer each (views), so the
+            # end-to-end step moves its inputs and results with one copy per direction
+            na = sum(r.act.numel() for r in self.runs)
+            no = sum(r.out.numel() for r in self.runs)
+            self.flat_act = torch.empty(na + 16 * len(self.runs), dtype=torch.uint8, device=dev)
+            self.flat_out = torch.empty(no + 4 * len(self.runs), dtype=torch.int32, device=dev)
+            oa = oo = 0
+            for r in self.runs:
+                a = self.flat_act[oa:oa + r.act.numel()].view(r.act.shape)
+                a.copy_(r.act)
+                r.act = a
+                r.out = self.flat_out[oo:oo + r.out.numel()].view(r.out.shape)
+                oa += (r.act.numel() + 15) // 16 * 16  # 16-byte aligned views
+                oo += (r.out.numel() + 3) // 4 * 4
+            self.tcd_items = [r.tcd_item() for r in self.runs]
         if args.path == "small":  # every layer in ONE launch of the small-problem path (packing fused)
             self.small_items = [dict(act=r.act, w_packed=r.wp, out=r.out, w_enc=r.enc, oc=r.L.oc, kh=r.L.k, kw=r.L.k,
                                      stride=r.L.s, pad=r.L.pad) for r in self.runs]
@@ -243,6 +269,10 @@ class ConvWorkload:
         }
 
     def describe_step(self, args):
+        if args.path == "tcd":
+            return ("every layer's activations digit-packed by ONE bs_digitpack_group launch, then every layer's conv "
+                    "in ONE bs_bitserial_conv2d_nhwc_tcd_group launch (TMA-fed tcgen05 kind::mxf4 on digit-packed "
+                    "operands; weights packed + digit-prepared once, untimed)")
         if args.path == "small":
             return ("every layer's conv from raw uint8 codes in ONE bs_bitserial_conv2d_nhwc_i8_group launch (activation "
                     "packing fused in shared memory, AND+POPC, K slices summed through cluster shared memory; weights "
@@ -264,6 +294,11 @@ class ConvWorkload:
         return f"{packs}; {convs} (weights packed + plane-expanded once, untimed)"
 
     def step(self):
+        if self.args.path == "tcd":
+            bs = self.runs[0].bs
+            bs.digitpack_group([r.act for r in self.runs], self.args.a_bits, outs=[r.dig for r in self.runs])
+            bs.bitserial_conv2d_nhwc_tcd_group(self.tcd_items, self.args.a_bits, self.args.w_bits)
+            return
         if self.args.path == "small":
             self.runs[0].bs.bitserial_conv2d_nhwc_i8_group(self.small_items, self.args.a_bits, self.args.w_bits)
             return
@@ -342,12 +377,30 @@ class ConvWorkload:
                                           "AND+POPC, cluster split-K)", "ops": ops, "ms": ms, "launches": 1,
                 "bytes": nbytes, "breakdown": {"step_kernel_us": 1e3 * ms}}
 
+    def roofline_tcd(self, reps):
+        """The digit path's conv launch (all layers, one launch) and its pack launch, each
+        graph-replayed; algorithmic bytes: activation digits + weight digits + int32 outputs."""
+        bs = self.runs[0].bs
+        bs.digitpack_group([r.act for r in self.runs], self.args.a_bits, outs=[r.dig for r in self.runs])
+        conv = lambda: bs.bitserial_conv2d_nhwc_tcd_group(self.tcd_items, self.args.a_bits, self.args.w_bits)  # noqa
+        pack = lambda: bs.digitpack_group([r.act for r in self.runs], self.args.a_bits,  # noqa
+                                          outs=[r.dig for r in self.runs])
+        ms, pms = graph_launch_ms(conv, reps), graph_launch_ms(pack, reps)
+        nbytes = sum(r.dig.numel() + r.w_dig.numel() + r.out.numel() * 4 for r in self.runs)
+        ops = sum(r.binops() for r in self.runs)
+        return {"kind": "tensor", "kernel": f"tcd_conv_kernel (TMA-fed tcgen05 kind::mxf4 on digit-packed operands; "
+                                            f"one launch for the {len(self.runs)} layers, rank 0)",
+                "ops": ops, "ms": ms, "launches": 1, "bytes": nbytes,
+                "breakdown": {"conv_group_us": 1e3 * ms, "digit_pack_group_us": 1e3 * pms}}
+
     def roofline(self, reps):
         """Per-launch device time of the pack and conv kernels of every layer: each
         kernel captured `reps` times back to back in a CUDA graph, timed with events on
         the stream that replays it (no host launch gaps), per launch = graph time / reps."""
         if self.args.path == "small":
             return self.roofline_small(reps)
+        if self.args.path == "tcd":
+            return self.roofline_tcd(reps)
         for r in self.runs:
             r.pack_only()
             r.conv_only()
@@ -411,6 +464,16 @@ class ConvWorkload:
 
             def step():
                 bs.bitserial_conv2d_nhwc_tc_host_group(layers, self.args.a_bits, self.args.w_bits, tc_format=fmt)
+        elif self.args.path == "tcd":  # one upload of every layer's codes, the step's two launches, one download
+            host_in = self.flat_act.cpu().pin_memory()
+            host_out = torch.empty(self.flat_out.shape, dtype=torch.int32).pin_memory()
+            bufs = [(host_in, host_out)]
+
+            def step():
+                self.flat_act.copy_(host_in, non_blocking=True)
+                self.step()
+                host_out.copy_(self.flat_out, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
         else:
             def step():
                 for r, b in zip(self.runs, bufs):
@@ -928,7 +991,7 @@ def run_ours(args):
 
 def dtype_of(args, wl):
     """The arithmetic the timed path computes in (not a precision claim)."""
-    if getattr(wl, "digit", False):
+    if getattr(wl, "digit", False) or args.path == "tcd":
         return ("u8 codes -> digit-packed e2m1 fields (two bit-planes per nibble, 0.5 x {0..3}) x ue8m0 4^d scales on "
                 "tcgen05 kind::mxf4 (fp32 accum, exact) -> i32")
     if args.path == "tc":
@@ -1062,7 +1125,7 @@ def main():
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
-    ap.add_argument("--path", choices=["auto", "tc", "popc", "small"], default="auto",
+    ap.add_argument("--path", choices=["auto", "tc", "tcd", "popc", "small"], default="auto",
                     help="conv/GEMM kernel: tensor-core bitserial, the AND/POPC integer-pipe kernel, or the one-launch "
                          "small-problem path; auto = small for conv1, else tc")
     ap.add_argument("--fused-gather", action="store_true",
@@ -1071,8 +1134,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step's outputs")
     args = ap.parse_args()
-    if args.path == "auto":  # measured: small wins the single batch-1 layer, tc the ten-layer batch-1 step
-        args.path = "small" if args.workload == "conv1" else "tc"
+    if args.path == "auto":  # measured: small wins the single batch-1 layer, the digit path the ten-layer batch-1
+        # step (two launches), the expansion kernel the batch-256 step (profiles/r02g_*)
+        args.path = {"conv1": "small", "resnet1": "tcd"}.get(args.workload, "tc")
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if world == 0 and args.gpus > 1:  # not launched by torchrun: launch N ranks (one per GPU) ourselves
         return relaunch(args.gpus)

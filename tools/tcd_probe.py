@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--epi", choices=["tma", "direct"], default="tma")
     ap.add_argument("--asrc", type=int, default=0, help="BS_TUNE_TCD_A_SRC (1 TMA im2col, 2 cp.async)")
     ap.add_argument("--bstream", type=int, default=0, help="BS_TUNE_TCD_B_STREAM")
+    ap.add_argument("--batch", type=int, default=256)
     a = ap.parse_args()
     bs.set_tuning(bs.TUNE_TCD_A_SRC, a.asrc)
     bs.set_tuning(bs.TUNE_TCD_B_STREAM, a.bstream)
@@ -57,7 +58,7 @@ def main():
     hbm = peaks["hbm_gbs"]
     res = {"hbm_peak_gbs": hbm}
     layers = list(inputs.BASELINE_LAYERS)
-    runs = conv_setup(256, 2, 1, layers)
+    runs = conv_setup(a.batch, 2, 1, layers)
     pack = lambda: bs.digitpack_group([r["act"] for r in runs], 2, outs=[r["ad"] for r in runs])  # noqa: E731
     pack()
     torch.cuda.synchronize()
