@@ -130,6 +130,9 @@ int64_t bs_kernel_launches(void);
  *                            gathers by producer warps (the default)
  *   BS_TUNE_TCD_B_STREAM   : 1 = digit-path weights always streamed per stage (default: a weight
  *                            block of up to 96 KB stays resident per N block)
+ *   BS_TUNE_TCD_MCAST      : 2-CTA clusters that each load half of every streamed weight chunk and
+ *                            multicast it to both (dense, even number of M blocks): 1 = never,
+ *                            2 = always, 0 = at >= 128 M blocks or several digits
  * bs_set_tuning returns BS_ERR_INVALID_ARG for an unknown knob or value; bs_get_tuning returns
  * the current value (0 for an unknown knob). */
 typedef enum {
@@ -139,7 +142,8 @@ typedef enum {
   BS_TUNE_TC_B_SLOTS = 3,
   BS_TUNE_SMALL_KSPLIT = 4,
   BS_TUNE_TCD_A_SRC = 5,
-  BS_TUNE_TCD_B_STREAM = 6
+  BS_TUNE_TCD_B_STREAM = 6,
+  BS_TUNE_TCD_MCAST = 7
 } bs_tune_knob;
 int bs_set_tuning(int knob, int value);
 int bs_get_tuning(int knob);

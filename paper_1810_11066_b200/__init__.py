@@ -29,7 +29,7 @@ __all__ = [
     "TC_F4", "EXPORTED_SYMBOLS", "TcConvDesc", "bitserial_conv2d_nhwc_tc_group", "PackDesc", "bitpack_group",
     "bitserial_dense_tc_gather", "TcHostDesc", "bitserial_conv2d_nhwc_tc_host_group", "set_tuning", "get_tuning",
     "TUNE_TC_TILE_N", "TUNE_TC_EPILOGUE", "TUNE_TC_GROUP_SPLIT", "TUNE_TC_B_SLOTS", "TUNE_SMALL_KSPLIT",
-    "TUNE_TCD_A_SRC", "TUNE_TCD_B_STREAM", "ConvI8Desc",
+    "TUNE_TCD_A_SRC", "TUNE_TCD_B_STREAM", "TUNE_TCD_MCAST", "ConvI8Desc",
     "bitserial_conv2d_nhwc_i8_group", "bitserial_dense_tc_multicast",
     "digit_row_bytes", "digitpack", "DigitPackDesc", "digitpack_group", "conv2d_tcd_weight_bytes",
     "dense_tcd_weight_bytes", "conv2d_tcd_prepare_weights", "dense_tcd_prepare_weights", "bitserial_conv2d_nhwc_tcd",
@@ -41,7 +41,7 @@ A_UNSIGNED, A_BIPOLAR, A_SIGNED = 0, 1, 2    # activation encodings (bs_a_encodi
 TC_DEFAULT, TC_I8, TC_F4 = 0, 1, 2  # bs_tc_format
 ALGO_AUTO, ALGO_POPC, ALGO_POPC_LIT, ALGO_GEMV, ALGO_TC = 0, 1, 2, 3, 4
 TUNE_TC_TILE_N, TUNE_TC_EPILOGUE, TUNE_TC_GROUP_SPLIT, TUNE_TC_B_SLOTS, TUNE_SMALL_KSPLIT = 0, 1, 2, 3, 4  # bs_tune_knob
-TUNE_TCD_A_SRC, TUNE_TCD_B_STREAM = 5, 6
+TUNE_TCD_A_SRC, TUNE_TCD_B_STREAM, TUNE_TCD_MCAST = 5, 6, 7
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # BITSERIAL_LIB selects an experiment build of the same library (A/B timing of compile-time

@@ -319,6 +319,9 @@ int bs_set_tuning(int knob, int value) {
     case BS_TUNE_TCD_A_SRC:
       if (value < 0 || value > 2) return fail(BS_ERR_INVALID_ARG, "%s: value %d not in {0,1,2}", fn, value);
       break;
+    case BS_TUNE_TCD_MCAST:
+      if (value < 0 || value > 2) return fail(BS_ERR_INVALID_ARG, "%s: value %d not in {0,1,2}", fn, value);
+      break;
     case BS_TUNE_TCD_B_STREAM:
       if (value != 0 && value != 1) return fail(BS_ERR_INVALID_ARG, "%s: value %d not 0 or 1", fn, value);
       break;

@@ -38,7 +38,7 @@ int64_t launch_count();
 // Process-wide tuning knobs (bs_set_tuning; atomics, read per launch; 0 = library choice).
 enum TuneKnob : int {
   kTuneTileN = 0, kTuneEpilogue = 1, kTuneGroupSplit = 2, kTuneBSlots = 3, kTuneSmallKs = 4, kTuneTcdASrc = 5,
-  kTuneTcdBStream = 6, kTuneCount = 7
+  kTuneTcdBStream = 6, kTuneTcdMcast = 7, kTuneCount = 8
 };
 int tuning(int knob);
 // SM count of the current device (cached per device).

@@ -92,6 +92,8 @@ struct TdArgs {
   int stages;      // A ring stages (runtime: depends on the B region)
   int b_region;    // bytes of the B region (resident blocks, or streamed chunk slots)
   int gather;      // the producer warps gather every problem's activations (else all come by TMA)
+  int mc;          // clusters of 2 CTAs on adjacent tiles of one N block: each CTA loads half of every weight
+                   // chunk and multicasts it to both (dense, streamed weights, even tile counts)
   TdProb prob[NP];
 };
 template <int NP>
@@ -120,6 +122,33 @@ __device__ __forceinline__ void spin_wait(uint32_t addr, uint32_t parity) {
       "}\n" ::"r"(addr),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar), "h"(mask)
+      : "memory");
+}
+// tcgen05.commit arriving on the barrier at this shared-memory offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc_elect(uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "{.reg .pred e; .reg .b32 x; elect.sync x|e, 0xffffffff;\n"
+      "@!e bra SKIP%=;\n"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "SKIP%=:\n}" ::"r"(mbar),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -187,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(smem_u32(full + s), args.gather ? 1 + kProdWarps : 1);  // TMA thread (+ each producer warp)
-      tc::mbar_init(smem_u32(empty + s), 1);
+      tc::mbar_init(smem_u32(empty + s), args.mc ? 2 : 1);  // (multicast: both CTAs' MMAs release a stage)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(smem_u32(acc_full + a), 1);
@@ -210,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (args.mc) cluster_sync();  // the peer's multicasts and commits target these barriers
   tc::tc_fence_after();
   if (*tmem_slot != 0u) asm volatile("trap;");  // all 512 columns, from column 0
   constexpr uint32_t tmem = 0;
@@ -286,7 +316,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!P.b_res) {
             const uint32_t sB = smem_u32(s_b + stage * C::kBSlot);
 #pragma unroll
-            for (int e = 0; e < DW; ++e) tc::tma_load_2d(sB + e * C::kBBytes, &maps.w[pi], p0 * cb, e * P.oc + n0, fb);
+            for (int e = 0; e < DW; ++e) {
+              if (args.mc) {  // this CTA's half of the rows, into both CTAs' slots
+                const int half = BN / 2, cr = int(cluster_rank());
+                tma_load_2d_mc(sB + e * C::kBBytes + uint32_t(cr * half * kStageK), &maps.w[pi], p0 * cb,
+                               e * P.oc + n0 + cr * half, fb, uint16_t(3));
+              } else {
+                tc::tma_load_2d(sB + e * C::kBBytes, &maps.w[pi], p0 * cb, e * P.oc + n0, fb);
+              }
+            }
           }
           if (P.a_tma) {
             for (int pc = 0; pc < npc; ++pc) {
@@ -440,7 +478,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
-        tc::mma_commit_elect(smem_u32(empty + stage));
+        if (args.mc)
+          mma_commit_mc_elect(smem_u32(empty + stage), uint16_t(3));
+        else
+          tc::mma_commit_elect(smem_u32(empty + stage));
         if (++stage == S) {
           stage = 0;
           phase ^= 1u;
@@ -557,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc::tc_fence_before();
   __syncthreads();
+  if (args.mc) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == kMmaWarp) {
     tc::tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -707,7 +749,53 @@ cudaError_t launch(const TcdProblem* ps, int count, cudaStream_t stream) {
   if (a.b_region + S * C::kAStage > C::kBudget) return cudaErrorInvalidValue;
   int smem = 1024 + a.b_region + S * C::kAStage + C::kEpiBytes + kBarBytes;
   if (smem < kMinSmem) smem = kMinSmem;
-  const int grid = a.ntiles < device_sms() ? a.ntiles : device_sms();
+  // clusters of two on adjacent tiles of one N block multicast the weight chunks (dense, streamed
+  // weights): each CTA loads half of every chunk's rows, so per CTA the operand bytes per stage drop
+  // from A + B to A + B/2
+  const TdProb& P0 = a.prob[0];
+  // (measured, profiles/r02h_tcd_probe_mc.json: +3-4% at 16384^3 and A4W2, -4% at 8192^3 A2W1, where the
+  // pairs' lock-step release of each stage costs more than the halved weight bytes save)
+  const int mknob = tuning(kTuneTcdMcast);
+  a.mc = count == 1 && P0.dense && !P0.b_res && P0.nmb % 2 == 0 && a.ntiles >= 4 && BN % 16 == 0 && mknob != 1 &&
+         (mknob == 2 || P0.nmb >= 128 || DA * DW > 1);
+  int grid = a.ntiles < device_sms() ? a.ntiles : device_sms();
+  if (a.mc) {
+    static std::atomic<int> max_clusters[64];  // co-resident 2-CTA clusters, per device (persistent grid)
+    int mcl = dev < 64 ? max_clusters[dev].load(std::memory_order_relaxed) : 0;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = size_t(smem);
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (mcl == 0) {
+      cfg.gridDim = dim3(unsigned(device_sms() / 2 * 2));
+      if (cudaOccupancyMaxActiveClusters(&mcl, kern, &cfg) != cudaSuccess || mcl < 1) {
+        cudaGetLastError();
+        mcl = -1;
+      }
+      if (dev < 64) max_clusters[dev].store(mcl, std::memory_order_relaxed);
+    }
+    if (mcl > 0) {
+      grid = std::min(grid, 2 * mcl) / 2 * 2;
+      // the weight map's box: half of the tile's rows per CTA
+      const TcdProblem& p = ps[0];
+      const int64_t wrow = tcd_wrow_bytes(digit_row_bytes(p.c) / 16);
+      if (!tc::encode_2d(&maps.w[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, p.wdig, uint64_t(wrow),
+                         uint64_t(p.w_digits) * p.oc, uint64_t(wrow), kStageK, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+      cfg.gridDim = dim3(unsigned(grid));
+      if (cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, maps)) return e;
+      note_launch();
+      return cudaPeekAtLastError();
+    }
+    a.mc = 0;
+  }
   kern<<<grid, kThreads, smem, stream>>>(a, maps);
   note_launch();
   return cudaPeekAtLastError();

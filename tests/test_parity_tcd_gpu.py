@@ -291,3 +291,19 @@ def test_conv_tcd_operand_sources(tuning, a_src, b_stream, a_bits, w_bits):
         ref = oracle.conv2d_nhwc_enc(act.numpy(), a_bits, 0, wt.numpy(), w_bits, 1, stride=(s, s), pad=(p, p))
         got = run_conv(act, a_bits, 0, wt, w_bits, 1, s, p)
         np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"{case} a_src={a_src} b_stream={b_stream}")
+
+
+@pytest.mark.parametrize("mcast_off", [2, 1])
+@pytest.mark.parametrize("m,n,k,a_bits,w_bits", [(512, 1024, 4096, 2, 1), (256, 1000, 2000, 2, 2), (384, 2048, 1500, 4, 1),
+                                                 (258, 1030, 2600, 1, 3)])
+def test_dense_tcd_cluster_multicast(tuning, mcast_off, m, n, k, a_bits, w_bits):
+    """Dense products with streamed weights: 2-CTA clusters that each load half of every weight
+    chunk and multicast it to both (knob 2), and the same without the clusters (knob 1); ragged N."""
+    tuning(bs.TUNE_TCD_MCAST, mcast_off)
+    for w_enc in (bs.UNIPOLAR, bs.BIPOLAR):
+        a, w = inputs.dense_operands(m, n, k, a_bits, w_bits, seed=m + n + k + a_bits + w_bits + w_enc)
+        ref = oracle.dense_enc(a.numpy(), a_bits, 0, w.numpy(), w_bits, w_enc)
+        ad = bs.digitpack(a.to(DEV), a_bits)
+        wd = bs.dense_tcd_prepare_weights(bs.bitpack(w.to(DEV), w_bits), w_bits, w_enc, n, k)
+        got = bs.bitserial_dense_tcd(ad, a_bits, wd, w_bits, m, n, k, w_enc=w_enc)
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"{m}x{n}x{k} mcast_off={mcast_off}")
