@@ -228,3 +228,77 @@ def digitpack(x, bits: int, enc: int = UNSIGNED) -> np.ndarray:
     if _load().oracle_digitpack(_ptr(x), _ptr(out), rows, k, bits, enc) != 0:
         raise ValueError("oracle_digitpack rejected its arguments")
     return out
+
+
+# ---------------------------------------------------------------- window layout (R26)
+def win_geometry(n: int, h: int, w: int, c: int, kh: int, kw: int, stride: int, pad_h: int, pad_w: int) -> dict:
+    """Geometry of the window layout (reading R26), written out from its definition.
+
+    The conv's zero-padded input (PAPER.md:573 NHWC conv; padding = value 0, reading R20) is
+    split into the stride x stride phases (py, px) its taps read: phase pixel (gy, gx) is padded
+    pixel (gy*s + py, gx*s + px).  Output (oy, ox) with tap (ky, kx) reads phase
+    (ky % s, kx % s) at (oy + ky // s, ox + kx // s), so on a phase grid of hg x wg pixels per
+    image (flattened q = (img*hg + gy)*wg + gx) it reads q_out + (ky // s)*wg + kx // s.
+    """
+    s = stride
+    oh = conv_out_extent(h, kh, s, pad_h)
+    ow = conv_out_extent(w, kw, s, pad_w)
+    hg = oh + (kh - 1) // s
+    wg = ow + (kw - 1) // s
+    phases = sorted({(ky % s) * s + (kx % s) for ky in range(kh) for kx in range(kw)})
+    maxoff = ((kh - 1) // s) * wg + (kw - 1) // s
+    lwin = (128 + maxoff + 7) // 8 * 8           # pixels a 128-row tile reads per window
+    gpix = n * hg * wg
+    pstride = (gpix + lwin + 7) // 8 * 8         # zero tail: the last tile's window stays inside
+    return dict(s=s, oh=oh, ow=ow, hg=hg, wg=wg, phases=phases, nph=len(phases), maxoff=maxoff, lwin=lwin,
+                gpix=gpix, pstride=pstride, cw=packed_row_words(c))
+
+
+def digitpack_win(x, bits: int, enc: int, kh: int, kw: int, stride: int, pad_h: int, pad_w: int) -> np.ndarray:
+    """Window layout of NHWC activation codes x [n][h][w][c] (R26): uint8
+    [D][nph][cw][pstride][16], D = ceil(bits/2).  Entry (d, phase slot, channel slab cs, q)
+    holds the 16 digit-packed bytes (oracle.digitpack, R24) of channels [32cs, 32cs+32) of the
+    input pixel that phase-grid position q maps to, or zeros where q is padding, lies past
+    the image, or is in the tail (q >= n*hg*wg)."""
+    x = _u8(x)
+    if x.ndim != 4:
+        raise ValueError("digitpack_win: x [n][h][w][c]")
+    n, h, w, c = x.shape
+    g = win_geometry(n, h, w, c, kh, kw, stride, pad_h, pad_w)
+    s, hg, wg, cw, ps = g["s"], g["hg"], g["wg"], g["cw"], g["pstride"]
+    dig = digitpack(x.reshape(n * h * w, c), bits, enc)          # [D][pixels][16*cw]
+    D = dig.shape[0]
+    out = np.zeros((D, g["nph"], cw, ps, 16), dtype=np.uint8)
+    q = np.arange(g["gpix"])
+    img, rem = q // (hg * wg), q % (hg * wg)
+    gy, gx = rem // wg, rem % wg
+    for f, phase in enumerate(g["phases"]):
+        py, px = phase // s, phase % s
+        y = gy * s + py - pad_h
+        xx = gx * s + px - pad_w
+        ok = (y >= 0) & (y < h) & (xx >= 0) & (xx < w)
+        pix = (img[ok] * h + y[ok]) * w + xx[ok]
+        for cs in range(cw):
+            out[:, f, cs, q[ok], :] = dig[:, pix, 16 * cs:16 * cs + 16]
+    return out
+
+
+def conv2d_tcw_weights(wt, w_bits: int, w_enc: int) -> np.ndarray:
+    """Window-path weight digits of OHWI weight codes wt [oc][kh][kw][c] (R26):
+    uint8 [nblk][pairs][Dw][kh*kw][2][BN][16], BN = 64 if oc <= 64 else 128,
+    nblk = ceil(oc / BN), pairs = cw / 2; entry (nb, p, e, tap, j, r) holds the 16 digit bytes
+    (oracle.digitpack) of channels [32(2p+j), 32(2p+j)+32) of filter nb*BN + r at that tap
+    (zeros for filters >= oc)."""
+    wt = _u8(wt)
+    oc, kh, kw, c = wt.shape
+    bn = 64 if oc <= 64 else 128
+    nblk = (oc + bn - 1) // bn
+    cw = packed_row_words(c)
+    dig = digitpack(wt.reshape(oc * kh * kw, c), w_bits, w_enc)   # [Dw][oc*taps][16*cw]
+    D = dig.shape[0]
+    taps = kh * kw
+    full = np.zeros((D, nblk * bn, taps, cw, 16), dtype=np.uint8)
+    full[:, :oc] = dig.reshape(D, oc, taps, cw, 16)
+    # [e][nb][r][tap][p][j][16] -> [nb][p][e][tap][j][r][16]
+    t = full.reshape(D, nblk, bn, taps, cw // 2, 2, 16)
+    return np.ascontiguousarray(t.transpose(1, 4, 0, 3, 5, 2, 6))

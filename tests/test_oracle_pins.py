@@ -501,3 +501,88 @@ def test_digitpack_dot_product_matches_dense_enc():
                     for e in range(vw.shape[0]):
                         out += 4 ** (d + e) * (va[d] @ vw[e].T)
                 np.testing.assert_array_equal(out, oracle.dense_enc(a, a_bits, a_enc, w, w_bits, w_enc))
+
+
+# ---------------------------------------------------------------- window layout (R26)
+def test_win_layout_golden():
+    """Hand-derived window-layout bytes (tests/golden/win_examples.json, each case cites R26)."""
+    for case in _gold("win_examples.json")["cases"]:
+        x = np.array(case["codes"], dtype=np.uint8)
+        got = oracle.digitpack_win(x, case["bits"], case["enc"], case["kh"], case["kw"], case["stride"],
+                                   case["pad"], case["pad"])
+        d, f, cs, nq, nb = case["shape"]
+        assert got.shape[:3] == (d, f, cs), case["note"]
+        want = np.zeros_like(got)
+        for dd, ff, cc, q, b, v in case["nonzero"]:
+            want[dd, ff, cc, q, b] = v
+        np.testing.assert_array_equal(got, want, err_msg=case["note"])
+
+
+def _e2m1_vals(p):
+    """Digit values of a byte array's two nibbles, last axis doubled: element 2b = low nibble."""
+    lo = np.vectorize(oracle.e2m1_twice)(p & 0xF)
+    hi = np.vectorize(oracle.e2m1_twice)(p >> 4)
+    return np.stack([lo, hi], axis=-1).reshape(*p.shape[:-1], -1).astype(np.int64)
+
+
+WIN_CASES = [  # (n, h, w, c, oc, kh, kw, stride, pad, a_bits, w_bits)
+    (2, 5, 4, 40, 24, 3, 3, 1, 1, 2, 1),
+    (1, 6, 7, 33, 70, 3, 3, 2, 1, 3, 2),
+    (2, 6, 6, 64, 8, 1, 1, 2, 0, 2, 2),
+    (1, 5, 6, 20, 5, 2, 3, 1, 0, 4, 1),
+    (1, 7, 5, 96, 130, 3, 2, 2, 2, 1, 3),
+    (3, 3, 3, 16, 4, 3, 3, 1, 2, 2, 1),
+]
+
+
+@pytest.mark.parametrize("case", WIN_CASES)
+@pytest.mark.parametrize("enc", [(0, 0), (0, 1), (1, 1), (2, 2)])
+def test_win_layout_conv_brute_force(case, enc):
+    """Convolution evaluated FROM the two window layouts with the tap-offset rule of R26 —
+    out[q] = sum_{d,e} 4^(d+e) sum_tap sum_ch A_d[phase(tap)][ch][q + off(tap)] W_e[o][tap][ch],
+    q = (img*hg + oy)*wg + ox, off = (ky//s)*wg + kx//s — decoded here with Python E2M1
+    arithmetic, equals the oracle's plain NHWC convolution (a wrong phase, offset, padding
+    position, slab order or filter block fails it)."""
+    n, h, w, c, oc, kh, kw, s, pad, a_bits, w_bits = case
+    a_enc, w_enc = enc
+    g = np.random.default_rng(hash(case) % 1000 + 17 * a_enc + w_enc)
+    act = g.integers(0, 1 << a_bits, size=(n, h, w, c), dtype=np.uint8)
+    wt = g.integers(0, 1 << w_bits, size=(oc, kh, kw, c), dtype=np.uint8)
+    geo = oracle.win_geometry(n, h, w, c, kh, kw, s, pad, pad)
+    A = _e2m1_vals(oracle.digitpack_win(act, a_bits, a_enc, kh, kw, s, pad, pad))   # [D][f][cs][q][32]
+    Wt = _e2m1_vals(oracle.conv2d_tcw_weights(wt, w_bits, w_enc))                   # [nb][p][e][tap][j][r][32]
+    nblk, pairs, De, taps, _, bn, _ = Wt.shape
+    # weights back to [e][o][tap][ch]
+    Wl = Wt.transpose(2, 0, 5, 3, 1, 4, 6).reshape(De, nblk * bn, taps, pairs * 2 * 32)
+    A = A.transpose(0, 1, 3, 2, 4).reshape(A.shape[0], A.shape[1], A.shape[3], -1)   # [D][f][q][ch]
+    hg, wg, oh, ow = geo["hg"], geo["wg"], geo["oh"], geo["ow"]
+    q = ((np.arange(n)[:, None, None] * hg + np.arange(oh)[None, :, None]) * wg + np.arange(ow)[None, None, :]).ravel()
+    out = np.zeros((q.size, nblk * bn), dtype=np.int64)
+    for d in range(A.shape[0]):
+        for e in range(De):
+            for ky in range(kh):
+                for kx in range(kw):
+                    f = geo["phases"].index((ky % s) * s + kx % s)
+                    off = (ky // s) * wg + kx // s
+                    out += 4 ** (d + e) * (A[d, f, q + off] @ Wl[e, :, ky * kw + kx].T)
+    want = oracle.conv2d_nhwc_enc(act, a_bits, a_enc, wt, w_bits, w_enc, stride=(s, s), pad=(pad, pad))
+    np.testing.assert_array_equal(out[:, :oc].reshape(want.shape), want)
+    assert not out[:, oc:].any()  # filters past oc (block padding) are zero
+
+
+def test_win_layout_zero_outside_image():
+    """Every window-layout entry that is padding, junk grid position or tail is zero, and the
+    number of non-zero slab entries equals the number of (pixel, slab) pairs the phases keep
+    (stride 1: every pixel once)."""
+    g = np.random.default_rng(3)
+    act = g.integers(1, 4, size=(2, 5, 6, 32), dtype=np.uint8)   # codes >= 1: every real pixel non-zero
+    lay = oracle.digitpack_win(act, 2, 0, 3, 3, 1, 1, 1)
+    geo = oracle.win_geometry(2, 5, 6, 32, 3, 3, 1, 1, 1)
+    nz = lay[0, 0, 0].any(axis=1)
+    assert nz.sum() == 2 * 5 * 6
+    q = np.nonzero(nz)[0]
+    assert q.max() < geo["gpix"]
+    rem = q % (geo["hg"] * geo["wg"])
+    gy, gx = rem // geo["wg"], rem % geo["wg"]
+    assert gy.min() == 1 and gy.max() == 5 and gx.min() == 1 and gx.max() == 6
+    assert not lay[0, 0, 1].any()   # c = 32: the second (pad) slab is zero
