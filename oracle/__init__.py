@@ -247,19 +247,31 @@ def win_geometry(n: int, h: int, w: int, c: int, kh: int, kw: int, stride: int, 
     wg = ow + (kw - 1) // s
     phases = sorted({(ky % s) * s + (kx % s) for ky in range(kh) for kx in range(kw)})
     maxoff = ((kh - 1) // s) * wg + (kw - 1) // s
-    lwin = (128 + maxoff + 7) // 8 * 8           # pixels a 128-row tile reads per window
+    lwin = (128 + maxoff + 8 + 7) // 8 * 8       # rows a 128-row tile reads per window (from an 8-row boundary)
     gpix = n * hg * wg
     pstride = (gpix + lwin + 7) // 8 * 8         # zero tail: the last tile's window stays inside
+    cw = packed_row_words(c)
     return dict(s=s, oh=oh, ow=ow, hg=hg, wg=wg, phases=phases, nph=len(phases), maxoff=maxoff, lwin=lwin,
-                gpix=gpix, pstride=pstride, cw=packed_row_words(c))
+                gpix=gpix, pstride=pstride, cw=cw, pairs=cw // 2)
+
+
+def _swap_halves(rows32: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """32-byte rows with their two 16-byte halves exchanged where bit 2 of the row index r is
+    set (the 32-byte shared-memory swizzle the rows are stored in, R26)."""
+    out = rows32.copy()
+    sw = ((r >> 2) & 1).astype(bool)
+    out[..., sw, :16] = rows32[..., sw, 16:]
+    out[..., sw, 16:] = rows32[..., sw, :16]
+    return out
 
 
 def digitpack_win(x, bits: int, enc: int, kh: int, kw: int, stride: int, pad_h: int, pad_w: int) -> np.ndarray:
     """Window layout of NHWC activation codes x [n][h][w][c] (R26): uint8
-    [D][nph][cw][pstride][16], D = ceil(bits/2).  Entry (d, phase slot, channel slab cs, q)
-    holds the 16 digit-packed bytes (oracle.digitpack, R24) of channels [32cs, 32cs+32) of the
-    input pixel that phase-grid position q maps to, or zeros where q is padding, lies past
-    the image, or is in the tail (q >= n*hg*wg)."""
+    [D][nph][pairs][pstride][32], D = ceil(bits/2), pairs = cw / 2.  Row (d, phase slot, pair p,
+    q) holds the 16 digit-packed bytes (oracle.digitpack, R24) of channels [64p, 64p+32) and of
+    [64p+32, 64p+64) of the input pixel that phase-grid position q maps to — in that order, or
+    exchanged when bit 2 of q is set — or zeros where q is padding, lies past the image, or is
+    in the tail (q >= n*hg*wg)."""
     x = _u8(x)
     if x.ndim != 4:
         raise ValueError("digitpack_win: x [n][h][w][c]")
@@ -268,7 +280,7 @@ def digitpack_win(x, bits: int, enc: int, kh: int, kw: int, stride: int, pad_h: 
     s, hg, wg, cw, ps = g["s"], g["hg"], g["wg"], g["cw"], g["pstride"]
     dig = digitpack(x.reshape(n * h * w, c), bits, enc)          # [D][pixels][16*cw]
     D = dig.shape[0]
-    out = np.zeros((D, g["nph"], cw, ps, 16), dtype=np.uint8)
+    plain = np.zeros((D, g["nph"], cw // 2, ps, 32), dtype=np.uint8)
     q = np.arange(g["gpix"])
     img, rem = q // (hg * wg), q % (hg * wg)
     gy, gx = rem // wg, rem % wg
@@ -278,17 +290,17 @@ def digitpack_win(x, bits: int, enc: int, kh: int, kw: int, stride: int, pad_h: 
         xx = gx * s + px - pad_w
         ok = (y >= 0) & (y < h) & (xx >= 0) & (xx < w)
         pix = (img[ok] * h + y[ok]) * w + xx[ok]
-        for cs in range(cw):
-            out[:, f, cs, q[ok], :] = dig[:, pix, 16 * cs:16 * cs + 16]
-    return out
+        for p in range(cw // 2):
+            plain[:, f, p, q[ok], :] = dig[:, pix, 32 * p:32 * p + 32]
+    return _swap_halves(plain, np.arange(ps))
 
 
 def conv2d_tcw_weights(wt, w_bits: int, w_enc: int) -> np.ndarray:
     """Window-path weight digits of OHWI weight codes wt [oc][kh][kw][c] (R26):
-    uint8 [nblk][pairs][Dw][kh*kw][2][BN][16], BN = 64 if oc <= 64 else 128,
-    nblk = ceil(oc / BN), pairs = cw / 2; entry (nb, p, e, tap, j, r) holds the 16 digit bytes
-    (oracle.digitpack) of channels [32(2p+j), 32(2p+j)+32) of filter nb*BN + r at that tap
-    (zeros for filters >= oc)."""
+    uint8 [nblk][pairs][Dw][kh*kw][BN][32], BN = 64 if oc <= 64 else 128,
+    nblk = ceil(oc / BN), pairs = cw / 2; row (nb, p, e, tap, r) holds the digit bytes
+    (oracle.digitpack) of channels [64p, 64p+64) of filter nb*BN + r at that tap, its two
+    16-byte halves exchanged when bit 2 of r is set (zeros for filters >= oc)."""
     wt = _u8(wt)
     oc, kh, kw, c = wt.shape
     bn = 64 if oc <= 64 else 128
@@ -297,8 +309,8 @@ def conv2d_tcw_weights(wt, w_bits: int, w_enc: int) -> np.ndarray:
     dig = digitpack(wt.reshape(oc * kh * kw, c), w_bits, w_enc)   # [Dw][oc*taps][16*cw]
     D = dig.shape[0]
     taps = kh * kw
-    full = np.zeros((D, nblk * bn, taps, cw, 16), dtype=np.uint8)
-    full[:, :oc] = dig.reshape(D, oc, taps, cw, 16)
-    # [e][nb][r][tap][p][j][16] -> [nb][p][e][tap][j][r][16]
-    t = full.reshape(D, nblk, bn, taps, cw // 2, 2, 16)
-    return np.ascontiguousarray(t.transpose(1, 4, 0, 3, 5, 2, 6))
+    full = np.zeros((D, nblk * bn, taps, cw // 2, 32), dtype=np.uint8)
+    full[:, :oc] = dig.reshape(D, oc, taps, cw // 2, 32)
+    # [e][nb][r][tap][p][32] -> [nb][p][e][tap][r][32]
+    t = np.ascontiguousarray(full.reshape(D, nblk, bn, taps, cw // 2, 32).transpose(1, 4, 0, 3, 2, 5))
+    return _swap_halves(t, np.arange(bn))

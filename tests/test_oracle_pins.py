@@ -539,22 +539,29 @@ WIN_CASES = [  # (n, h, w, c, oc, kh, kw, stride, pad, a_bits, w_bits)
 @pytest.mark.parametrize("enc", [(0, 0), (0, 1), (1, 1), (2, 2)])
 def test_win_layout_conv_brute_force(case, enc):
     """Convolution evaluated FROM the two window layouts with the tap-offset rule of R26 —
-    out[q] = sum_{d,e} 4^(d+e) sum_tap sum_ch A_d[phase(tap)][ch][q + off(tap)] W_e[o][tap][ch],
-    q = (img*hg + oy)*wg + ox, off = (ky//s)*wg + kx//s — decoded here with Python E2M1
-    arithmetic, equals the oracle's plain NHWC convolution (a wrong phase, offset, padding
-    position, slab order or filter block fails it)."""
+    out[q] = sum_{d,e} 4^(d+e) sum_tap sum_ch A_d[phase(tap)][q + off(tap)][ch] W_e[o][tap][ch],
+    q = (img*hg + oy)*wg + ox, off = (ky//s)*wg + kx//s, each 32-byte row read back through the
+    half exchange of rows with bit 2 set — decoded here with Python E2M1 arithmetic, equals the
+    oracle's plain NHWC convolution (a wrong phase, offset, padding position, slab order,
+    swizzle or filter block fails it)."""
     n, h, w, c, oc, kh, kw, s, pad, a_bits, w_bits = case
     a_enc, w_enc = enc
     g = np.random.default_rng(hash(case) % 1000 + 17 * a_enc + w_enc)
     act = g.integers(0, 1 << a_bits, size=(n, h, w, c), dtype=np.uint8)
     wt = g.integers(0, 1 << w_bits, size=(oc, kh, kw, c), dtype=np.uint8)
     geo = oracle.win_geometry(n, h, w, c, kh, kw, s, pad, pad)
-    A = _e2m1_vals(oracle.digitpack_win(act, a_bits, a_enc, kh, kw, s, pad, pad))   # [D][f][cs][q][32]
-    Wt = _e2m1_vals(oracle.conv2d_tcw_weights(wt, w_bits, w_enc))                   # [nb][p][e][tap][j][r][32]
-    nblk, pairs, De, taps, _, bn, _ = Wt.shape
-    # weights back to [e][o][tap][ch]
-    Wl = Wt.transpose(2, 0, 5, 3, 1, 4, 6).reshape(De, nblk * bn, taps, pairs * 2 * 32)
-    A = A.transpose(0, 1, 3, 2, 4).reshape(A.shape[0], A.shape[1], A.shape[3], -1)   # [D][f][q][ch]
+
+    def unswizzle(b):   # [..., rows, 32]: exchange the halves back where bit 2 of the row is set
+        r = np.arange(b.shape[-2])
+        sw = ((r >> 2) & 1).astype(bool)
+        out = b.copy()
+        out[..., sw, :16], out[..., sw, 16:] = b[..., sw, 16:], b[..., sw, :16]
+        return out
+    A = _e2m1_vals(unswizzle(oracle.digitpack_win(act, a_bits, a_enc, kh, kw, s, pad, pad)))  # [D][f][p][q][64]
+    Wt = _e2m1_vals(unswizzle(oracle.conv2d_tcw_weights(wt, w_bits, w_enc)))                  # [nb][p][e][tap][r][64]
+    nblk, pairs, De, taps, bn, _ = Wt.shape
+    Wl = Wt.transpose(2, 0, 4, 3, 1, 5).reshape(De, nblk * bn, taps, pairs * 64)             # [e][o][tap][ch]
+    A = A.transpose(0, 1, 3, 2, 4).reshape(A.shape[0], A.shape[1], A.shape[3], -1)            # [D][f][q][ch]
     hg, wg, oh, ow = geo["hg"], geo["wg"], geo["oh"], geo["ow"]
     q = ((np.arange(n)[:, None, None] * hg + np.arange(oh)[None, :, None]) * wg + np.arange(ow)[None, None, :]).ravel()
     out = np.zeros((q.size, nblk * bn), dtype=np.int64)
@@ -576,7 +583,7 @@ def test_win_layout_zero_outside_image():
     (stride 1: every pixel once)."""
     g = np.random.default_rng(3)
     act = g.integers(1, 4, size=(2, 5, 6, 32), dtype=np.uint8)   # codes >= 1: every real pixel non-zero
-    lay = oracle.digitpack_win(act, 2, 0, 3, 3, 1, 1, 1)
+    lay = oracle.digitpack_win(act, 2, 0, 3, 3, 1, 1, 1)      # [1][1][1][pstride][32]
     geo = oracle.win_geometry(2, 5, 6, 32, 3, 3, 1, 1, 1)
     nz = lay[0, 0, 0].any(axis=1)
     assert nz.sum() == 2 * 5 * 6
@@ -585,4 +592,8 @@ def test_win_layout_zero_outside_image():
     rem = q % (geo["hg"] * geo["wg"])
     gy, gx = rem // geo["wg"], rem % geo["wg"]
     assert gy.min() == 1 and gy.max() == 5 and gx.min() == 1 and gx.max() == 6
-    assert not lay[0, 0, 1].any()   # c = 32: the second (pad) slab is zero
+    # c = 32: the pair's second (pad) slab is zero: per row exactly one 16-byte half is non-zero,
+    # the first half unless bit 2 of q is set
+    half1 = lay[0, 0, 0, q, 16:].any(axis=1)
+    np.testing.assert_array_equal(half1, ((q >> 2) & 1).astype(bool))
+    assert not (lay[0, 0, 0, q, :16].any(axis=1) & half1).any()
