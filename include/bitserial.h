@@ -506,6 +506,67 @@ typedef struct bs_tcd_conv_desc {
 int bs_bitserial_conv2d_nhwc_tcd_group(const bs_tcd_conv_desc* descs, int count, int a_bits, int w_bits,
                                        void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Window layout and the windowed tensor-core conv (reading R26).  The conv's
+ * zero-padded input (padding = value 0, R20) is split into the stride's phases
+ * (py, px) that its taps read, each on a phase grid of hg x wg pixels per image:
+ *   s = stride (stride_h == stride_w, 1 or 2), oh/ow the output extent,
+ *   hg = oh + (kh-1)/s, wg = ow + (kw-1)/s; phase pixel (gy, gx) = padded pixel
+ *   (gy*s + py, gx*s + px); q = (img*hg + gy)*wg + gx; output (oy, ox) with tap (ky, kx)
+ *   reads phase (ky%s, kx%s) at q_out + (ky/s)*wg + kx/s, q_out = (img*hg + oy)*wg + ox.
+ * Layout ("windows"): uint8 [D][nph][cw/2][pstride][32], D = ceil(bits/2), nph = the phases
+ * some tap reads (ascending py*s+px), cw = bs_packed_row_words(c) 32-channel slabs taken in
+ * pairs, pstride = ceil8(n*hg*wg + ceil8(128 + (kh-1)/s*wg + (kw-1)/s + 8)) grid positions (a
+ * zero tail); 32-byte row (d, phase, pair p, q) holds the digit-packed bytes (R24) of channels
+ * [64p, 64p+32) then [64p+32, 64p+64) of the input pixel the position maps to — the two 16-byte
+ * halves exchanged when bit 2 of q is set (the 32-byte shared-memory swizzle the tensor core
+ * reads) — and zeros for padding, grid positions past the image and the tail.
+ * Because a 128-row tile of consecutive grid positions reads every tap's operand from one
+ * contiguous window per (digit, phase, slab), the conv kernel moves the operands with plain
+ * bulk copies and the tensor core reads each tap as a shifted view (no im2col, no gather).
+ * The packing is the timed activation-packing step emitting this layout.
+ * Supported: stride_h == stride_w in {1, 2}; wg <= 128; oc % 4 == 0;
+ * bits in [1,4]; the FP4 exactness bound (BS_ERR_OVERFLOW); BS_ERR_UNSUPPORTED otherwise.
+ */
+int64_t bs_tcw_act_bytes(int n, int h, int w, int c, int kh, int kw, int stride, int pad_h, int pad_w, int bits);
+/* in: uint8 codes [n][h][w][c]; out: the window layout (out_bytes >= bs_tcw_act_bytes); every
+ * byte of it is written (no clearing needed). */
+int bs_digitpack_win(const uint8_t* in, uint8_t* out, int64_t out_bytes, int n, int h, int w, int c, int kh, int kw,
+                     int stride, int pad_h, int pad_w, int bits, int enc, void* stream);
+typedef struct bs_win_pack_desc {
+  const uint8_t* in; /* [n][h][w][c] codes */
+  uint8_t* out;      /* window layout of the conv below */
+  int64_t out_bytes;
+  int n, h, w, c, kh, kw, stride, pad_h, pad_w;
+} bs_win_pack_desc;
+/* Several tensors of one bit width and encoding in ONE launch (the bench step's packing). */
+int bs_digitpack_win_group(const bs_win_pack_desc* descs, int count, int bits, int enc, void* stream);
+/* Window-path weight digits from PACKED OHWI weight planes (bs_bitpack of [oc*kh*kw][c]):
+ * [nblk][cw/2][ceil(w_bits/2)][kh*kw][bn][32] bytes, bn = 64 if oc <= 64 else 128,
+ * nblk = ceil(oc/bn): one 64-channel slab pair of one filter block is contiguous; filter row r's
+ * two 16-byte halves are exchanged when bit 2 of r is set; filters past oc and channels past c
+ * are 0.  Untimed, like the weight packing. */
+int64_t bs_conv2d_tcw_weight_bytes(int oc, int kh, int kw, int c, int w_bits);
+int bs_conv2d_tcw_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                                  uint8_t* w_win, int64_t w_win_bytes, void* stream);
+/* Conv2d NHWC on window-layout activations and window-path weights: one persistent
+ * warp-specialized launch (bulk copies of the windows and weights, tcgen05.mma kind::mxf4 on
+ * shifted shared-memory views, FP32 accumulation in TMEM, F2I, one TMA store per valid output
+ * row segment).  out: int32 [n][oh][ow][oc]. */
+int bs_bitserial_conv2d_nhwc_tcw(const uint8_t* act_win, int a_bits, int a_enc, const uint8_t* w_win, int w_bits,
+                                 int w_enc, int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                 int stride_h, int stride_w, int pad_h, int pad_w, void* stream);
+typedef struct bs_tcw_conv_desc {
+  const uint8_t* act_win; /* bs_digitpack_win */
+  const uint8_t* w_win;   /* bs_conv2d_tcw_prepare_weights */
+  int32_t* out;           /* [n][oh][ow][oc] */
+  int a_enc, w_enc;
+  int n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w;
+} bs_tcw_conv_desc;
+/* Several convolutions of one (a_bits, w_bits) in one launch per 16 (tiles concatenated). */
+int bs_bitserial_conv2d_nhwc_tcw_group(const bs_tcw_conv_desc* descs, int count, int a_bits, int w_bits,
+                                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,6 +34,8 @@ __all__ = [
     "digit_row_bytes", "digitpack", "DigitPackDesc", "digitpack_group", "conv2d_tcd_weight_bytes",
     "dense_tcd_weight_bytes", "conv2d_tcd_prepare_weights", "dense_tcd_prepare_weights", "bitserial_conv2d_nhwc_tcd",
     "bitserial_dense_tcd", "TcdConvDesc", "bitserial_conv2d_nhwc_tcd_group",
+    "tcw_act_bytes", "digitpack_win", "WinPackDesc", "digitpack_win_group", "conv2d_tcw_weight_bytes",
+    "conv2d_tcw_prepare_weights", "bitserial_conv2d_nhwc_tcw", "TcwConvDesc", "bitserial_conv2d_nhwc_tcw_group",
 ]
 
 UNIPOLAR, BIPOLAR, SIGNED = 0, 1, 2          # weight encodings (bs_encoding)
@@ -70,7 +72,9 @@ EXPORTED_SYMBOLS = (
     "bs_bitserial_dense_tc_prepared_multicast", "bs_digit_row_bytes", "bs_digitpack", "bs_digitpack_group",
     "bs_conv2d_tcd_weight_bytes", "bs_dense_tcd_weight_bytes", "bs_conv2d_tcd_prepare_weights",
     "bs_dense_tcd_prepare_weights", "bs_bitserial_conv2d_nhwc_tcd", "bs_bitserial_dense_tcd",
-    "bs_bitserial_conv2d_nhwc_tcd_group",
+    "bs_bitserial_conv2d_nhwc_tcd_group", "bs_tcw_act_bytes", "bs_digitpack_win", "bs_digitpack_win_group",
+    "bs_conv2d_tcw_weight_bytes", "bs_conv2d_tcw_prepare_weights", "bs_bitserial_conv2d_nhwc_tcw",
+    "bs_bitserial_conv2d_nhwc_tcw_group",
 )
 
 
@@ -140,6 +144,13 @@ def _load():
         "bs_bitserial_conv2d_nhwc_tcd": ([P, I, I, P, I, I, P] + [I] * 11 + [P], I),
         "bs_bitserial_dense_tcd": ([P, I, I, P, I, I, P, L, L, L, P], I),
         "bs_bitserial_conv2d_nhwc_tcd_group": ([P, I, I, I, P], I),
+        "bs_tcw_act_bytes": ([I] * 10, L),
+        "bs_digitpack_win": ([P, P, L] + [I] * 11 + [P], I),
+        "bs_digitpack_win_group": ([P, I, I, I, P], I),
+        "bs_conv2d_tcw_weight_bytes": ([I, I, I, I, I], L),
+        "bs_conv2d_tcw_prepare_weights": ([P, I, I, I, I, I, I, P, L, P], I),
+        "bs_bitserial_conv2d_nhwc_tcw": ([P, I, I, P, I, I, P] + [I] * 11 + [P], I),
+        "bs_bitserial_conv2d_nhwc_tcw_group": ([P, I, I, I, P], I),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("BITSERIAL_LIB") and not hasattr(lib, name):
@@ -725,5 +736,115 @@ def bitserial_conv2d_nhwc_tcd_group(convs, a_bits, w_bits, stream=None):
         d.stride_h, d.stride_w, d.pad_h, d.pad_w = sh, sw, ph, pw
         outs.append(out)
     _check(_load().bs_bitserial_conv2d_nhwc_tcd_group(ctypes.cast(descs, ctypes.c_void_p), len(convs), a_bits, w_bits,
+                                                      _stream(stream)))
+    return outs
+
+
+# ---------------------------------------------------------------- window path (R26)
+def tcw_act_bytes(n, h, w, c, kh, kw, stride, pad, bits) -> int:
+    """bs_tcw_act_bytes: bytes of the window layout of an [n][h][w][c] input for this conv
+    geometry (0 outside the layout's domain)."""
+    ph, pw = (pad, pad) if isinstance(pad, int) else pad
+    return int(_load().bs_tcw_act_bytes(n, h, w, c, kh, kw, int(stride), ph, pw, bits))
+
+
+def digitpack_win(x: torch.Tensor, bits: int, kh: int, kw: int, stride: int = 1, pad=0, enc: int = A_UNSIGNED,
+                  out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """bs_digitpack_win: uint8 NHWC codes [n][h][w][c] -> the window layout of the conv
+    (kh x kw, stride, pad) as a flat uint8 tensor of bs_tcw_act_bytes bytes."""
+    n, h, w, c = x.shape
+    ph, pw = (pad, pad) if isinstance(pad, int) else pad
+    nbytes = tcw_act_bytes(n, h, w, c, kh, kw, stride, (ph, pw), bits)
+    if out is None:
+        out = torch.empty(max(16, nbytes), dtype=torch.uint8, device=x.device)
+    _check(_load().bs_digitpack_win(_dev(x, "x", torch.uint8), _dev(out, "out", torch.uint8), out.numel(), n, h, w, c,
+                                    kh, kw, int(stride), ph, pw, bits, int(enc), _stream(stream)))
+    return out
+
+
+class WinPackDesc(ctypes.Structure):
+    """bs_win_pack_desc (include/bitserial.h): one member of a grouped window-layout pack."""
+    _fields_ = [("in_", ctypes.c_void_p), ("out", ctypes.c_void_p), ("out_bytes", ctypes.c_int64)] + \
+        [(f, ctypes.c_int) for f in ("n", "h", "w", "c", "kh", "kw", "stride", "pad_h", "pad_w")]
+
+
+def digitpack_win_group(items, bits, enc=A_UNSIGNED, outs=None, stream=None):
+    """bs_digitpack_win_group: window-pack several NHWC tensors in one launch.  `items`:
+    dicts with x, kh, kw and optional stride, pad.  Returns the flat layouts in order."""
+    descs = (WinPackDesc * max(len(items), 1))()
+    res = []
+    for i, it in enumerate(items):
+        x = it["x"]
+        n, h, w, c = x.shape
+        st = int(it.get("stride", 1))
+        pad = it.get("pad", 0)
+        ph, pw = (pad, pad) if isinstance(pad, int) else pad
+        nbytes = tcw_act_bytes(n, h, w, c, it["kh"], it["kw"], st, (ph, pw), bits)
+        out = outs[i] if outs is not None else torch.empty(max(16, nbytes), dtype=torch.uint8, device=x.device)
+        d = descs[i]
+        d.in_ = _dev(x, "x", torch.uint8).value
+        d.out = _dev(out, "out", torch.uint8).value
+        d.out_bytes = out.numel()
+        d.n, d.h, d.w, d.c, d.kh, d.kw, d.stride, d.pad_h, d.pad_w = n, h, w, c, it["kh"], it["kw"], st, ph, pw
+        res.append(out)
+    _check(_load().bs_digitpack_win_group(ctypes.cast(descs, ctypes.c_void_p), len(items), bits, int(enc),
+                                          _stream(stream)))
+    return res
+
+
+def conv2d_tcw_weight_bytes(oc, kh, kw, c, w_bits) -> int:
+    return int(_load().bs_conv2d_tcw_weight_bytes(oc, kh, kw, c, w_bits))
+
+
+def conv2d_tcw_prepare_weights(w_packed, w_bits, w_enc, oc, kh, kw, c, out=None, stream=None):
+    """bs_conv2d_tcw_prepare_weights: packed OHWI weight planes -> window-path weight digits."""
+    if out is None:
+        out = torch.empty(max(16, conv2d_tcw_weight_bytes(oc, kh, kw, c, w_bits)), dtype=torch.uint8,
+                          device=w_packed.device)
+    _check(_load().bs_conv2d_tcw_prepare_weights(_dev(w_packed, "w_packed", torch.int32), w_bits, int(w_enc), oc, kh,
+                                                 kw, c, _dev(out, "w_win", torch.uint8), out.numel(), _stream(stream)))
+    return out
+
+
+def bitserial_conv2d_nhwc_tcw(act_win, a_bits, w_win, w_bits, n, h, w, c, oc, kh, kw, stride=1, pad=0, out=None,
+                              a_enc=A_UNSIGNED, w_enc=UNIPOLAR, stream=None):
+    """bs_bitserial_conv2d_nhwc_tcw: window-layout activations x window-path weights -> int32 NHWC."""
+    sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, stride, pad)
+    if out is None:
+        out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=act_win.device)
+    _check(_load().bs_bitserial_conv2d_nhwc_tcw(
+        _dev(act_win, "act_win", torch.uint8), a_bits, int(a_enc), _dev(w_win, "w_win", torch.uint8), w_bits,
+        int(w_enc), _dev(out, "out", torch.int32), n, h, w, c, oc, kh, kw, sh, sw, ph, pw, _stream(stream)))
+    return out
+
+
+class TcwConvDesc(ctypes.Structure):
+    """bs_tcw_conv_desc (include/bitserial.h): one member of a grouped window-path launch."""
+    _fields_ = [("act_win", ctypes.c_void_p), ("w_win", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("a_enc", ctypes.c_int), ("w_enc", ctypes.c_int)] + \
+        [(f, ctypes.c_int) for f in ("n", "h", "w", "c", "oc", "kh", "kw", "stride_h", "stride_w", "pad_h", "pad_w")]
+
+
+def bitserial_conv2d_nhwc_tcw_group(convs, a_bits, w_bits, stream=None):
+    """bs_bitserial_conv2d_nhwc_tcw_group: several window-path convolutions of one precision in
+    one launch.  `convs`: dicts with act_win, w_win, n, h, w, c, oc, kh, kw and optional stride,
+    pad, out, a_enc, w_enc.  Returns the outputs in order."""
+    descs = (TcwConvDesc * max(len(convs), 1))()
+    outs = []
+    for i, cv in enumerate(convs):
+        n, h, w, c, oc, kh, kw = (cv[k] for k in ("n", "h", "w", "c", "oc", "kh", "kw"))
+        sh, sw, ph, pw, oh, ow = _conv_geom(n, h, w, kh, kw, cv.get("stride", 1), cv.get("pad", 0))
+        out = cv.get("out")
+        if out is None:
+            out = torch.empty((n, max(oh, 0), max(ow, 0), oc), dtype=torch.int32, device=cv["act_win"].device)
+        d = descs[i]
+        d.act_win = _dev(cv["act_win"], "act_win", torch.uint8).value
+        d.w_win = _dev(cv["w_win"], "w_win", torch.uint8).value
+        d.out = _dev(out, "out", torch.int32).value
+        d.a_enc, d.w_enc = int(cv.get("a_enc", A_UNSIGNED)), int(cv.get("w_enc", UNIPOLAR))
+        d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw = n, h, w, c, oc, kh, kw
+        d.stride_h, d.stride_w, d.pad_h, d.pad_w = sh, sw, ph, pw
+        outs.append(out)
+    _check(_load().bs_bitserial_conv2d_nhwc_tcw_group(ctypes.cast(descs, ctypes.c_void_p), len(convs), a_bits, w_bits,
                                                       _stream(stream)))
     return outs

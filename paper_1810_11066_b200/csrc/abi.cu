@@ -275,6 +275,36 @@ bs::TcdProblem make_tcd(const uint8_t* act, const uint8_t* wdig, int32_t* out, i
   return p;
 }
 
+// ---- window path (digit.cu, tcw_conv.cu)
+int check_tcw_geom(const ConvArgs& g, int oc, bs::TcwGeom& G, const char* fn) {
+  if (!bs::tcw_geom(g.n, g.h, g.w, g.c, oc, g.kh, g.kw, g.sh, g.sw, g.ph, g.pw, G))
+    return fail(BS_ERR_UNSUPPORTED,
+                "%s: the window layout needs stride_h == stride_w in {1,2} and output rows of at most 128 grid "
+                "positions", fn);
+  return BS_OK;
+}
+
+int check_tcw_conv(const ConvArgs& g, int a_bits, int w_bits, int a_enc, int w_enc, const char* fn) {
+  if (int st = check_tc_enc(a_enc, w_enc, BS_TC_F4, fn)) return st;
+  if (int st = check_conv(g, a_bits, w_bits, BS_UNIPOLAR, fn)) return st;
+  if (int st = check_tc_bound(int64_t(g.kh) * g.kw * g.c, a_bits, w_bits, BS_TC_F4, fn, a_enc, w_enc)) return st;
+  if (!bs::tc_supported(a_bits, w_bits)) return fail(BS_ERR_UNSUPPORTED, "%s: a_bits in [1,4], w_bits in [1,4]", fn);
+  bs::TcwGeom G;
+  if (int st = check_tcw_geom(g, g.oc, G, fn)) return st;
+  if (g.oc % 4 != 0) return fail(BS_ERR_UNSUPPORTED, "%s: oc must be a multiple of 4", fn);
+  return BS_OK;
+}
+
+bs::TcwProblem make_tcw(const uint8_t* act, const uint8_t* wt, int32_t* out, int a_bits, int w_bits,
+                        const ConvArgs& g) {
+  bs::TcwProblem p{};
+  p.act = act; p.wt = wt; p.out = out;
+  p.n = g.n; p.h = g.h; p.w = g.w; p.c = g.c; p.oc = g.oc; p.kh = g.kh; p.kw = g.kw;
+  p.sh = g.sh; p.sw = g.sw; p.ph = g.ph; p.pw = g.pw;
+  p.a_digits = (a_bits + 1) / 2; p.w_digits = (w_bits + 1) / 2;
+  return p;
+}
+
 }  // namespace
 
 extern "C" {
@@ -968,6 +998,108 @@ int bs_bitserial_dense_tcd(const uint8_t* a_dig, int a_bits, int a_enc, const ui
   bs::TcdProblem p = make_tcd(a_dig, w_dig, out, a_bits, w_bits, g);
   p.dense = 1;
   return cuda_status(bs::launch_tcd_group(&p, 1, static_cast<cudaStream_t>(stream)), fn);
+}
+
+// ------------------------------------------------------------------ window path
+int64_t bs_tcw_act_bytes(int n, int h, int w, int c, int kh, int kw, int stride, int pad_h, int pad_w, int bits) {
+  bs::TcwGeom G;
+  if (bits < 1 || bits > 4 || pad_h < 0 || pad_w < 0 ||
+      !bs::tcw_geom(n, h, w, c, 1, kh, kw, stride, stride, pad_h, pad_w, G))
+    return 0;
+  return int64_t((bits + 1) / 2) * G.digit_bytes;
+}
+
+int bs_digitpack_win_group(const bs_win_pack_desc* descs, int count, int bits, int enc, void* stream) {
+  const char* fn = "bs_digitpack_win_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  if (bits < 1 || bits > 4) return fail(BS_ERR_INVALID_ARG, "%s: bits=%d not in [1,4]", fn, bits);
+  if (enc < BS_A_UNSIGNED || enc > BS_A_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad encoding %d", fn, enc);
+  std::vector<bs::WinSeg> segs(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_win_pack_desc& d = descs[q];
+    if (!d.in || !d.out) return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    const ConvArgs g{d.n, d.h, d.w, d.c, 1, d.kh, d.kw, d.stride, d.stride, d.pad_h, d.pad_w};
+    if (int st = check_conv(g, 1, 1, BS_UNIPOLAR, fn)) return st;
+    bs::TcwGeom G;
+    if (int st = check_tcw_geom(g, 1, G, fn)) return st;
+    const int64_t need = int64_t((bits + 1) / 2) * G.digit_bytes;
+    if (d.out_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: descriptor %d: out needs %lld bytes", fn, q,
+                                        (long long)need);
+    if (!aligned16(d.out)) return fail(BS_ERR_ALIGN, "%s: descriptor %d: out must be 16-byte aligned", fn, q);
+    bs::WinSeg s{};
+    s.in = d.in;
+    s.out = d.out;
+    s.n = d.n; s.h = d.h; s.w = d.w; s.c = d.c; s.kh = d.kh; s.kw = d.kw; s.s = d.stride;
+    s.ph = d.pad_h; s.pw = d.pad_w;
+    segs[q] = s;
+  }
+  return cuda_status(bs::launch_digitpack_win_group(segs.data(), count, bits, enc, static_cast<cudaStream_t>(stream)),
+                     fn);
+}
+
+int bs_digitpack_win(const uint8_t* in, uint8_t* out, int64_t out_bytes, int n, int h, int w, int c, int kh, int kw,
+                     int stride, int pad_h, int pad_w, int bits, int enc, void* stream) {
+  const bs_win_pack_desc d{in, out, out_bytes, n, h, w, c, kh, kw, stride, pad_h, pad_w};
+  const int st = bs_digitpack_win_group(&d, 1, bits, enc, stream);
+  if (st != BS_OK) {
+    char tmp[512];
+    snprintf(tmp, sizeof(tmp), "%s", g_last_error);
+    const char* rest = strncmp(tmp, "bs_digitpack_win_group", 22) == 0 ? tmp + 22 : tmp;
+    fail(st, "bs_digitpack_win%s", rest);
+  }
+  return st;
+}
+
+int64_t bs_conv2d_tcw_weight_bytes(int oc, int kh, int kw, int c, int w_bits) {
+  return bs::tcw_weight_bytes(oc, kh, kw, c, w_bits);
+}
+
+int bs_conv2d_tcw_prepare_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                                  uint8_t* w_win, int64_t w_win_bytes, void* stream) {
+  const char* fn = "bs_conv2d_tcw_prepare_weights";
+  if (!w_packed || !w_win) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (w_bits < 1 || w_bits > 4) return fail(BS_ERR_UNSUPPORTED, "%s: w_bits=%d not in [1,4]", fn, w_bits);
+  if (w_enc < BS_UNIPOLAR || w_enc > BS_SIGNED) return fail(BS_ERR_INVALID_ARG, "%s: bad w_enc %d", fn, w_enc);
+  if (oc <= 0 || kh <= 0 || kw <= 0 || c <= 0) return fail(BS_ERR_SHAPE, "%s: non-positive extent", fn);
+  const int64_t need = bs_conv2d_tcw_weight_bytes(oc, kh, kw, c, w_bits);
+  if (w_win_bytes < need) return fail(BS_ERR_WORKSPACE, "%s: w_win needs %lld bytes", fn, (long long)need);
+  if (!aligned16(w_packed) || !aligned16(w_win)) return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  return cuda_status(bs::launch_tcw_weights(w_packed, w_bits, w_enc, oc, kh, kw, c, w_win,
+                                            static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tcw_group(const bs_tcw_conv_desc* descs, int count, int a_bits, int w_bits,
+                                       void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tcw_group";
+  if (count < 0 || count > (1 << 20)) return fail(BS_ERR_SHAPE, "%s: count out of range", fn);
+  if (count == 0) return BS_OK;
+  if (!descs) return fail(BS_ERR_NULL, "%s: NULL descriptor array", fn);
+  std::vector<bs::TcwProblem> ps(static_cast<size_t>(count));
+  for (int q = 0; q < count; ++q) {
+    const bs_tcw_conv_desc& d = descs[q];
+    const ConvArgs g{d.n, d.h, d.w, d.c, d.oc, d.kh, d.kw, d.stride_h, d.stride_w, d.pad_h, d.pad_w};
+    if (int st = check_tcw_conv(g, a_bits, w_bits, d.a_enc, d.w_enc, fn)) return st;
+    if (!d.act_win || !d.w_win || !d.out) return fail(BS_ERR_NULL, "%s: NULL pointer in descriptor %d", fn, q);
+    if (!aligned16(d.act_win) || !aligned16(d.w_win) || !aligned16(d.out))
+      return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
+    ps[q] = make_tcw(d.act_win, d.w_win, d.out, a_bits, w_bits, g);
+  }
+  return cuda_status(bs::launch_tcw_group(ps.data(), count, static_cast<cudaStream_t>(stream)), fn);
+}
+
+int bs_bitserial_conv2d_nhwc_tcw(const uint8_t* act_win, int a_bits, int a_enc, const uint8_t* w_win, int w_bits,
+                                 int w_enc, int32_t* out, int n, int h, int w, int c, int oc, int kh, int kw,
+                                 int stride_h, int stride_w, int pad_h, int pad_w, void* stream) {
+  const char* fn = "bs_bitserial_conv2d_nhwc_tcw";
+  const ConvArgs g{n, h, w, c, oc, kh, kw, stride_h, stride_w, pad_h, pad_w};
+  if (int st = check_tcw_conv(g, a_bits, w_bits, a_enc, w_enc, fn)) return st;
+  if (!act_win || !w_win || !out) return fail(BS_ERR_NULL, "%s: NULL pointer", fn);
+  if (!aligned16(act_win) || !aligned16(w_win) || !aligned16(out))
+    return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
+  const bs::TcwProblem p = make_tcw(act_win, w_win, out, a_bits, w_bits, g);
+  return cuda_status(bs::launch_tcw_group(&p, 1, static_cast<cudaStream_t>(stream)), fn);
 }
 
 }  // extern "C"

@@ -78,4 +78,21 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 __device__ __forceinline__ uint4 lds128p(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 __device__ __forceinline__ uint2 lds64p(const uint32_t* p) { return *reinterpret_cast<const uint2*>(p); }
 
+// n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method):
+// q = (umulhi(n, mul) + n) >> shr, shr = ceil(log2 d), mul = floor(2^32 (2^shr - d) / d) + 1.
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shr; }
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  if (d > 1) {
+    uint32_t p = 0;
+    while ((uint64_t(1) << p) < d) ++p;
+    f.shr = p;
+    f.mul = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << p) - d)) / d + 1);
+  }
+  return f;
+}
+
 }  // namespace bs

@@ -209,6 +209,154 @@ cudaError_t launch_digitpack_group(const DigitSeg* segs, int count, int bits, in
   return cudaSuccess;
 }
 
+// ------------------------------------------------------------------ window layout (R26)
+// One task = one 16-byte half of a 32-byte row (one 32-channel slab, all digits) of the window
+// layout [D][nph][cw/2][pstride][32]: task index lt = ((slot * pairs + pair) * pstride + q) * 2 + j,
+// so consecutive threads write consecutive 16-byte pieces (coalesced) and read the 32-channel
+// halves of consecutive phase-grid pixels.  Half j of row q lands in position j ^ (bit 2 of q)
+// (the 32-byte shared-memory swizzle).  Padding, grid positions past the image and the tail are
+// written as 0 (value 0 in every encoding, R20) on every call: no separate clearing.
+namespace {
+template <int BITS>
+__global__ void __launch_bounds__(256) digitpack_win_kernel(const __grid_constant__ WinPackArgs a) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int s = 0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < a.tasks; t += stride) {
+    while (s + 1 < a.nseg && t >= a.seg[s + 1].task0) ++s;
+    const WinSeg& g = a.seg[s];
+    const uint32_t lt = uint32_t(t - g.task0);
+    const uint32_t j = lt & 1u, row = lt >> 1;  // row = (slot * pairs + pair) * pstride + q
+    const uint32_t fp = g.div_ps.div(row);
+    const uint32_t q = row - fp * g.div_ps.d;
+    const uint32_t f = g.div_pairs.div(fp), cs = 2 * (fp - f * g.div_pairs.d) + j;
+    bool ok = int64_t(q) < g.gpix && int64_t(cs) * 32 < g.c;
+    int64_t pix = 0;
+    if (ok) {
+      const uint32_t img = g.div_img.div(q), rem = q - img * g.div_img.d;
+      const uint32_t gy = g.div_wg.div(rem), gx = rem - gy * g.div_wg.d;
+      const int y = int(gy) * g.s + g.py[f] - g.ph, x = int(gx) * g.s + g.px[f] - g.pw;
+      ok = unsigned(y) < unsigned(g.h) && unsigned(x) < unsigned(g.w);
+      pix = (int64_t(img) * g.h + y) * g.w + x;
+    }
+    uint8_t* dst = g.out + int64_t(row) * 32 + ((j ^ ((q >> 2) & 1u)) << 4);
+    if (!ok) {
+#pragma unroll
+      for (int d = 0; 2 * d < BITS; ++d) *reinterpret_cast<uint4*>(dst + d * g.dstride) = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    uint32_t v[8];
+    load32(g.in, pix, cs, g.c, g.aligned16, v);
+    const int64_t left = g.c - 32 * int64_t(cs);
+    store_digits<0, BITS>(dst, g.dstride, v, g.lut, g.ident, left >= 32 ? 32 : int(left));
+  }
+}
+}  // namespace
+
+cudaError_t launch_digitpack_win_group(const WinSeg* segs, int count, int bits, int enc, cudaStream_t stream) {
+  for (int q0 = 0; q0 < count; q0 += kPackGroupMax) {
+    WinPackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.nseg = count - q0 < kPackGroupMax ? count - q0 : kPackGroupMax;
+    int64_t tasks = 0;
+    for (int q = 0; q < a.nseg; ++q) {
+      WinSeg g = segs[q0 + q];
+      TcwGeom G;
+      if (!tcw_geom(g.n, g.h, g.w, g.c, 1, g.kh, g.kw, g.s, g.s, g.ph, g.pw, G)) return cudaErrorNotSupported;
+      g.hg = G.hg;
+      g.wg = G.wg;
+      g.cw = G.cw;
+      g.gpix = G.gpix;
+      g.dstride = G.digit_bytes;
+      for (int f = 0; f < 4; ++f) {
+        g.py[f] = f < G.nph ? G.phase[f] / G.s : 0;
+        g.px[f] = f < G.nph ? G.phase[f] % G.s : 0;
+      }
+      g.tasks = int64_t(G.nph) * G.cw * G.pstride;
+      g.task0 = tasks;
+      g.div_ps = make_fastdiv(uint32_t(G.pstride));
+      g.div_pairs = make_fastdiv(uint32_t(G.cw / 2));
+      g.div_img = make_fastdiv(uint32_t(G.hg) * uint32_t(G.wg));
+      g.div_wg = make_fastdiv(uint32_t(G.wg));
+      g.aligned16 = (reinterpret_cast<uintptr_t>(g.in) % 16 == 0) && (g.c % 16 == 0);
+      g.lut[0] = digit_lut(bits, enc, 0);
+      g.lut[1] = digit_lut(bits, enc, 1);
+      g.ident = enc == 0;
+      tasks += g.tasks;
+      a.seg[q] = g;
+    }
+    a.tasks = tasks;
+    int64_t blocks = (tasks + 255) / 256;
+    const int64_t max_blocks = int64_t(device_sms()) * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) continue;
+    switch (bits) {
+      case 1: digitpack_win_kernel<1><<<blocks, 256, 0, stream>>>(a); break;
+      case 2: digitpack_win_kernel<2><<<blocks, 256, 0, stream>>>(a); break;
+      case 3: digitpack_win_kernel<3><<<blocks, 256, 0, stream>>>(a); break;
+      default: digitpack_win_kernel<4><<<blocks, 256, 0, stream>>>(a); break;
+    }
+    note_launch();
+    if (cudaError_t e = cudaPeekAtLastError()) return e;
+  }
+  return cudaSuccess;
+}
+
+// Window-path weight digits [nblk][cw/2][Dw][taps][bn][32] from packed planes [W][oc][taps*cw]
+// (the stage's weights of one 64-channel slab pair are one contiguous block: one bulk copy);
+// half j of filter row r lands in position j ^ (bit 2 of r) (the 32-byte smem swizzle);
+// filters past oc and channels past c are 0.
+namespace {
+__global__ void tcw_weight_kernel(const uint32_t* __restrict__ wp, int w_bits, int oc, int taps, int cw, int c, int bn,
+                                  int nblk, uint32_t lut0, uint32_t lut1, uint8_t* __restrict__ out) {
+  const int P = (w_bits + 1) / 2, pairs = cw / 2;
+  const int64_t total = int64_t(nblk) * pairs * P * taps * bn * 2;
+  const int64_t kp = int64_t(taps) * cw;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t x = idx;
+    const int j = int(x % 2);
+    x /= 2;
+    const int r = int(x % bn);
+    const int64_t rowi = x;  // ((((nb * pairs + p) * P + e) * taps + t) * bn + r)
+    x /= bn;
+    const int t = int(x % taps);
+    x /= taps;
+    const int e = int(x % P);
+    x /= P;
+    const int p = int(x % pairs);
+    const int nb = int(x / pairs);
+    const int o = nb * bn + r, cs = 2 * p + j;
+    uint32_t w4[4] = {0u, 0u, 0u, 0u};
+    if (o < oc) {
+      const int64_t rk = int64_t(o) * kp + int64_t(t) * cw + cs;
+      const bool has_hi = 2 * e + 1 < w_bits;
+      const uint32_t lo = wp[int64_t(2 * e) * oc * kp + rk];
+      const uint32_t hi = has_hi ? wp[int64_t(2 * e + 1) * oc * kp + rk] : 0u;
+      const uint32_t lut = e == 0 ? lut0 : lut1;
+      for (int b = 0; b < 32; ++b) {
+        if (cs * 32 + b >= c) break;  // channel padding: value 0
+        const uint32_t cc = ((lo >> b) & 1u) | (((hi >> b) & 1u) << 1);
+        w4[b >> 3] |= ((lut >> (8 * cc)) & 0xFu) << (4 * (b & 7));
+      }
+    }
+    *reinterpret_cast<uint4*>(out + rowi * 32 + ((j ^ ((r >> 2) & 1)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+}  // namespace
+
+cudaError_t launch_tcw_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                               uint8_t* out, cudaStream_t stream) {
+  const int64_t bytes = tcw_weight_bytes(oc, kh, kw, c, w_bits);
+  if (bytes <= 0) return cudaErrorInvalidValue;
+  const int cw = int(digit_row_bytes(c) / 16), bn = oc <= 64 ? 64 : 128;
+  int64_t blocks = (bytes / 16 + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  tcw_weight_kernel<<<blocks, 256, 0, stream>>>(w_packed, w_bits, oc, kh * kw, cw, c, bn, (oc + bn - 1) / bn,
+                                                digit_lut(w_bits, w_enc, 0), digit_lut(w_bits, w_enc, 1), out);
+  note_launch();
+  return cudaPeekAtLastError();
+}
+
 // ------------------------------------------------------------------ weight digits
 // Packed weight planes [W][n][kp] words (filter rows of `taps` taps of kw_tap words, c_tap
 // elements per tap) -> digit rows [P][n][tcd_wrow_bytes(kp)] bytes, P = ceil(W/2), in the same

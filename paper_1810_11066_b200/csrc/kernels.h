@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace bs {
 
 // Implicit-GEMM problem.  A dense product is the 1x1 convolution of M "pixels"
@@ -149,6 +151,55 @@ struct TcdProblem {
   int dense;  // 1: tiled 2-D operand map over [DA*n][row_bytes] (no im2col)
 };
 cudaError_t launch_tcd_group(const TcdProblem* ps, int count, cudaStream_t stream);
+
+// ---- window layout and the windowed tensor-core conv (digit.cu, tcw_conv.cu; R26)
+// The conv's zero-padded input split into its stride phases on a phase grid of hg x wg pixels
+// per image; per (digit, phase slot, 32-channel slab) one contiguous array of pstride pixels x
+// 16 bytes (digit-packed, R24).  Output (oy, ox) with tap (ky, kx) reads phase
+// (ky % s, kx % s) at grid position q_out + (ky / s) * wg + kx / s, q_out = (img*hg + oy)*wg + ox,
+// so a 128-row tile of consecutive grid positions reads every tap's A operand from ONE
+// contiguous window per (phase, slab): a shifted shared-memory view, no gather.
+constexpr int kTcwBM = 128;
+struct TcwGeom {
+  int s, oh, ow, hg, wg, nph, cw, taps, maxoff, lwin, R, ow8, bn, nblk;
+  int phase[4];    // slot -> phase py*s + px
+  int slot_of[4];  // phase -> slot (-1: not stored)
+  int64_t gpix, pstride, digit_bytes;  // digit_bytes = nph * cw * pstride * 16
+};
+// false: outside the windowed kernel's domain (sh != sw, stride > 2, grid rows wider than a
+// 128-row tile, 32-bit index limits)
+bool tcw_geom(int n, int h, int w, int c, int oc, int kh, int kw, int sh, int sw, int ph, int pw, TcwGeom& g);
+// prepared weights [nblk][cw/2][Dw][kh*kw][bn][32] bytes (bn = 64 if oc <= 64 else 128), rows
+// with bit 2 set hold their 16-byte halves exchanged (the 32-byte smem swizzle)
+int64_t tcw_weight_bytes(int oc, int kh, int kw, int c, int w_bits);
+struct WinSeg {
+  const uint8_t* in;  // [n][h][w][c] codes
+  uint8_t* out;       // [D][nph][cw/2][pstride][32], halves exchanged on rows with bit 2 set
+  int n, h, w, c, kh, kw, s, ph, pw;
+  // set by the launcher
+  int64_t task0, tasks, dstride;
+  int hg, wg, cw, aligned16, ident;
+  int py[4], px[4];
+  int64_t gpix;
+  FastDiv div_ps, div_pairs, div_img, div_wg;
+  uint32_t lut[2];
+};
+struct WinPackArgs {
+  int nseg;
+  int64_t tasks;
+  WinSeg seg[kPackGroupMax];
+};
+cudaError_t launch_digitpack_win_group(const WinSeg* segs, int count, int bits, int enc, cudaStream_t stream);
+cudaError_t launch_tcw_weights(const uint32_t* w_packed, int w_bits, int w_enc, int oc, int kh, int kw, int c,
+                               uint8_t* out, cudaStream_t stream);
+struct TcwProblem {
+  const uint8_t* act;  // window layout (launch_digitpack_win_group)
+  const uint8_t* wt;   // launch_tcw_weights
+  int32_t* out;        // int32 [n][oh][ow][oc]
+  int n, h, w, c, oc, kh, kw, sh, sw, ph, pw;
+  int a_digits, w_digits;
+};
+cudaError_t launch_tcw_group(const TcwProblem* ps, int count, cudaStream_t stream);
 
 // Matrix-vector kernel for m <= 8 dense products.
 //   a_packed : packed [a_bits][m][kwp] (or nullptr when a_codes is given)

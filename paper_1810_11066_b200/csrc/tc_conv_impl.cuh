@@ -611,22 +611,8 @@ __device__ __forceinline__ void multimem_st_v4(int32_t* p, uint4 v) {
                : "memory");
 }
 
-// n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method):
-// q = (umulhi(n, mul) + n) >> shr, shr = ceil(log2 d), mul = floor(2^32 (2^shr - d) / d) + 1.
-struct FastDiv {
-  uint32_t d, mul, shr;
-  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shr; }
-};
-inline FastDiv make_fastdiv(uint32_t d) {
-  FastDiv f{d, 0, 0};
-  if (d > 1) {
-    uint32_t p = 0;
-    while ((uint64_t(1) << p) < d) ++p;
-    f.shr = p;
-    f.mul = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << p) - d)) / d + 1);
-  }
-  return f;
-}
+using bs::FastDiv;  // (common.cuh)
+using bs::make_fastdiv;
 
 // One problem of a launch (a single conv / dense, or one member of a group).
 struct TcProb {

@@ -1,0 +1,6 @@
+timeout 600 python -m pytest tests/test_parity_tcw_gpu.py -q --timeout 300 -k "conv_tcw_parity and (2-1 or 4-2) or encodings or group or sentinel" > gpurun_out/w18_pytest.log 2>&1; tail -2 gpurun_out/w18_pytest.log
+for L in 2 12; do
+BITSERIAL_LIB=build/prof/libbitserial.so timeout 120 python tools/tcw_one.py --layers $L --iters 1 > gpurun_out/w18_prof_l$L.log 2>&1
+done
+timeout 300 python tools/tcw_probe.py --layers --reps 10 > gpurun_out/w18_base.json 2>&1
+echo done
