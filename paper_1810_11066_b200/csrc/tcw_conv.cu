@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = tid; i < args.nprob * kWords; i += kThreads) dst[i] = src[i];
   }
 #ifdef BS_TCW_PROFILE
-  long long pw_empty = 0, pm_acc = 0, pm_full = 0, pe_acc = 0, pe_bar = 0, pm_issue = 0, pm_commit = 0, pe_ld = 0, pe_cvt = 0, pe_sts = 0, pe_st = 0, pe_wr = 0;
+  long long pw_empty = 0, pm_acc = 0, pm_full = 0, pe_acc = 0, pe_bar = 0, pm_issue = 0, pm_commit = 0, pe_ld = 0, pe_cvt = 0, pe_sts = 0, pe_st = 0, pe_wr = 0, pm_top = 0,
+            pm_loop = 0;
   const long long p_start = clock64();
 #endif
   if (tid == 0) {
@@ -368,7 +369,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0, acc = 0, pi = 0, key = -1;
     uint32_t phase = 0, acc_phase = 0, bfpar = 0;
     const uint32_t sa0 = smem_u32(s_a), sb0 = smem_u32(s_b);
+#ifdef BS_TCW_PROFILE
+    long long t_tile = clock64();
+#endif
     for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
+#ifdef BS_TCW_PROFILE
+      pm_loop += clock64() - t_tile;  // previous tile's tail (acc commit, next-tile check, loop)
+      const long long t_top = clock64();
+#endif
       next_prob(tile, pi);
       const TwProb& P = sprob[pi];
       uint32_t mb, nb;
@@ -391,6 +399,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool bres = P.b_res;
       const uint32_t bslot = P.bslot;
       const uint32_t delta = uint32_t(int64_t(mb) * P.R * P.wg) & 7u;  // tile start inside the window's first 8 rows
+#ifdef BS_TCW_PROFILE
+      pm_top += clock64() - t_top;
+#endif
       { PROF_T0();
       spin_wait(smem_u32(acc_empty + acc), acc_phase ^ 1u);
       PROF_ADD(pm_acc); }
@@ -451,6 +462,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1u;
         }
       }
+#ifdef BS_TCW_PROFILE
+      t_tile = clock64();
+#endif
       tc::mma_commit_elect(smem_u32(acc_full + acc));
       if (++acc == 2) {
         acc = 0;
@@ -580,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (blockIdx.x == 0 && lane == 0) {
     const long long tot = clock64() - p_start;
     if (warp == kTmaWarp) printf("tcw prof: tma   total %lld wait_empty %lld\n", tot, pw_empty);
-    if (warp == kMmaWarp) printf("tcw prof: mma   total %lld wait_full %lld wait_acc %lld issue %lld commit %lld\n", tot, pm_full, pm_acc, pm_issue, pm_commit);
+    if (warp == kMmaWarp) printf("tcw prof: mma   total %lld wait_full %lld wait_acc %lld issue %lld commit %lld top %lld tail %lld\n", tot, pm_full, pm_acc, pm_issue, pm_commit, pm_top, pm_loop);
     if (warp >= kEpiWarp0) printf("tcw prof: epi%d  total %lld wait_acc %lld bar %lld ld %lld cvt %lld sts %lld st %lld wr %lld\n", warp, tot, pe_acc, pe_bar, pe_ld, pe_cvt, pe_sts, pe_st, pe_wr);
   }
 #endif
