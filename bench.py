@@ -222,8 +222,11 @@ class ConvWorkload:
             L = inputs.TABLE1[li]
             act, wt = inputs.conv_operands(L, batch, args.a_bits, args.w_bits,
                                            inputs.seed_for(config_id, args.a_bits, args.w_bits, enc, li))
+            lpath = args.path
+            if args.path == "hybrid":  # window path for the layers it runs faster, expansion kernel for the rest
+                lpath = "tcw" if li in hybrid_tcw_layers(args) else "tc"
             self.runs.append(ConvLayerRun(L, act[lo:hi].contiguous(), wt, args.a_bits, args.w_bits, args.bipolar,
-                                          dev, args.path, tc_fmt(args)))
+                                          dev, lpath, tc_fmt(args)))
         self.total_binops = self.replicas * sum(binops_conv(inputs.TABLE1[li], batch, args.a_bits, args.w_bits)
                                                 for li in layers)
         self.config_id = config_id
@@ -249,7 +252,7 @@ class ConvWorkload:
                                for part in args.group_layers.split("|")]
                 assert sorted(i for grp in self.groups for i in grp) == list(range(len(self.runs)))
             self.group_items = [[self.runs[i].group_item() for i in grp] for grp in self.groups]
-        if args.path in ("tcd", "tcw"):  # one pack launch + one tensor-core conv launch for every layer
+        if args.path in ("tcd", "tcw", "hybrid"):  # few pack + conv launches for every layer
             # every layer's activations and outputs live in one flat device buffer each (views), so the
             # end-to-end step moves its inputs and results with one copy per direction
             na = sum(r.act.numel() for r in self.runs)
@@ -265,26 +268,39 @@ class ConvWorkload:
                 oa += (r.act.numel() + 15) // 16 * 16  # 16-byte aligned views
                 oo += (r.out.numel() + 3) // 4 * 4
             self.tcd_items = [r.tcd_item() for r in self.runs] if args.path == "tcd" else None
-            self.tcw_items = [r.tcw_item() for r in self.runs] if args.path == "tcw" else None
-            self.tcw_pack = [r.tcw_pack_item() for r in self.runs] if args.path == "tcw" else None
+            self.w_runs = [r for r in self.runs if r.path == "tcw"]
+            self.t_runs = [r for r in self.runs if r.path == "tc"]
+            self.tcw_items = [r.tcw_item() for r in self.w_runs]
+            self.tcw_pack = [r.tcw_pack_item() for r in self.w_runs]
+            self.tc_items = [r.group_item() for r in self.t_runs]
+            if args.path == "hybrid":
+                self.hy_streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
         if args.path == "small":  # every layer in ONE launch of the small-problem path (packing fused)
             self.small_items = [dict(act=r.act, w_packed=r.wp, out=r.out, w_enc=r.enc, oc=r.L.oc, kh=r.L.k, kw=r.L.k,
                                      stride=r.L.s, pad=r.L.pad) for r in self.runs]
         self.config = {
             "workload": f"{name}_a{args.a_bits}w{args.w_bits}_{enc}", "global_batch": batch, "layers": list(layers),
+            "window_path_layers": ([r.L.name for r in self.runs if r.path == "tcw"] if args.path == "hybrid" else
+                                   None),
             "layout": "NHWC/OHWI",
             "parallelism": (f"{world} independent replicas (batch 1 does not shard)" if self.replicas > 1 else
                             f"batch-sharded dp{world} (no collective)"),
             "rank0_images": [lo, hi],
             "step": self.describe_step(args),
             "path": args.path,
-            "tc_format": args.tc_format if args.path == "tc" else None,
+            "tc_format": args.tc_format if args.path in ("tc", "hybrid") else None,
             "conv_groups": (args.conv_groups if self.overlap else 0),
             "pack_group": bool(self.overlap and args.pack_group),
             "pack_split": bool(self.overlap and args.pack_group and args.pack_split and self.groups),
         }
 
     def describe_step(self, args):
+        if args.path == "hybrid":
+            return (f"layers {[r.L.name for r in self.runs if r.path == 'tcw']} on the window path (ONE "
+                    "bs_digitpack_win_group + ONE bs_bitserial_conv2d_nhwc_tcw_group launch, own stream) beside layers "
+                    f"{[r.L.name for r in self.runs if r.path == 'tc']} on the expansion kernel (ONE bs_bitpack_group "
+                    "launch on a side stream, then ONE bs_bitserial_conv2d_nhwc_tc_group call); weights packed and "
+                    "prepared once, untimed")
         if args.path == "tcw":
             return ("every layer's activations packed into its conv's window layout (zero-padded stride phases, 32-byte "
                     "swizzled digit rows, DESIGN.md R26) by ONE bs_digitpack_win_group launch, then every layer's conv "
@@ -315,6 +331,22 @@ class ConvWorkload:
         return f"{packs}; {convs} (weights packed + plane-expanded once, untimed)"
 
     def step(self):
+        if self.args.path == "hybrid":
+            bs = self.runs[0].bs
+            main = torch.cuda.current_stream()
+            s_w, s_p = self.hy_streams
+            s_w.wait_stream(main)
+            s_p.wait_stream(main)
+            with torch.cuda.stream(s_w):
+                bs.digitpack_win_group(self.tcw_pack, self.args.a_bits, outs=[r.win for r in self.w_runs])
+                bs.bitserial_conv2d_nhwc_tcw_group(self.tcw_items, self.args.a_bits, self.args.w_bits)
+            with torch.cuda.stream(s_p):
+                bs.bitpack_group([r.act for r in self.t_runs], self.args.a_bits, outs=[r.packed for r in self.t_runs])
+            main.wait_stream(s_p)
+            bs.bitserial_conv2d_nhwc_tc_group(self.tc_items, self.args.a_bits, self.args.w_bits,
+                                              tc_format=tc_fmt(self.args))
+            main.wait_stream(s_w)
+            return
         if self.args.path == "tcw":
             bs = self.runs[0].bs
             bs.digitpack_win_group(self.tcw_pack, self.args.a_bits, outs=[r.win for r in self.runs])
@@ -434,6 +466,36 @@ class ConvWorkload:
                 "ops": ops, "ms": ms, "launches": 1, "bytes": nbytes,
                 "breakdown": {"conv_group_us": 1e3 * ms, "window_pack_group_us": 1e3 * pms}}
 
+    def roofline_hybrid(self, reps):
+        """The hybrid step's two conv calls (the window-path launch and the grouped expansion-kernel
+        call) and two pack launches, each graph-replayed; algorithmic bytes per conv call: packed
+        activations (window layout / bit planes) + prepared weights + int32 outputs."""
+        bs, fmt = self.runs[0].bs, tc_fmt(self.args)
+        wpack = lambda: bs.digitpack_win_group(self.tcw_pack, self.args.a_bits, outs=[r.win for r in self.w_runs])  # noqa
+        tpack = lambda: bs.bitpack_group([r.act for r in self.t_runs], self.args.a_bits,  # noqa
+                                         outs=[r.packed for r in self.t_runs])
+        wconv = lambda: bs.bitserial_conv2d_nhwc_tcw_group(self.tcw_items, self.args.a_bits, self.args.w_bits)  # noqa
+        tconv = lambda: bs.bitserial_conv2d_nhwc_tc_group(self.tc_items, self.args.a_bits, self.args.w_bits,  # noqa
+                                                          tc_format=fmt)
+        wpack()
+        tpack()
+        torch.cuda.synchronize()
+        wms, tms = graph_launch_ms(wconv, reps), graph_launch_ms(tconv, reps)
+        wpms, tpms = graph_launch_ms(wpack, reps), graph_launch_ms(tpack, reps)
+        wbytes = sum(r.win.numel() + r.w_win.numel() + r.out.numel() * 4 for r in self.w_runs)
+        tbytes = sum(r.packed.numel() * 4 + r.w_tc.numel() + r.out.numel() * 4 for r in self.t_runs)
+        per = [{"layers": [r.L.name for r in self.w_runs], "binops": sum(r.binops() for r in self.w_runs),
+                "bytes": wbytes, "ms": wms},
+               {"layers": [r.L.name for r in self.t_runs], "binops": sum(r.binops() for r in self.t_runs),
+                "bytes": tbytes, "ms": tms}]
+        return {"kind": "tensor", "kernel": "the step's conv launches: tcw_conv_kernel (window path, layers "
+                                            f"{per[0]['layers']}) + tc_conv_kernel (expansion kernel, layers "
+                                            f"{per[1]['layers']}), tcgen05 kind::mxf4, rank 0",
+                "ops": per[0]["binops"] + per[1]["binops"], "ms": wms + tms, "launches": 2, "bytes": wbytes + tbytes,
+                "per_layer": per,
+                "breakdown": {"tcw_conv_us": 1e3 * wms, "tc_conv_group_us": 1e3 * tms, "window_pack_us": 1e3 * wpms,
+                              "bitplane_pack_us": 1e3 * tpms}}
+
     def roofline(self, reps):
         """Per-launch device time of the pack and conv kernels of every layer: each
         kernel captured `reps` times back to back in a CUDA graph, timed with events on
@@ -444,6 +506,8 @@ class ConvWorkload:
             return self.roofline_tcd(reps)
         if self.args.path == "tcw":
             return self.roofline_tcw(reps)
+        if self.args.path == "hybrid":
+            return self.roofline_hybrid(reps)
         for r in self.runs:
             r.pack_only()
             r.conv_only()
@@ -507,7 +571,43 @@ class ConvWorkload:
 
             def step():
                 bs.bitserial_conv2d_nhwc_tc_host_group(layers, self.args.a_bits, self.args.w_bits, tc_format=fmt)
-        elif self.args.path in ("tcd", "tcw"):  # one upload of every layer's codes, the two launches, one download
+        elif self.args.path == "hybrid":
+            # the expansion-kernel layers through the pipelined host-buffer call (uploads, pack + conv,
+            # downloads on three streams), the window-path layers beside it on three more streams
+            # (upload -> window pack + conv -> download): both share the PCIe link full duplex
+            t_bufs = [r.host_buffers() for r in self.t_runs]
+            layers = [dict(act_host=b[0], out_host=b[1], act_dev=b[2], packed_dev=r.packed, out_dev=b[3], w_tc=r.w_tc,
+                           oc=r.L.oc, kh=r.L.k, kw=r.L.k, stride=r.L.s, pad=r.L.pad, w_enc=r.enc)
+                      for r, b in zip(self.t_runs, t_bufs)]
+            layers.sort(key=lambda d: d["act_host"].numel())
+            w_host = [(r.act_cpu.contiguous().pin_memory(), torch.empty(r.out.shape, dtype=torch.int32).pin_memory())
+                      for r in self.w_runs]
+            bufs = [(b[0], b[1]) for b in t_bufs] + w_host
+            bs, fmt = self.runs[0].bs, tc_fmt(self.args)
+            su, sc, sd = (torch.cuda.Stream(device=self.dev) for _ in range(3))
+            # per layer, smallest upload first (as the host-group call orders its layers): each
+            # layer's download starts as soon as its own conv is done
+            order = sorted(range(len(self.w_runs)), key=lambda i: self.w_runs[i].act.numel())
+            ev_up = [torch.cuda.Event() for _ in order]
+            ev_c = [torch.cuda.Event() for _ in order]
+
+            def step():
+                for j, i in enumerate(order):
+                    r, (ah, oh_) = self.w_runs[i], w_host[i]
+                    with torch.cuda.stream(su):
+                        r.act.copy_(ah, non_blocking=True)
+                        ev_up[j].record(su)
+                    sc.wait_event(ev_up[j])
+                    with torch.cuda.stream(sc):
+                        bs.digitpack_win_group([self.tcw_pack[i]], self.args.a_bits, outs=[r.win])
+                        bs.bitserial_conv2d_nhwc_tcw_group([self.tcw_items[i]], self.args.a_bits, self.args.w_bits)
+                        ev_c[j].record(sc)
+                    sd.wait_event(ev_c[j])
+                    with torch.cuda.stream(sd):
+                        oh_.copy_(r.out, non_blocking=True)
+                bs.bitserial_conv2d_nhwc_tc_host_group(layers, self.args.a_bits, self.args.w_bits, tc_format=fmt)
+                sd.synchronize()
+        elif self.args.path in ("tcd", "tcw"):  # one upload of every layer's codes, the step, one download
             host_in = self.flat_act.cpu().pin_memory()
             host_out = torch.empty(self.flat_out.shape, dtype=torch.int32).pin_memory()
             bufs = [(host_in, host_out)]
@@ -990,7 +1090,8 @@ def run_ours(args):
                     "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": roof["kernel"],
                     "peak_basis": f"HBM copy bandwidth, {peaks_src}",
                     "binary_tops": roof["ops"] / (roof["ms"] / 1e3) / 1e12}
-    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    # the ncu traffic capture committed for this workload and path (the expansion-kernel step: no suffix)
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}{'' if args.path == 'tc' else '_' + args.path}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             roofline["traffic"] = json.load(f).get("dram_bytes_per_launch_unit")
@@ -1040,8 +1141,16 @@ def run_ours(args):
     return 0
 
 
+def hybrid_tcw_layers(args):
+    return [int(x) for x in args.tcw_layers.split(",") if x]
+
+
 def dtype_of(args, wl):
     """The arithmetic the timed path computes in (not a precision claim)."""
+    if args.path == "hybrid":
+        return ("u8 codes -> window-layout e2m1 digit fields (window-path layers) | packed u32 bit-planes -> radix-4 "
+                "e2m1 digits (expansion-kernel layers), x ue8m0 4^d scales on tcgen05 kind::mxf4 (fp32 accum, exact) "
+                "-> i32")
     if args.path == "tcw":
         return ("u8 codes -> window-layout e2m1 digit fields (two bit-planes per nibble, 0.5 x {0..3}) x ue8m0 4^d "
                 "scales on tcgen05 kind::mxf4 (fp32 accum, exact) -> i32")
@@ -1179,10 +1288,13 @@ def main():
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
-    ap.add_argument("--path", choices=["auto", "tc", "tcd", "tcw", "popc", "small"], default="auto",
+    ap.add_argument("--tcw-layers", default="2,5,8",
+                    help="--path hybrid: the layers on the window path (measured best partition, profiles/r02w_hybrid*)")
+    ap.add_argument("--path", choices=["auto", "tc", "tcd", "tcw", "hybrid", "popc", "small"], default="auto",
                     help="conv/GEMM kernel: tensor-core bitserial (tc), the digit path (tcd), the window path (tcw), the "
-                         "AND/POPC integer-pipe kernel, or the one-launch small-problem path; auto = small for conv1, "
-                         "tcw for resnet1, else tc")
+                         "AND/POPC integer-pipe kernel, the one-launch small-problem path, or hybrid (--tcw-layers on "
+                         "the window path, the rest on tc); auto = small for conv1, tcw for resnet1, hybrid for "
+                         "resnet256, else tc")
     ap.add_argument("--fused-gather", action="store_true",
                     help="gemm, N>1: all-gather fused into the tensor-core epilogue over symmetric memory (SURVEY 8 f2)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -1190,9 +1302,9 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step's outputs")
     args = ap.parse_args()
     if args.path == "auto":  # measured: small ties the window path on the single batch-1 layer, the window path wins
-        # the ten-layer batch-1 step (two launches; 20.5 vs 22.5 us for the digit path), the expansion kernel the
-        # batch-256 step (profiles/r02g_*, profiles/r02w_bench_*)
-        args.path = {"conv1": "small", "resnet1": "tcw"}.get(args.workload, "tc")
+        # the ten-layer batch-1 step (two launches; 20.5 vs 22.5 us for the digit path), the hybrid (layers 2, 5, 8 on
+        # the window path beside the expansion kernel) the batch-256 step (0.254 vs 0.270 ms; profiles/r02w_*)
+        args.path = {"conv1": "small", "resnet1": "tcw", "resnet256": "hybrid"}.get(args.workload, "tc")
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if world == 0 and args.gpus > 1:  # not launched by torchrun: launch N ranks (one per GPU) ourselves
         return relaunch(args.gpus)

@@ -484,12 +484,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // rows 32q .. 32q+31), splitting the 32-column blocks.  Each warp works on its own: the valid
     // rows among its 32 (grid positions inside the image) are consecutive NHWC output rows
     // m_w .. m_w + nv - 1 in grid order, so each valid lane stages its 32 outputs at its
-    // compacted position (rank among the valid lanes; 128-byte rows written conflict-free by
-    // rotating the lane's 16-byte chunks by lane % 8) and lane 0 stores the block with one TMA
-    // box per set bit of nv (32 columns x 2^k rows) — no barrier between warps.
+    // compacted position (rank among the valid lanes; 128-byte rows, 128-byte swizzle by address
+    // bits: conflict-free, and TMA boxes may start inside a swizzle atom) and lane 0 stores the
+    // block with at most two TMA boxes of 32 columns x 2^k rows — no barrier between warps.
     const int q4 = warp & 3, ew = warp - kEpiWarp0, cb0 = ew >> 2;
     constexpr int kCbStep = kEpiWarps / 4;
-    const uint32_t rot = uint32_t(lane & 7);
     const int ebufs = args.ebufs;
     uint8_t* const s_w = s_epi + ew * ebufs * kStageBuf;
     int acc = 0, buf = 0, pi = 0;
@@ -536,16 +535,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // mantissa bits (FADD + IADD on the full-rate pipes instead of the quarter-rate F2I)
 #pragma unroll
         for (int c = 0; c < 32; ++c) r[c] = uint32_t(__float_as_int(__uint_as_float(r[c]) + 12582912.0f) - 0x4B400000);
-        // rotate the 8 chunks of 4 words: chunk i <- chunk (i + rot) & 7
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const bool on = (rot >> b) & 1u;
-          uint32_t t[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) t[c] = on ? r[(c + (4 << b)) & 31] : r[c];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) r[c] = t[c];
-        }
         PROF_ADD(pe_cvt);
         uint8_t* sb = s_w + buf * kStageBuf;
         {
@@ -554,9 +543,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (valid) {
             const uint32_t row = smem_u32(sb) + uint32_t(rank * 128);
+            const uint32_t sw = uint32_t(rank & 7);  // 128-byte swizzle by the row's address bits (as the TMA map)
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              sts128(row + (((uint32_t(i) + rot) & 7u) << 4), r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+              sts128(row + ((uint32_t(i) ^ sw) << 4), r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
           }
           tc::fence_proxy_async();
           __syncwarp();
@@ -565,12 +555,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef BS_TCW_NOSTORE
         if (lane == 0) {
           PROF_T0();
-          int off = 0;
-          for (int k = kBoxMaps - 1; k >= 0; --k)
-            if (nv & (1 << k)) {
-              tc::tma_store_2d(&maps.out[pi][k], n0 + cb * 32, m_w + off, smem_u32(sb) + uint32_t(off * 128));
-              off += 1 << k;
-            }
+          // at most two boxes of the largest power of two <= nv, at 0 and at nv - 2^k (rows both
+          // boxes cover are written twice with the same values, all inside this warp's rows)
+          const int k = 31 - __clz(nv), box = 1 << k;
+          tc::tma_store_2d(&maps.out[pi][k], n0 + cb * 32, m_w, smem_u32(sb));
+          if (nv != box)
+            tc::tma_store_2d(&maps.out[pi][k], n0 + cb * 32, m_w + nv - box, smem_u32(sb) + uint32_t((nv - box) * 128));
           tc::bulk_commit();
           PROF_ADD(pe_st);
         }
@@ -672,7 +662,7 @@ cudaError_t launch(const TcwProblem* ps, int count, cudaStream_t stream) {
     const int64_t M = int64_t(p.n) * G.oh * G.ow;
     for (int k = 0; k < kBoxMaps; ++k)
       if (!tc::encode_2d(&maps.out[q][k], CU_TENSOR_MAP_DATA_TYPE_INT32, p.out, uint64_t(p.oc), uint64_t(M),
-                         uint64_t(p.oc) * 4, 32, 1u << k, CU_TENSOR_MAP_SWIZZLE_NONE))
+                         uint64_t(p.oc) * 4, 32, 1u << k, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
   }
   if (total == 0) return cudaSuccess;
