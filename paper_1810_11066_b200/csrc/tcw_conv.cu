@@ -369,6 +369,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0, acc = 0, pi = 0, key = -1;
     uint32_t phase = 0, acc_phase = 0, bfpar = 0;
     const uint32_t sa0 = smem_u32(s_a), sb0 = smem_u32(s_b);
+    // the current problem's fields in registers, reloaded only when the tile sequence enters the
+    // next problem (per-tile shared-memory reads of the record were ~40% of the MMA warp's time
+    // on single-stage tiles)
+    int cpi = -1, c_tile0 = 0, c_next0 = 0, c_pairs = 0, c_kh = 0, c_kw = 0, c_wg = 0, c_nph = 0, c_taps = 0, c_sl = 0,
+        c_R = 0;
+    uint32_t c_idesc = 0, c_wrows = 0, c_bn = 0, c_s0 = 0, c_s1 = 0, c_s2 = 0, c_s3 = 0, c_bslot = 0;
+    uint32_t c_a0off0 = 0, c_a0off1 = 0;  // kw == 3 rows: first tap's phase offset, per row parity
+    uint64_t c_da10 = 0, c_da11 = 0, c_da2 = 0;
+    bool c_bres = false;
+    FastDiv c_divnm{1u, 0u, 0u};
+    auto load_prob = [&](int q) {
+      const TwProb& P = sprob[q];
+      cpi = q;
+      c_tile0 = P.tile0;
+      c_next0 = q + 1 < args.nprob ? sprob[q + 1].tile0 : args.ntiles;
+      c_pairs = P.pairs; c_kh = P.kh; c_kw = P.kw; c_wg = P.wg; c_nph = P.nph; c_taps = P.taps; c_sl = P.s - 1;
+      c_R = P.R;
+      c_idesc = P.idesc; c_wrows = uint32_t(P.lwin); c_bn = uint32_t(P.bn);
+      c_s0 = uint32_t(P.slot_of[0]); c_s1 = uint32_t(P.slot_of[1]); c_s2 = uint32_t(P.slot_of[2]);
+      c_s3 = uint32_t(P.slot_of[3]);
+      c_bslot = P.bslot; c_bres = P.b_res != 0; c_divnm = P.div_nm;
+      c_a0off0 = c_s0 * c_wrows * 32u;
+      c_a0off1 = c_s2 * c_wrows * 32u;
+      c_da10 = uint64_t(((c_s1 * c_wrows + uint32_t(1 >> c_sl)) * 32u - c_a0off0) >> 4);
+      c_da11 = uint64_t(((c_s3 * c_wrows + uint32_t(1 >> c_sl)) * 32u - c_a0off1) >> 4);
+      c_da2 = uint64_t((uint32_t(2 >> c_sl) * 32u) >> 4);
+    };
 #ifdef BS_TCW_PROFILE
     long long t_tile = clock64();
 #endif
@@ -377,28 +404,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       pm_loop += clock64() - t_tile;  // previous tile's tail (acc commit, next-tile check, loop)
       const long long t_top = clock64();
 #endif
-      next_prob(tile, pi);
-      const TwProb& P = sprob[pi];
-      uint32_t mb, nb;
-      tile_mn(P, tile, mb, nb);
-      const int k = bkey(P, pi, nb);
+      if (cpi < 0 || tile >= c_next0) {
+        next_prob(tile, pi);
+        load_prob(pi);
+      }
+      const uint32_t tl = uint32_t(tile - c_tile0);
+      const uint32_t nb = c_divnm.div(tl), mb = tl - nb * c_divnm.d;
+      const int k = c_bres ? (pi << 16) | int(nb) : -2;
       if (k != key) {
         key = k;
-        if (P.b_res) {
+        if (c_bres) {
           spin_wait(smem_u32(b_full), bfpar);
           bfpar ^= 1u;
         }
       }
-      // per-tile constants in registers: the issue loop below does arithmetic only (no
-      // parameter-space loads in the MMA chain).  Addresses in 32-byte rows.
-      const uint32_t idesc = P.idesc, wrows = uint32_t(P.lwin), bn = uint32_t(P.bn);
-      const int sl = P.s - 1;  // stride 1 or 2: shift / mask
-      const int kh = P.kh, kw = P.kw, wg = P.wg, nph = P.nph, taps = P.taps;
-      const uint32_t s0 = uint32_t(P.slot_of[0]), s1 = uint32_t(P.slot_of[1]), s2 = uint32_t(P.slot_of[2]),
-                     s3 = uint32_t(P.slot_of[3]);
-      const bool bres = P.b_res;
-      const uint32_t bslot = P.bslot;
-      const uint32_t delta = uint32_t(int64_t(mb) * P.R * P.wg) & 7u;  // tile start inside the window's first 8 rows
+      const uint32_t delta = (mb * uint32_t(c_R) * uint32_t(c_wg)) & 7u;  // tile start inside the window's first 8 rows
 #ifdef BS_TCW_PROFILE
       pm_top += clock64() - t_top;
 #endif
@@ -407,13 +427,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_ADD(pm_acc); }
       tc::tc_fence_after();
       const uint32_t tacc = uint32_t(acc * kAccCols);
-      for (int p = 0; p < P.pairs; ++p) {
+      for (int p = 0; p < c_pairs; ++p) {
         { PROF_T0();
         spin_wait(smem_u32(full + stage), phase);
         PROF_ADD(pm_full); }
         tc::tc_fence_after();
         const uint32_t sA = sa0 + uint32_t(stage * args.astage);
-        const uint32_t sB = bres ? sb0 + uint32_t(p) * bslot : sb0 + uint32_t(stage * args.bstride);
+        const uint32_t sB = c_bres ? sb0 + uint32_t(p) * c_bslot : sb0 + uint32_t(stage * args.bstride);
 #ifdef BS_TCW_NOMMA  // experiment builds only: no MMAs (the pipeline's barriers still run)
         if (false) {
 #else
@@ -424,27 +444,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < DW; ++e)
 #pragma unroll
             for (int d = 0; d < DA; ++d) {
-              const uint32_t ad0 = sA + (uint32_t(d * nph) * wrows + delta) * 32u;
-              uint32_t bd = sB + uint32_t(e * taps) * bn * 32u;
-              int t = 0;
-              for (int ky = 0; ky < kh; ++ky) {
-                const uint32_t rowoff = ad0 + uint32_t((ky >> sl) * wg) * 32u;
-                const bool oy = (ky & sl) != 0;
-                const uint32_t fe = oy ? s2 : s0, fo = oy ? s3 : s1;  // phase slots of even / odd kx
-                if (kw == 3) {
-                  const uint32_t a0 = rowoff + fe * wrows * 32u;
-                  const uint64_t da1 = uint64_t(((fo * wrows + uint32_t(1 >> sl)) * 32u - fe * wrows * 32u) >> 4);
-                  const uint64_t da2 = uint64_t((uint32_t(2 >> sl) * 32u) >> 4);
-                  mma3_f4(tacc, sdesc32(a0), sdesc32(bd), da1, da2, uint64_t(bn * 2u), idesc, uint32_t(kSF0 + 4 * d),
-                          uint32_t(kSF0 + 16 + 8 * e), (p | e | d | t) != 0);
-                  t += 3;
-                  bd += 3u * bn * 32u;
-                  continue;
+              const uint32_t ad0 = sA + (uint32_t(d * c_nph) * c_wrows + delta) * 32u;
+              uint32_t bd = sB + uint32_t(e * c_taps) * c_bn * 32u;
+              if (c_kw == 3) {  // three taps per row, one issue block
+                for (int ky = 0, t = 0; ky < c_kh; ++ky, t += 3, bd += 3u * c_bn * 32u) {
+                  const bool oy = (ky & c_sl) != 0;
+                  const uint32_t a0 = ad0 + uint32_t((ky >> c_sl) * c_wg) * 32u + (oy ? c_a0off1 : c_a0off0);
+                  mma3_f4(tacc, sdesc32(a0), sdesc32(bd), oy ? c_da11 : c_da10, c_da2, uint64_t(c_bn * 2u), c_idesc,
+                          uint32_t(kSF0 + 4 * d), uint32_t(kSF0 + 16 + 8 * e), (p | e | d | t) != 0);
                 }
-                for (int kx = 0; kx < kw; ++kx, ++t, bd += bn * 32u) {
-                  const uint32_t f = (kx & sl) ? fo : fe;
-                  const uint32_t a = rowoff + (f * wrows + uint32_t(kx >> sl)) * 32u;
-                  mma_f4_ss_elect(tacc, sdesc32(a), sdesc32(bd), idesc, uint32_t(kSF0 + 4 * d),
+                continue;
+              }
+              int t = 0;
+              for (int ky = 0; ky < c_kh; ++ky) {
+                const uint32_t rowoff = ad0 + uint32_t((ky >> c_sl) * c_wg) * 32u;
+                const bool oy = (ky & c_sl) != 0;
+                const uint32_t fe = oy ? c_s2 : c_s0, fo = oy ? c_s3 : c_s1;  // phase slots of even / odd kx
+                for (int kx = 0; kx < c_kw; ++kx, ++t, bd += c_bn * 32u) {
+                  const uint32_t f = (kx & c_sl) ? fo : fe;
+                  const uint32_t a = rowoff + (f * c_wrows + uint32_t(kx >> c_sl)) * 32u;
+                  mma_f4_ss_elect(tacc, sdesc32(a), sdesc32(bd), c_idesc, uint32_t(kSF0 + 4 * d),
                                   uint32_t(kSF0 + 16 + 8 * e), (p | e | d | t) != 0);
                 }
               }
@@ -472,11 +491,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int nt = tile + int(gridDim.x);  // release the weights when the next tile reads others
       if (nt < args.ntiles) {
-        int npi = pi;
-        next_prob(nt, npi);
-        uint32_t mb2, nb2;
-        tile_mn(sprob[npi], nt, mb2, nb2);
-        if (bkey(sprob[npi], npi, nb2) != key) tc::mma_commit_elect(smem_u32(b_empty));
+        int k2;
+        if (nt < c_next0) {
+          const uint32_t tl2 = uint32_t(nt - c_tile0);
+          k2 = c_bres ? (pi << 16) | int(c_divnm.div(tl2)) : -2;
+        } else {
+          int npi = pi;
+          next_prob(nt, npi);
+          uint32_t mb2, nb2;
+          tile_mn(sprob[npi], nt, mb2, nb2);
+          k2 = bkey(sprob[npi], npi, nb2);
+        }
+        if (k2 != key) tc::mma_commit_elect(smem_u32(b_empty));
       }
     }
   } else {
@@ -493,23 +519,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* const s_w = s_epi + ew * ebufs * kStageBuf;
     int acc = 0, buf = 0, pi = 0;
     uint32_t acc_phase = 0;
+    // the current problem's fields (and this lane's tile-row coordinates) in registers, reloaded
+    // only when the tile sequence enters the next problem
+    int cpi = -1, c_tile0 = 0, c_next0 = 0, c_bn = 0, c_oc = 0, c_R = 0, c_G = 0, c_oh = 0, c_ow = 0, c_hg = 0;
+    uint32_t c_gr = 0, c_gx = 0;
+    bool c_lane_ok = false;
+    FastDiv c_divnm{1u, 0u, 0u}, c_divhg{1u, 0u, 0u};
     for (int tile = blockIdx.x; tile < args.ntiles; tile += gridDim.x) {
-      next_prob(tile, pi);
-      const TwProb& P = sprob[pi];
-      uint32_t mb, nb;
-      tile_mn(P, tile, mb, nb);
-      const int n0 = int(nb) * P.bn, g0 = int(mb) * P.R;
-      const int ncb = (min(P.bn, P.oc - n0) + 31) / 32;
-      // this lane's tile row: grid row g0 + gr, column gx
-      const uint32_t l = uint32_t(q4 * 32 + lane);
-      const uint32_t gr = P.div_wg.div(l), gx = l - gr * uint32_t(P.wg);
-      const uint32_t g = uint32_t(g0) + gr;
-      const uint32_t img = P.div_hg.div(g), gy = g - img * uint32_t(P.hg);
-      const bool valid = int(gr) < P.R && int(gx) < P.ow && int(g) < P.G && int(gy) < P.oh;
+      if (cpi < 0 || tile >= c_next0) {
+        next_prob(tile, pi);
+        const TwProb& P = sprob[pi];
+        cpi = pi;
+        c_tile0 = P.tile0;
+        c_next0 = pi + 1 < args.nprob ? sprob[pi + 1].tile0 : args.ntiles;
+        c_bn = P.bn; c_oc = P.oc; c_R = P.R; c_G = P.G; c_oh = P.oh; c_ow = P.ow; c_hg = P.hg;
+        c_divnm = P.div_nm;
+        c_divhg = P.div_hg;
+        const uint32_t l = uint32_t(q4 * 32 + lane);  // this lane's tile row: grid row gr, column gx
+        c_gr = P.div_wg.div(l);
+        c_gx = l - c_gr * uint32_t(P.wg);
+        c_lane_ok = int(c_gr) < P.R && int(c_gx) < P.ow;
+      }
+      const uint32_t tl = uint32_t(tile - c_tile0);
+      const uint32_t nb = c_divnm.div(tl), mb = tl - nb * c_divnm.d;
+      const int n0 = int(nb) * c_bn, g0 = int(mb) * c_R;
+      const int ncb = (min(c_bn, c_oc - n0) + 31) / 32;
+      const uint32_t gx = c_gx;
+      const uint32_t g = uint32_t(g0) + c_gr;
+      const uint32_t img = c_divhg.div(g), gy = g - img * uint32_t(c_hg);
+      const bool valid = c_lane_ok && int(g) < c_G && int(gy) < c_oh;
       const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
       const int nv = __popc(vmask);
       const int rank = __popc(vmask & ((1u << lane) - 1u));
-      const int m = valid ? (int(img) * P.oh + int(gy)) * P.ow + int(gx) : 0;
+      const int m = valid ? (int(img) * c_oh + int(gy)) * c_ow + int(gx) : 0;
       const int m_w = __shfl_sync(0xffffffffu, m, nv ? __ffs(vmask) - 1 : 0);  // first valid row
       { PROF_T0();
       tc::mbar_wait_sleep(smem_u32(acc_full + acc), acc_phase);
