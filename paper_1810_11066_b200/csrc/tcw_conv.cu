@@ -168,6 +168,39 @@ __device__ __forceinline__ void mma_f4_ss_elect(uint32_t d, uint64_t a, uint64_t
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate));
 }
+// All nine MMAs of a 3x3 filter from one elected lane: row r's three taps read A at ar, ar + da1r,
+// ar + da2 (da1 of rows 0 and 2 is da1e, of row 1 da1o: the phase of an odd kernel row differs at
+// stride 2) and B at b + t * db for tap t = 3r + c; one register -> uniform move per operand and
+// stage instead of per MMA.
+__device__ __forceinline__ void mma9_f4(uint32_t d, uint64_t a0, uint64_t a1, uint64_t a2, uint64_t b,
+                                       uint64_t da1e, uint64_t da1o, uint64_t da2, uint64_t db, uint32_t idesc,
+                                       uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b32 x;\n.reg .b64 t, bb;\n"
+      "elect.sync x|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %12, 0;\n"
+      "@!e bra SKIP%=;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %4, %9, [%10], [%11], p;\n"
+      "add.s64 t, %1, %5;\nadd.s64 bb, %4, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], t, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 t, %1, %7;\nadd.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], t, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %2, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 t, %2, %6;\nadd.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], t, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 t, %2, %7;\nadd.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], t, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %3, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 t, %3, %5;\nadd.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], t, bb, %9, [%10], [%11], 1;\n"
+      "add.s64 t, %3, %7;\nadd.s64 bb, bb, %8;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], t, bb, %9, [%10], [%11], 1;\n"
+      "SKIP%=:\n}" ::"r"(d),
+      "l"(a0), "l"(a1), "l"(a2), "l"(b), "l"(da1e), "l"(da1o), "l"(da2), "l"(db), "r"(idesc), "r"(sfa), "r"(sfb),
+      "r"(accumulate));
+}
 // K-major shared-memory descriptor, 32-byte swizzle (SM100, version 1, layout code 6): rows of
 // 32 bytes (one 64-element MMA K step), 8-row atoms of 256 B (SBO), the two 16-byte halves of
 // a row exchanged when address bit 7 (row bit 2) is set — the layout the packer wrote (R26).
@@ -446,6 +479,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int d = 0; d < DA; ++d) {
               const uint32_t ad0 = sA + (uint32_t(d * c_nph) * c_wrows + delta) * 32u;
               uint32_t bd = sB + uint32_t(e * c_taps) * c_bn * 32u;
+              if (c_kw == 3 && c_kh == 3) {  // all nine taps in one issue block
+                const uint32_t a0 = ad0 + c_a0off0;
+                const uint32_t a1 = ad0 + uint32_t((1 >> c_sl) * c_wg) * 32u + (c_sl ? c_a0off1 : c_a0off0);
+                const uint32_t a2 = ad0 + uint32_t((2 >> c_sl) * c_wg) * 32u + c_a0off0;
+                mma9_f4(tacc, sdesc32(a0), sdesc32(a1), sdesc32(a2), sdesc32(bd), c_da10, c_sl ? c_da11 : c_da10, c_da2,
+                        uint64_t(c_bn * 2u), c_idesc, uint32_t(kSF0 + 4 * d), uint32_t(kSF0 + 16 + 8 * e),
+                        (p | e | d) != 0);
+                continue;
+              }
               if (c_kw == 3) {  // three taps per row, one issue block
                 for (int ky = 0, t = 0; ky < c_kh; ++ky, t += 3, bd += 3u * c_bn * 32u) {
                   const bool oy = (ky & c_sl) != 0;
