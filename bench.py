@@ -1288,7 +1288,7 @@ def main():
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
-    ap.add_argument("--tcw-layers", default="2,5,8",
+    ap.add_argument("--tcw-layers", default="2,5,6,8",
                     help="--path hybrid: the layers on the window path (measured best partition, profiles/r02w_hybrid*)")
     ap.add_argument("--path", choices=["auto", "tc", "tcd", "tcw", "hybrid", "popc", "small"], default="auto",
                     help="conv/GEMM kernel: tensor-core bitserial (tc), the digit path (tcd), the window path (tcw), the "
