@@ -51,12 +51,41 @@ def main():
         tcg = [[int(x) for x in g.split(",")] for g in parts.get("tc", "").split("|") if g]
         tcl = [li for g in tcg for li in g]
         s_pack, s_w, s2 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        evp = torch.cuda.Event()
+        evp, evw = torch.cuda.Event(), torch.cuda.Event()
+        mode = parts.get("mode", "")
 
         def step():
             main = torch.cuda.current_stream()
             for s in (s_pack, s_w, s2):
                 s.wait_stream(main)
+            if mode == "sp":  # packs serialized on one stream (bit planes first), each conv after its own pack
+                with torch.cuda.stream(s_pack):
+                    bs.bitpack_group([data[li]["act"] for li in tcl], 2, outs=[data[li]["packed"] for li in tcl])
+                    evp.record(s_pack)
+                    bs.digitpack_win_group([data[li]["pk"] for li in tcw], 2, outs=[data[li]["aw"] for li in tcw])
+                    evw.record(s_pack)
+                main.wait_event(evp)
+                bs.bitserial_conv2d_nhwc_tc_group([data[li]["tc"] for g in tcg for li in g], 2, 1)
+                s_w.wait_event(evw)
+                with torch.cuda.stream(s_w):
+                    bs.bitserial_conv2d_nhwc_tcw_group([data[li]["tcw"] for li in tcw], 2, 1)
+                for s in (s_pack, s_w, s2):
+                    main.wait_stream(s)
+                return
+            if mode == "wp":  # packs serialized, window layout first
+                with torch.cuda.stream(s_pack):
+                    bs.digitpack_win_group([data[li]["pk"] for li in tcw], 2, outs=[data[li]["aw"] for li in tcw])
+                    evw.record(s_pack)
+                    bs.bitpack_group([data[li]["act"] for li in tcl], 2, outs=[data[li]["packed"] for li in tcl])
+                    evp.record(s_pack)
+                s_w.wait_event(evw)
+                with torch.cuda.stream(s_w):
+                    bs.bitserial_conv2d_nhwc_tcw_group([data[li]["tcw"] for li in tcw], 2, 1)
+                main.wait_event(evp)
+                bs.bitserial_conv2d_nhwc_tc_group([data[li]["tc"] for g in tcg for li in g], 2, 1)
+                for s in (s_pack, s_w, s2):
+                    main.wait_stream(s)
+                return
             if tcw:
                 with torch.cuda.stream(s_w):
                     bs.digitpack_win_group([data[li]["pk"] for li in tcw], 2, outs=[data[li]["aw"] for li in tcw])
