@@ -639,12 +639,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef BS_TCW_NOSTORE
         if (lane == 0) {
           PROF_T0();
-          // at most two boxes of the largest power of two <= nv, at 0 and at nv - 2^k (rows both
-          // boxes cover are written twice with the same values, all inside this warp's rows)
-          const int k = 31 - __clz(nv), box = 1 << k;
+          // at most two boxes: the largest power of two <= nv at 0, and the smallest power of two
+          // >= the remainder ending at nv (rows both cover are written twice with the same values,
+          // all inside this warp's rows; fewer than the remainder)
+          const int k = 31 - __clz(nv), rem = nv - (1 << k);
           tc::tma_store_2d(&maps.out[pi][k], n0 + cb * 32, m_w, smem_u32(sb));
-          if (nv != box)
-            tc::tma_store_2d(&maps.out[pi][k], n0 + cb * 32, m_w + nv - box, smem_u32(sb) + uint32_t((nv - box) * 128));
+          if (rem) {
+            const int j = 32 - __clz(rem - 1), box = 1 << j;  // ceil(log2(rem)) (0 for rem = 1)
+            tc::tma_store_2d(&maps.out[pi][j], n0 + cb * 32, m_w + nv - box, smem_u32(sb) + uint32_t((nv - box) * 128));
+          }
           tc::bulk_commit();
           PROF_ADD(pe_st);
         }
