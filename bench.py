@@ -178,6 +178,12 @@ class ConvLayerRun:
         return dict(act_dig=self.dig, w_dig=self.w_dig, out=self.out, n=self.n, h=L.h, w=L.w, c=L.ic, oc=L.oc,
                     kh=L.k, kw=L.k, stride=L.s, pad=L.pad, w_enc=self.enc)
 
+    def packed_bytes(self):
+        """Algorithmic activation bytes of this layer's conv: its input bit-packed (A bit planes of
+        packed_row_words(c) words per pixel) — the window path's layout carries padding, junk grid
+        positions and 4-bit digit fields and is not counted beyond this."""
+        return self.a_bits * self.n * self.L.h * self.L.w * self.bs.packed_row_words(self.L.ic) * 4
+
     def tcw_item(self):
         L = self.L
         return dict(act_win=self.win, w_win=self.w_win, out=self.out, n=self.n, h=L.h, w=L.w, c=L.ic, oc=L.oc,
@@ -453,13 +459,13 @@ class ConvWorkload:
 
     def roofline_tcw(self, reps):
         """The window path's conv launch (all layers, one launch) and its pack launch, each
-        graph-replayed; algorithmic bytes: window-layout activations + weight digits + int32 outputs."""
+        graph-replayed; algorithmic bytes: bit-packed activations + packed weights + int32 outputs."""
         bs = self.runs[0].bs
         pack = lambda: bs.digitpack_win_group(self.tcw_pack, self.args.a_bits, outs=[r.win for r in self.runs])  # noqa
         conv = lambda: bs.bitserial_conv2d_nhwc_tcw_group(self.tcw_items, self.args.a_bits, self.args.w_bits)  # noqa
         pack()
         ms, pms = graph_launch_ms(conv, reps), graph_launch_ms(pack, reps)
-        nbytes = sum(r.win.numel() + r.w_win.numel() + r.out.numel() * 4 for r in self.runs)
+        nbytes = sum(r.packed_bytes() + r.wp.numel() * 4 + r.out.numel() * 4 for r in self.runs)
         ops = sum(r.binops() for r in self.runs)
         return {"kind": "tensor", "kernel": f"tcw_conv_kernel (window path: bulk-copied windows, shifted-view taps, "
                                             f"tcgen05 kind::mxf4; one launch for the {len(self.runs)} layers, rank 0)",
@@ -468,8 +474,10 @@ class ConvWorkload:
 
     def roofline_hybrid(self, reps):
         """The hybrid step's two conv calls (the window-path launch and the grouped expansion-kernel
-        call) and two pack launches, each graph-replayed; algorithmic bytes per conv call: packed
-        activations (window layout / bit planes) + prepared weights + int32 outputs."""
+        call) and two pack launches, each graph-replayed; algorithmic bytes per conv call: the
+        bit-packed activations (window-path layers: the same bit-plane count, not the larger window
+        layout), the weights (packed bit planes for the window path, the prepared form for the
+        expansion kernel) and the int32 outputs."""
         bs, fmt = self.runs[0].bs, tc_fmt(self.args)
         wpack = lambda: bs.digitpack_win_group(self.tcw_pack, self.args.a_bits, outs=[r.win for r in self.w_runs])  # noqa
         tpack = lambda: bs.bitpack_group([r.act for r in self.t_runs], self.args.a_bits,  # noqa
@@ -482,7 +490,7 @@ class ConvWorkload:
         torch.cuda.synchronize()
         wms, tms = graph_launch_ms(wconv, reps), graph_launch_ms(tconv, reps)
         wpms, tpms = graph_launch_ms(wpack, reps), graph_launch_ms(tpack, reps)
-        wbytes = sum(r.win.numel() + r.w_win.numel() + r.out.numel() * 4 for r in self.w_runs)
+        wbytes = sum(r.packed_bytes() + r.wp.numel() * 4 + r.out.numel() * 4 for r in self.w_runs)
         tbytes = sum(r.packed.numel() * 4 + r.w_tc.numel() + r.out.numel() * 4 for r in self.t_runs)
         per = [{"layers": [r.L.name for r in self.w_runs], "binops": sum(r.binops() for r in self.w_runs),
                 "bytes": wbytes, "ms": wms},
