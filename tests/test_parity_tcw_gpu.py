@@ -218,3 +218,37 @@ def test_conv_tcw_rejects():
         bs.digitpack_win(x, 2, 3, 3, 1, 1, out=torch.zeros(16, dtype=torch.uint8, device=DEV))
     torch.cuda.synchronize()
     assert bool((out == -7).all())
+
+
+def _near_max_codes(rows, k, g, base, alts, p_alt=0.002):
+    x = torch.full((rows, k), base, dtype=torch.uint8)
+    sel = torch.rand((rows, k), generator=g) < p_alt
+    pick = torch.randint(0, len(alts), (rows, k), generator=g)
+    return torch.where(sel, torch.tensor(alts, dtype=torch.uint8)[pick], x)
+
+
+# (a_bits, a_enc, w_bits, w_enc, C): C * max|a| * max|w| just under the FP4 bound 2^22 (1x1 convs,
+# the reduction along the channels: every 64-channel slab pair one pipeline stage)
+TCW_FP4_BOUND_CASES = [
+    (1, 0, 1, 0, 4_194_303), (4, 0, 4, 0, 18_641), (4, 0, 4, 1, 18_641), (4, 2, 4, 2, 65_535),
+    (2, 1, 2, 1, 466_033),
+]
+
+
+@pytest.mark.parametrize("a_bits,a_enc,w_bits,w_enc,c", TCW_FP4_BOUND_CASES)
+def test_conv_tcw_at_fp4_bound(a_bits, a_enc, w_bits, w_enc, c):
+    """The window path's FP32 accumulation exact at the ABI bound: a 1x1 conv over 5 pixels with
+    C channels, near-max codes with a sparse sprinkle of other codes (odd low bits on a running
+    sum near 2^22), against the oracle's dense product of the same codes."""
+    m, oc = 5, 12
+    g = inputs.gen(c * 31 + a_bits * 7 + w_bits + 100 * a_enc + 1000 * w_enc)
+    a_max = (1 << a_bits) - 1 if a_enc != 2 else 1 << (a_bits - 1)
+    w_max = (1 << w_bits) - 1 if w_enc != 2 else 1 << (w_bits - 1)
+    a = _near_max_codes(m, c, g, a_max, [0, 1, (1 << a_bits) - 1] + ([9, 11, 15] if a_enc == 2 else []))
+    w = _near_max_codes(oc, c, g, w_max, [0, 1] + ([9, 11, 15] if w_enc == 2 else []))
+    w[oc - 1] = 0 if w_enc == 1 else w_max
+    ref = oracle.dense_enc(a.numpy(), a_bits, a_enc, w.numpy(), w_bits, w_enc)
+    bound = c * (a_max if a_enc != 1 else (1 << a_bits) - 1) * (w_max if w_enc != 1 else (1 << w_bits) - 1)
+    assert bound < 1 << 22 and int(np.abs(ref).max()) > 0.99 * bound
+    got = run_conv(a.view(1, 1, m, c), a_bits, a_enc, w.view(oc, 1, 1, c), w_bits, w_enc, 1, 0)
+    np.testing.assert_array_equal(got.view(m, oc).cpu().numpy(), ref)
