@@ -579,6 +579,40 @@ class ConvWorkload:
 
             def step():
                 bs.bitserial_conv2d_nhwc_tc_host_group(layers, self.args.a_bits, self.args.w_bits, tc_format=fmt)
+        elif self.args.path == "hybrid" and self.args.e2e_mode == "unified":
+            # every layer, smallest upload first, through one pipeline of three streams: upload ->
+            # pack + conv (bs_bitpack + bs_bitserial_conv2d_nhwc_tc_prepared, or bs_digitpack_win +
+            # bs_bitserial_conv2d_nhwc_tcw) -> download, each layer's download as soon as its conv is done
+            host = [(r.act_cpu.contiguous().pin_memory(), torch.empty(r.out.shape, dtype=torch.int32).pin_memory())
+                    for r in self.runs]
+            bufs = host
+            bs = self.runs[0].bs
+            su, sc, sd = (torch.cuda.Stream(device=self.dev) for _ in range(3))
+            order = sorted(range(len(self.runs)), key=lambda i: self.runs[i].act.numel())
+            ev_up = [torch.cuda.Event() for _ in order]
+            ev_c = [torch.cuda.Event() for _ in order]
+            widx = {id(r): k for k, r in enumerate(self.w_runs)}
+
+            def step():
+                for j, i in enumerate(order):
+                    r, (ah, oh_) = self.runs[i], host[i]
+                    with torch.cuda.stream(su):
+                        r.act.copy_(ah, non_blocking=True)
+                        ev_up[j].record(su)
+                    sc.wait_event(ev_up[j])
+                    with torch.cuda.stream(sc):
+                        if r.path == "tcw":
+                            k = widx[id(r)]
+                            bs.digitpack_win_group([self.tcw_pack[k]], self.args.a_bits, outs=[r.win])
+                            bs.bitserial_conv2d_nhwc_tcw_group([self.tcw_items[k]], self.args.a_bits, self.args.w_bits)
+                        else:
+                            r.pack_only()
+                            r.conv_only()
+                        ev_c[j].record(sc)
+                    sd.wait_event(ev_c[j])
+                    with torch.cuda.stream(sd):
+                        oh_.copy_(r.out, non_blocking=True)
+                sd.synchronize()
         elif self.args.path == "hybrid":
             # the expansion-kernel layers through the pipelined host-buffer call (uploads, pack + conv,
             # downloads on three streams), the window-path layers beside it on three more streams
@@ -1296,6 +1330,9 @@ def main():
                     help="overlapped packs: grid cap in CTAs per SM (0 = library choice)")
     ap.add_argument("--tc-format", choices=["f4", "i8"], default="f4",
                     help="tensor-core operand format: block-scaled FP4 (default) or INT8")
+    ap.add_argument("--e2e-mode", choices=["split", "unified"], default="unified",
+                    help="--path hybrid e2e: split = the host-group call for the expansion-kernel layers beside a "
+                         "window-path pipeline; unified = one per-layer pipeline for all layers")
     ap.add_argument("--tcw-layers", default="2,5,6,8",
                     help="--path hybrid: the layers on the window path (measured best partition, profiles/r02w_hybrid*)")
     ap.add_argument("--path", choices=["auto", "tc", "tcd", "tcw", "hybrid", "popc", "small"], default="auto",
