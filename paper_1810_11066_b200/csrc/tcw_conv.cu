@@ -82,10 +82,17 @@ int64_t tcw_weight_bytes(int oc, int kh, int kw, int c, int w_bits) {
 
 namespace tcw {
 
-constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kEpiWarps = 8;
+#ifndef BS_TCW_EPI_WARPS
+#define BS_TCW_EPI_WARPS 8  // epilogue warps (a multiple of 4: warp % 4 = TMEM lane quarter)
+#endif
+#ifndef BS_TCW_EPI_BUFS_MIN
+#define BS_TCW_EPI_BUFS_MIN 2
+#endif
+
+constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kEpiWarps = BS_TCW_EPI_WARPS;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kStageBuf = 32 * 128;  // per-warp epilogue staging: 32 compacted rows x 32 int32 (dense)
-constexpr int kEpiBufsMin = 2, kEpiBufsMax = 4;  // staging buffers per epilogue warp: runtime
+constexpr int kEpiBufsMin = BS_TCW_EPI_BUFS_MIN, kEpiBufsMax = 4;  // staging buffers per epilogue warp: runtime
 constexpr int kBoxMaps = 6;  // output maps with boxes of 32 columns x 1, 2, 4, ..., 32 rows
 constexpr int kBarBytes = 512;
 constexpr int kSmemLimit = 222 * 1024;  // dynamic; + static problem records (NP x ~180 B) <= 227 KB
