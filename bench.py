@@ -1299,7 +1299,7 @@ def relaunch(n, argv=None):
     return subprocess.call(cmd)
 
 
-def main():
+def build_parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -1345,11 +1345,19 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed step's outputs")
-    args = ap.parse_args()
+    return ap
+
+
+def resolve_path(args):
     if args.path == "auto":  # measured: small ties the window path on the single batch-1 layer, the window path wins
-        # the ten-layer batch-1 step (two launches; 20.5 vs 22.5 us for the digit path), the hybrid (layers 2, 5, 8 on
-        # the window path beside the expansion kernel) the batch-256 step (0.254 vs 0.270 ms; profiles/r02w_*)
+        # the ten-layer batch-1 step (two launches; 20.4 vs 22.5 us for the digit path), the hybrid (layers 2, 5, 6, 8
+        # on the window path beside the expansion kernel) the batch-256 step (0.242 vs 0.270 ms; profiles/r02v8_*)
         args.path = {"conv1": "small", "resnet1": "tcw", "resnet256": "hybrid"}.get(args.workload, "tc")
+    return args
+
+
+def main():
+    args = resolve_path(build_parser().parse_args())
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if world == 0 and args.gpus > 1:  # not launched by torchrun: launch N ranks (one per GPU) ourselves
         return relaunch(args.gpus)
