@@ -212,3 +212,44 @@ def test_tc_host_group_validation(lib):
     assert f(p, 1, 2, 1, bs.TC_F4, NULL) == 5
     x.out_dev, x.oc = 1 << 21, 0
     assert f(p, 1, 2, 1, bs.TC_F4, NULL) == 4
+
+
+@pytest.mark.parametrize("geom", [
+    (256, 56, 56, 64, 3, 3, 1, 1), (256, 56, 56, 64, 3, 3, 2, 1), (256, 56, 56, 64, 1, 1, 2, 0),
+    (256, 7, 7, 512, 3, 3, 1, 1), (2, 5, 4, 40, 3, 3, 1, 1), (1, 6, 7, 33, 3, 3, 2, 1), (1, 5, 6, 20, 2, 3, 1, 0),
+    (1, 7, 5, 96, 3, 2, 2, 2), (4, 11, 11, 3, 5, 3, 1, 2), (1, 5, 6, 64, 7, 7, 1, 3)])
+@pytest.mark.parametrize("bits", [1, 2, 3, 4])
+def test_tcw_layout_size_matches_the_oracle_definition(lib, geom, bits):
+    """The library's window-layout size (host code, no GPU) equals the size the oracle's
+    definition of the layout (R26) gives: ceil(bits/2) x phases x slab pairs x
+    pstride x 32 bytes."""
+    import oracle
+    n, h, w, c, kh, kw, s, p = geom
+    g = oracle.win_geometry(n, h, w, c, kh, kw, s, p, p)
+    assert bs.tcw_act_bytes(n, h, w, c, kh, kw, s, p, bits) == (bits + 1) // 2 * g["nph"] * g["pairs"] * g["pstride"] * 32
+
+
+@pytest.mark.parametrize("oc,kh,kw,c,w_bits", [(64, 3, 3, 64, 1), (100, 1, 1, 33, 2), (512, 3, 3, 512, 4), (4, 2, 3, 5, 3)])
+def test_tcw_weight_size_matches_the_oracle_definition(lib, oc, kh, kw, c, w_bits):
+    import numpy as np
+    import oracle
+    ref = oracle.conv2d_tcw_weights(np.zeros((oc, kh, kw, c), dtype=np.uint8), w_bits, 0)
+    assert bs.conv2d_tcw_weight_bytes(oc, kh, kw, c, w_bits) == ref.size
+
+
+def test_tcw_validation_before_launch(lib):
+    # outside the window layout's domain: stride 3, unequal strides, a grid row wider than a tile
+    assert bs.tcw_act_bytes(1, 12, 12, 8, 3, 3, 3, 1, 2) == 0
+    assert bs.tcw_act_bytes(1, 8, 300, 8, 3, 3, 1, 1, 2) == 0
+    conv = lib.bs_bitserial_conv2d_nhwc_tcw
+    #                 act   A  enc  w     W  enc  out   n  h  w  c  oc kh kw sh sw ph pw stream
+    assert conv(FAKE, 2, 0, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 8, 3, 3, 1, 2, 1, 1, NULL) == 3
+    assert b"stride" in lib.bs_last_error()
+    assert conv(FAKE, 2, 0, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 6, 3, 3, 1, 1, 1, 1, NULL) == 3   # oc % 4 != 0
+    assert b"multiple of 4" in lib.bs_last_error()
+    assert conv(FAKE, 4, 0, FAKE, 4, 0, FAKE, 1, 4, 4, 20000, 8, 3, 3, 1, 1, 1, 1, NULL) == 6  # FP4 bound
+    assert conv(NULL, 2, 0, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 8, 3, 3, 1, 1, 1, 1, NULL) == 1     # NULL operand
+    # pack: output buffer too small, bad bit width
+    pack = lib.bs_digitpack_win
+    assert pack(FAKE, FAKE, 16, 1, 8, 8, 8, 3, 3, 1, 1, 1, 2, 0, NULL) == 8
+    assert pack(FAKE, FAKE, 1 << 30, 1, 8, 8, 8, 3, 3, 1, 1, 1, 5, 0, NULL) == 2
