@@ -526,7 +526,10 @@ int bs_bitserial_conv2d_nhwc_tcd_group(const bs_tcd_conv_desc* descs, int count,
  * bulk copies and the tensor core reads each tap as a shifted view (no im2col, no gather).
  * The packing is the timed activation-packing step emitting this layout.
  * Supported: stride_h == stride_w in {1, 2}; wg <= 128; oc % 4 == 0;
- * bits in [1,4]; the FP4 exactness bound (BS_ERR_OVERFLOW); BS_ERR_UNSUPPORTED otherwise.
+ * bits in [1,4]; the FP4 exactness bound (BS_ERR_OVERFLOW); one pipeline stage (every activation
+ * digit's windows of a 64-channel slab pair, plus the streamed weight digits of every tap when the
+ * filter block does not stay resident) must fit shared memory — with three or four bits on both
+ * operands a wide stride-2 or many-channel layer can exceed it; BS_ERR_UNSUPPORTED otherwise.
  */
 int64_t bs_tcw_act_bytes(int n, int h, int w, int c, int kh, int kw, int stride, int pad_h, int pad_w, int bits);
 /* in: uint8 codes [n][h][w][c]; out: the window layout (out_bytes >= bs_tcw_act_bytes); every

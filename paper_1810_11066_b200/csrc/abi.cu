@@ -295,6 +295,16 @@ int check_tcw_conv(const ConvArgs& g, int a_bits, int w_bits, int a_enc, int w_e
   return BS_OK;
 }
 
+// The window-path launcher refuses (cudaErrorNotSupported) only when one pipeline stage does not
+// fit shared memory (the arguments were validated before).
+int tcw_status(cudaError_t e, const char* fn) {
+  if (e == cudaErrorNotSupported)
+    return fail(BS_ERR_UNSUPPORTED,
+                "%s: one window-path stage (every digit's windows of a 64-channel slab pair and the streamed "
+                "weight digits of every tap) exceeds shared memory for these bit widths and geometry", fn);
+  return cuda_status(e, fn);
+}
+
 bs::TcwProblem make_tcw(const uint8_t* act, const uint8_t* wt, int32_t* out, int a_bits, int w_bits,
                         const ConvArgs& g) {
   bs::TcwProblem p{};
@@ -1086,7 +1096,7 @@ int bs_bitserial_conv2d_nhwc_tcw_group(const bs_tcw_conv_desc* descs, int count,
       return fail(BS_ERR_ALIGN, "%s: descriptor %d: pointers must be 16-byte aligned", fn, q);
     ps[q] = make_tcw(d.act_win, d.w_win, d.out, a_bits, w_bits, g);
   }
-  return cuda_status(bs::launch_tcw_group(ps.data(), count, static_cast<cudaStream_t>(stream)), fn);
+  return tcw_status(bs::launch_tcw_group(ps.data(), count, static_cast<cudaStream_t>(stream)), fn);
 }
 
 int bs_bitserial_conv2d_nhwc_tcw(const uint8_t* act_win, int a_bits, int a_enc, const uint8_t* w_win, int w_bits,
@@ -1099,7 +1109,7 @@ int bs_bitserial_conv2d_nhwc_tcw(const uint8_t* act_win, int a_bits, int a_enc, 
   if (!aligned16(act_win) || !aligned16(w_win) || !aligned16(out))
     return fail(BS_ERR_ALIGN, "%s: pointers must be 16-byte aligned", fn);
   const bs::TcwProblem p = make_tcw(act_win, w_win, out, a_bits, w_bits, g);
-  return cuda_status(bs::launch_tcw_group(&p, 1, static_cast<cudaStream_t>(stream)), fn);
+  return tcw_status(bs::launch_tcw_group(&p, 1, static_cast<cudaStream_t>(stream)), fn);
 }
 
 }  // extern "C"
