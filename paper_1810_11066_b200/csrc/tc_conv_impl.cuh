@@ -113,7 +113,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   do {                \
   } while (0);
 #endif
-#define PROF_DECL long long _pt = 0, _pacc[4] = {0, 0, 0, 0};
+#define PROF_DECL long long _pt = 0, _pacc[7] = {0, 0, 0, 0, 0, 0, 0};
 #define PROF_BEGIN _pt = clock64();
 #define PROF_END(i) _pacc[i] += clock64() - _pt;
 #else
@@ -1109,6 +1109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wreload) {  // this chunk's weights: packed planes -> E2M1 digit rows of the B slot
           const TcProb& P = args.prob[0];
           uint2 wnx[kRW][4];
+          PROF_BEGIN  // slot 4 (RAW): weight-word loads
           {
             const int kp = int(P.p.kp);
             const bool rowok = arow < BN && wn < P.p.oc;
@@ -1120,12 +1121,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 wnx[j][q] = (rowok && wkk0 + 2 * q < kp) ? ldg_nc_v2(wrow + int64_t(j) * P.p.oc * kp + 2 * q)
                                                          : make_uint2(0u, 0u);
           }
+          PROF_END(4)
+          PROF_BEGIN  // slot 5 (RAW): wait for the slot's release
           for (;;) {  // the TMA warp released the slot to this chunk (its previous use consumed)
             int r;
             asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(r) : "r"(smem_u32(s_ready + wslot)) : "memory");
             if (r >= wg) break;
             __nanosleep(64);
           }
+          PROF_END(5)
+          PROF_BEGIN  // slot 6 (RAW): weight digit formation + shared-memory stores
           if (arow < BN) {
             uint8_t* brow = s_stage + wslot * C::kBBytes + arow * C::kBRow;
             const int wenc = P.p.bipolar;
@@ -1170,6 +1175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           fence_proxy_async();  // generic-proxy stores -> visible to the tensor core's smem reads
           __syncwarp();
+          PROF_END(6)
           if (lane == 0) mbar_arrive(smem_u32(full_b + wslot));
         }
       }
@@ -1456,8 +1462,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 #ifdef BS_TC_PROFILE
   if (blockIdx.x == 0 && lane == 0)
-    printf("TCPROF warp %d total %lld w0 %lld w1 %lld w2 %lld w3 %lld\n", warp, clock64() - _t_start, _pacc[0],
-           _pacc[1], _pacc[2], _pacc[3]);
+    printf("TCPROF warp %d total %lld w0 %lld w1 %lld w2 %lld w3 %lld w4 %lld w5 %lld w6 %lld\n", warp,
+           clock64() - _t_start, _pacc[0], _pacc[1], _pacc[2], _pacc[3], _pacc[4], _pacc[5], _pacc[6]);
 #endif
   tc_fence_before();
   __syncthreads();

@@ -20,6 +20,7 @@ from paper_1810_11066_b200 import inputs  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--batch", type=int, default=256)
+ap.add_argument("--tile-sweep", action="store_true")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 N = a.batch
@@ -80,5 +81,17 @@ for r in runs:
                                                  L.k, L.s, L.pad, out=r["out"]))
     per.append({"layer": r["li"], "pack_us": tp * 1e3, "conv_us": tc * 1e3})
 res["per_layer"] = per
+if a.tile_sweep:  # the raw launch's tile width per layer: library choice vs forced 64 / 128
+    sweep = []
+    for r in runs:
+        L = r["L"]
+        row = {"layer": r["li"]}
+        for bn in (0, 64, 128):
+            bs.set_tuning(bs.TUNE_TC_TILE_N, bn)
+            row["conv_us_bn%d" % bn] = 1e3 * timed(lambda: bs.bitserial_conv2d_nhwc(
+                r["ap"], 2, r["wp"], 1, bs.BIPOLAR, N, L.h, L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=r["out"]))
+        bs.set_tuning(bs.TUNE_TC_TILE_N, 0)
+        sweep.append(row)
+    res["tile_sweep"] = sweep
 res["sum_per_layer_ms"] = sum(p["pack_us"] + p["conv_us"] for p in per) / 1e3
 print(json.dumps(res))
