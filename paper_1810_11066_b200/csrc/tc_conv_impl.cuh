@@ -1296,6 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fpar ^= 1u << slot;
         }
         PROF_END(2)
+        PROF_BEGIN  // slot 4 (MMA warp): fence + MMA issue
         tc_fence_after();
         const uint32_t a_base = uint32_t(C::kAcol0 + stage * C::kACols);
         const uint64_t b_desc = bdesc0 + uint64_t((slot * C::kBBytes) >> 4);
@@ -1311,8 +1312,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma4_ts<kIdesc>(tacc, a_base + uint32_t(i * (BKB / 4)), b_desc + uint64_t((j * BN * BKB) >> 4), idesc,
                       (kc | i | j) != 0);
           }
+        PROF_END(4)
+        PROF_BEGIN  // slot 5 (MMA warp): stage / slot release commits
         mma_commit_elect(smem_u32(empty + stage));
         if (!keep) mma_commit_elect(smem_u32(empty_b + slot));
+        PROF_END(5)
         if (++stage == S) {
           stage = 0;
           phase ^= 1u;
