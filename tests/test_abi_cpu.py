@@ -90,6 +90,21 @@ def test_validation_before_launch(lib):
     assert b"workspace" in lib.bs_last_error()
 
 
+def test_output_row_bound(lib):
+    """Launches index output rows (M) in 32 bits: shapes past 2^31 - 257 rows are refused
+    before launch (BS_ERR_SHAPE), including a conv whose padding makes the output larger
+    than its input (n*h*w < 2^31 but n*oh*ow > 2^31; 3x3, pad 2 -> oh = h + 2)."""
+    n, h = 131072, 127
+    assert n * h * h < 2 ** 31 - 1 and n * (h + 2) * (h + 2) > 2 ** 31 - 257
+    assert lib.bs_bitserial_conv2d_nhwc(FAKE, 2, FAKE, 1, 1, FAKE, n, h, h, 32, 4, 3, 3, 1, 1, 2, 2, NULL) == 4
+    assert b"output pixels" in lib.bs_last_error()
+    # dense: m past the row bound; n past 2^31 - 1 on the tile kernels (m > 8; the GEMV for
+    # m <= 8 indexes n in 64 bits and takes it)
+    assert lib.bs_bitserial_dense(FAKE, 2, FAKE, 1, 1, FAKE, 2 ** 31 - 1, 8, 64, NULL) == 4
+    assert lib.bs_bitserial_dense(FAKE, 2, FAKE, 1, 1, FAKE, 16, 2 ** 31, 64, NULL) == 4
+    assert b"m or n too large" in lib.bs_last_error()
+
+
 def test_gemv_algo_rejected_for_conv(lib):
     assert lib.bs_bitserial_conv2d_nhwc_ex(FAKE, 2, FAKE, 1, 1, FAKE, 1, 8, 8, 8, 4, 3, 3, 1, 1, 1, 1, 3, NULL) == 3
 
