@@ -776,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_conv_kernel(const __grid_constant__ TcArgs<NP> args, const __grid_constant__ TcMaps<NP> maps) {
   constexpr bool RAW = VAR == kVarRaw, MCAST = VAR == kVarMcast;
   static_assert(!RAW || (F4 && NP == 1), "raw-weight launches: FP4 format, single problem");
+  static_assert(!RAW || BN == 64 || BN == 128, "raw-weight launches: the team's rows split a power-of-two BN");
   using C = Cfg<A_BITS, W_BITS, BN, F4, NP>;
   constexpr int S = C::kStages;   // A ring stages (tensor memory)
   constexpr int NB = C::kBSlots;  // B chunk slots (shared memory)
@@ -1057,7 +1058,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // when weights stay resident, and holding them from here would spill registers)
           uint32_t mb_, nb_;
           tile_mn(args.prob[pi], t, mb_, nb_);
-          wn = int(nb_) * BN + arow;
+          wn = int(nb_) * BN + (arow & (BN - 1));  // BN = 64: two threads per filter row (halves of it)
           wkk0 = kc * C::kCW;
         }
       }
@@ -1108,18 +1109,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (RAW) {
         if (wreload) {  // this chunk's weights: packed planes -> E2M1 digit rows of the B slot
           const TcProb& P = args.prob[0];
-          uint2 wnx[kRW][4];
+          // the team's 128 threads share the slot's BN rows: with BN = 64 each row's eight 16-byte
+          // units are split between two threads (part 0: units 0-3, part 1: units 4-7)
+          constexpr int kSplit = BM / BN, kQd = 4 / kSplit;
+          const int wr = arow & (BN - 1), part = arow / BN;
+          uint2 wnx[kRW][kQd];
           PROF_BEGIN  // slot 4 (RAW): weight-word loads
           {
             const int kp = int(P.p.kp);
-            const bool rowok = arow < BN && wn < P.p.oc;
+            const bool rowok = wn < P.p.oc;
             const uint32_t* wrow = P.p.wt + (int64_t(wn) * kp + wkk0);
 #pragma unroll
             for (int j = 0; j < kRW; ++j)
 #pragma unroll
-              for (int q = 0; q < 4; ++q)  // packed rows have an even word count: 2-word pieces are all-in or all-out
-                wnx[j][q] = (rowok && wkk0 + 2 * q < kp) ? ldg_nc_v2(wrow + int64_t(j) * P.p.oc * kp + 2 * q)
-                                                         : make_uint2(0u, 0u);
+              for (int q = 0; q < kQd; ++q) {  // packed rows have an even word count: 2-word pieces are all-in or all-out
+                const int qq = part * kQd + q;
+                wnx[j][q] = (rowok && wkk0 + 2 * qq < kp) ? ldg_nc_v2(wrow + int64_t(j) * P.p.oc * kp + 2 * qq)
+                                                          : make_uint2(0u, 0u);
+              }
           }
           PROF_END(4)
           PROF_BEGIN  // slot 5 (RAW): wait for the slot's release
@@ -1131,19 +1138,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           PROF_END(5)
           PROF_BEGIN  // slot 6 (RAW): weight digit formation + shared-memory stores
-          if (arow < BN) {
-            uint8_t* brow = s_stage + wslot * C::kBBytes + arow * C::kBRow;
+          {
+            uint8_t* brow = s_stage + wslot * C::kBBytes + wr * C::kBRow;
             const int wenc = P.p.bipolar;
 #pragma unroll
             for (int e = 0; e < C::kWP; ++e) {
               constexpr int kDummy = 0;
               (void)kDummy;
 #pragma unroll
-              for (int wd = 0; wd < 8; ++wd) {
-                const uint32_t lo = wd & 1 ? wnx[2 * e][wd >> 1].y : wnx[2 * e][wd >> 1].x;
+              for (int wi = 0; wi < 2 * kQd; ++wi) {
+                const int wd = part * 2 * kQd + wi;  // the 16-byte unit (packed word) of the row
+                const uint32_t lo = wi & 1 ? wnx[2 * e][wi >> 1].y : wnx[2 * e][wi >> 1].x;
                 const bool has_hi = 2 * e + 1 < W_BITS;
-                const uint32_t hi = has_hi ? (wd & 1 ? wnx[(2 * e + 1) % kRW][wd >> 1].y
-                                                     : wnx[(2 * e + 1) % kRW][wd >> 1].x) : 0u;
+                const uint32_t hi = has_hi ? (wi & 1 ? wnx[(2 * e + 1) % kRW][wi >> 1].y
+                                                     : wnx[(2 * e + 1) % kRW][wi >> 1].x) : 0u;
                 uint32_t o[4];
                 if (wenc == 1) {  // bipolar: +-0.5 / +-1.5 digits; padding elements must stay 0
                   const uint32_t valid = tap_word_mask(wkk0 + wd, P.p.kp, P.p.c_tap, P.p.kw_a);
@@ -1168,7 +1176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   }
                 }
                 // 16-byte unit wd of this 128-byte row, 128B-swizzled as TMA would place it
-                *reinterpret_cast<uint4*>(brow + e * BN * C::kBRow + ((uint32_t(wd) ^ uint32_t(arow & 7)) << 4)) =
+                *reinterpret_cast<uint4*>(brow + e * BN * C::kBRow + ((uint32_t(wd) ^ uint32_t(wr & 7)) << 4)) =
                     make_uint4(o[0], o[1], o[2], o[3]);
               }
             }
