@@ -156,9 +156,9 @@ class ConvLayerRun:
         if self.path == "tc":
             self.bs.bitserial_conv2d_nhwc_tc_i8(self.act, self.a_bits, self.w_tc, self.w_bits, L.oc, L.k, L.k,
                                                 L.s, L.pad, out=self.out, workspace=self.ws, tc_format=self.fmt)
-        else:
-            self.bs.bitserial_conv2d_nhwc_i8(self.act, self.a_bits, self.wp, self.w_bits, self.enc, L.oc, L.k, L.k,
-                                             L.s, L.pad, out=self.out, workspace=self.ws)
+        else:  # --path popc: the integer-pipe kernel by name (BS_ALGO_AUTO would take the tensor cores)
+            self.bs.bitpack(self.act, self.a_bits, out=self.packed)
+            self.conv_only()
 
     def pack_only(self, max_ctas=0):
         self.bs.bitpack(self.act, self.a_bits, out=self.packed, max_ctas=max_ctas)
@@ -171,7 +171,8 @@ class ConvLayerRun:
                                                       tc_format=self.fmt)
         else:
             self.bs.bitserial_conv2d_nhwc(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, self.n, L.h,
-                                          L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out)
+                                          L.w, L.ic, L.oc, L.k, L.k, L.s, L.pad, out=self.out,
+                                          algo=self.bs.ALGO_POPC)
 
     def tcd_item(self):
         L = self.L
@@ -825,7 +826,7 @@ class DenseWorkload:
                                                     self.k, out=self.out, tc_format=self.fmt)
             else:
                 self.bs.bitserial_dense(self.packed, self.a_bits, self.wp, self.w_bits, self.enc, rows, self.n,
-                                        self.k, out=self.out)
+                                        self.k, out=self.out, algo=self.bs.ALGO_POPC)
         if self.digit:
             self.bs.digitpack(self.a, self.a_bits, out=self.a_dig)
         elif not gemv:
