@@ -295,6 +295,7 @@ class ConvWorkload:
             "rank0_images": [lo, hi],
             "step": self.describe_step(args),
             "path": args.path,
+            "hybrid_order": ([args.hybrid_order, args.hybrid_pack_ctas_per_sm] if args.path == "hybrid" else None),
             "tc_format": args.tc_format if args.path in ("tc", "hybrid") else None,
             "conv_groups": (args.conv_groups if self.overlap else 0),
             "pack_group": bool(self.overlap and args.pack_group),
@@ -306,8 +307,11 @@ class ConvWorkload:
             return (f"layers {[r.L.name for r in self.runs if r.path == 'tcw']} on the window path (ONE "
                     "bs_digitpack_win_group + ONE bs_bitserial_conv2d_nhwc_tcw_group launch, own stream) beside layers "
                     f"{[r.L.name for r in self.runs if r.path == 'tc']} on the expansion kernel (ONE bs_bitpack_group "
-                    "launch on a side stream, then ONE bs_bitserial_conv2d_nhwc_tc_group call); weights packed and "
-                    "prepared once, untimed")
+                    "launch on a side stream, then ONE bs_bitserial_conv2d_nhwc_tc_group call); " +
+                    {0: "the two packs start together",
+                     1: "the bit-plane pack starts when the window pack ends, beside the window conv",
+                     2: "the window pack starts when the bit-plane pack ends, beside the expansion conv"}[
+                         args.hybrid_order] + "; weights packed and prepared once, untimed")
         if args.path == "tcw":
             return ("every layer's activations packed into its conv's window layout (zero-padded stride phases, 32-byte "
                     "swizzled digit rows, DESIGN.md R26) by ONE bs_digitpack_win_group launch, then every layer's conv "
@@ -344,6 +348,39 @@ class ConvWorkload:
             s_w, s_p = self.hy_streams
             s_w.wait_stream(main)
             s_p.wait_stream(main)
+            ho = self.args.hybrid_order
+            if ho:  # one path's pack beside the OTHER path's conv instead of beside its pack
+                sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
+                cap = self.args.hybrid_pack_ctas_per_sm * sm
+                wpack = lambda: bs.digitpack_win_group(self.tcw_pack, self.args.a_bits,  # noqa: E731
+                                                       outs=[r.win for r in self.w_runs])
+                tpack = lambda c: bs.bitpack_group([r.act for r in self.t_runs], self.args.a_bits,  # noqa: E731
+                                                   outs=[r.packed for r in self.t_runs], max_ctas=c)
+                wconv = lambda: bs.bitserial_conv2d_nhwc_tcw_group(self.tcw_items, self.args.a_bits,  # noqa: E731
+                                                                   self.args.w_bits)
+                tconv = lambda: bs.bitserial_conv2d_nhwc_tc_group(self.tc_items, self.args.a_bits,  # noqa: E731
+                                                                  self.args.w_bits, tc_format=tc_fmt(self.args))
+                if ho == 1:  # window pack; then [window conv || bit-plane pack]; then expansion conv
+                    with torch.cuda.stream(s_w):
+                        wpack()
+                    s_p.wait_stream(s_w)
+                    with torch.cuda.stream(s_w):
+                        wconv()
+                    with torch.cuda.stream(s_p):
+                        tpack(cap)
+                        tconv()
+                else:  # bit-plane pack; then [expansion conv || window pack (no cap option)]; then window conv
+                    with torch.cuda.stream(s_p):
+                        tpack(0)
+                    s_w.wait_stream(s_p)
+                    with torch.cuda.stream(s_p):
+                        tconv()
+                    with torch.cuda.stream(s_w):
+                        wpack()
+                        wconv()
+                main.wait_stream(s_p)
+                main.wait_stream(s_w)
+                return
             with torch.cuda.stream(s_w):
                 bs.digitpack_win_group(self.tcw_pack, self.args.a_bits, outs=[r.win for r in self.w_runs])
                 bs.bitserial_conv2d_nhwc_tcw_group(self.tcw_items, self.args.a_bits, self.args.w_bits)
@@ -1336,6 +1373,13 @@ def build_parser():
                          "window-path pipeline; unified = one per-layer pipeline for all layers")
     ap.add_argument("--tcw-layers", default="2,5,6,8",
                     help="--path hybrid: the layers on the window path (measured best partition, profiles/r02w_hybrid*)")
+    ap.add_argument("--hybrid-order", type=int, default=1, choices=[0, 1, 2],
+                    help="--path hybrid step composition: 1 (default) = window pack, then the bit-plane pack beside the "
+                         "window conv (its 320-thread CTAs leave room on every SM), then the expansion conv; 0 = the two "
+                         "packs side by side, then the two convs; 2 = window pack beside the expansion conv "
+                         "(profiles/r02zj_hybrid_order.jsonl: 0.2357 / 0.2425 / 0.263 ms)")
+    ap.add_argument("--hybrid-pack-ctas-per-sm", type=int, default=0,
+                    help="--hybrid-order 1: grid cap of the bit-plane pack in CTAs per SM (0 = library choice)")
     ap.add_argument("--path", choices=["auto", "tc", "tcd", "tcw", "hybrid", "popc", "small"], default="auto",
                     help="conv/GEMM kernel: tensor-core bitserial (tc), the digit path (tcd), the window path (tcw), the "
                          "AND/POPC integer-pipe kernel, the one-launch small-problem path, or hybrid (--tcw-layers on "
