@@ -49,25 +49,27 @@ uint32_t digit_lut(int bits, int enc, int d) {
 
 namespace {
 
-// 4 bytes holding values < 16 -> one 16-bit field of 4 nibbles (byte r -> nibble r)
-__device__ __forceinline__ uint32_t nib4(uint32_t x) {
-  const uint32_t y = x | (x >> 4);
-  return (y & 0xFFu) | ((y >> 8) & 0xFF00u);
-}
-
-// 32 codes (element 4q+r in byte r of v[q]) -> the 16 digit bytes of digit D
+// 32 codes (element 4q+r in byte r of v[q]) -> the 16 digit bytes of digit D.  Two words (8 elements) at a
+// time: y = x | x >> 4 leaves the nibble pairs of elements (0,1) and (2,3) in bytes 0 and 2, and one PRMT
+// gathers those bytes of both words (the window pack had been ALU-bound at ~175 instructions per task with
+// a per-word compress: ncu, profiles/r02zn_ncu_full_winpack.json).
 template <int D, int BITS>
 __device__ __forceinline__ uint4 digit_row16(const uint32_t (&v)[8], uint32_t lut, bool ident) {
   constexpr bool kHi = 2 * D + 1 < BITS;
   constexpr uint32_t kMask = kHi ? 0x03030303u : 0x01010101u;
-  uint32_t h[8];
+  uint32_t o[4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const uint32_t x = (v[q] >> (2 * D)) & kMask;  // byte r = plane bits of element 4q+r
-    const uint32_t sel = nib4(x);                 // byte selectors
-    h[q] = nib4(ident ? x : __byte_perm(lut, 0u, sel));
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t x0 = (v[2 * q] >> (2 * D)) & kMask, x1 = (v[2 * q + 1] >> (2 * D)) & kMask;  // byte r = plane bits
+    const uint32_t nib = __byte_perm(x0 | (x0 >> 4), x1 | (x1 >> 4), 0x6420);  // nibble e = plane bits of element e
+    if (ident) {
+      o[q] = nib;
+    } else {  // nibbles as byte selectors into the digit table, then compressed the same way
+      const uint32_t r0 = __byte_perm(lut, 0u, nib), r1 = __byte_perm(lut, 0u, nib >> 16);
+      o[q] = __byte_perm(r0 | (r0 >> 4), r1 | (r1 >> 4), 0x6420);
+    }
   }
-  return make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+  return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 // nvalid < 32: elements past the row end are value 0 whatever the encoding (a bipolar code 0
